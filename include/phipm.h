@@ -1,0 +1,174 @@
+/*
+ * phipm.h — C ABI of libphipm.so, a B200 (sm_100a) implementation of the hot path of
+ * J. Niesen & W. M. Wright, "Algorithm 919: A Krylov subspace algorithm for evaluating the
+ * phi-functions appearing in exponential integrators" (arXiv:0907.4631; PAPER.md).
+ *
+ * phipm evaluates  w(t) = phi_0(tA) u_0 + sum_{k=1..p} t^k phi_k(tA) u_k   (Eq. lincomb2,
+ * PAPER.md P:485-489), i.e. the solution at t of u' = A u + sum_{j<p} s^j/j! u_{j+1}, u(0) = u_0
+ * (Eq. phide), for a large sparse A given as CSR or as a 3/5/7-point stencil, by the
+ * adaptive Krylov time stepping of Algorithms 3-4.
+ *
+ * Conventions for every entry point:
+ *   - Pointers documented "device" must be CUDA device pointers of the current device (e.g. from
+ *     torch); "host" pointers are ordinary CPU memory.  The library never frees, keeps or
+ *     retains caller memory after a call returns.
+ *   - All fp64.  Vectors are contiguous, length n.  Small dense matrices are column-major.
+ *   - All GPU work is enqueued on the stream given to phipm_create (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream).  Calls are host-blocking: they return after the
+ *     result is complete (the controller reads a few scalars back every attempt).
+ *   - Errors are returned as status codes (PHIPM_*); nothing aborts or throws across the ABI.
+ *     phipm_strerror() gives a message; phipm_last_error() a detailed one for the context.
+ *   - One context per host thread; a context runs one call at a time.
+ */
+#ifndef PHIPM_H
+#define PHIPM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define PHIPM_OK          0  /* success */
+#define PHIPM_EINVAL      1  /* bad argument: null pointer, n <= 0, p < 0 or p > p_max, tol <= 0, t < 0,
+                                m_init not in [1, m_max], n > n_max, malformed descriptor */
+#define PHIPM_ENOMEM      2  /* device or pinned allocation failed */
+#define PHIPM_ECUDA       3  /* CUDA launch / runtime error (message in phipm_last_error) */
+#define PHIPM_ESTEP       4  /* step size underflow (tau < 1e-15 t) or > 100 attempts in one step;
+                                w holds u(t_reached), stats->t_reached < t */
+#define PHIPM_ENONFINITE  5  /* NaN/Inf in beta, H, exp(Hhat) or the error estimate */
+#define PHIPM_ESINGULAR   6  /* singular Pade denominator in the small exponential */
+
+typedef struct phipm_ctx phipm_ctx;
+
+/* Sparse matrix in CSR form, DEVICE arrays.  row_ptr[n+1], col[nnz] (int32, strictly ascending
+ * within a row, in [0,n)), val[nnz].  nnz = row_ptr[n] - row_ptr[0] < 2^31. */
+typedef struct {
+    int64_t n, nnz;
+    const int32_t *row_ptr;
+    const int32_t *col;
+    const double *val;
+} phipm_csr;
+
+/* Constant-coefficient stencil on an nx*ny*nz grid with zero Dirichlet data (neighbours outside
+ * the grid are 0).  Row r = i + nx*(j + ny*k).  dim in {1,2,3}: dim=1 uses c_center,c_xm,c_xp
+ * (ny = nz = 1); dim=2 adds c_ym,c_yp (nz = 1); dim=3 adds c_zm,c_zp.  Unused coefficients are
+ * ignored.  (A 3-point 1-D, 5-point 2-D or 7-point 3-D operator; BASELINE.json configs c1-c4.) */
+typedef struct {
+    int dim, nx, ny, nz;
+    double c_center, c_xm, c_xp, c_ym, c_yp, c_zm, c_zp;
+} phipm_stencil;
+
+/* Orthogonalisation of the Arnoldi step (ignored for symmetric = 1, which runs Lanczos, Alg. 2) */
+#define PHIPM_ORTH_CGS   0   /* one classical Gram-Schmidt pass (equal to Alg. 1's MGS in exact
+                                arithmetic; the default) */
+#define PHIPM_ORTH_CGS2  1   /* CGS with one full re-orthogonalisation pass every step */
+
+/* Options.  Defaults (phipm_default_opts): tol 1e-7, m_init 10 (Alg. 3),
+ * m_max 100, symmetric 0, fixed_m 0, eq6_variant 0, orth CGS, profile 0. */
+typedef struct {
+    double tol;          /* Tol of Eq. (taunew) P:588-593 (absolute 2-norm error per unit time) */
+    int m_init;          /* initial Krylov dimension m (Alg. 3) */
+    int m_max;           /* cap on m (and on m <= n) */
+    int symmetric;       /* 1: Lanczos (A symmetric), 0: Arnoldi */
+    int fixed_m;         /* 1: "phip" mode: m fixed to m_init, only tau adapts */
+    int eq6_variant;     /* 0: Eq. (6) as printed; 1: log(eps/eps_old)/log(tau/tau_old) - 1 (R13) */
+    int orth;            /* PHIPM_ORTH_* */
+    int profile;         /* 1: time every kernel class with CUDA events (phipm_get_profile) */
+} phipm_opts;
+
+/* Statistics (the paper's stats(1..4), plus the Krylov dimension). */
+typedef struct {
+    int32_t nsteps;      /* accepted time steps */
+    int32_t nreject;     /* rejected attempts */
+    int32_t nspmv;       /* products of A with a vector actually executed */
+    int32_t nexpm;       /* small matrix exponentials */
+    int32_t m_last;      /* m of the last accepted attempt */
+    int32_t m_peak;      /* largest m attempted */
+    double t_reached;    /* time reached (== t on success) */
+} phipm_stats;
+
+/* Per-kernel-class device time (CUDA events on the context stream) and algorithmic bytes, summed
+ * over the calls made since the last phipm_reset_profile; valid when opts.profile = 1. */
+typedef struct {
+    double ms_spmv_dot;    /* fused SpMV (+ w-recurrence epilogue / Gram-Schmidt dot products) */
+    double ms_orth;        /* fused orthogonalisation update + norm (and re-orth passes) */
+    double ms_expm;        /* single-CTA augmented exponential + error estimate */
+    double ms_combine;     /* w / u assembly (Eq. step) */
+    double ms_other;       /* norms, copies */
+    double bytes_spmv_dot; /* algorithmic bytes */
+    double bytes_orth;
+    double bytes_combine;
+    int64_t launches;      /* kernels launched */
+    int64_t n_spmv_dot, n_orth, n_expm, n_combine;
+} phipm_profile;
+
+void phipm_default_opts(phipm_opts *opts);
+
+/* Create a context that can solve problems with n <= n_max, m_max <= m_max, p <= p_max.
+ * Allocates the device workspace (Krylov basis (m_max+1) x n_max, w vectors, small matrices,
+ * reduction scratch) and a pinned result block.  stream: cudaStream_t or NULL. */
+int phipm_create(phipm_ctx **ctx, int64_t n_max, int m_max, int p_max, void *stream);
+void phipm_destroy(phipm_ctx *ctx);
+const char *phipm_strerror(int status);
+const char *phipm_last_error(const phipm_ctx *ctx);
+int phipm_get_profile(const phipm_ctx *ctx, phipm_profile *out);
+void phipm_reset_profile(phipm_ctx *ctx);
+
+/* w = phi_0(tA)u_0 + sum_k t^k phi_k(tA) u_k.  u: HOST array of p+1 DEVICE pointers, each length
+ * A->n; w: DEVICE, length n (may alias u[0] only).  opts NULL = defaults.  stats may be NULL.
+ * t = 0 -> w = u_0.  All u_k = 0 -> w = 0.  t < 0 -> PHIPM_EINVAL (negate A and use
+ * (-1)^k u_k instead). */
+int phipm_solve_csr(phipm_ctx *ctx, double t, const phipm_csr *A, int p, const double *const *u,
+                    const phipm_opts *opts, double *w, phipm_stats *stats);
+int phipm_solve_stencil(phipm_ctx *ctx, double t, const phipm_stencil *S, int p,
+                        const double *const *u, const phipm_opts *opts, double *w,
+                        phipm_stats *stats);
+
+/* Same computation with HOST buffers: A's arrays (host_csr), u_k and w are HOST pointers (pinned
+ * memory copies fastest).  The call copies inputs to the context's device workspace, solves, and
+ * copies w back; n <= n_max and nnz <= nnz_max of phipm_reserve_host_csr. */
+int phipm_reserve_host_csr(phipm_ctx *ctx, int64_t nnz_max);
+int phipm_solve_csr_host(phipm_ctx *ctx, double t, const phipm_csr *host_A, int p,
+                         const double *const *host_u, const phipm_opts *opts, double *host_w,
+                         phipm_stats *stats);
+int phipm_solve_stencil_host(phipm_ctx *ctx, double t, const phipm_stencil *S, int p,
+                             const double *const *host_u, const phipm_opts *opts, double *host_w,
+                             phipm_stats *stats);
+
+/* ---- kernel-level entry points (parity tests; all DEVICE pointers unless stated) ---- */
+
+/* structural nonzeros of the stencil's CSR form (N_A of Eq. 4); -1 on a bad descriptor */
+int64_t phipm_stencil_nnz(const phipm_stencil *S);
+/* CSR of the stencil (row order as above; entries of a row in ascending column order:
+ * z-, y-, x-, centre, x+, y+, z+); row_ptr[n+1], col[nnz], val[nnz] device, caller-allocated */
+int phipm_csr_from_stencil(phipm_ctx *ctx, const phipm_stencil *S, int32_t *row_ptr, int32_t *col,
+                           double *val);
+/* y = A x */
+int phipm_spmv_csr(phipm_ctx *ctx, const phipm_csr *A, const double *x, double *y);
+int phipm_spmv_stencil(phipm_ctx *ctx, const phipm_stencil *S, const double *x, double *y);
+/* *result (HOST) = x^T y, deterministic grid reduction */
+int phipm_dot(phipm_ctx *ctx, int64_t n, const double *x, const double *y, double *result);
+/* *result (HOST) = ||A||_inf */
+int phipm_inf_norm_csr(phipm_ctx *ctx, const phipm_csr *A, double *result);
+/* E = exp(A), K x K column-major (Pade-13 scaling and squaring), K <= m_max + p_max + 1 */
+int phipm_expm(phipm_ctx *ctx, int K, const double *A, double *E);
+/* phi_p(tau H) e1 and phi_{p+1}(tau H) e1 from one augmented exponential (Eq. hathm), H mu x mu
+ * with leading dimension ldh (device); phip, phip1 device length mu; *normH1 (HOST) = ||H||_1 */
+int phipm_phi_pair(phipm_ctx *ctx, int mu, const double *H, int ldh, double tau, int p,
+                   double *phip, double *phip1, double *normH1);
+/* Krylov basis from seed v (Alg. 1 via CGS per opts->orth, or Alg. 2 if symmetric): V device
+ * n x (m+1) column-major (ld n, normalised columns), H device (m+1) x m column-major; *k (HOST)
+ * columns of H built, *brk (HOST) 1 on breakdown, *beta (HOST) = ||v||. */
+int phipm_krylov_csr(phipm_ctx *ctx, const phipm_csr *A, const double *v, int m,
+                     const phipm_opts *opts, double *V, double *H, int *k, int *brk, double *beta);
+int phipm_krylov_stencil(phipm_ctx *ctx, const phipm_stencil *S, const double *v, int m,
+                         const phipm_opts *opts, double *V, double *H, int *k, int *brk,
+                         double *beta);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PHIPM_H */

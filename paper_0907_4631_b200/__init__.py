@@ -1,0 +1,360 @@
+"""phipm on B200: Python binding of libphipm.so (include/phipm.h).
+
+Argument marshalling only — every step of the method runs in the library's CUDA kernels.  Device
+vectors are torch CUDA tensors (float64, contiguous); PyTorch supplies memory and streams.
+There is no CPU fallback: if the library is missing or no GPU is present, calls raise.
+
+    import paper_0907_4631_b200 as P
+    ctx = P.Context(n_max=n, m_max=100, p_max=4)
+    w, stats = ctx.solve_stencil(t, P.Stencil(2, 256, 256, 1, coeffs), [u0, u1, u2, u3],
+                                 tol=1e-10, symmetric=True)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import Optional, Sequence, Tuple
+
+from .build import LIB, build  # noqa: F401
+
+__all__ = ["Context", "Stencil", "Stats", "Profile", "PhipmError", "lib", "LIB", "build"]
+
+OK, EINVAL, ENOMEM, ECUDA, ESTEP, ENONFINITE, ESINGULAR = 0, 1, 2, 3, 4, 5, 6
+ORTH_CGS, ORTH_CGS2 = 0, 1
+
+
+class PhipmError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"phipm status {status}: {msg}")
+        self.status = status
+
+
+class _Csr(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nnz", C.c_int64), ("row_ptr", C.c_void_p), ("col", C.c_void_p),
+                ("val", C.c_void_p)]
+
+
+class _Stencil(C.Structure):
+    _fields_ = [("dim", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+                ("c_center", C.c_double), ("c_xm", C.c_double), ("c_xp", C.c_double),
+                ("c_ym", C.c_double), ("c_yp", C.c_double), ("c_zm", C.c_double), ("c_zp", C.c_double)]
+
+
+class _Opts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("m_init", C.c_int), ("m_max", C.c_int), ("symmetric", C.c_int),
+                ("fixed_m", C.c_int), ("eq6_variant", C.c_int), ("orth", C.c_int), ("profile", C.c_int)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("nsteps", C.c_int32), ("nreject", C.c_int32), ("nspmv", C.c_int32), ("nexpm", C.c_int32),
+                ("m_last", C.c_int32), ("m_peak", C.c_int32), ("t_reached", C.c_double)]
+
+
+class _Profile(C.Structure):
+    _fields_ = [("ms_spmv_dot", C.c_double), ("ms_orth", C.c_double), ("ms_expm", C.c_double),
+                ("ms_combine", C.c_double), ("ms_other", C.c_double), ("bytes_spmv_dot", C.c_double),
+                ("bytes_orth", C.c_double), ("bytes_combine", C.c_double), ("launches", C.c_int64),
+                ("n_spmv_dot", C.c_int64), ("n_orth", C.c_int64), ("n_expm", C.c_int64),
+                ("n_combine", C.c_int64)]
+
+
+@dataclasses.dataclass(frozen=True)
+class Stencil:
+    """phipm_stencil: coeffs = (c_center, c_xm, c_xp, c_ym, c_yp, c_zm, c_zp)."""
+    dim: int
+    nx: int
+    ny: int
+    nz: int
+    coeffs: Tuple[float, ...]
+
+    @property
+    def n(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def _c(self) -> _Stencil:
+        return _Stencil(self.dim, self.nx, self.ny, self.nz, *[float(x) for x in self.coeffs])
+
+    @classmethod
+    def of(cls, s) -> "Stencil":
+        return cls(s.dim, s.nx, s.ny, s.nz, tuple(s.coeffs))
+
+
+@dataclasses.dataclass
+class Stats:
+    nsteps: int
+    nreject: int
+    nspmv: int
+    nexpm: int
+    m_last: int
+    m_peak: int
+    t_reached: float
+
+
+Profile = dict
+
+_lib = None
+
+
+def lib():
+    """Load libphipm.so (raises if it has not been built: there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            raise ImportError(f"{LIB} not built; run paper_0907_4631_b200.build() (nvcc, sm_100a)")
+        L = C.CDLL(LIB)
+        vp, i64, i32, d = C.c_void_p, C.c_int64, C.c_int, C.c_double
+        P = C.POINTER
+        sig = {
+            "phipm_default_opts": (None, [P(_Opts)]),
+            "phipm_create": (i32, [P(vp), i64, i32, i32, vp]),
+            "phipm_destroy": (None, [vp]),
+            "phipm_strerror": (C.c_char_p, [i32]),
+            "phipm_last_error": (C.c_char_p, [vp]),
+            "phipm_get_profile": (i32, [vp, P(_Profile)]),
+            "phipm_reset_profile": (None, [vp]),
+            "phipm_solve_csr": (i32, [vp, d, P(_Csr), i32, P(vp), P(_Opts), vp, P(_Stats)]),
+            "phipm_solve_stencil": (i32, [vp, d, P(_Stencil), i32, P(vp), P(_Opts), vp, P(_Stats)]),
+            "phipm_reserve_host_csr": (i32, [vp, i64]),
+            "phipm_solve_csr_host": (i32, [vp, d, P(_Csr), i32, P(vp), P(_Opts), vp, P(_Stats)]),
+            "phipm_solve_stencil_host": (i32, [vp, d, P(_Stencil), i32, P(vp), P(_Opts), vp, P(_Stats)]),
+            "phipm_stencil_nnz": (i64, [P(_Stencil)]),
+            "phipm_csr_from_stencil": (i32, [vp, P(_Stencil), vp, vp, vp]),
+            "phipm_spmv_csr": (i32, [vp, P(_Csr), vp, vp]),
+            "phipm_spmv_stencil": (i32, [vp, P(_Stencil), vp, vp]),
+            "phipm_dot": (i32, [vp, i64, vp, vp, P(d)]),
+            "phipm_inf_norm_csr": (i32, [vp, P(_Csr), P(d)]),
+            "phipm_expm": (i32, [vp, i32, vp, vp]),
+            "phipm_phi_pair": (i32, [vp, i32, vp, i32, d, i32, vp, vp, P(d)]),
+            "phipm_krylov_csr": (i32, [vp, P(_Csr), vp, i32, P(_Opts), vp, vp, P(i32), P(i32), P(d)]),
+            "phipm_krylov_stencil": (i32, [vp, P(_Stencil), vp, i32, P(_Opts), vp, vp, P(i32), P(i32), P(d)]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+EXPORTED = [
+    "phipm_default_opts", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
+    "phipm_get_profile", "phipm_reset_profile", "phipm_solve_csr", "phipm_solve_stencil",
+    "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_stencil_nnz",
+    "phipm_csr_from_stencil", "phipm_spmv_csr", "phipm_spmv_stencil", "phipm_dot", "phipm_inf_norm_csr",
+    "phipm_expm", "phipm_phi_pair", "phipm_krylov_csr", "phipm_krylov_stencil",
+]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(t) -> int:
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+def _f64(t):
+    if t.dtype != _torch().float64:
+        raise TypeError("expected float64")
+    return _ptr(t)
+
+
+def _i32(t):
+    if t.dtype != _torch().int32:
+        raise TypeError("expected int32")
+    return _ptr(t)
+
+
+class Context:
+    """phipm_ctx: workspace for problems with n <= n_max, m <= m_max, p <= p_max."""
+
+    def __init__(self, n_max: int, m_max: int = 100, p_max: int = 4, stream=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("phipm needs a CUDA GPU (no CPU fallback)")
+        self._L = lib()
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        h = C.c_void_p()
+        st = self._L.phipm_create(C.byref(h), int(n_max), int(m_max), int(p_max),
+                                  C.c_void_p(self.stream.cuda_stream))
+        if st != OK:
+            raise PhipmError(st, self._L.phipm_strerror(st).decode())
+        self._h = h
+        self.n_max, self.m_max, self.p_max = n_max, m_max, p_max
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.phipm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st):
+        if st != OK:
+            raise PhipmError(st, self._L.phipm_last_error(self._h).decode())
+
+    # ---------------------------------------------------------------- options / profile
+    def opts(self, tol=1e-7, m_init=10, m_max=None, symmetric=False, fixed_m=False,
+             eq6_variant=False, orth=ORTH_CGS, profile=False) -> _Opts:
+        o = _Opts()
+        self._L.phipm_default_opts(C.byref(o))
+        o.tol = tol
+        o.m_init = m_init
+        o.m_max = self.m_max if m_max is None else m_max
+        o.symmetric = int(bool(symmetric))
+        o.fixed_m = int(bool(fixed_m))
+        o.eq6_variant = int(bool(eq6_variant))
+        o.orth = int(orth)
+        o.profile = int(bool(profile))
+        return o
+
+    def profile(self) -> dict:
+        p = _Profile()
+        self._check(self._L.phipm_get_profile(self._h, C.byref(p)))
+        return {k: getattr(p, k) for k, _ in _Profile._fields_}
+
+    def reset_profile(self):
+        self._L.phipm_reset_profile(self._h)
+
+    # ---------------------------------------------------------------- solves
+    @staticmethod
+    def _csr(A, device=True) -> _Csr:
+        rp, col, val = A
+        if device:
+            return _Csr(rp.numel() - 1, col.numel(), _i32(rp), _i32(col), _f64(val))
+        return _Csr(len(rp) - 1, len(col), rp.ctypes.data, col.ctypes.data, val.ctypes.data)
+
+    def _uptrs(self, u, host=False):
+        arr = (C.c_void_p * len(u))()
+        for k, x in enumerate(u):
+            arr[k] = x.ctypes.data if host else _f64(x)
+        return arr
+
+    def solve_csr(self, t: float, A, u: Sequence, out=None, stats_only=False, **kw):
+        """A = (row_ptr int32, col int32, val float64) CUDA tensors; u = p+1 CUDA float64 vectors."""
+        torch = _torch()
+        n = A[0].numel() - 1
+        w = out if out is not None else torch.empty(n, dtype=torch.float64, device=u[0].device)
+        s = _Stats()
+        o = self.opts(**kw)
+        st = self._L.phipm_solve_csr(self._h, float(t), C.byref(self._csr(A)), len(u) - 1,
+                                     self._uptrs(u), C.byref(o), _f64(w), C.byref(s))
+        self._check(st)
+        return w, Stats(*[getattr(s, k) for k, _ in _Stats._fields_])
+
+    def solve_stencil(self, t: float, S: Stencil, u: Sequence, out=None, **kw):
+        torch = _torch()
+        w = out if out is not None else torch.empty(S.n, dtype=torch.float64, device=u[0].device)
+        s = _Stats()
+        o = self.opts(**kw)
+        st = self._L.phipm_solve_stencil(self._h, float(t), C.byref(S._c()), len(u) - 1, self._uptrs(u),
+                                         C.byref(o), _f64(w), C.byref(s))
+        self._check(st)
+        return w, Stats(*[getattr(s, k) for k, _ in _Stats._fields_])
+
+    def solve_csr_host(self, t: float, A, u: Sequence, out, **kw):
+        """HOST (numpy) operands; `out` a host float64 array (pinned memory copies fastest)."""
+        s = _Stats()
+        o = self.opts(**kw)
+        st = self._L.phipm_solve_csr_host(self._h, float(t), C.byref(self._csr(A, device=False)), len(u) - 1,
+                                          self._uptrs(u, host=True), C.byref(o), C.c_void_p(out.ctypes.data),
+                                          C.byref(s))
+        self._check(st)
+        return out, Stats(*[getattr(s, k) for k, _ in _Stats._fields_])
+
+    def solve_stencil_host(self, t: float, S: Stencil, u: Sequence, out, **kw):
+        s = _Stats()
+        o = self.opts(**kw)
+        st = self._L.phipm_solve_stencil_host(self._h, float(t), C.byref(S._c()), len(u) - 1,
+                                              self._uptrs(u, host=True), C.byref(o),
+                                              C.c_void_p(out.ctypes.data), C.byref(s))
+        self._check(st)
+        return out, Stats(*[getattr(s, k) for k, _ in _Stats._fields_])
+
+    def reserve_host_csr(self, nnz_max: int):
+        self._check(self._L.phipm_reserve_host_csr(self._h, int(nnz_max)))
+
+    # ---------------------------------------------------------------- kernel level
+    def stencil_nnz(self, S: Stencil) -> int:
+        return int(self._L.phipm_stencil_nnz(C.byref(S._c())))
+
+    def csr_from_stencil(self, S: Stencil):
+        torch = _torch()
+        nnz = self.stencil_nnz(S)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        rp = torch.empty(S.n + 1, dtype=torch.int32, device=dev)
+        col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)[:nnz]
+        val = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)[:nnz]
+        self._check(self._L.phipm_csr_from_stencil(self._h, C.byref(S._c()), _i32(rp), _i32(col), _f64(val)))
+        return rp, col, val
+
+    def spmv_csr(self, A, x, y=None):
+        torch = _torch()
+        y = y if y is not None else torch.empty_like(x)
+        self._check(self._L.phipm_spmv_csr(self._h, C.byref(self._csr(A)), _f64(x), _f64(y)))
+        return y
+
+    def spmv_stencil(self, S: Stencil, x, y=None):
+        torch = _torch()
+        y = y if y is not None else torch.empty_like(x)
+        self._check(self._L.phipm_spmv_stencil(self._h, C.byref(S._c()), _f64(x), _f64(y)))
+        return y
+
+    def dot(self, x, y) -> float:
+        r = C.c_double()
+        self._check(self._L.phipm_dot(self._h, x.numel(), _f64(x), _f64(y), C.byref(r)))
+        return r.value
+
+    def inf_norm_csr(self, A) -> float:
+        r = C.c_double()
+        self._check(self._L.phipm_inf_norm_csr(self._h, C.byref(self._csr(A)), C.byref(r)))
+        return r.value
+
+    def expm(self, A):
+        """A: K x K float64 CUDA tensor (row-major torch layout); returns exp(A) (same layout)."""
+        torch = _torch()
+        K = A.shape[0]
+        Acm = A.t().contiguous()                  # column-major for the library
+        E = torch.empty_like(Acm)
+        self._check(self._L.phipm_expm(self._h, K, _f64(Acm), _f64(E)))
+        return E.t().contiguous()
+
+    def phi_pair(self, H, tau: float, p: int):
+        """H: mu x mu CUDA tensor (row-major torch); returns (phi_p e1, phi_{p+1} e1, ||H||_1)."""
+        torch = _torch()
+        mu = H.shape[0]
+        Hcm = H.t().contiguous()
+        a = torch.empty(mu, dtype=torch.float64, device=H.device)
+        b = torch.empty(mu, dtype=torch.float64, device=H.device)
+        nh = C.c_double()
+        self._check(self._L.phipm_phi_pair(self._h, mu, _f64(Hcm), mu, float(tau), int(p), _f64(a), _f64(b),
+                                           C.byref(nh)))
+        return a, b, nh.value
+
+    def krylov(self, A, v, m: int, symmetric=False, orth=ORTH_CGS):
+        """A: Stencil or CSR tuple of CUDA tensors.  Returns (V n x (m+1), H (m+1) x m, k, brk, beta)."""
+        torch = _torch()
+        n = v.numel()
+        Vcm = torch.zeros((m + 1, n), dtype=torch.float64, device=v.device)      # column-major n x (m+1)
+        Hcm = torch.zeros((m, m + 1), dtype=torch.float64, device=v.device)      # column-major (m+1) x m
+        k, brk, beta = C.c_int(), C.c_int(), C.c_double()
+        o = self.opts(symmetric=symmetric, orth=orth)
+        if isinstance(A, Stencil):
+            st = self._L.phipm_krylov_stencil(self._h, C.byref(A._c()), _f64(v), m, C.byref(o), _f64(Vcm),
+                                              _f64(Hcm), C.byref(k), C.byref(brk), C.byref(beta))
+        else:
+            st = self._L.phipm_krylov_csr(self._h, C.byref(self._csr(A)), _f64(v), m, C.byref(o), _f64(Vcm),
+                                          _f64(Hcm), C.byref(k), C.byref(brk), C.byref(beta))
+        self._check(st)
+        return Vcm.t(), Hcm.t(), k.value, bool(brk.value), beta.value

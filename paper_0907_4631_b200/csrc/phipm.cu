@@ -1,0 +1,1190 @@
+// phipm.cu — host side of libphipm: context/workspace, kernel launches, the step-size and
+// Krylov-dimension controller (Sec. 3.3-3.4, Algorithms 3-4), and the C ABI of
+// include/phipm.h.
+//
+// The controller reads back one small result block per attempt (mapped pinned memory written
+// by the expm kernel); everything n-sized runs in the kernels of kernels.cuh / expm.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "phipm.h"
+#include "kernels.cuh"
+#include "expm.cuh"
+
+using namespace phipm;
+
+namespace {
+
+constexpr int P_MAX_ABS = 6;          // MAXZ bounds the epilogue vector count
+constexpr double EPS_MACH = 2.220446049250313080847e-16;
+
+enum ProfClass { PC_SPMV = 0, PC_ORTH, PC_EXPM, PC_COMBINE, PC_OTHER, PC_N };
+
+struct ProfRec {
+    cudaEvent_t a, b;
+    int cls;
+    double bytes;
+};
+
+} // namespace
+
+struct phipm_ctx {
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    int64_t n_max = 0, ldv = 0;
+    int m_max = 0, p_max = 0, kmax = 0;
+    int sm_count = 0, occ_spmv = 1, occ_axpy = 1;
+    int pstride = 0;
+    size_t expm_smem_limit = 0;
+    // device workspace
+    double *V = nullptr, *W = nullptr, *Y = nullptr, *H = nullptr, *sigma = nullptr, *g = nullptr;
+    double *part = nullptr, *comb = nullptr, *combd = nullptr, *scratch = nullptr, *raw = nullptr;
+    unsigned *counter = nullptr;
+    DevState *st = nullptr;
+    AttemptResult *res_h = nullptr, *res_d = nullptr;
+    double *raw_h = nullptr;                 // pinned staging for small readbacks
+    // host-buffer solve staging
+    double *hu = nullptr, *hw = nullptr;
+    int32_t *hrp = nullptr, *hcol = nullptr;
+    double *hval = nullptr;
+    int64_t nnz_cap = 0;
+    // profiling
+    bool prof = false;
+    std::vector<ProfRec> pending;
+    std::vector<cudaEvent_t> pool;
+    phipm_profile acc{};
+    int seq = 0;
+    char err[512] = {0};
+};
+
+namespace {
+
+int set_err(phipm_ctx *c, int code, const char *fmt, ...)
+{
+    if (c) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(c->err, sizeof(c->err), fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return set_err(c, PHIPM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                           __FILE__, __LINE__);                                                    \
+    } while (0)
+
+Work make_work(phipm_ctx *c)
+{
+    Work w;
+    w.V = c->V;
+    w.ldv = c->ldv;
+    w.H = c->H;
+    w.ldh = c->m_max + 1;
+    w.hcols = c->m_max;
+    w.sigma = c->sigma;
+    w.g = c->g;
+    w.part = c->part;
+    w.pstride = c->pstride;
+    w.counter = c->counter;
+    w.st = c->st;
+    w.out_raw = c->raw;
+    return w;
+}
+
+cudaEvent_t ev_get(phipm_ctx *c)
+{
+    if (!c->pool.empty()) {
+        cudaEvent_t e = c->pool.back();
+        c->pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+void prof_begin(phipm_ctx *c, ProfRec &r, int cls, double bytes)
+{
+    if (!c->prof) return;
+    r.cls = cls;
+    r.bytes = bytes;
+    r.a = ev_get(c);
+    r.b = ev_get(c);
+    cudaEventRecord(r.a, c->stream);
+}
+
+void prof_end(phipm_ctx *c, ProfRec &r)
+{
+    if (!c->prof) return;
+    cudaEventRecord(r.b, c->stream);
+    c->pending.push_back(r);
+}
+
+// after a stream sync: fold pending event pairs into the accumulators
+void prof_collect(phipm_ctx *c)
+{
+    for (auto &r : c->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        switch (r.cls) {
+        case PC_SPMV: c->acc.ms_spmv_dot += ms; c->acc.bytes_spmv_dot += r.bytes; c->acc.n_spmv_dot++; break;
+        case PC_ORTH: c->acc.ms_orth += ms; c->acc.bytes_orth += r.bytes; c->acc.n_orth++; break;
+        case PC_EXPM: c->acc.ms_expm += ms; c->acc.n_expm++; break;
+        case PC_COMBINE: c->acc.ms_combine += ms; c->acc.bytes_combine += r.bytes; c->acc.n_combine++; break;
+        default: c->acc.ms_other += ms; break;
+        }
+        c->pool.push_back(r.a);
+        c->pool.push_back(r.b);
+    }
+    c->pending.clear();
+}
+
+int grid_for(phipm_ctx *c, int64_t units, int occ)
+{
+    int64_t g = std::min<int64_t>(units, (int64_t)occ * c->sm_count);
+    if (g < 1) g = 1;
+    if (g > c->pstride) g = c->pstride;
+    return (int)g;
+}
+
+// ---------------------------------------------------------------------------------------------
+// launches
+
+template <class Op>
+int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a, double bytes_op)
+{
+    const int64_t tiles = (op.n + TILE - 1) / TILE;
+    const int grid = grid_for(c, tiles, c->occ_spmv);
+    const size_t smem = (size_t)(TILE + a.nd * 32) * sizeof(double);
+    ProfRec r;
+    double bytes = bytes_op + 8.0 * (double)op.n * (a.nd + a.nz);
+    prof_begin(c, r, PC_SPMV, bytes);
+    spmv_fused_kernel<Op><<<grid, NT, smem, c->stream>>>(op, a, make_work(c));
+    prof_end(c, r);
+    c->acc.launches++;
+    CK(cudaGetLastError());
+    return PHIPM_OK;
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
+
+int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a, int cls)
+{
+    bool vec = aligned16(a.out) && (a.a0h == 0.0 || aligned16(a.base)) && (a.ldv % 2 == 0) && aligned16(a.V);
+    for (int i = 0; i < a.ne; i++) vec = vec && aligned16(a.e[i]);
+    const int64_t units = vec ? ((n / 2) + NT - 1) / NT : (n + NT - 1) / NT;
+    const int grid = grid_for(c, std::max<int64_t>(units, 1), c->occ_axpy);
+    ProfRec r;
+    const double bytes = 8.0 * (double)n * (a.nc + a.ne + 1 + (a.a0h != 0.0 ? 1 : 0));
+    prof_begin(c, r, cls, bytes);
+    if (vec)
+        axpy_fused_kernel<true><<<grid, NT, 0, c->stream>>>(n, a, make_work(c));
+    else
+        axpy_fused_kernel<false><<<grid, NT, 0, c->stream>>>(n, a, make_work(c));
+    prof_end(c, r);
+    c->acc.launches++;
+    CK(cudaGetLastError());
+    return PHIPM_OK;
+}
+
+int launch_expm(phipm_ctx *c, ExpmArgs &a, int K)
+{
+    const size_t need = (size_t)6 * K * K * sizeof(double);
+    a.use_smem = need <= c->expm_smem_limit;
+    a.scratch = c->scratch;
+    a.res = c->res_d;
+    a.seq = ++c->seq;
+    ProfRec r;
+    prof_begin(c, r, PC_EXPM, 0.0);
+    expm_kernel<<<1, EXPM_NT, a.use_smem ? need : 0, c->stream>>>(a);
+    prof_end(c, r);
+    c->acc.launches++;
+    CK(cudaGetLastError());
+    return PHIPM_OK;
+}
+
+int sync(phipm_ctx *c)
+{
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->prof) prof_collect(c);
+    return PHIPM_OK;
+}
+
+AxpyArgs axpy0()
+{
+    AxpyArgs a;
+    memset(&a, 0, sizeof(a));
+    a.gsign = 1.0;
+    return a;
+}
+
+SpmvArgs spmv0()
+{
+    SpmvArgs a;
+    memset(&a, 0, sizeof(a));
+    return a;
+}
+
+// ---------------------------------------------------------------------------------------------
+// controller (Algorithm 4 then Algorithm 3's choice; DESIGN.md §3 readings R1-R38)
+
+struct CtlMem {
+    bool rejected = false;
+    int last_branch = 0;     // 1: tau changed, 2: m changed
+    bool q_valid = false;
+    double q = 0.0;
+    bool k_valid = false;
+    double kappa = 2.0;
+    double tau_old = 0.0, eps_old = 0.0;
+    int m_old = 0;
+};
+
+struct Problem {
+    int p;
+    int64_t n, NA;
+    bool symmetric;
+    int m_max;               // min(m_max, n)
+    bool fixed_m, eq6_variant;
+};
+
+// M(.) of Eq. (8) with ceil_+ = max(0, ceil(.))
+double cost_M(double x)
+{
+    if (!(x > 0.0)) return 44.0 / 3.0;
+    double l = std::ceil(std::log2(x / 5.37));
+    return 44.0 / 3.0 + 2.0 * (l > 0.0 ? l : 0.0);
+}
+
+// Eq. (4)
+double cost_step(const Problem &P, int m, double M)
+{
+    const double mp = m + P.p, K = m + P.p + 1;
+    const double vec = P.symmetric ? 3.0 * mp : (double)m * m + 3.0 * P.p + 2.0;
+    return mp * (double)P.NA + vec * (double)P.n + M * K * K * K;
+}
+
+struct Decision {
+    double tau_next;
+    int m_next;
+    int branch;
+};
+
+Decision control(const Problem &P, CtlMem &mem, double tau, int m, double eps, double omega, double normH1,
+                 double remaining, bool accepted)
+{
+    const double gamma = 0.8;
+    double q;
+    bool q_now = false;
+    if (mem.rejected && mem.last_branch == 1) {                     // Eq. (6)
+        const double lt = std::log(tau / mem.tau_old), le = std::log(eps / mem.eps_old);
+        q = P.eq6_variant ? le / lt - 1.0 : lt / le - 1.0;
+        if (std::isfinite(q) && q + 1.0 > 0.0) q_now = true;
+        else q = m / 4.0;
+    } else if (mem.rejected && mem.q_valid) {
+        q = mem.q;
+        q_now = true;
+    } else {
+        q = m / 4.0;
+    }
+    const double tau_new = tau * std::pow(gamma / omega, 1.0 / (q + 1.0));   // Eq. (2)
+    double kap;
+    bool k_now = false;
+    if (mem.rejected && mem.last_branch == 2) {                     // Eq. (7)
+        kap = std::pow(eps / mem.eps_old, 1.0 / (double)(mem.m_old - m));
+        if (std::isfinite(kap) && kap > 1.0) k_now = true;
+        else kap = 2.0;
+    } else if (mem.rejected && mem.k_valid) {
+        kap = mem.kappa;
+        k_now = true;
+    } else {
+        kap = 2.0;
+    }
+    const double m_new = m + std::log(omega / gamma) / std::log(kap);   // Eq. (3)
+    // clamps of Algorithm 3
+    double tc = tau_new;
+    if (!(tc >= tau / 5.0)) tc = tau / 5.0;
+    tc = std::min(tc, 2.0 * tau);
+    tc = std::min(tc, remaining);
+    int lo = std::max((3 * m) / 4, 1);
+    int hi = std::min((4 * m + 2) / 3, P.m_max);
+    lo = std::min(lo, hi);
+    int mc;
+    const double mr = std::ceil(m_new);
+    if (!(mr >= (double)lo)) mc = lo;
+    else if (mr > (double)hi) mc = hi;
+    else mc = (int)mr;
+    // Eq. (5) on the clamped candidates
+    const double c_tau = std::ceil(remaining / tc) * cost_step(P, m, cost_M(std::max(tc * normH1, 1.0)));
+    const double c_m = std::ceil(remaining / tau) * cost_step(P, mc, cost_M(std::max(tau * normH1, 1.0)));
+    int br = (c_tau < c_m) ? 1 : 2;
+    if (P.fixed_m) br = 1;
+    if (!accepted && br == 2 && mc == m) br = 1;
+    Decision d;
+    d.branch = br;
+    d.tau_next = br == 1 ? tc : tau;
+    d.m_next = br == 2 ? mc : m;
+    mem.q = q;
+    mem.q_valid = q_now;
+    mem.kappa = kap;
+    mem.k_valid = k_now;
+    if (!accepted) {
+        mem.rejected = true;
+        mem.last_branch = br;
+        mem.tau_old = tau;
+        mem.eps_old = eps;
+        mem.m_old = m;
+    }
+    return d;
+}
+
+// Eq. (tau_0)
+double tau0(double normA, double b_inf, double tol, double mbar)
+{
+    const double e = 2.718281828459045235360287, pi = 3.141592653589793238462643;
+    const double a = tol * std::pow((mbar + 1.0) / e, mbar + 1.0) * std::sqrt(2.0 * pi * (mbar + 1.0));
+    return (10.0 / normA) * std::pow(a / (4.0 * normA * b_inf), 1.0 / mbar);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Krylov extension: steps j = k0 .. k1-1 (0-based), all on the device
+
+template <class Op>
+int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1, double bthr)
+{
+    const int64_t n = op.n;
+    for (int j = k0; j < k1; j++) {
+        double *vj = c->V + (int64_t)j * c->ldv;
+        double *vn = c->V + (int64_t)(j + 1) * c->ldv;
+        SpmvArgs s = spmv0();
+        s.x = vj;
+        s.xscale = c->sigma + j;
+        s.y = c->Y;
+        s.V = c->V;
+        s.ldv = c->ldv;
+        s.ynorm = 1;
+        s.j = j;
+        s.check_brk = 1;
+        AxpyArgs u = axpy0();
+        u.out = vn;
+        u.base = c->Y;
+        u.a0h = 1.0;
+        u.V = c->V;
+        u.ldv = c->ldv;
+        u.g = c->g;
+        u.gsign = -1.0;
+        u.onorm = 1;
+        u.fin = FIN_NORM;
+        u.j = j;
+        u.check_brk = 1;
+        u.bthr = bthr;
+        if (symmetric) {
+            // Alg. 2: w = A v_j - t_{j,j-1} v_{j-1}; t_jj = v_j^T w; w -= t_jj v_j
+            if (j > 0) {
+                s.nz = 1;
+                s.z[0] = c->V + (int64_t)(j - 1) * c->ldv;
+                s.zc[0] = -1.0;
+                s.zcd[0] = &c->st->lz;
+            }
+            s.d0 = j;
+            s.nd = 1;
+            s.fin = FIN_LANCZOS;
+            u.c0 = j;
+            u.nc = 1;
+            u.lanczos = 1;
+        } else {
+            // Alg. 1 (classical Gram-Schmidt form): h = V_j^T w; w -= V_j h
+            s.d0 = 0;
+            s.nd = j + 1;
+            s.fin = FIN_ARNOLDI;
+            u.c0 = 0;
+            u.nc = j + 1;
+        }
+        int rc = launch_spmv(c, op, s, bytes_op);
+        if (rc) return rc;
+        rc = launch_axpy(c, n, u, PC_ORTH);
+        if (rc) return rc;
+        if (!symmetric && orth == PHIPM_ORTH_CGS2) {
+            SpmvArgs d = spmv0();
+            d.x = vn;
+            d.V = c->V;
+            d.ldv = c->ldv;
+            d.d0 = 0;
+            d.nd = j + 1;
+            d.fin = FIN_REORTH;
+            d.j = j;
+            d.check_brk = 1;
+            rc = launch_spmv(c, IdentOp{n}, d, 8.0 * (double)n);
+            if (rc) return rc;
+            AxpyArgs r = u;
+            r.base = vn;
+            rc = launch_axpy(c, n, r, PC_ORTH);
+            if (rc) return rc;
+        }
+    }
+    return PHIPM_OK;
+}
+
+// ---------------------------------------------------------------------------------------------
+// the solve (Algorithm 3)
+
+template <class Op>
+int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_t NA, double normA, int p,
+               const double *const *u, const phipm_opts &o, double *w, phipm_stats *stats)
+{
+    const int64_t n = op.n;
+    phipm_stats S{};
+    S.t_reached = 0.0;
+    auto finish = [&](int rc) {
+        if (stats) *stats = S;
+        return rc;
+    };
+    if (t_end == 0.0) {
+        if (w != u[0]) CK(cudaMemcpyAsync(w, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        int rc = sync(c);
+        return finish(rc);
+    }
+    // ||u_k||_inf for all k: the all-zero test and b_inf of Eq. (tau_0) (R7)
+    {
+        MaxAbsArgs ma;
+        memset(&ma, 0, sizeof(ma));
+        ma.nv = p + 1;
+        for (int k = 0; k <= p; k++) ma.x[k] = u[k];
+        const int grid = grid_for(c, (n + NT - 1) / NT, c->occ_axpy);
+        maxabs_kernel<<<grid, NT, 0, c->stream>>>(n, ma, make_work(c));
+        c->acc.launches++;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(c->raw_h, c->raw, (p + 1) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        int rc = sync(c);
+        if (rc) return finish(rc);
+    }
+    double b_inf = 0.0;
+    for (int k = 0; k <= p && b_inf == 0.0; k++) b_inf = c->raw_h[k];
+    if (b_inf == 0.0) {
+        CK(cudaMemsetAsync(w, 0, n * sizeof(double), c->stream));
+        S.t_reached = t_end;
+        return finish(sync(c));
+    }
+    if (!std::isfinite(b_inf)) return finish(set_err(c, PHIPM_ENONFINITE, "non-finite input vector"));
+
+    Problem P;
+    P.p = p;
+    P.n = n;
+    P.NA = NA;
+    P.symmetric = o.symmetric != 0;
+    P.m_max = (int)std::min<int64_t>(o.m_max, n);
+    P.fixed_m = o.fixed_m != 0;
+    P.eq6_variant = o.eq6_variant != 0;
+    int m = std::min(o.m_init, P.m_max);
+    const double mbar = 0.5 * ((double)o.m_init + (double)P.m_max);
+    double tau = (normA == 0.0) ? t_end : std::min(t_end, tau0(normA, b_inf, o.tol, mbar));
+    if (!(tau > 0.0)) tau = t_end;
+    const double bthr = (double)n * EPS_MACH * normA;
+
+    double *ucur = w;
+    if (w != u[0]) CK(cudaMemcpyAsync(w, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    double tk = 0.0;
+    S.m_peak = m;
+    while (tk < t_end) {
+        if (tau > t_end - tk) tau = t_end - tk;
+        // Eq. (wrecurrence): w_0 = u_k, w_j = A w_{j-1} + sum_l t_k^l/l! u_{j+l}; w_p -> V[:,0]
+        if (p == 0) {
+            AxpyArgs a = axpy0();
+            a.out = c->V;
+            a.base = ucur;
+            a.a0h = 1.0;
+            a.V = c->V;
+            a.ldv = c->ldv;
+            a.onorm = 1;
+            a.fin = FIN_SEED;
+            int rc = launch_axpy(c, n, a, PC_OTHER);
+            if (rc) return finish(rc);
+        }
+        for (int j = 1; j <= p; j++) {
+            SpmvArgs s = spmv0();
+            s.x = (j == 1) ? ucur : c->W + (int64_t)(j - 1) * c->ldv;
+            s.y = (j == p) ? c->V : c->W + (int64_t)j * c->ldv;
+            double coef = 1.0;
+            for (int l = 0; l <= p - j; l++) {
+                if (l > 0) coef = coef * tk / (double)l;
+                s.z[l] = u[j + l];
+                s.zc[l] = coef;
+            }
+            s.nz = p - j + 1;
+            s.ynorm = (j == p);
+            s.fin = (j == p) ? FIN_SEED : FIN_NONE;
+            int rc = launch_spmv(c, op, s, bytes_op);
+            if (rc) return finish(rc);
+        }
+        S.nspmv += p;
+        int k = 0;
+        bool brk = false;
+        CtlMem mem;
+        int attempts = 0;
+        double tau_used = tau;
+        int m_used = m, mu = 0;
+        bool corr = false;
+        for (;;) {
+            attempts++;
+            if (k < m && !brk) {
+                int rc = enqueue_krylov(c, op, bytes_op, P.symmetric, o.orth, k, m, bthr);
+                if (rc) return finish(rc);
+            }
+            ExpmArgs ea;
+            memset(&ea, 0, sizeof(ea));
+            ea.mode = 0;
+            ea.m = m;
+            ea.p = p;
+            ea.tau = tau;
+            ea.H = c->H;
+            ea.ldh = c->m_max + 1;
+            ea.sigma = c->sigma;
+            ea.st = c->st;
+            ea.comb = c->comb;
+            ea.combd = c->combd;
+            int rc = launch_expm(c, ea, m + p + 1);
+            if (rc) return finish(rc);
+            rc = sync(c);
+            if (rc) return finish(rc);
+            AttemptResult R;
+    memcpy(&R, (const void *)c->res_h, sizeof(R));
+            if (R.seq != c->seq) return finish(set_err(c, PHIPM_ECUDA, "stale attempt result"));
+            S.nexpm++;
+            // basis actually built
+            int kb;
+            if (R.brk >= 0) { kb = std::max(k, R.brk); brk = true; }
+            else kb = std::max(k, m);
+            if (R.brk >= 0 && R.brk < k) kb = k;
+            S.nspmv += kb - k;
+            k = kb;
+            if (R.status == 5) return finish(set_err(c, PHIPM_ENONFINITE, "non-finite value in the Krylov step"));
+            if (R.status == 6) return finish(set_err(c, PHIPM_ESINGULAR, "singular Pade denominator"));
+            mu = R.mu;
+            corr = R.h != 0.0 && !(R.brk >= 0 && R.brk <= mu);
+            const double eps = R.eps;
+            const double omega = t_end * eps / (tau * o.tol);
+            if (!std::isfinite(omega)) return finish(set_err(c, PHIPM_ENONFINITE, "non-finite error estimate"));
+            const bool accepted = omega <= 1.2;
+            Decision d = control(P, mem, tau, m, eps, omega, R.normH1, t_end - tk, accepted);
+            tau_used = tau;
+            m_used = m;
+            S.m_peak = std::max(S.m_peak, m);
+            tau = d.tau_next;
+            m = d.m_next;
+            if (accepted) break;
+            S.nreject++;
+            if (attempts >= 100 || tau < 1e-15 * t_end) {
+                S.t_reached = tk;
+                return finish(set_err(c, PHIPM_ESTEP, "step size control failed at t = %g", tk));
+            }
+        }
+        // Eq. (step): u_{k+1} = sum_{i<=mu} comb_i v~_i + sum_{j<p} tau^j/j! w_j  (w_0 = u_k in place)
+        {
+            AxpyArgs a = axpy0();
+            a.out = ucur;
+            a.base = ucur;
+            a.a0h = (p >= 1) ? 1.0 : 0.0;
+            a.a0d = (p >= 1) ? c->combd : nullptr;
+            a.V = c->V;
+            a.ldv = c->ldv;
+            a.c0 = 0;
+            a.nc = mu + (corr ? 1 : 0);
+            a.g = c->comb;
+            a.gsign = 1.0;
+            a.ne = std::max(p - 1, 0);
+            for (int j = 1; j < p; j++) {
+                a.e[j - 1] = c->W + (int64_t)j * c->ldv;
+                a.ec[j - 1] = 1.0;
+            }
+            a.ecd = c->combd + 1;
+            int rc = launch_axpy(c, n, a, PC_COMBINE);
+            if (rc) return finish(rc);
+        }
+        if (tau_used >= t_end - tk) tk = t_end;
+        else tk += tau_used;
+        S.nsteps++;
+        S.m_last = m_used;
+        S.t_reached = tk;
+    }
+    int rc = sync(c);
+    return finish(rc);
+}
+
+// ---------------------------------------------------------------------------------------------
+// operator construction / validation
+
+int make_stencil(phipm_ctx *c, const phipm_stencil *S, StencilOp &op)
+{
+    if (!S) return set_err(c, PHIPM_EINVAL, "null stencil");
+    if (S->dim < 1 || S->dim > 3 || S->nx < 1 || S->ny < 1 || S->nz < 1)
+        return set_err(c, PHIPM_EINVAL, "bad stencil dims");
+    if ((S->dim < 2 && S->ny != 1) || (S->dim < 3 && S->nz != 1))
+        return set_err(c, PHIPM_EINVAL, "stencil: unused dimensions must be 1");
+    op.dim = S->dim;
+    op.nx = S->nx;
+    op.ny = S->ny;
+    op.nz = S->nz;
+    op.n = (int64_t)S->nx * S->ny * S->nz;
+    if (op.n >= ((int64_t)1 << 31)) return set_err(c, PHIPM_EINVAL, "stencil too large");
+    const double cc[7] = {S->c_center, S->c_xm, S->c_xp, S->c_ym, S->c_yp, S->c_zm, S->c_zp};
+    for (int i = 0; i < 7; i++) op.c[i] = cc[i];
+    if (S->dim < 3) op.c[5] = op.c[6] = 0.0;
+    if (S->dim < 2) op.c[3] = op.c[4] = 0.0;
+    return PHIPM_OK;
+}
+
+int64_t stencil_nnz(const StencilOp &s)
+{
+    const int64_t nx = s.nx, ny = s.ny, nz = s.nz, n = s.n;
+    int64_t nnz = n + 2 * (n - ny * nz);                       // x neighbours: 2(nx-1) per line
+    if (s.dim >= 2) nnz += 2 * (n - nx * nz);
+    if (s.dim >= 3) nnz += 2 * (n - nx * ny);
+    return nnz;
+}
+
+// ||A||_inf of the stencil: max over the boundary classes present, each row summed in ascending
+// column order (z-, y-, x-, centre, x+, y+, z+) like a sequential CSR row sum.
+double stencil_infnorm(const StencilOp &s)
+{
+    double best = 0.0;
+    auto classes = [](int N, int *lo, int *hi, int &cnt) {
+        // positions: first, interior, last (those that exist)
+        cnt = 0;
+        if (N == 1) { lo[cnt] = 0; hi[cnt] = 0; cnt++; return; }
+        lo[cnt] = 0; hi[cnt] = 1; cnt++;
+        if (N > 2) { lo[cnt] = 1; hi[cnt] = 1; cnt++; }
+        lo[cnt] = 1; hi[cnt] = 0; cnt++;
+    };
+    int xl[3], xh[3], yl[3], yh[3], zl[3], zh[3], cx, cy, cz;
+    classes(s.nx, xl, xh, cx);
+    classes(s.dim >= 2 ? s.ny : 1, yl, yh, cy);
+    classes(s.dim >= 3 ? s.nz : 1, zl, zh, cz);
+    for (int a = 0; a < cz; a++)
+        for (int b = 0; b < cy; b++)
+            for (int d = 0; d < cx; d++) {
+                double t = 0.0;
+                if (s.dim >= 3 && zl[a]) t = t + std::fabs(s.c[5]);
+                if (s.dim >= 2 && yl[b]) t = t + std::fabs(s.c[3]);
+                if (xl[d]) t = t + std::fabs(s.c[1]);
+                t = t + std::fabs(s.c[0]);
+                if (xh[d]) t = t + std::fabs(s.c[2]);
+                if (s.dim >= 2 && yh[b]) t = t + std::fabs(s.c[4]);
+                if (s.dim >= 3 && zh[a]) t = t + std::fabs(s.c[6]);
+                best = std::max(best, t);
+            }
+    return best;
+}
+
+int make_csr(phipm_ctx *c, const phipm_csr *A, CsrOp &op)
+{
+    if (!A || !A->row_ptr || !A->col || !A->val || A->n <= 0 || A->nnz < 0)
+        return set_err(c, PHIPM_EINVAL, "bad csr descriptor");
+    if (A->nnz >= ((int64_t)1 << 31) || A->n >= ((int64_t)1 << 31)) return set_err(c, PHIPM_EINVAL, "csr too large");
+    op.n = A->n;
+    op.rp = A->row_ptr;
+    op.col = A->col;
+    op.val = A->val;
+    const double mean = A->n > 0 ? (double)A->nnz / (double)A->n : 1.0;
+    int glog = 0;
+    while (glog < 5 && (double)(1 << (glog + 1)) <= mean) glog++;
+    op.glog = glog;
+    return PHIPM_OK;
+}
+
+double csr_bytes(const CsrOp &op, int64_t nnz)
+{
+    return 12.0 * (double)nnz + 4.0 * (double)(op.n + 1) + 16.0 * (double)op.n;
+}
+
+int check_common(phipm_ctx *c, double t, int64_t n, int p, const double *const *u, const double *w,
+                 phipm_opts &o)
+{
+    if (!c) return PHIPM_EINVAL;
+    if (!(t >= 0.0) || !std::isfinite(t)) return set_err(c, PHIPM_EINVAL, "t must be finite and >= 0");
+    if (n <= 0 || n > c->n_max) return set_err(c, PHIPM_EINVAL, "n=%lld out of range (n_max %lld)", (long long)n, (long long)c->n_max);
+    if (p < 0 || p > c->p_max) return set_err(c, PHIPM_EINVAL, "p=%d out of range (p_max %d)", p, c->p_max);
+    if (!u || !w) return set_err(c, PHIPM_EINVAL, "null u or w");
+    for (int k = 0; k <= p; k++)
+        if (!u[k]) return set_err(c, PHIPM_EINVAL, "null u[%d]", k);
+    for (int k = 1; k <= p; k++)
+        if (u[k] == w) return set_err(c, PHIPM_EINVAL, "w may alias u[0] only");
+    if (!(o.tol > 0.0)) return set_err(c, PHIPM_EINVAL, "tol must be > 0");
+    if (o.m_max > c->m_max) return set_err(c, PHIPM_EINVAL, "opts.m_max %d > context m_max %d", o.m_max, c->m_max);
+    if (o.m_init < 1 || o.m_init > o.m_max) return set_err(c, PHIPM_EINVAL, "m_init must be in [1, m_max]");
+    if (o.orth != PHIPM_ORTH_CGS && o.orth != PHIPM_ORTH_CGS2) return set_err(c, PHIPM_EINVAL, "bad orth");
+    return PHIPM_OK;
+}
+
+phipm_opts resolve_opts(const phipm_opts *o)
+{
+    phipm_opts r;
+    phipm_default_opts(&r);
+    if (o) r = *o;
+    return r;
+}
+
+} // namespace
+
+// =============================================================================================
+// C ABI
+
+extern "C" {
+
+void phipm_default_opts(phipm_opts *o)
+{
+    if (!o) return;
+    o->tol = 1e-7;
+    o->m_init = 10;
+    o->m_max = 100;
+    o->symmetric = 0;
+    o->fixed_m = 0;
+    o->eq6_variant = 0;
+    o->orth = PHIPM_ORTH_CGS;
+    o->profile = 0;
+}
+
+const char *phipm_strerror(int s)
+{
+    switch (s) {
+    case PHIPM_OK: return "ok";
+    case PHIPM_EINVAL: return "invalid argument";
+    case PHIPM_ENOMEM: return "out of memory";
+    case PHIPM_ECUDA: return "CUDA error";
+    case PHIPM_ESTEP: return "step size control failed";
+    case PHIPM_ENONFINITE: return "non-finite value";
+    case PHIPM_ESINGULAR: return "singular Pade denominator";
+    default: return "unknown status";
+    }
+}
+
+const char *phipm_last_error(const phipm_ctx *c) { return c ? c->err : "null context"; }
+
+int phipm_get_profile(const phipm_ctx *c, phipm_profile *out)
+{
+    if (!c || !out) return PHIPM_EINVAL;
+    *out = c->acc;
+    return PHIPM_OK;
+}
+
+void phipm_reset_profile(phipm_ctx *c)
+{
+    if (c) c->acc = phipm_profile{};
+}
+
+void phipm_destroy(phipm_ctx *c)
+{
+    if (!c) return;
+    cudaStreamSynchronize(c->stream);
+    for (auto &r : c->pending) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
+    for (auto e : c->pool) cudaEventDestroy(e);
+    cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
+    cudaFree(c->part); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
+    cudaFree(c->counter); cudaFree(c->st);
+    cudaFree(c->hu); cudaFree(c->hw); cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
+    if (c->res_h) cudaFreeHost(c->res_h);
+    if (c->raw_h) cudaFreeHost(c->raw_h);
+    delete c;
+}
+
+int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *stream)
+{
+    if (!out) return PHIPM_EINVAL;
+    *out = nullptr;
+    if (n_max <= 0 || n_max >= ((int64_t)1 << 31) || m_max < 1 || m_max + 1 > MAXD || p_max < 0 || p_max > P_MAX_ABS - 0)
+        return PHIPM_EINVAL;
+    phipm_ctx *c = new phipm_ctx();
+    c->stream = (cudaStream_t)stream;
+    c->n_max = n_max;
+    c->m_max = m_max;
+    c->p_max = p_max;
+    c->ldv = (n_max + 31) / 32 * 32;
+    c->kmax = m_max + p_max + 1;
+    cudaError_t e = cudaGetDevice(&c->dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->dev);
+    if (e != cudaSuccess) {
+        snprintf(c->err, sizeof(c->err), "no CUDA device: %s", cudaGetErrorString(e));
+        delete c;
+        return PHIPM_ECUDA;
+    }
+    // occupancy-derived persistent grid sizes
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_fused_kernel<CsrOp>, NT, (TILE + MAXD * 32) * sizeof(double));
+    int occ2 = 1;
+    cudaFuncSetAttribute(spmv_fused_kernel<CsrOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (TILE + MAXD * 32) * sizeof(double));
+    cudaFuncSetAttribute(spmv_fused_kernel<StencilOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (TILE + MAXD * 32) * sizeof(double));
+    cudaFuncSetAttribute(spmv_fused_kernel<IdentOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (TILE + MAXD * 32) * sizeof(double));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_fused_kernel<CsrOp>, NT, (TILE + MAXD * 32) * sizeof(double));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, spmv_fused_kernel<StencilOp>, NT, (TILE + MAXD * 32) * sizeof(double));
+    c->occ_spmv = std::max(1, std::min(occ, occ2));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, axpy_fused_kernel<true>, NT, 0);
+    c->occ_axpy = std::max(1, occ);
+    c->pstride = std::max(c->sm_count * std::max(c->occ_spmv, c->occ_axpy), 256);
+    int smem_optin = 0;
+    cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+    c->expm_smem_limit = (size_t)std::max(0, smem_optin - 4096);
+    cudaFuncSetAttribute(expm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->expm_smem_limit);
+    cudaGetLastError();
+
+    const size_t vbytes = (size_t)c->ldv * sizeof(double);
+    bool ok = true;
+    auto A = [&](void **p, size_t b) {
+        if (!ok) return;
+        if (cudaMalloc(p, b) != cudaSuccess) ok = false;
+        else cudaMemset(*p, 0, b);
+    };
+    A((void **)&c->V, vbytes * (m_max + 1));
+    A((void **)&c->W, vbytes * (p_max + 1));
+    A((void **)&c->Y, vbytes);
+    A((void **)&c->H, sizeof(double) * (m_max + 1) * m_max);
+    A((void **)&c->sigma, sizeof(double) * (MAXD + 1));
+    A((void **)&c->g, sizeof(double) * (MAXD + 1));
+    A((void **)&c->part, sizeof(double) * (size_t)c->pstride * (MAXD + 2));
+    A((void **)&c->comb, sizeof(double) * (MAXD + 1));
+    A((void **)&c->combd, sizeof(double) * (P_MAX_ABS + 1));
+    A((void **)&c->scratch, sizeof(double) * 6 * (size_t)c->kmax * c->kmax);
+    A((void **)&c->raw, sizeof(double) * (MAXD + 2));
+    A((void **)&c->counter, sizeof(unsigned) * 4);
+    A((void **)&c->st, sizeof(DevState));
+    if (ok && cudaHostAlloc((void **)&c->res_h, sizeof(AttemptResult), cudaHostAllocMapped) != cudaSuccess) ok = false;
+    if (ok && cudaHostGetDevicePointer((void **)&c->res_d, c->res_h, 0) != cudaSuccess) ok = false;
+    if (ok && cudaHostAlloc((void **)&c->raw_h, sizeof(double) * (MAXD + 2), cudaHostAllocDefault) != cudaSuccess) ok = false;
+    if (ok && cudaDeviceSynchronize() != cudaSuccess) ok = false;
+    if (!ok) {
+        cudaGetLastError();
+        phipm_destroy(c);
+        return PHIPM_ENOMEM;
+    }
+    memset(c->res_h, 0, sizeof(AttemptResult));
+    *out = c;
+    return PHIPM_OK;
+}
+
+int phipm_solve_stencil(phipm_ctx *c, double t, const phipm_stencil *S, int p, const double *const *u,
+                        const phipm_opts *opts, double *w, phipm_stats *stats)
+{
+    if (!c) return PHIPM_EINVAL;
+    StencilOp op;
+    int rc = make_stencil(c, S, op);
+    if (rc) return rc;
+    phipm_opts o = resolve_opts(opts);
+    rc = check_common(c, t, op.n, p, u, w, o);
+    if (rc) return rc;
+    c->prof = o.profile != 0;
+    return solve_impl(c, t, op, 16.0 * (double)op.n, stencil_nnz(op), stencil_infnorm(op), p, u, o, w, stats);
+}
+
+int phipm_solve_csr(phipm_ctx *c, double t, const phipm_csr *A, int p, const double *const *u,
+                    const phipm_opts *opts, double *w, phipm_stats *stats)
+{
+    if (!c) return PHIPM_EINVAL;
+    CsrOp op;
+    int rc = make_csr(c, A, op);
+    if (rc) return rc;
+    phipm_opts o = resolve_opts(opts);
+    rc = check_common(c, t, op.n, p, u, w, o);
+    if (rc) return rc;
+    c->prof = o.profile != 0;
+    // ||A||_inf (a1 setup, once per call)
+    const int grid = grid_for(c, (op.n + NT - 1) / NT, c->occ_axpy);
+    ProfRec r;
+    prof_begin(c, r, PC_OTHER, 0.0);
+    csr_infnorm_kernel<<<grid, NT, 0, c->stream>>>(op, make_work(c));
+    prof_end(c, r);
+    c->acc.launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->raw_h, c->raw, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    rc = sync(c);
+    if (rc) return rc;
+    const double normA = c->raw_h[0];
+    return solve_impl(c, t, op, csr_bytes(op, A->nnz), A->nnz, normA, p, u, o, w, stats);
+}
+
+int phipm_reserve_host_csr(phipm_ctx *c, int64_t nnz_max)
+{
+    if (!c || nnz_max < 0) return PHIPM_EINVAL;
+    if (nnz_max <= c->nnz_cap && c->hrp) return PHIPM_OK;
+    cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
+    c->hrp = nullptr; c->hcol = nullptr; c->hval = nullptr; c->nnz_cap = 0;
+    if (cudaMalloc(&c->hrp, sizeof(int32_t) * (c->n_max + 1)) != cudaSuccess ||
+        cudaMalloc(&c->hcol, sizeof(int32_t) * std::max<int64_t>(nnz_max, 1)) != cudaSuccess ||
+        cudaMalloc(&c->hval, sizeof(double) * std::max<int64_t>(nnz_max, 1)) != cudaSuccess) {
+        cudaGetLastError();
+        return set_err(c, PHIPM_ENOMEM, "reserve_host_csr: allocation failed");
+    }
+    c->nnz_cap = nnz_max;
+    return PHIPM_OK;
+}
+
+static int host_stage_u(phipm_ctx *c, int64_t n, int p, const double *const *host_u, const double **du)
+{
+    if (!host_u) return set_err(c, PHIPM_EINVAL, "null u");
+    if (!c->hu) {
+        if (cudaMalloc(&c->hu, sizeof(double) * c->ldv * (c->p_max + 1)) != cudaSuccess ||
+            cudaMalloc(&c->hw, sizeof(double) * c->ldv) != cudaSuccess) {
+            cudaGetLastError();
+            return set_err(c, PHIPM_ENOMEM, "host staging allocation failed");
+        }
+    }
+    for (int k = 0; k <= p; k++) {
+        if (!host_u[k]) return set_err(c, PHIPM_EINVAL, "null u[%d]", k);
+        double *d = c->hu + (int64_t)k * c->ldv;
+        CK(cudaMemcpyAsync(d, host_u[k], n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+        du[k] = d;
+    }
+    return PHIPM_OK;
+}
+
+int phipm_solve_csr_host(phipm_ctx *c, double t, const phipm_csr *A, int p, const double *const *host_u,
+                         const phipm_opts *opts, double *host_w, phipm_stats *stats)
+{
+    if (!c || !A || !host_w || !A->row_ptr || !A->col || !A->val) return PHIPM_EINVAL;
+    if (A->n <= 0 || A->n > c->n_max || p < 0 || p > c->p_max) return set_err(c, PHIPM_EINVAL, "bad size");
+    int rc = phipm_reserve_host_csr(c, std::max(A->nnz, c->nnz_cap));
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->hrp, A->row_ptr, sizeof(int32_t) * (A->n + 1), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->hcol, A->col, sizeof(int32_t) * A->nnz, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->hval, A->val, sizeof(double) * A->nnz, cudaMemcpyHostToDevice, c->stream));
+    const double *du[P_MAX_ABS + 1];
+    rc = host_stage_u(c, A->n, p, host_u, du);
+    if (rc) return rc;
+    phipm_csr dA = *A;
+    dA.row_ptr = c->hrp;
+    dA.col = c->hcol;
+    dA.val = c->hval;
+    rc = phipm_solve_csr(c, t, &dA, p, du, opts, c->hw, stats);
+    if (rc && rc != PHIPM_ESTEP) return rc;
+    CK(cudaMemcpyAsync(host_w, c->hw, sizeof(double) * A->n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return rc;
+}
+
+int phipm_solve_stencil_host(phipm_ctx *c, double t, const phipm_stencil *S, int p, const double *const *host_u,
+                             const phipm_opts *opts, double *host_w, phipm_stats *stats)
+{
+    if (!c || !host_w) return PHIPM_EINVAL;
+    StencilOp op;
+    int rc = make_stencil(c, S, op);
+    if (rc) return rc;
+    if (op.n > c->n_max || p < 0 || p > c->p_max) return set_err(c, PHIPM_EINVAL, "bad size");
+    const double *du[P_MAX_ABS + 1];
+    rc = host_stage_u(c, op.n, p, host_u, du);
+    if (rc) return rc;
+    rc = phipm_solve_stencil(c, t, S, p, du, opts, c->hw, stats);
+    if (rc && rc != PHIPM_ESTEP) return rc;
+    CK(cudaMemcpyAsync(host_w, c->hw, sizeof(double) * op.n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return rc;
+}
+
+// ---- kernel-level entry points ----
+
+int64_t phipm_stencil_nnz(const phipm_stencil *S)
+{
+    StencilOp op;
+    if (make_stencil(nullptr, S, op) != PHIPM_OK) return -1;
+    return stencil_nnz(op);
+}
+
+int phipm_csr_from_stencil(phipm_ctx *c, const phipm_stencil *S, int32_t *row_ptr, int32_t *col, double *val)
+{
+    if (!c || !row_ptr || !col || !val) return PHIPM_EINVAL;
+    StencilOp op;
+    int rc = make_stencil(c, S, op);
+    if (rc) return rc;
+    const int grid = (int)std::min<int64_t>((op.n + 1 + NT - 1) / NT, (int64_t)c->sm_count * 8);
+    csr_from_stencil_kernel<<<grid, NT, 0, c->stream>>>(op, row_ptr, col, val);
+    c->acc.launches++;
+    CK(cudaGetLastError());
+    return sync(c);
+}
+
+int phipm_spmv_csr(phipm_ctx *c, const phipm_csr *A, const double *x, double *y)
+{
+    if (!c || !x || !y) return PHIPM_EINVAL;
+    CsrOp op;
+    int rc = make_csr(c, A, op);
+    if (rc) return rc;
+    SpmvArgs s = spmv0();
+    s.x = x;
+    s.y = y;
+    rc = launch_spmv(c, op, s, csr_bytes(op, A->nnz));
+    if (rc) return rc;
+    return sync(c);
+}
+
+int phipm_spmv_stencil(phipm_ctx *c, const phipm_stencil *S, const double *x, double *y)
+{
+    if (!c || !x || !y) return PHIPM_EINVAL;
+    StencilOp op;
+    int rc = make_stencil(c, S, op);
+    if (rc) return rc;
+    SpmvArgs s = spmv0();
+    s.x = x;
+    s.y = y;
+    rc = launch_spmv(c, op, s, 16.0 * (double)op.n);
+    if (rc) return rc;
+    return sync(c);
+}
+
+int phipm_dot(phipm_ctx *c, int64_t n, const double *x, const double *y, double *result)
+{
+    if (!c || !x || !y || !result || n <= 0) return PHIPM_EINVAL;
+    if (((uintptr_t)y & 7u) != 0) return set_err(c, PHIPM_EINVAL, "misaligned y");
+    SpmvArgs s = spmv0();
+    s.x = x;
+    s.V = y;
+    s.ldv = n;
+    s.d0 = 0;
+    s.nd = 1;
+    s.fin = FIN_RAW;
+    int rc = launch_spmv(c, IdentOp{n}, s, 8.0 * (double)n);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->raw_h, c->raw, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    rc = sync(c);
+    if (rc) return rc;
+    *result = c->raw_h[0];
+    return PHIPM_OK;
+}
+
+int phipm_inf_norm_csr(phipm_ctx *c, const phipm_csr *A, double *result)
+{
+    if (!c || !result) return PHIPM_EINVAL;
+    CsrOp op;
+    int rc = make_csr(c, A, op);
+    if (rc) return rc;
+    const int grid = grid_for(c, (op.n + NT - 1) / NT, c->occ_axpy);
+    csr_infnorm_kernel<<<grid, NT, 0, c->stream>>>(op, make_work(c));
+    c->acc.launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->raw_h, c->raw, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    rc = sync(c);
+    if (rc) return rc;
+    *result = c->raw_h[0];
+    return PHIPM_OK;
+}
+
+int phipm_expm(phipm_ctx *c, int K, const double *A, double *E)
+{
+    if (!c || !A || !E || K < 1 || K > c->kmax) return PHIPM_EINVAL;
+    ExpmArgs a;
+    memset(&a, 0, sizeof(a));
+    a.mode = 1;
+    a.K = K;
+    a.Ain = A;
+    a.Eout = E;
+    int rc = launch_expm(c, a, K);
+    if (rc) return rc;
+    rc = sync(c);
+    if (rc) return rc;
+    AttemptResult R;
+    memcpy(&R, (const void *)c->res_h, sizeof(R));
+    if (R.status == 5) return set_err(c, PHIPM_ENONFINITE, "expm: non-finite");
+    if (R.status == 6) return set_err(c, PHIPM_ESINGULAR, "expm: singular");
+    return PHIPM_OK;
+}
+
+int phipm_phi_pair(phipm_ctx *c, int mu, const double *H, int ldh, double tau, int p, double *phip, double *phip1,
+                   double *normH1)
+{
+    if (!c || !H || !phip || !phip1 || mu < 1 || ldh < mu || p < 0 || p > c->p_max || mu > c->m_max)
+        return PHIPM_EINVAL;
+    ExpmArgs a;
+    memset(&a, 0, sizeof(a));
+    a.mode = 2;
+    a.m = mu;
+    a.p = p;
+    a.tau = tau;
+    a.H = H;
+    a.ldh = ldh;
+    a.phip_out = phip;
+    a.phip1_out = phip1;
+    int rc = launch_expm(c, a, mu + p + 1);
+    if (rc) return rc;
+    rc = sync(c);
+    if (rc) return rc;
+    AttemptResult R;
+    memcpy(&R, (const void *)c->res_h, sizeof(R));
+    if (normH1) *normH1 = R.normH1;
+    if (R.status == 5) return set_err(c, PHIPM_ENONFINITE, "phi_pair: non-finite");
+    if (R.status == 6) return set_err(c, PHIPM_ESINGULAR, "phi_pair: singular");
+    return PHIPM_OK;
+}
+
+} // extern "C"
+
+template <class Op>
+static int krylov_export(phipm_ctx *c, const Op &op, double bytes_op, double normA, const double *v, int m,
+                         const phipm_opts *opts, double *V, double *H, int *k, int *brk, double *beta)
+{
+    phipm_opts o = resolve_opts(opts);
+    if (!v || !V || !H || m < 1 || m > c->m_max) return set_err(c, PHIPM_EINVAL, "krylov: bad args");
+    const int64_t n = op.n;
+    if (n > c->n_max) return set_err(c, PHIPM_EINVAL, "krylov: n > n_max");
+    CK(cudaMemsetAsync(c->H, 0, sizeof(double) * (c->m_max + 1) * c->m_max, c->stream));
+    AxpyArgs a = axpy0();
+    a.out = c->V;
+    a.base = v;
+    a.a0h = 1.0;
+    a.V = c->V;
+    a.ldv = c->ldv;
+    a.onorm = 1;
+    a.fin = FIN_SEED;
+    int rc = launch_axpy(c, n, a, PC_OTHER);
+    if (rc) return rc;
+    rc = enqueue_krylov(c, op, bytes_op, o.symmetric != 0, o.orth, 0, m, (double)n * EPS_MACH * normA);
+    if (rc) return rc;
+    DevState ds;
+    CK(cudaMemcpyAsync(&ds, c->st, sizeof(ds), cudaMemcpyDeviceToHost, c->stream));
+    rc = sync(c);
+    if (rc) return rc;
+    const int kk = (ds.brk >= 0) ? std::min(ds.brk, m) : m;
+    const int ncols = (ds.brk >= 0) ? kk : m + 1;
+    dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)std::max(ncols, 1));
+    if (ncols > 0) scale_columns_kernel<<<grid, 256, 0, c->stream>>>(n, ncols, c->V, c->ldv, c->sigma, V, n);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy2DAsync(H, sizeof(double) * (m + 1), c->H, sizeof(double) * (c->m_max + 1),
+                         sizeof(double) * (m + 1), m, cudaMemcpyDeviceToDevice, c->stream));
+    rc = sync(c);
+    if (rc) return rc;
+    *k = kk;
+    *brk = ds.brk >= 0 ? 1 : 0;
+    *beta = ds.beta;
+    return PHIPM_OK;
+}
+
+extern "C" {
+
+int phipm_krylov_csr(phipm_ctx *c, const phipm_csr *A, const double *v, int m, const phipm_opts *opts, double *V,
+                     double *H, int *k, int *brk, double *beta)
+{
+    if (!c || !k || !brk || !beta) return PHIPM_EINVAL;
+    CsrOp op;
+    int rc = make_csr(c, A, op);
+    if (rc) return rc;
+    double normA = 0.0;
+    rc = phipm_inf_norm_csr(c, A, &normA);
+    if (rc) return rc;
+    return krylov_export(c, op, csr_bytes(op, A->nnz), normA, v, m, opts, V, H, k, brk, beta);
+}
+
+int phipm_krylov_stencil(phipm_ctx *c, const phipm_stencil *S, const double *v, int m, const phipm_opts *opts,
+                         double *V, double *H, int *k, int *brk, double *beta)
+{
+    if (!c || !k || !brk || !beta) return PHIPM_EINVAL;
+    StencilOp op;
+    int rc = make_stencil(c, S, op);
+    if (rc) return rc;
+    return krylov_export(c, op, 16.0 * (double)op.n, stencil_infnorm(op), v, m, opts, V, H, k, brk, beta);
+}
+
+} // extern "C"

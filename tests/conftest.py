@@ -19,3 +19,16 @@ def orc():
     import oracle
     oracle.build()
     return oracle
+
+
+@pytest.fixture(scope="session")
+def ctx():
+    """One product context for all GPU tests (n_max covers c5, the largest config)."""
+    import torch
+    import paper_0907_4631_b200 as P
+    if not torch.cuda.is_available():
+        pytest.fail("GPU test requested but no CUDA device (the product has no CPU fallback)")
+    P.build()
+    c = P.Context(n_max=4_194_304, m_max=100, p_max=5)
+    yield c
+    c.close()

@@ -1,0 +1,201 @@
+"""Full phipm parity: the CUDA path (through the C ABI) vs the oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): ||w_gpu - w_ref||_2 / ||w_ref||_2 <= max(10 tol, 1e-12).  Only w
+is compared; the controller's trajectory may legitimately differ when rounding flips a decision
+near a threshold (parity unpinned), so stats are reported, not asserted equal.
+"""
+import numpy as np
+import pytest
+
+import workloads as W
+from gpu_common import to_dev, stencil_of, parity_bound, relerr
+
+pytestmark = pytest.mark.gpu
+
+
+def run_gpu(ctx, Pb, path, **kw):
+    u = [to_dev(x) for x in Pb.u]
+    kw.setdefault("tol", Pb.tol)
+    kw.setdefault("symmetric", Pb.symmetric)
+    kw.setdefault("m_init", Pb.m_init)
+    if path == "stencil":
+        w, s = ctx.solve_stencil(Pb.t, stencil_of(Pb), u, **kw)
+    else:
+        if Pb.csr is not None:
+            A = tuple(to_dev(a) for a in Pb.csr)
+        else:
+            A = ctx.csr_from_stencil(stencil_of(Pb))     # the product's own CSR builder
+        w, s = ctx.solve_csr(Pb.t, A, u, **kw)
+    return w.cpu().numpy(), s
+
+
+def run_oracle(orc, Pb, **kw):
+    w, s, _ = orc.solve(Pb, **kw)
+    assert s["status"] == 0
+    return w, s
+
+
+CASES = [
+    ("c1_mini", "csr"), ("c1_mini", "stencil"),
+    ("c2_mini", "stencil"), ("c2_mini", "csr"),
+    ("c3_mini", "stencil"), ("c3_mini", "csr"),
+    ("c4_mini", "stencil"),
+    ("c5_mini", "csr"),
+    ("c2_med", "stencil"), ("c3_med", "stencil"), ("c4_med", "stencil"), ("c5_med", "csr"),
+]
+
+
+@pytest.mark.parametrize("name,path", CASES)
+def test_solve_parity_small(ctx, orc, name, path):
+    Pb = W.make(name)
+    wg, sg = run_gpu(ctx, Pb, path)
+    wo, so = run_oracle(orc, Pb)
+    assert sg.t_reached == Pb.t
+    assert relerr(wg, wo) <= parity_bound(Pb.tol), (sg, so)
+
+
+FULL = [("c1", "csr"), ("c1", "stencil"), ("c2", "csr"), ("c2", "stencil"), ("c3", "stencil"),
+        ("c4", "stencil"), ("c5", "csr")]
+
+
+@pytest.mark.parametrize("name,path", FULL)
+def test_solve_parity_full_configs(ctx, orc, name, path):
+    """BASELINE.json configs at full size, in the launch configuration bench.py times."""
+    Pb = W.make(name)
+    wg, sg = run_gpu(ctx, Pb, path)
+    wo, so = run_oracle(orc, Pb)
+    err = relerr(wg, wo)
+    print(f"{name}/{path}: relerr {err:.3e} gpu {sg} oracle {so}")
+    assert err <= parity_bound(Pb.tol)
+
+
+def test_csr_and_stencil_agree(ctx):
+    Pb = W.make("c2_med")
+    a, sa = run_gpu(ctx, Pb, "stencil")
+    b, sb = run_gpu(ctx, Pb, "csr")
+    assert relerr(a, b) <= parity_bound(Pb.tol)
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 3, 4, 5])
+def test_all_p(ctx, orc, p):
+    rng = np.random.default_rng(50 + p)
+    Pb = W.c5(n=20_011, band=128, seed=300 + p)
+    Pb.u = [rng.standard_normal(Pb.n) for _ in range(p + 1)]
+    Pb.p = p
+    Pb.t = 0.7
+    wg, sg = run_gpu(ctx, Pb, "csr")
+    wo, so = run_oracle(orc, Pb)
+    assert relerr(wg, wo) <= parity_bound(Pb.tol)
+
+
+def test_multistep_stiff(ctx, orc):
+    Pb = W.make("c1")            # t ||A|| = 4008: ~15-30 steps with rejections
+    wg, sg = run_gpu(ctx, Pb, "stencil")
+    wo, so = run_oracle(orc, Pb)
+    assert sg.nsteps > 5
+    assert relerr(wg, wo) <= parity_bound(Pb.tol)
+
+
+def test_cgs2_and_fixed_m(ctx, orc):
+    Pb = W.make("c3_med")
+    wo, so = run_oracle(orc, Pb)
+    wg, sg = run_gpu(ctx, Pb, "stencil", orth=1)
+    assert relerr(wg, wo) <= parity_bound(Pb.tol)
+    Pb = W.make("c1_mini")
+    wo, so = run_oracle(orc, Pb, m_init=30, fixed_m=True)
+    wg, sg = run_gpu(ctx, Pb, "csr", m_init=30, fixed_m=True)
+    assert sg.m_peak == 30 and sg.m_last == 30
+    assert relerr(wg, wo) <= parity_bound(Pb.tol)
+
+
+def test_eq6_variant(ctx, orc):
+    Pb = W.make("c1")
+    wo, so = run_oracle(orc, Pb, eq6_variant=True)
+    wg, sg = run_gpu(ctx, Pb, "stencil", eq6_variant=True)
+    assert relerr(wg, wo) <= parity_bound(Pb.tol)
+
+
+def test_degenerate_inputs(ctx, orc):
+    import torch
+    Pb = W.make("c2_mini")
+    S = stencil_of(Pb)
+    u = [to_dev(x) for x in Pb.u]
+    # t = 0 -> u0
+    w, s = ctx.solve_stencil(0.0, S, u, tol=1e-8, symmetric=True)
+    assert np.array_equal(w.cpu().numpy(), Pb.u[0])
+    # all zero -> 0
+    z = [torch.zeros_like(x) for x in u]
+    w, s = ctx.solve_stencil(Pb.t, S, z, tol=1e-8, symmetric=True)
+    assert torch.count_nonzero(w).item() == 0
+    # w_p = 0 with u0 != 0 (R23)
+    u2 = [u[0], torch.zeros_like(u[0])]
+    w, s = ctx.solve_stencil(Pb.t, S, u2, tol=1e-10, symmetric=True)
+    wo, so, _ = orc.phipm(Pb.t, orc.operator_csr(Pb), [Pb.u[0], np.zeros(Pb.n)], 1e-10, symmetric=True)
+    assert relerr(w.cpu().numpy(), wo) <= 1e-9
+    # w may alias u0
+    uu = [x.clone() for x in u]
+    w, s = ctx.solve_stencil(Pb.t, S, uu, out=uu[0], tol=Pb.tol, symmetric=True)
+    wo, so = run_oracle(orc, Pb)
+    assert relerr(uu[0].cpu().numpy(), wo) <= parity_bound(Pb.tol)
+    # bad arguments -> EINVAL, no crash
+    import paper_0907_4631_b200 as P
+    with pytest.raises(P.PhipmError) as e:
+        ctx.solve_stencil(-1.0, S, u, tol=1e-8)
+    assert e.value.status == P.EINVAL
+    with pytest.raises(P.PhipmError):
+        ctx.solve_stencil(Pb.t, S, u, tol=0.0)
+    with pytest.raises(P.PhipmError):
+        ctx.solve_stencil(Pb.t, S, u, m_init=0)
+
+
+def test_a_zero_and_tiny_n(ctx, orc):
+    import torch
+    # A = 0 (empty CSR): w = sum t^k/k! u_k exactly (phi_l(0) = 1/l!)
+    n = 7
+    rng = np.random.default_rng(1)
+    uu = [rng.standard_normal(n) for _ in range(3)]
+    A = (to_dev(np.zeros(n + 1, np.int32)), torch.zeros(0, dtype=torch.int32, device="cuda"),
+         torch.zeros(0, dtype=torch.float64, device="cuda"))
+    w, s = ctx.solve_csr(1.7, A, [to_dev(x) for x in uu], tol=1e-10)
+    ref = uu[0] + 1.7 * uu[1] + 1.7 ** 2 / 2 * uu[2]
+    assert np.allclose(w.cpu().numpy(), ref, rtol=1e-15, atol=1e-15)
+    # n = 1 and n < m (breakdown inside the Krylov space)
+    for n in (1, 5, 33):
+        Pb = W.c5(n=max(n, 40), band=16, seed=11) if n >= 40 else None
+        Dg = -np.abs(rng.standard_normal(n)) - 0.5
+        rp = np.arange(n + 1, dtype=np.int32)
+        col = np.arange(n, dtype=np.int32)
+        u3 = [rng.standard_normal(n) for _ in range(2)]
+        wg, sg = ctx.solve_csr(0.9, (to_dev(rp), to_dev(col), to_dev(Dg)), [to_dev(x) for x in u3], tol=1e-10)
+        wo, so, _ = orc.phipm(0.9, (rp, col, Dg), u3, 1e-10)
+        assert relerr(wg.cpu().numpy(), wo) <= 1e-9
+
+
+def test_host_buffers_match_device(ctx):
+    Pb = W.make("c3_mini")
+    wd, sd = run_gpu(ctx, Pb, "stencil")
+    out = np.empty(Pb.n)
+    wh, sh = ctx.solve_stencil_host(Pb.t, stencil_of(Pb), Pb.u, out, tol=Pb.tol, symmetric=Pb.symmetric)
+    assert np.array_equal(wd, wh)
+    Pb = W.make("c5_mini")
+    wd, sd = run_gpu(ctx, Pb, "csr")
+    out = np.empty(Pb.n)
+    wh, sh = ctx.solve_csr_host(Pb.t, Pb.csr, Pb.u, out, tol=Pb.tol, symmetric=False)
+    assert np.array_equal(wd, wh)
+
+
+def test_deterministic(ctx):
+    Pb = W.make("c5_med")
+    a, sa = run_gpu(ctx, Pb, "csr")
+    b, sb = run_gpu(ctx, Pb, "csr")
+    assert np.array_equal(a, b) and sa == sb
+
+
+def test_profile_counts(ctx):
+    Pb = W.make("c3_med")
+    ctx.reset_profile()
+    w, s = run_gpu(ctx, Pb, "stencil", profile=True)
+    prof = ctx.profile()
+    assert prof["n_expm"] == s.nexpm
+    assert prof["n_spmv_dot"] == s.nspmv          # one fused SpMV launch per product
+    assert prof["ms_spmv_dot"] > 0 and prof["bytes_spmv_dot"] > 0

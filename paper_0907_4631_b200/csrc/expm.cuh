@@ -33,6 +33,7 @@ struct AttemptResult {
 struct ExpmArgs {
     int mode;          // 0: phipm attempt; 1: plain expm of Ain; 2: phi pair of H (mu = m)
     int m, p;          // requested Krylov dimension, phi order
+    int tridiag;       // Lanczos: H is tridiagonal, read only the band
     double tau;
     const double *H;   // Hessenberg (ld ldh)
     int ldh;
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
         __syncthreads();
         for (size_t e = t; e < (size_t)mu * mu; e += blockDim.x) {
             const int i = (int)(e % mu), jc = (int)(e / mu);
-            M0[i + (size_t)jc * K] = a.tau * a.H[i + (size_t)jc * a.ldh];
+            if (!a.tridiag || (i - jc <= 1 && jc - i <= 1)) M0[i + (size_t)jc * K] = a.tau * a.H[i + (size_t)jc * a.ldh];
         }
         if (t == 0) {
             M0[0 + (size_t)mu * K] = 1.0;
@@ -281,7 +282,8 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
         double m = 0.0;
         for (int jc = t; jc < mu; jc += blockDim.x) {
             double s = 0.0;
-            for (int i = 0; i < mu; i++) s += fabs(a.H[i + (size_t)jc * a.ldh]);
+            const int i0 = a.tridiag ? max(jc - 1, 0) : 0, i1 = a.tridiag ? min(jc + 2, mu) : mu;
+            for (int i = i0; i < i1; i++) s += fabs(a.H[i + (size_t)jc * a.ldh]);
             m = fmax(m, s);
         }
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));

@@ -492,6 +492,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     const double bthr = (double)n * EPS_MACH * normA;
 
     double *ucur = w;
+    CK(cudaMemsetAsync(c->H, 0, sizeof(double) * (c->m_max + 1) * c->m_max, c->stream));
     if (w != u[0]) CK(cudaMemcpyAsync(w, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     double tk = 0.0;
     S.m_peak = m;
@@ -543,6 +544,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             ExpmArgs ea;
             memset(&ea, 0, sizeof(ea));
             ea.mode = 0;
+            ea.tridiag = P.symmetric ? 1 : 0;
             ea.m = m;
             ea.p = p;
             ea.tau = tau;
@@ -687,7 +689,7 @@ double stencil_infnorm(const StencilOp &s)
 
 int make_csr(phipm_ctx *c, const phipm_csr *A, CsrOp &op)
 {
-    if (!A || !A->row_ptr || !A->col || !A->val || A->n <= 0 || A->nnz < 0)
+    if (!A || !A->row_ptr || A->n <= 0 || A->nnz < 0 || (A->nnz > 0 && (!A->col || !A->val)))
         return set_err(c, PHIPM_EINVAL, "bad csr descriptor");
     if (A->nnz >= ((int64_t)1 << 31) || A->n >= ((int64_t)1 << 31)) return set_err(c, PHIPM_EINVAL, "csr too large");
     op.n = A->n;
@@ -947,13 +949,15 @@ static int host_stage_u(phipm_ctx *c, int64_t n, int p, const double *const *hos
 int phipm_solve_csr_host(phipm_ctx *c, double t, const phipm_csr *A, int p, const double *const *host_u,
                          const phipm_opts *opts, double *host_w, phipm_stats *stats)
 {
-    if (!c || !A || !host_w || !A->row_ptr || !A->col || !A->val) return PHIPM_EINVAL;
+    if (!c || !A || !host_w || !A->row_ptr || (A->nnz > 0 && (!A->col || !A->val))) return PHIPM_EINVAL;
     if (A->n <= 0 || A->n > c->n_max || p < 0 || p > c->p_max) return set_err(c, PHIPM_EINVAL, "bad size");
     int rc = phipm_reserve_host_csr(c, std::max(A->nnz, c->nnz_cap));
     if (rc) return rc;
     CK(cudaMemcpyAsync(c->hrp, A->row_ptr, sizeof(int32_t) * (A->n + 1), cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->hcol, A->col, sizeof(int32_t) * A->nnz, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->hval, A->val, sizeof(double) * A->nnz, cudaMemcpyHostToDevice, c->stream));
+    if (A->nnz > 0) {
+        CK(cudaMemcpyAsync(c->hcol, A->col, sizeof(int32_t) * A->nnz, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->hval, A->val, sizeof(double) * A->nnz, cudaMemcpyHostToDevice, c->stream));
+    }
     const double *du[P_MAX_ABS + 1];
     rc = host_stage_u(c, A->n, p, host_u, du);
     if (rc) return rc;

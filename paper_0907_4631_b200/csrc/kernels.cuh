@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace phipm {
 
 constexpr int NT = 256;               // threads per block of the streaming kernels
@@ -76,7 +78,8 @@ struct CsrOp {
 };
 
 struct SpmvArgs {
-    const double *x;
+    const double *x;             // workspace vector padded to ldx (TMA halo reads) or, for CSR, any
+    int64_t ldx;
     const double *xscale;        // device scalar s (sigma_j) or null -> 1
     double *y;
     int nz;
@@ -224,265 +227,12 @@ __device__ void finalize(int fin, int j, int nd, const double *red, const Work &
 }
 
 // ------------------------------------------------------------------------------------------
-// operator rows (phase 1): raw (A x)_r for the rows of a tile, into ys[]
-
-// Stencil row, summed in ascending column order with separately rounded products (no FMA), the
-// same order and rounding as a CSR row of orc-style sequential SpMV: bit-exact y.
-__device__ __forceinline__ double stencil_row(const StencilOp &S, const double *__restrict__ x, int64_t r)
-{
-    const unsigned ur = (unsigned)r, unx = (unsigned)S.nx;
-    const unsigned q = ur / unx;
-    const int i = (int)(ur - q * unx);
-    int jj = 0, kk = 0;
-    if (S.dim >= 2) {
-        const unsigned uny = (unsigned)S.ny;
-        const unsigned q2 = q / uny;
-        jj = (int)(q - q2 * uny);
-        kk = (int)q2;
-    }
-    const int64_t pl = (int64_t)S.nx * S.ny;
-    double s = 0.0;
-    if (S.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(S.c[5], __ldg(x + r - pl)));
-    if (S.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(S.c[3], __ldg(x + r - S.nx)));
-    if (i > 0) s = __dadd_rn(s, __dmul_rn(S.c[1], __ldg(x + r - 1)));
-    s = __dadd_rn(s, __dmul_rn(S.c[0], __ldg(x + r)));
-    if (i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[2], __ldg(x + r + 1)));
-    if (S.dim >= 2 && jj < S.ny - 1) s = __dadd_rn(s, __dmul_rn(S.c[4], __ldg(x + r + S.nx)));
-    if (S.dim >= 3 && kk < S.nz - 1) s = __dadd_rn(s, __dmul_rn(S.c[6], __ldg(x + r + pl)));
-    return s;
-}
-
-__device__ __forceinline__ void op_tile(const StencilOp &S, const double *__restrict__ x, int64_t r0, int rows,
-                                        double *ys)
-{
-    for (int q = threadIdx.x; q < rows; q += NT) ys[q] = stencil_row(S, x, r0 + q);
-}
-
-// CSR: G = 2^glog lanes per row, strided over the row's entries, tree-reduced with shuffles.
-__device__ __forceinline__ void op_tile(const CsrOp &A, const double *__restrict__ x, int64_t r0, int rows,
-                                        double *ys)
-{
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int G = 1 << A.glog;
-    const int rpw = 32 >> A.glog;                      // rows per warp iteration
-    const int sub = lane >> A.glog, li = lane & (G - 1);
-    for (int base = warp * rpw; base < rows; base += NWARP * rpw) {
-        const int q = base + sub;
-        double acc = 0.0;
-        if (q < rows) {
-            const int64_t r = r0 + q;
-            const int e1 = __ldg(A.rp + r + 1);
-            for (int e = __ldg(A.rp + r) + li; e < e1; e += G)
-                acc = fma(ldg_stream(A.val + e), __ldg(x + __ldg(A.col + e)), acc);
-        }
-        for (int o = G >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (q < rows && li == 0) ys[q] = acc;
-    }
-}
+// operators
 
 // identity "operator" (multi-dot of a stored vector against V columns; CGS2 second pass)
 struct IdentOp {
     int64_t n;
 };
-
-__device__ __forceinline__ void op_tile(const IdentOp &, const double *__restrict__ x, int64_t r0, int rows, double *ys)
-{
-    for (int q = threadIdx.x; q < rows; q += NT) ys[q] = ldg_stream(x + r0 + q);
-}
-
-template <class Op>
-__device__ __forceinline__ int64_t op_n(const Op &op) { return op.n; }
-
-// ------------------------------------------------------------------------------------------
-// spmv_fused
-
-template <class Op>
-__global__ void __launch_bounds__(NT) spmv_fused_kernel(Op op, SpmvArgs a, Work wk)
-{
-    extern __shared__ double smem[];
-    double *ys = smem;                     // TILE
-    double *lacc = smem + TILE;            // nd x 32 per-lane dot partials
-    __shared__ double bsum[MAXD + 2];
-    __shared__ double wsum[NWARP];
-    __shared__ int s_exit;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (a.check_brk) {
-        if (tid == 0) s_exit = wk.st->brk >= 0;
-        __syncthreads();
-        if (s_exit) return;
-    }
-    const int64_t n = op_n(op);
-    const double s = a.xscale ? *a.xscale : 1.0;
-    double zc[MAXZ];
-#pragma unroll
-    for (int i = 0; i < MAXZ; i++) zc[i] = (i < a.nz) ? a.zc[i] * (a.zcd[i] ? *a.zcd[i] : 1.0) : 0.0;
-    for (int i = tid; i < a.nd * 32; i += NT) lacc[i] = 0.0;
-    double ysq = 0.0;
-    __syncthreads();
-
-    for (int64_t r0 = (int64_t)blockIdx.x * TILE; r0 < n; r0 += (int64_t)gridDim.x * TILE) {
-        const int rows = (int)min((int64_t)TILE, n - r0);
-        op_tile(op, a.x, r0, rows, ys);
-        __syncthreads();
-        // phase 2: scale + epilogue, store y, ||y||^2
-        for (int q = tid; q < rows; q += NT) {
-            const int64_t r = r0 + q;
-            double y = s * ys[q];
-#pragma unroll
-            for (int i = 0; i < MAXZ; i++)
-                if (i < a.nz) y = fma(zc[i], __ldg(a.z[i] + r), y);
-            ys[q] = y;
-            if (a.y) a.y[r] = y;
-            ysq = fma(y, y, ysq);
-        }
-        __syncthreads();
-        // phase 3: dots with V columns, one warp per column, lane partials kept in smem
-        if (a.nd > 0) {
-            for (int kk = warp; kk < a.nd; kk += NWARP) {
-                const double *__restrict__ vc = a.V + (int64_t)(a.d0 + kk) * a.ldv + r0;
-                double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-                int q = lane;
-                for (; q + 96 < rows; q += 128) {
-                    const double v0 = ldg_stream(vc + q), v1 = ldg_stream(vc + q + 32);
-                    const double v2 = ldg_stream(vc + q + 64), v3 = ldg_stream(vc + q + 96);
-                    c0 = fma(v0, ys[q], c0);
-                    c1 = fma(v1, ys[q + 32], c1);
-                    c2 = fma(v2, ys[q + 64], c2);
-                    c3 = fma(v3, ys[q + 96], c3);
-                }
-                for (; q < rows; q += 32) c0 = fma(ldg_stream(vc + q), ys[q], c0);
-                lacc[kk * 32 + lane] += (c0 + c1) + (c2 + c3);
-            }
-        }
-        __syncthreads();
-    }
-    // block totals
-    const int nv = a.nd + (a.ynorm ? 1 : 0);
-    if (nv == 0) return;
-    for (int kk = warp; kk < a.nd; kk += NWARP) {
-        double v = warp_sum(lacc[kk * 32 + lane]);
-        if (lane == 0) bsum[kk] = v;
-    }
-    if (a.ynorm) {
-        double v = warp_sum(ysq);
-        if (lane == 0) wsum[warp] = v;
-        __syncthreads();
-        if (tid == 0) {
-            double t = 0.0;
-            for (int w = 0; w < NWARP; w++) t += wsum[w];
-            bsum[a.nd] = t;
-        }
-    }
-    __syncthreads();
-    if (!publish_partials(wk, bsum, nv)) return;
-    __shared__ double red[MAXD + 2];
-    final_reduce(wk, nv, red);
-    finalize(a.fin, a.j, a.nd, red, wk, 0.0, 0);
-}
-
-// ------------------------------------------------------------------------------------------
-// axpy_fused: out = a0 base + gsign sum_k g_k V[:, c0+k] + sum_i ec_i E_i  [+ ||out||^2]
-
-template <bool VEC2>
-__global__ void __launch_bounds__(NT) axpy_fused_kernel(int64_t n, AxpyArgs a, Work wk)
-{
-    __shared__ double gs[MAXD];
-    __shared__ double bsum[2];
-    __shared__ double wsum[NWARP];
-    __shared__ int s_exit;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (a.check_brk) {
-        if (tid == 0) s_exit = wk.st->brk >= 0;
-        __syncthreads();
-        if (s_exit) return;
-    }
-    for (int k = tid; k < a.nc; k += NT) gs[k] = a.gsign * a.g[k];
-    const double a0 = a.a0h * (a.a0d ? *a.a0d : 1.0);
-    double ec[MAXZ];
-#pragma unroll
-    for (int i = 0; i < MAXZ; i++) ec[i] = (i < a.ne) ? a.ec[i] * (a.ecd ? a.ecd[i] : 1.0) : 0.0;
-    __syncthreads();
-    double nrm = 0.0;
-    const double *__restrict__ V = a.V + (int64_t)a.c0 * a.ldv;
-    if (VEC2) {
-        const int64_t npair = n >> 1;
-        for (int64_t pi = (int64_t)blockIdx.x * NT + tid; pi < npair; pi += (int64_t)gridDim.x * NT) {
-            const int64_t r = pi * 2;
-            double2 acc = make_double2(0.0, 0.0);
-            if (a.a0h != 0.0) {
-                const double2 b = *reinterpret_cast<const double2 *>(a.base + r);
-                acc.x = a0 * b.x;
-                acc.y = a0 * b.y;
-            }
-            int k = 0;
-            for (; k + 8 <= a.nc; k += 8) {
-                double2 v[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) v[u] = ldg_stream2(V + (int64_t)(k + u) * a.ldv + r);
-#pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    acc.x = fma(gs[k + u], v[u].x, acc.x);
-                    acc.y = fma(gs[k + u], v[u].y, acc.y);
-                }
-            }
-            for (; k < a.nc; k++) {
-                const double2 v = ldg_stream2(V + (int64_t)k * a.ldv + r);
-                acc.x = fma(gs[k], v.x, acc.x);
-                acc.y = fma(gs[k], v.y, acc.y);
-            }
-#pragma unroll
-            for (int i = 0; i < MAXZ; i++)
-                if (i < a.ne) {
-                    const double2 e = ldg_stream2(a.e[i] + r);
-                    acc.x = fma(ec[i], e.x, acc.x);
-                    acc.y = fma(ec[i], e.y, acc.y);
-                }
-            *reinterpret_cast<double2 *>(a.out + r) = acc;
-            nrm = fma(acc.x, acc.x, nrm);
-            nrm = fma(acc.y, acc.y, nrm);
-        }
-        if ((n & 1) && blockIdx.x == 0 && tid == 0) {
-            const int64_t r = n - 1;
-            double acc = (a.a0h != 0.0) ? a0 * a.base[r] : 0.0;
-            for (int k = 0; k < a.nc; k++) acc = fma(gs[k], V[(int64_t)k * a.ldv + r], acc);
-            for (int i = 0; i < a.ne; i++) acc = fma(ec[i], a.e[i][r], acc);
-            a.out[r] = acc;
-            nrm = fma(acc, acc, nrm);
-        }
-    } else {
-        for (int64_t r = (int64_t)blockIdx.x * NT + tid; r < n; r += (int64_t)gridDim.x * NT) {
-            double acc = (a.a0h != 0.0) ? a0 * a.base[r] : 0.0;
-            int k = 0;
-            for (; k + 8 <= a.nc; k += 8) {
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) v[u] = ldg_stream(V + (int64_t)(k + u) * a.ldv + r);
-#pragma unroll
-                for (int u = 0; u < 8; u++) acc = fma(gs[k + u], v[u], acc);
-            }
-            for (; k < a.nc; k++) acc = fma(gs[k], ldg_stream(V + (int64_t)k * a.ldv + r), acc);
-#pragma unroll
-            for (int i = 0; i < MAXZ; i++)
-                if (i < a.ne) acc = fma(ec[i], __ldg(a.e[i] + r), acc);
-            a.out[r] = acc;
-            nrm = fma(acc, acc, nrm);
-        }
-    }
-    if (!a.onorm) return;
-    double v = warp_sum(nrm);
-    if (lane == 0) wsum[warp] = v;
-    __syncthreads();
-    if (tid == 0) {
-        double t = 0.0;
-        for (int w = 0; w < NWARP; w++) t += wsum[w];
-        bsum[0] = t;
-    }
-    __syncthreads();
-    if (!publish_partials(wk, bsum, 1)) return;
-    __shared__ double red[2];
-    final_reduce(wk, 1, red);
-    finalize(a.fin, a.j, 1, red, wk, a.bthr, a.lanczos);
-}
 
 // ------------------------------------------------------------------------------------------
 // small utility kernels

@@ -16,6 +16,7 @@
 #include "phipm.h"
 #include "kernels.cuh"
 #include "expm.cuh"
+#include "stream.cuh"
 
 using namespace phipm;
 
@@ -41,9 +42,9 @@ struct phipm_ctx {
     int m_max = 0, p_max = 0, kmax = 0;
     int sm_count = 0, occ_spmv = 1, occ_axpy = 1;
     int pstride = 0;
-    size_t expm_smem_limit = 0;
+    size_t expm_smem_limit = 0, stream_smem_budget = 0;
     // device workspace
-    double *V = nullptr, *W = nullptr, *Y = nullptr, *H = nullptr, *sigma = nullptr, *g = nullptr;
+    double *V = nullptr, *W = nullptr, *Y = nullptr, *U = nullptr, *H = nullptr, *sigma = nullptr, *g = nullptr;
     double *part = nullptr, *comb = nullptr, *combd = nullptr, *scratch = nullptr, *raw = nullptr;
     unsigned *counter = nullptr;
     DevState *st = nullptr;
@@ -162,36 +163,44 @@ int grid_for(phipm_ctx *c, int64_t units, int occ)
 // launches
 
 template <class Op>
-int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a, double bytes_op)
+int nseg_host(const Op &);
+template <>
+int nseg_host<StencilOp>(const StencilOp &S) { return S.dim == 1 ? 1 : (S.dim == 2 ? 3 : 5); }
+template <>
+int nseg_host<IdentOp>(const IdentOp &) { return 1; }
+template <>
+int nseg_host<CsrOp>(const CsrOp &) { return 0; }
+
+template <class Op>
+int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
 {
+    SpmvArgs a = a0;
+    if (a.ldx == 0) a.ldx = c->ldv;
     const int64_t tiles = (op.n + TILE - 1) / TILE;
-    const int grid = grid_for(c, tiles, c->occ_spmv);
-    const size_t smem = (size_t)(TILE + a.nd * 32) * sizeof(double);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->sm_count));
+    const int nseg = nseg_host(op);
+    const int nring = stream_nring(nseg, true, c->stream_smem_budget);
+    const size_t smem = stream_smem_bytes(nseg, true, nring);
     ProfRec r;
-    double bytes = bytes_op + 8.0 * (double)op.n * (a.nd + a.nz);
+    const double bytes = bytes_op + 8.0 * (double)op.n * (a.nd + a.nz);
     prof_begin(c, r, PC_SPMV, bytes);
-    spmv_fused_kernel<Op><<<grid, NT, smem, c->stream>>>(op, a, make_work(c));
+    spmv_stream_kernel<Op><<<grid, NTHR, smem, c->stream>>>(op, a, make_work(c), nring);
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
     return PHIPM_OK;
 }
 
-bool aligned16(const void *p) { return ((uintptr_t)p & 15u) == 0; }
-
 int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a, int cls)
 {
-    bool vec = aligned16(a.out) && (a.a0h == 0.0 || aligned16(a.base)) && (a.ldv % 2 == 0) && aligned16(a.V);
-    for (int i = 0; i < a.ne; i++) vec = vec && aligned16(a.e[i]);
-    const int64_t units = vec ? ((n / 2) + NT - 1) / NT : (n + NT - 1) / NT;
-    const int grid = grid_for(c, std::max<int64_t>(units, 1), c->occ_axpy);
+    const int64_t tiles = (n + TILE - 1) / TILE;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->sm_count));
+    const int nring = stream_nring(0, false, c->stream_smem_budget);
+    const size_t smem = stream_smem_bytes(0, false, nring);
     ProfRec r;
     const double bytes = 8.0 * (double)n * (a.nc + a.ne + 1 + (a.a0h != 0.0 ? 1 : 0));
     prof_begin(c, r, cls, bytes);
-    if (vec)
-        axpy_fused_kernel<true><<<grid, NT, 0, c->stream>>>(n, a, make_work(c));
-    else
-        axpy_fused_kernel<false><<<grid, NT, 0, c->stream>>>(n, a, make_work(c));
+    axpy_stream_kernel<<<grid, NTHR, smem, c->stream>>>(n, a, make_work(c), nring);
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -491,9 +500,10 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     if (!(tau > 0.0)) tau = t_end;
     const double bthr = (double)n * EPS_MACH * normA;
 
-    double *ucur = w;
+    // the running solution u_k lives in the padded workspace vector U (TMA-readable)
+    double *ucur = c->U;
     CK(cudaMemsetAsync(c->H, 0, sizeof(double) * (c->m_max + 1) * c->m_max, c->stream));
-    if (w != u[0]) CK(cudaMemcpyAsync(w, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(ucur, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     double tk = 0.0;
     S.m_peak = m;
     while (tk < t_end) {
@@ -587,6 +597,8 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             S.nreject++;
             if (attempts >= 100 || tau < 1e-15 * t_end) {
                 S.t_reached = tk;
+                cudaMemcpyAsync(w, ucur, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+                cudaStreamSynchronize(c->stream);
                 return finish(set_err(c, PHIPM_ESTEP, "step size control failed at t = %g", tk));
             }
         }
@@ -618,6 +630,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         S.m_last = m_used;
         S.t_reached = tk;
     }
+    CK(cudaMemcpyAsync(w, ucur, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     int rc = sync(c);
     return finish(rc);
 }
@@ -789,7 +802,7 @@ void phipm_destroy(phipm_ctx *c)
     cudaStreamSynchronize(c->stream);
     for (auto &r : c->pending) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
-    cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
+    cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
     cudaFree(c->part); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
     cudaFree(c->counter); cudaFree(c->st);
     cudaFree(c->hu); cudaFree(c->hw); cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
@@ -818,19 +831,23 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         delete c;
         return PHIPM_ECUDA;
     }
-    // occupancy-derived persistent grid sizes
-    int occ = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_fused_kernel<CsrOp>, NT, (TILE + MAXD * 32) * sizeof(double));
-    int occ2 = 1;
-    cudaFuncSetAttribute(spmv_fused_kernel<CsrOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (TILE + MAXD * 32) * sizeof(double));
-    cudaFuncSetAttribute(spmv_fused_kernel<StencilOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (TILE + MAXD * 32) * sizeof(double));
-    cudaFuncSetAttribute(spmv_fused_kernel<IdentOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (TILE + MAXD * 32) * sizeof(double));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmv_fused_kernel<CsrOp>, NT, (TILE + MAXD * 32) * sizeof(double));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, spmv_fused_kernel<StencilOp>, NT, (TILE + MAXD * 32) * sizeof(double));
-    c->occ_spmv = std::max(1, std::min(occ, occ2));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, axpy_fused_kernel<true>, NT, 0);
-    c->occ_axpy = std::max(1, occ);
-    c->pstride = std::max(c->sm_count * std::max(c->occ_spmv, c->occ_axpy), 256);
+    // persistent streaming kernels: one CTA per SM; other kernels size grids by occupancy
+    {
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+        // leave room for the kernels' static shared memory (barriers, reduction scratch)
+        c->stream_smem_budget = (size_t)std::max(0, optin - 6 * 1024);
+        const int mx = (int)c->stream_smem_budget;
+        cudaFuncSetAttribute(spmv_stream_kernel<StencilOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<CsrOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<IdentOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(axpy_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, maxabs_kernel, NT, 0);
+        c->occ_axpy = std::max(1, occ);
+        c->occ_spmv = 1;
+        c->pstride = std::max(c->sm_count * std::max(c->occ_spmv, c->occ_axpy), 256);
+    }
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
     c->expm_smem_limit = (size_t)std::max(0, smem_optin - 4096);
@@ -847,6 +864,7 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     A((void **)&c->V, vbytes * (m_max + 1));
     A((void **)&c->W, vbytes * (p_max + 1));
     A((void **)&c->Y, vbytes);
+    A((void **)&c->U, vbytes);
     A((void **)&c->H, sizeof(double) * (m_max + 1) * m_max);
     A((void **)&c->sigma, sizeof(double) * (MAXD + 1));
     A((void **)&c->g, sizeof(double) * (MAXD + 1));
@@ -1032,8 +1050,10 @@ int phipm_spmv_stencil(phipm_ctx *c, const phipm_stencil *S, const double *x, do
     StencilOp op;
     int rc = make_stencil(c, S, op);
     if (rc) return rc;
+    if (op.n > c->n_max) return set_err(c, PHIPM_EINVAL, "n > n_max");
+    CK(cudaMemcpyAsync(c->Y, x, op.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     SpmvArgs s = spmv0();
-    s.x = x;
+    s.x = c->Y;
     s.y = y;
     rc = launch_spmv(c, op, s, 16.0 * (double)op.n);
     if (rc) return rc;
@@ -1043,11 +1063,14 @@ int phipm_spmv_stencil(phipm_ctx *c, const phipm_stencil *S, const double *x, do
 int phipm_dot(phipm_ctx *c, int64_t n, const double *x, const double *y, double *result)
 {
     if (!c || !x || !y || !result || n <= 0) return PHIPM_EINVAL;
-    if (((uintptr_t)y & 7u) != 0) return set_err(c, PHIPM_EINVAL, "misaligned y");
+    if (n > c->n_max) return set_err(c, PHIPM_EINVAL, "n > n_max");
+    // stage both operands in padded workspace vectors (TMA segment reads)
+    CK(cudaMemcpyAsync(c->Y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->U, y, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     SpmvArgs s = spmv0();
-    s.x = x;
-    s.V = y;
-    s.ldv = n;
+    s.x = c->Y;
+    s.V = c->U;
+    s.ldv = c->ldv;
     s.d0 = 0;
     s.nd = 1;
     s.fin = FIN_RAW;
@@ -1135,9 +1158,10 @@ static int krylov_export(phipm_ctx *c, const Op &op, double bytes_op, double nor
     const int64_t n = op.n;
     if (n > c->n_max) return set_err(c, PHIPM_EINVAL, "krylov: n > n_max");
     CK(cudaMemsetAsync(c->H, 0, sizeof(double) * (c->m_max + 1) * c->m_max, c->stream));
+    CK(cudaMemcpyAsync(c->Y, v, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     AxpyArgs a = axpy0();
     a.out = c->V;
-    a.base = v;
+    a.base = c->Y;
     a.a0h = 1.0;
     a.V = c->V;
     a.ldv = c->ldv;

@@ -43,6 +43,8 @@ struct phipm_ctx {
     int sm_count = 0, occ_spmv = 1, occ_axpy = 1;
     int pstride = 0;
     size_t expm_smem_limit = 0, stream_smem_budget = 0;
+    struct OccEntry { const void *fn; size_t smem; int occ; };
+    std::vector<OccEntry> occ_cache;
     // device workspace
     double *V = nullptr, *W = nullptr, *Y = nullptr, *U = nullptr, *H = nullptr, *sigma = nullptr, *g = nullptr;
     double *part = nullptr, *comb = nullptr, *combd = nullptr, *scratch = nullptr, *raw = nullptr;
@@ -162,29 +164,50 @@ int grid_for(phipm_ctx *c, int64_t units, int occ)
 // ---------------------------------------------------------------------------------------------
 // launches
 
+// occupancy-limited grid for a streaming kernel (cached per kernel/smem)
+int stream_grid(phipm_ctx *c, const void *fn, size_t smem, int64_t ntiles)
+{
+    int occ = 0;
+    for (auto &e : c->occ_cache)
+        if (e.fn == fn && e.smem == smem) { occ = e.occ; break; }
+    if (occ == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, SNT, smem);
+        occ = std::max(occ, 1);
+        c->occ_cache.push_back({fn, smem, occ});
+    }
+    return (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)occ * c->sm_count));
+}
+
 template <class Op>
-int nseg_host(const Op &);
+int halo_cap_host(const Op &, int tile) { return tile; }
 template <>
-int nseg_host<StencilOp>(const StencilOp &S) { return S.dim == 1 ? 1 : (S.dim == 2 ? 3 : 5); }
-template <>
-int nseg_host<IdentOp>(const IdentOp &) { return 1; }
-template <>
-int nseg_host<CsrOp>(const CsrOp &) { return 0; }
+int halo_cap_host<StencilOp>(const StencilOp &S, int tile) { return halo_capacity(S.dim, S.nx, tile); }
+
+// rows per thread: 8 (TILE 2048) when there are enough tiles to fill the GPU, else 2 (TILE 512)
+int pick_rpt(phipm_ctx *c, int64_t n) { return n >= (int64_t)SNT * 8 * 2 * c->sm_count ? 8 : 2; }
+
+template <class Op, int RPT>
+int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a)
+{
+    constexpr int TILE_ = SNT * RPT;
+    const int64_t ntiles = (op.n + TILE_ - 1) / TILE_;
+    const size_t smem = spmv_smem_bytes(halo_cap_host(op, TILE_), TILE_, a.nd);
+    const void *fn = (const void *)spmv_stream_kernel<Op, RPT>;
+    const int grid = std::min(stream_grid(c, fn, smem, ntiles), c->pstride);
+    spmv_stream_kernel<Op, RPT><<<grid, SNT, smem, c->stream>>>(op, a, make_work(c));
+    return PHIPM_OK;
+}
 
 template <class Op>
 int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
 {
     SpmvArgs a = a0;
     if (a.ldx == 0) a.ldx = c->ldv;
-    const int64_t tiles = (op.n + TILE - 1) / TILE;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->sm_count));
-    const int nseg = nseg_host(op);
-    const int nring = stream_nring(nseg, true, c->stream_smem_budget);
-    const size_t smem = stream_smem_bytes(nseg, true, nring);
     ProfRec r;
     const double bytes = bytes_op + 8.0 * (double)op.n * (a.nd + a.nz);
     prof_begin(c, r, PC_SPMV, bytes);
-    spmv_stream_kernel<Op><<<grid, NTHR, smem, c->stream>>>(op, a, make_work(c), nring);
+    if (pick_rpt(c, op.n) == 8) launch_spmv_t<Op, 8>(c, op, a);
+    else launch_spmv_t<Op, 2>(c, op, a);
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -193,14 +216,18 @@ int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
 
 int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a, int cls)
 {
-    const int64_t tiles = (n + TILE - 1) / TILE;
-    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, c->sm_count));
-    const int nring = stream_nring(0, false, c->stream_smem_budget);
-    const size_t smem = stream_smem_bytes(0, false, nring);
     ProfRec r;
     const double bytes = 8.0 * (double)n * (a.nc + a.ne + 1 + (a.a0h != 0.0 ? 1 : 0));
     prof_begin(c, r, cls, bytes);
-    axpy_stream_kernel<<<grid, NTHR, smem, c->stream>>>(n, a, make_work(c), nring);
+    if (pick_rpt(c, n) == 8) {
+        const int64_t ntiles = (n + SNT * 8 - 1) / (SNT * 8);
+        const int grid = std::min(stream_grid(c, (const void *)axpy_stream_kernel<8>, 0, ntiles), c->pstride);
+        axpy_stream_kernel<8><<<grid, SNT, 0, c->stream>>>(n, a, make_work(c));
+    } else {
+        const int64_t ntiles = (n + SNT * 2 - 1) / (SNT * 2);
+        const int grid = std::min(stream_grid(c, (const void *)axpy_stream_kernel<2>, 0, ntiles), c->pstride);
+        axpy_stream_kernel<2><<<grid, SNT, 0, c->stream>>>(n, a, make_work(c));
+    }
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -831,22 +858,20 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         delete c;
         return PHIPM_ECUDA;
     }
-    // persistent streaming kernels: one CTA per SM; other kernels size grids by occupancy
+    // streaming kernels: grid = min(tiles, occupancy x SMs); allow large dynamic smem (halo tiles)
     {
-        int optin = 0;
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
-        // leave room for the kernels' static shared memory (barriers, reduction scratch)
-        c->stream_smem_budget = (size_t)std::max(0, optin - 6 * 1024);
-        const int mx = (int)c->stream_smem_budget;
-        cudaFuncSetAttribute(spmv_stream_kernel<StencilOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(spmv_stream_kernel<CsrOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(spmv_stream_kernel<IdentOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(axpy_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        const int mx = 200 * 1024;
+        cudaFuncSetAttribute(spmv_stream_kernel<StencilOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<StencilOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, maxabs_kernel, NT, 0);
         c->occ_axpy = std::max(1, occ);
-        c->occ_spmv = 1;
-        c->pstride = std::max(c->sm_count * std::max(c->occ_spmv, c->occ_axpy), 256);
+        c->occ_spmv = 4;
+        c->pstride = std::max(c->sm_count * 8, 1024);
     }
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);

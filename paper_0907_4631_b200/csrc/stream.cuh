@@ -1,29 +1,33 @@
-// stream.cuh — the two n-sized kernels of a phipm step, B200 style: persistent (one CTA per SM),
-// one producer warp issuing 1-D TMA bulk copies (cp.async.bulk, SASS UBLKCP) of 8 KB vector
-// segments into an mbarrier ring in shared memory, sixteen consumer warps doing the fp64 arithmetic
-// from shared memory.  Stencil operators get their halo tiles (centre row range plus the +-nx and
-// +-nx*ny neighbour ranges) the same way, double-buffered, so x is read from L2/HBM once per tile
-// range rather than through per-thread gathers.
+// stream.cuh — the two n-sized kernels of a phipm step (sm_100a, fp64):
 //
-//   spmv_stream   y = s (A x) + sum_i c_i z_i ; d_k = v~_k^T y (k in a column range) ; ||y||^2
-//   axpy_stream   out = sum over streamed sources (a0 base, -g_k v~_k or +c_k v~_k, e_i E_i) ; ||out||^2
+//   spmv_stream   y = s (A x) + sum_i c_i z_i ; d_k = v~_k^T y for a column range ; ||y||^2
+//   axpy_stream   out = a0 base + sum_k c_k v~_k + sum_i e_i E_i ; ||out||^2
 //
-// Both end in the deterministic last-block grid reduction + finalize of kernels.cuh.
-// All TMA sources are workspace vectors padded to ldv (a multiple of 32 doubles), so every
-// segment can be rounded out to 16-byte boundaries without leaving the allocation.
+// Design (measured on this B200 with tools/stream_roof.cu: plain 16-B loads reach ~7.0 TB/s
+// read-only, 1-D TMA bulk copies only do so with >= 16-32 KB per copy):
+//   * Tiles of TILE = 256 * RPT rows; each thread owns RPT rows as RPT/2 double2 pairs
+//     (rows 2 tid + 512 h, +1) and keeps its y values in registers from the SpMV through the
+//     dot products, so y never round-trips through memory inside the kernel.
+//   * Streamed Krylov columns are read with 16-B non-allocating loads, CU columns x RPT/2 pairs
+//     in flight per thread (64-128 B/thread, 4 CTAs/SM), which saturates HBM.
+//   * Stencil operators stage their halo tile in shared memory with 1-D TMA (cp.async.bulk,
+//     SASS UBLKCP): in 2-D/3-D the centre row range and the +-nx neighbour ranges are one
+//     contiguous copy [r0 - nx, r0 + TILE + nx), the +-nx*ny ranges (3-D) two more; the next
+//     tile's halo is issued as soon as the current one has been consumed, so the copy overlaps
+//     the epilogue and the dot products.
+//   * CSR rows are computed by groups of 2^glog lanes with 8 row groups in flight per lane.
+// Both kernels end in the deterministic last-block grid reduction + finalize of kernels.cuh.
+// All TMA sources are workspace vectors padded to ldv (a multiple of 32 doubles).
 #pragma once
 
 #include "kernels.cuh"
 
 namespace phipm {
 
-constexpr int NCW = 16;                 // consumer warps
-constexpr int NCT = NCW * 32;           // consumer threads
-constexpr int NTHR = NCT + 32;          // + producer warp
-constexpr int MAXRING = 28;             // ring slots (TILE doubles = 8 KB each); runtime count fills smem
-constexpr int HSEG = TILE + 8;          // halo segment capacity in doubles (alignment slack)
+constexpr int SNT = 256;                // threads per CTA
+constexpr int SNW = SNT / 32;
+constexpr int CU = 4;                   // columns in flight per thread
 constexpr int MAXITEM = MAXD + MAXZ + 2;
-static_assert(TILE == 2 * NCT, "2 rows (one double2) per consumer thread per slot");
 
 // ---------------------------------------------------------------------------------------------
 // mbarrier + bulk-copy primitives (PTX)
@@ -40,11 +44,6 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar)
-{
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 {
     asm volatile(
@@ -56,13 +55,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
-}
-
-__device__ __forceinline__ uint64_t policy_evict_first()
-{
-    uint64_t p;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
 }
 
 __device__ __forceinline__ uint64_t policy_evict_last()
@@ -82,77 +74,93 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
         : "memory");
 }
 
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(NCT) : "memory"); }
-
-struct Pipe {
-    uint64_t full[MAXRING], empty[MAXRING];
-    uint64_t hfull[2], hempty[2];
-};
-
-__device__ __forceinline__ void pipe_init(Pipe &pp, int nring)
+// 16-B read-only load that does not allocate in L1 (streamed Krylov columns)
+__device__ __forceinline__ double2 ld_stream2(const double *p)
 {
-    for (int s = 0; s < nring; s++) {
-        mbar_init(&pp.full[s], 1);
-        mbar_init(&pp.empty[s], NCW);
-    }
-    for (int s = 0; s < 2; s++) {
-        mbar_init(&pp.hfull[s], 1);
-        mbar_init(&pp.hempty[s], NCW);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
 }
 
 // ---------------------------------------------------------------------------------------------
-// halo plan: the x ranges a tile of stencil rows reads (centre [r0-1, r0+rows+1), y-/y+ ranges
-// [r0 -+ nx, ... + rows), z-/z+ ranges [r0 -+ nx*ny, ... + rows)), rounded out to even indices
-// and clamped to [0, ldv).
+// halo plan of a stencil tile: the x ranges the tile's rows read, rounded out to even indices,
+// clamped to [0, ldx).  Segment 0 = centre (1-D: [r0-1, r0+rows+1); 2-D/3-D with nx <= TILE the
+// union [r0-nx, r0+rows+nx)); with nx > TILE the y-/y+ ranges are separate segments; in 3-D the
+// z-/z+ ranges follow.  off[k] is the segment's offset in the shared halo buffer (doubles).
 
 struct HaloPlan {
+    int nseg;
     int64_t start[5];
     uint32_t bytes[5];
+    int off[5];
+    int ylo, yhi, zlo, zhi;          // segment holding the y-, y+, z-, z+ neighbours
 };
 
-template <class Op>
-__device__ __forceinline__ int halo_nseg(const Op &) { return 0; }
-template <>
-__device__ __forceinline__ int halo_nseg<StencilOp>(const StencilOp &S) { return S.dim == 1 ? 1 : (S.dim == 2 ? 3 : 5); }
-template <>
-__device__ __forceinline__ int halo_nseg<IdentOp>(const IdentOp &) { return 1; }
+__host__ __device__ inline bool halo_union(int nx, int tile) { return nx <= tile; }
 
-__device__ __forceinline__ void seg_range(int64_t lo, int64_t hi, int64_t ldv, int64_t &start, uint32_t &bytes)
+// capacity of the shared halo buffer (doubles) for a stencil with this geometry
+__host__ __device__ inline int halo_capacity(int dim, int nx, int tile)
+{
+    if (dim == 1) return tile + 4;
+    int c = halo_union(nx, tile) ? tile + 2 * nx + 4 : 3 * (tile + 4);
+    if (dim == 3) c += 2 * (tile + 4);
+    return c;
+}
+
+__device__ __forceinline__ void seg_range(int64_t lo, int64_t hi, int64_t ldx, int64_t &start, uint32_t &bytes)
 {
     lo = lo < 0 ? 0 : (lo & ~(int64_t)1);
-    hi = hi > ldv ? ldv : ((hi + 1) & ~(int64_t)1);
-    if (hi <= lo) { start = lo; bytes = 0; return; }
+    hi = hi > ldx ? ldx : ((hi + 1) & ~(int64_t)1);
     start = lo;
-    bytes = (uint32_t)((hi - lo) * 8);
+    bytes = hi > lo ? (uint32_t)((hi - lo) * 8) : 0u;
 }
 
-__device__ __forceinline__ void halo_plan(const StencilOp &S, int64_t r0, int rows, int64_t ldv, HaloPlan &h)
+__device__ __forceinline__ void halo_plan(const StencilOp &S, int tile, int64_t r0, int rows, int64_t ldx, HaloPlan &h)
 {
-    seg_range(r0 - 1, r0 + rows + 1, ldv, h.start[0], h.bytes[0]);
-    if (S.dim >= 2) {
-        seg_range(r0 - S.nx, r0 - S.nx + rows, ldv, h.start[1], h.bytes[1]);
-        seg_range(r0 + S.nx, r0 + S.nx + rows, ldv, h.start[2], h.bytes[2]);
+    int k = 0, off = 0;
+    auto add = [&](int64_t lo, int64_t hi, int cap) {
+        seg_range(lo, hi, ldx, h.start[k], h.bytes[k]);
+        h.off[k] = off;
+        off += cap;
+        return k++;
+    };
+    if (S.dim == 1) {
+        add(r0 - 1, r0 + rows + 1, tile + 4);
+        h.ylo = h.yhi = 0;
+    } else if (halo_union(S.nx, tile)) {
+        h.ylo = h.yhi = add(r0 - S.nx, r0 + rows + S.nx, tile + 2 * S.nx + 4);
+    } else {
+        add(r0 - 1, r0 + rows + 1, tile + 4);
+        h.ylo = add(r0 - S.nx, r0 - S.nx + rows, tile + 4);
+        h.yhi = add(r0 + S.nx, r0 + S.nx + rows, tile + 4);
     }
-    if (S.dim >= 3) {
+    h.zlo = h.zhi = 0;
+    if (S.dim == 3) {
         const int64_t pl = (int64_t)S.nx * S.ny;
-        seg_range(r0 - pl, r0 - pl + rows, ldv, h.start[3], h.bytes[3]);
-        seg_range(r0 + pl, r0 + pl + rows, ldv, h.start[4], h.bytes[4]);
+        h.zlo = add(r0 - pl, r0 - pl + rows, tile + 4);
+        h.zhi = add(r0 + pl, r0 + pl + rows, tile + 4);
     }
+    h.nseg = k;
 }
 
-__device__ __forceinline__ void halo_plan(const IdentOp &, int64_t r0, int rows, int64_t ldv, HaloPlan &h)
+__device__ __forceinline__ void halo_plan_ident(int64_t r0, int rows, int64_t ldx, HaloPlan &h)
 {
-    seg_range(r0, r0 + rows, ldv, h.start[0], h.bytes[0]);
+    h.nseg = 1;
+    h.off[0] = 0;
+    h.ylo = h.yhi = h.zlo = h.zhi = 0;
+    seg_range(r0, r0 + rows, ldx, h.start[0], h.bytes[0]);
 }
 
-__device__ __forceinline__ void halo_plan(const CsrOp &, int64_t, int, int64_t, HaloPlan &) {}
+// x value at global index g from segment k of the halo buffer
+__device__ __forceinline__ double hx(const double *hb, const HaloPlan &h, int k, int64_t g)
+{
+    return hb[h.off[k] + (int)(g - h.start[k])];
+}
 
-// Stencil row from the halo tile, summed in ascending column order with separately rounded
-// products (no FMA): the same operations, in the same order, as a sequential CSR row sum, so y
-// is bit-exact with it.
-__device__ __forceinline__ double stencil_row_halo(const StencilOp &S, const double *hb, const HaloPlan &h, int64_t r)
+// Stencil row, summed in ascending column order (z-, y-, x-, centre, x+, y+, z+) with separately
+// rounded products (no FMA): the same operations in the same order as a sequential CSR row sum,
+// so y is bit-exact with it.
+__device__ __forceinline__ double stencil_row(const StencilOp &S, const double *hb, const HaloPlan &h, int64_t r)
 {
     const unsigned ur = (unsigned)r, unx = (unsigned)S.nx;
     const unsigned q = ur / unx;
@@ -165,29 +173,27 @@ __device__ __forceinline__ double stencil_row_halo(const StencilOp &S, const dou
         kk = (int)q2;
     }
     const int64_t pl = (int64_t)S.nx * S.ny;
-    const double *c0 = hb + (r - h.start[0]);
     double s = 0.0;
-    if (S.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(S.c[5], hb[3 * HSEG + (r - pl - h.start[3])]));
-    if (S.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(S.c[3], hb[1 * HSEG + (r - S.nx - h.start[1])]));
-    if (i > 0) s = __dadd_rn(s, __dmul_rn(S.c[1], c0[-1]));
-    s = __dadd_rn(s, __dmul_rn(S.c[0], c0[0]));
-    if (i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[2], c0[1]));
-    if (S.dim >= 2 && jj < S.ny - 1) s = __dadd_rn(s, __dmul_rn(S.c[4], hb[2 * HSEG + (r + S.nx - h.start[2])]));
-    if (S.dim >= 3 && kk < S.nz - 1) s = __dadd_rn(s, __dmul_rn(S.c[6], hb[4 * HSEG + (r + pl - h.start[4])]));
+    if (S.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(S.c[5], hx(hb, h, h.zlo, r - pl)));
+    if (S.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(S.c[3], hx(hb, h, h.ylo, r - S.nx)));
+    if (i > 0) s = __dadd_rn(s, __dmul_rn(S.c[1], hx(hb, h, 0, r - 1)));
+    s = __dadd_rn(s, __dmul_rn(S.c[0], hx(hb, h, 0, r)));
+    if (i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[2], hx(hb, h, 0, r + 1)));
+    if (S.dim >= 2 && jj < S.ny - 1) s = __dadd_rn(s, __dmul_rn(S.c[4], hx(hb, h, h.yhi, r + S.nx)));
+    if (S.dim >= 3 && kk < S.nz - 1) s = __dadd_rn(s, __dmul_rn(S.c[6], hx(hb, h, h.zhi, r + pl)));
     return s;
 }
 
-// CSR rows of a tile: G = 2^glog lanes per row, U row groups in flight per lane (memory-level
-// parallelism for the col -> x gather chain), rows longer than G strided, shuffle reduction.
-__device__ __forceinline__ void csr_tile(const CsrOp &A, const double *__restrict__ x, int64_t r0, int rows, double *ys,
-                                         int ctid)
+// CSR rows of a tile into ys: G = 2^glog lanes per row, U row groups in flight per lane (memory-
+// level parallelism for the col -> x gather chain), rows longer than G strided, shuffle reduce.
+__device__ __forceinline__ void csr_tile(const CsrOp &A, const double *__restrict__ x, int64_t r0, int rows, double *ys)
 {
     constexpr int U = 8;
-    const int lane = ctid & 31, warp = ctid >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = 1 << A.glog;
     const int rpw = 32 >> A.glog;
     const int sub = lane >> A.glog, li = lane & (G - 1);
-    const int stride = NCW * rpw;
+    const int stride = SNW * rpw;
     for (int base = warp * rpw; base < rows; base += stride * U) {
         int q[U], e[U], e1[U];
         double acc[U];
@@ -219,183 +225,167 @@ __device__ __forceinline__ void csr_tile(const CsrOp &A, const double *__restric
     }
 }
 
-template <class Op>
-__device__ __forceinline__ constexpr bool has_halo() { return true; }
-template <>
-__device__ __forceinline__ constexpr bool has_halo<CsrOp>() { return false; }
-
-__device__ __forceinline__ uint32_t seg_bytes(int rows) { return (uint32_t)(((rows + 1) & ~1) * 8); }
-
-// dynamic shared memory layout (doubles): halo (2 x nseg x HSEG) | ys | lacc | ring (nring x TILE)
-__host__ __device__ inline size_t stream_fixed_doubles(int nseg, bool spmv)
+// dynamic shared memory of spmv_stream (bytes): halo (or ys for CSR), then per-warp dot partials
+__host__ __device__ inline size_t spmv_smem_bytes(int halo_cap, int tile, int nd)
 {
-    return (size_t)2 * nseg * HSEG + (spmv ? (size_t)TILE + (size_t)MAXD * NCW : 0);
-}
-
-// as many ring slots as fit in `budget` bytes of dynamic shared memory (>= 2)
-__host__ __device__ inline int stream_nring(int nseg, bool spmv, size_t budget)
-{
-    const size_t fixed = stream_fixed_doubles(nseg, spmv) * sizeof(double);
-    long r = budget > fixed ? (long)((budget - fixed) / (TILE * sizeof(double))) : 0;
-    if (r > MAXRING) r = MAXRING;
-    if (r < 2) r = 2;
-    return (int)r;
-}
-
-__host__ __device__ inline size_t stream_smem_bytes(int nseg, bool spmv, int nring)
-{
-    return (stream_fixed_doubles(nseg, spmv) + (size_t)nring * TILE) * sizeof(double);
+    const int h = halo_cap > 0 ? halo_cap : tile;
+    return ((size_t)((h + 15) & ~15) + (size_t)nd * SNW) * sizeof(double);
 }
 
 // ---------------------------------------------------------------------------------------------
+// spmv_stream
 
-template <class Op>
-__global__ void __launch_bounds__(NTHR, 1) spmv_stream_kernel(Op op, SpmvArgs a, Work wk, int nring)
+template <class Op, int RPT>
+__global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, Work wk)
 {
+    constexpr int TILE_ = SNT * RPT;
+    constexpr int NP = RPT / 2;                           // double2 pairs per thread
+    constexpr bool IS_ST = std::is_same<Op, StencilOp>::value;
+    constexpr bool HALO = !std::is_same<Op, CsrOp>::value;
     extern __shared__ __align__(128) double sm[];
-    __shared__ Pipe pp;
+    __shared__ uint64_t hbar;
     __shared__ double bsum[MAXD + 2];
-    __shared__ double wsum[NCW];
+    __shared__ double wsum[SNW];
     __shared__ int s_exit;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t n = op.n;
+    const int64_t ntiles = (n + TILE_ - 1) / TILE_;
+    int hcap = TILE_;
+    if constexpr (IS_ST) hcap = halo_capacity(op.dim, op.nx, TILE_);
+    double *hbuf = sm;                                    // halo (stencil/ident) or ys (CSR)
+    double *lacc = sm + ((hcap + 15) & ~15);
+    auto plan = [&](int64_t r0, int rows, HaloPlan &h) {
+        if constexpr (IS_ST) halo_plan(op, TILE_, r0, rows, a.ldx, h);
+        else halo_plan_ident(r0, rows, a.ldx, h);
+    };
+    auto issue_halo = [&](int64_t tl) {
+        const int64_t hr0 = tl * TILE_;
+        const int hrows = (int)min((int64_t)TILE_, n - hr0);
+        HaloPlan h;
+        plan(hr0, hrows, h);
+        uint32_t tot = 0;
+        for (int k = 0; k < h.nseg; k++) tot += h.bytes[k];
+        const uint64_t pol = policy_evict_last();
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of hbuf
+        mbar_arrive_expect_tx(&hbar, tot);
+        for (int k = 0; k < h.nseg; k++)
+            if (h.bytes[k]) tma_load_1d(hbuf + h.off[k], a.x + h.start[k], h.bytes[k], &hbar, pol);
+    };
     if (tid == 0) {
         s_exit = a.check_brk ? (wk.st->brk >= 0) : 0;
-        pipe_init(pp, nring);
+        if constexpr (HALO) {
+            if (!s_exit) {
+                mbar_init(&hbar, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                if ((int64_t)blockIdx.x < ntiles) issue_halo(blockIdx.x);
+            }
+        }
     }
+    const double sc = a.xscale ? *a.xscale : 1.0;
+    double zc[MAXZ];
+#pragma unroll
+    for (int i = 0; i < MAXZ; i++) zc[i] = (i < a.nz) ? a.zc[i] * (a.zcd[i] ? *a.zcd[i] : 1.0) : 0.0;
+    for (int i = tid; i < a.nd * SNW; i += SNT) lacc[i] = 0.0;
     __syncthreads();
     if (s_exit) return;
-    const int nseg = halo_nseg(op);
-    double *halo = sm;
-    double *ys = halo + 2 * nseg * HSEG;
-    double *lacc = ys + TILE;
-    double *ring = lacc + MAXD * NCW;
-    const int64_t n = op.n;
-    const int64_t ntiles = (n + TILE - 1) / TILE;
-    constexpr bool HALO = has_halo<Op>();
 
-    if (warp == NCW) {
-        // ------------------------------------------------------------------ producer
-        if (lane == 0) {
-            const uint64_t pol_v = policy_evict_first();
-            const uint64_t pol_x = policy_evict_last();
-            uint32_t it = 0, ht = 0;
-            auto issue_halo = [&](int64_t tl) {
-                const int64_t hr0 = tl * TILE;
-                const int hrows = (int)min((int64_t)TILE, n - hr0);
-                const int hb = ht & 1;
-                if (ht >= 2) mbar_wait(&pp.hempty[hb], ((ht >> 1) - 1) & 1);
-                HaloPlan h;
-                halo_plan(op, hr0, hrows, a.ldx, h);
-                uint32_t tot = 0;
-                for (int k = 0; k < nseg; k++) tot += h.bytes[k];
-                mbar_arrive_expect_tx(&pp.hfull[hb], tot);
-                for (int k = 0; k < nseg; k++)
-                    if (h.bytes[k])
-                        tma_load_1d(halo + (hb * nseg + k) * HSEG, a.x + h.start[k], h.bytes[k], &pp.hfull[hb], pol_x);
-                ht++;
-            };
-            if (HALO && (int64_t)blockIdx.x < ntiles) issue_halo(blockIdx.x);
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int64_t r0 = tile * TILE;
-                const int rows = (int)min((int64_t)TILE, n - r0);
-                // prefetch the next tile's halo before this tile's column segments (double buffer)
-                if (HALO && tile + gridDim.x < ntiles) issue_halo(tile + gridDim.x);
-                const uint32_t by = seg_bytes(rows);
-                for (int k = 0; k < a.nd; k++) {
-                    const int s = it % nring;
-                    const uint32_t r = it / nring;
-                    if (r >= 1) mbar_wait(&pp.empty[s], (r - 1) & 1);
-                    mbar_arrive_expect_tx(&pp.full[s], by);
-                    tma_load_1d(ring + s * TILE, a.V + (int64_t)(a.d0 + k) * a.ldv + r0, by, &pp.full[s], pol_v);
-                    it++;
+    double ysq = 0.0;
+    uint32_t ht = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = tile * TILE_;
+        const int rows = (int)min((int64_t)TILE_, n - r0);
+        double2 y[NP];
+        // ---- phase 1: raw (A x) rows into registers
+        if constexpr (HALO) {
+            mbar_wait(&hbar, ht & 1);
+            ht++;
+            HaloPlan h;
+            plan(r0, rows, h);
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                const int q = 2 * tid + 2 * SNT * p;
+                if constexpr (IS_ST) {
+                    y[p].x = q < rows ? stencil_row(op, hbuf, h, r0 + q) : 0.0;
+                    y[p].y = q + 1 < rows ? stencil_row(op, hbuf, h, r0 + q + 1) : 0.0;
+                } else {
+                    y[p].x = q < rows ? hx(hbuf, h, 0, r0 + q) : 0.0;
+                    y[p].y = q + 1 < rows ? hx(hbuf, h, 0, r0 + q + 1) : 0.0;
                 }
+            }
+            __syncthreads();                               // halo consumed
+            if (tid == 0 && tile + gridDim.x < ntiles) issue_halo(tile + gridDim.x);
+        } else {
+            csr_tile(op, a.x, r0, rows, hbuf);
+            __syncthreads();
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                const int q = 2 * tid + 2 * SNT * p;
+                y[p] = q + 1 < rows ? *reinterpret_cast<const double2 *>(hbuf + q)
+                                    : make_double2(q < rows ? hbuf[q] : 0.0, 0.0);
+            }
+            __syncthreads();                               // ys consumed
+        }
+        // ---- phase 2: scale + epilogue, store y, ||y||^2
+#pragma unroll
+        for (int p = 0; p < NP; p++) {
+            const int q = 2 * tid + 2 * SNT * p;
+            const int64_t r = r0 + q;
+            y[p].x *= sc;
+            y[p].y *= sc;
+#pragma unroll
+            for (int i = 0; i < MAXZ; i++)
+                if (i < a.nz) {
+                    if (q < rows) y[p].x = fma(zc[i], __ldg(a.z[i] + r), y[p].x);
+                    if (q + 1 < rows) y[p].y = fma(zc[i], __ldg(a.z[i] + r + 1), y[p].y);
+                }
+            if (a.y) {
+                if (q + 1 < rows) *reinterpret_cast<double2 *>(a.y + r) = y[p];
+                else if (q < rows) a.y[r] = y[p].x;
+            }
+            ysq = fma(y[p].x, y[p].x, ysq);
+            ysq = fma(y[p].y, y[p].y, ysq);
+        }
+        // ---- phase 3: d_k = V_k^T y over the tile, CU columns in flight
+        for (int k0 = 0; k0 < a.nd; k0 += CU) {
+            double2 v[CU][NP];
+#pragma unroll
+            for (int u = 0; u < CU; u++) {
+                const int k = k0 + u;
+                const double *vc = a.V + (int64_t)(a.d0 + (k < a.nd ? k : k0)) * a.ldv + r0;
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    const int q = 2 * tid + 2 * SNT * p;
+                    v[u][p] = (k < a.nd && q < rows) ? ld_stream2(vc + q) : make_double2(0.0, 0.0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < CU; u++) {
+                double d = 0.0;
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    d = fma(v[u][p].x, y[p].x, d);
+                    d = fma(v[u][p].y, y[p].y, d);
+                }
+                d = warp_sum(d);
+                if (lane == 0 && k0 + u < a.nd) lacc[(k0 + u) * SNW + warp] += d;
             }
         }
-    } else {
-        // ------------------------------------------------------------------ consumers
-        const double sc = a.xscale ? *a.xscale : 1.0;
-        double zc[MAXZ];
-#pragma unroll
-        for (int i = 0; i < MAXZ; i++) zc[i] = (i < a.nz) ? a.zc[i] * (a.zcd[i] ? *a.zcd[i] : 1.0) : 0.0;
-        for (int i = tid; i < a.nd * NCW; i += NCT) lacc[i] = 0.0;
-        double ysq = 0.0;
-        uint32_t it = 0, ht = 0;
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int64_t r0 = tile * TILE;
-            const int rows = (int)min((int64_t)TILE, n - r0);
-            // phase 1+2: y rows into ys (and global)
-            if constexpr (HALO) {
-                const int hb = ht & 1;
-                mbar_wait(&pp.hfull[hb], (ht >> 1) & 1);
-                HaloPlan h;
-                halo_plan(op, r0, rows, a.ldx, h);
-                const double *hbuf = halo + hb * nseg * HSEG;
-                for (int q = tid; q < rows; q += NCT) {
-                    const int64_t r = r0 + q;
-                    double y;
-                    if constexpr (std::is_same<Op, StencilOp>::value) y = stencil_row_halo(op, hbuf, h, r);
-                    else y = hbuf[r - h.start[0]];
-                    y = sc * y;
-#pragma unroll
-                    for (int i = 0; i < MAXZ; i++)
-                        if (i < a.nz) y = fma(zc[i], __ldg(a.z[i] + r), y);
-                    ys[q] = y;
-                    if (a.y) a.y[r] = y;
-                    ysq = fma(y, y, ysq);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&pp.hempty[hb]);
-                ht++;
-            } else {
-                csr_tile(op, a.x, r0, rows, ys, tid);
-                consumer_sync();
-                for (int q = tid; q < rows; q += NCT) {
-                    const int64_t r = r0 + q;
-                    double y = sc * ys[q];
-#pragma unroll
-                    for (int i = 0; i < MAXZ; i++)
-                        if (i < a.nz) y = fma(zc[i], __ldg(a.z[i] + r), y);
-                    ys[q] = y;
-                    if (a.y) a.y[r] = y;
-                    ysq = fma(y, y, ysq);
-                }
-            }
-            consumer_sync();
-            // phase 3: dot products of the tile with the streamed V column segments
-            if (a.nd > 0) {
-                const int qa = warp * 64 + 2 * lane;
-                const double2 ya = *reinterpret_cast<const double2 *>(ys + qa);
-                for (int k = 0; k < a.nd; k++) {
-                    const int s = it % nring;
-                    mbar_wait(&pp.full[s], (it / nring) & 1);
-                    const double2 va = *reinterpret_cast<const double2 *>(ring + s * TILE + qa);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&pp.empty[s]);
-                    double d = 0.0;
-                    if (qa < rows) d = va.x * ya.x;
-                    if (qa + 1 < rows) d = fma(va.y, ya.y, d);
-                    d = warp_sum(d);
-                    if (lane == 0) lacc[k * NCW + warp] += d;
-                    it++;
-                }
-            }
-            consumer_sync();
-        }
-        // block totals (fixed order)
-        for (int k = tid; k < a.nd; k += NCT) {
+    }
+    // ---- block totals (fixed order), grid reduction, finalize
+    __syncthreads();
+    for (int k = tid; k < a.nd; k += SNT) {
+        double t = 0.0;
+        for (int w = 0; w < SNW; w++) t += lacc[k * SNW + w];
+        bsum[k] = t;
+    }
+    if (a.ynorm) {
+        const double v = warp_sum(ysq);
+        if (lane == 0) wsum[warp] = v;
+        __syncthreads();
+        if (tid == 0) {
             double t = 0.0;
-            for (int w = 0; w < NCW; w++) t += lacc[k * NCW + w];
-            bsum[k] = t;
-        }
-        if (a.ynorm) {
-            const double v = warp_sum(ysq);
-            if (lane == 0) wsum[warp] = v;
-            consumer_sync();
-            if (tid == 0) {
-                double t = 0.0;
-                for (int w = 0; w < NCW; w++) t += wsum[w];
-                bsum[a.nd] = t;
-            }
+            for (int w = 0; w < SNW; w++) t += wsum[w];
+            bsum[a.nd] = t;
         }
     }
     const int nv = a.nd + (a.ynorm ? 1 : 0);
@@ -408,104 +398,91 @@ __global__ void __launch_bounds__(NTHR, 1) spmv_stream_kernel(Op op, SpmvArgs a,
 }
 
 // ---------------------------------------------------------------------------------------------
+// axpy_stream
 
-struct AxpySrc {
-    int nitem;
-};
-
-__device__ __forceinline__ const double *axpy_item(const AxpyArgs &a, int k)
+template <int RPT>
+__global__ void __launch_bounds__(SNT, 4) axpy_stream_kernel(int64_t n, AxpyArgs a, Work wk)
 {
-    // item order: [base], V columns c0.., extras
-    if (a.a0h != 0.0) {
-        if (k == 0) return a.base;
-        k--;
-    }
-    if (k < a.nc) return a.V + (int64_t)(a.c0 + k) * a.ldv;
-    return a.e[k - a.nc];
-}
-
-__global__ void __launch_bounds__(NTHR, 1) axpy_stream_kernel(int64_t n, AxpyArgs a, Work wk, int nring)
-{
-    extern __shared__ __align__(128) double sm[];
-    __shared__ Pipe pp;
+    constexpr int TILE_ = SNT * RPT;
+    constexpr int NP = RPT / 2;
     __shared__ double coef[MAXITEM];
+    __shared__ const double *src[MAXITEM];
     __shared__ double bsum[2];
-    __shared__ double wsum[NCW];
+    __shared__ double wsum[SNW];
     __shared__ int s_exit;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) {
-        s_exit = a.check_brk ? (wk.st->brk >= 0) : 0;
-        pipe_init(pp, nring);
-    }
+    if (tid == 0) s_exit = a.check_brk ? (wk.st->brk >= 0) : 0;
     const int nbase = (a.a0h != 0.0) ? 1 : 0;
     const int nitem = nbase + a.nc + a.ne;
-    for (int k = tid; k < nitem; k += NTHR) {
+    for (int k = tid; k < nitem; k += SNT) {
         double c;
-        if (k < nbase) c = a.a0h * (a.a0d ? *a.a0d : 1.0);
-        else if (k < nbase + a.nc) c = a.gsign * a.g[k - nbase];
-        else c = a.ec[k - nbase - a.nc] * (a.ecd ? a.ecd[k - nbase - a.nc] : 1.0);
+        const double *p;
+        if (k < nbase) {
+            c = a.a0h * (a.a0d ? *a.a0d : 1.0);
+            p = a.base;
+        } else if (k < nbase + a.nc) {
+            c = a.gsign * a.g[k - nbase];
+            p = a.V + (int64_t)(a.c0 + k - nbase) * a.ldv;
+        } else {
+            const int i = k - nbase - a.nc;
+            c = a.ec[i] * (a.ecd ? a.ecd[i] : 1.0);
+            p = a.e[i];
+        }
         coef[k] = c;
+        src[k] = p;
     }
     __syncthreads();
     if (s_exit) return;
-    double *ring = sm;
-    const int64_t ntiles = (n + TILE - 1) / TILE;
+    const int64_t ntiles = (n + TILE_ - 1) / TILE_;
     double nrm = 0.0;
-    if (warp == NCW) {
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            uint32_t it = 0;
-            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                const int64_t r0 = tile * TILE;
-                const int rows = (int)min((int64_t)TILE, n - r0);
-                const uint32_t by = seg_bytes(rows);
-                for (int k = 0; k < nitem; k++) {
-                    const int s = it % nring;
-                    const uint32_t r = it / nring;
-                    if (r >= 1) mbar_wait(&pp.empty[s], (r - 1) & 1);
-                    mbar_arrive_expect_tx(&pp.full[s], by);
-                    tma_load_1d(ring + s * TILE, axpy_item(a, k) + r0, by, &pp.full[s], pol);
-                    it++;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = tile * TILE_;
+        const int rows = (int)min((int64_t)TILE_, n - r0);
+        double2 acc[NP];
+#pragma unroll
+        for (int p = 0; p < NP; p++) acc[p] = make_double2(0.0, 0.0);
+        for (int k0 = 0; k0 < nitem; k0 += CU) {
+            double2 v[CU][NP];
+#pragma unroll
+            for (int u = 0; u < CU; u++) {
+                const int k = k0 + u;
+                const double *sp = src[k < nitem ? k : k0] + r0;
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    const int q = 2 * tid + 2 * SNT * p;
+                    v[u][p] = (k < nitem && q < rows) ? ld_stream2(sp + q) : make_double2(0.0, 0.0);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < CU; u++) {
+                const double c = (k0 + u < nitem) ? coef[k0 + u] : 0.0;
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    acc[p].x = fma(c, v[u][p].x, acc[p].x);
+                    acc[p].y = fma(c, v[u][p].y, acc[p].y);
                 }
             }
         }
-    } else {
-        uint32_t it = 0;
-        const int qa = 2 * tid;                               // rows qa, qa+1 of the tile
-        for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int64_t r0 = tile * TILE;
-            const int rows = (int)min((int64_t)TILE, n - r0);
-            double2 A = make_double2(0.0, 0.0);
-            for (int k = 0; k < nitem; k++) {
-                const int s = it % nring;
-                mbar_wait(&pp.full[s], (it / nring) & 1);
-                const double2 va = *reinterpret_cast<const double2 *>(ring + s * TILE + qa);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&pp.empty[s]);
-                const double c = coef[k];
-                A.x = fma(c, va.x, A.x);
-                A.y = fma(c, va.y, A.y);
-                it++;
-            }
-            double *o = a.out + r0;
-            if (qa + 1 < rows) *reinterpret_cast<double2 *>(o + qa) = A;
-            else if (qa < rows) o[qa] = A.x;
-            if (qa < rows) nrm = fma(A.x, A.x, nrm);
-            if (qa + 1 < rows) nrm = fma(A.y, A.y, nrm);
-        }
-        if (a.onorm) {
-            const double v = warp_sum(nrm);
-            if (lane == 0) wsum[warp] = v;
-            consumer_sync();
-            if (tid == 0) {
-                double t = 0.0;
-                for (int w = 0; w < NCW; w++) t += wsum[w];
-                bsum[0] = t;
-            }
+#pragma unroll
+        for (int p = 0; p < NP; p++) {
+            const int q = 2 * tid + 2 * SNT * p;
+            double *o = a.out + r0 + q;
+            if (q + 1 < rows) *reinterpret_cast<double2 *>(o) = acc[p];
+            else if (q < rows) o[0] = acc[p].x;
+            if (q < rows) nrm = fma(acc[p].x, acc[p].x, nrm);
+            if (q + 1 < rows) nrm = fma(acc[p].y, acc[p].y, nrm);
         }
     }
-    __syncthreads();
     if (!a.onorm) return;
+    const double v = warp_sum(nrm);
+    if (lane == 0) wsum[warp] = v;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < SNW; w++) t += wsum[w];
+        bsum[0] = t;
+    }
+    __syncthreads();
     if (!publish_partials(wk, bsum, 1)) return;
     __shared__ double red[2];
     final_reduce(wk, 1, red);

@@ -17,6 +17,7 @@
 namespace phipm {
 
 constexpr int EXPM_NT = 512;
+constexpr int EXPM_KMAX = 136;         // padded K bound (m_max + p_max + 1 <= 128 + 8)
 
 // result block read by the host controller (mapped pinned memory)
 struct AttemptResult {
@@ -51,22 +52,30 @@ struct ExpmArgs {
     int seq;
 };
 
-// C = A B (K x K, column-major); two accumulators to shorten the dependent FMA chain
-__device__ __forceinline__ void cta_matmul(int K, const double *A, const double *B, double *C)
+// C = A B for Kp x Kp column-major matrices (Kp a multiple of 8, zero padded) on the fp64 tensor
+// cores: each warp computes 8x8 output tiles with mma.sync.m8n8k4.f64 (SASS DMMA).
+// Fragment layouts (PTX ISA, m8n8k4 .f64): A row-major 8x4, a0 = A[lane/4][lane%4];
+// B column-major 4x8, b0 = B[lane%4][lane/4]; C 8x8, c_i = C[lane/4][2 (lane%4) + i].
+__device__ __forceinline__ void cta_matmul(int Kp, const double *A, const double *B, double *C)
 {
-    const int KK = K * K;
-    for (int o = threadIdx.x; o < KK; o += blockDim.x) {
-        const int i = o % K, jc = o / K;
-        const double *a = A + i;
-        const double *b = B + (size_t)jc * K;
-        double s0 = 0.0, s1 = 0.0;
-        int l = 0;
-        for (; l + 1 < K; l += 2) {
-            s0 = fma(a[(size_t)l * K], b[l], s0);
-            s1 = fma(a[(size_t)(l + 1) * K], b[l + 1], s1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int nt = Kp >> 3;
+    const int ar = lane >> 2, ac = lane & 3;
+    for (int t = warp; t < nt * nt; t += nw) {
+        const int ti = t % nt, tj = t / nt;
+        const double *Ap = A + (ti * 8 + ar) + (size_t)ac * Kp;
+        const double *Bp = B + ac + (size_t)(tj * 8 + ar) * Kp;
+        double c0 = 0.0, c1 = 0.0;
+        for (int kk = 0; kk < Kp; kk += 4) {
+            const double a = Ap[(size_t)kk * Kp];
+            const double b = Bp[kk];
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(c0), "+d"(c1)
+                         : "d"(a), "d"(b));
         }
-        if (l < K) s0 = fma(a[(size_t)l * K], b[l], s0);
-        C[o] = s0 + s1;
+        const int row = ti * 8 + ar, col = tj * 8 + 2 * ac;
+        C[row + (size_t)col * Kp] = c0;
+        C[row + (size_t)(col + 1) * Kp] = c1;
     }
     __syncthreads();
 }
@@ -97,15 +106,16 @@ __device__ __forceinline__ void pade13(double *c)
     for (int j = 0; j < 13; j++) c[j + 1] = c[j] * (double)(13 - j) / ((double)(26 - j) * (double)(j + 1));
 }
 
-// exp(M0) -> returned pointer (one of the buffers); M0..M5 are K x K buffers.  status: 0/5/6
-__device__ double *cta_expm(int K, double *M0, double *M1, double *M2, double *M3, double *M4, double *M5,
-                            double *sred, int *s_int, int *status)
+// exp(M0) -> returned pointer (one of the buffers); M0..M5 are Kp x Kp buffers (Kp = K rounded
+// up to a multiple of 8, padding zero: exp(blockdiag(A, 0)) = blockdiag(exp A, I)).  status 0/5/6
+__device__ double *cta_expm(int K, int Kp, double *M0, double *M1, double *M2, double *M3, double *M4, double *M5,
+                            double *sred, int *s_int, double *fcol, int *status)
 {
-    const int KK = K * K, t = threadIdx.x;
+    const int KK = Kp * Kp, t = threadIdx.x;
     double c[14];
     pade13(c);
     // scaling: s = ceil_+(log2(||A||_1 / 5.37)) (theta_13 = 5.37 as printed, R26)
-    const double nrm = block_max_colsum(K, M0, sred);
+    const double nrm = block_max_colsum(Kp, M0, sred);
     int s = 0;
     if (nrm > 0.0) {
         const double l = ceil(log2(nrm / 5.37));
@@ -115,29 +125,25 @@ __device__ double *cta_expm(int K, double *M0, double *M1, double *M2, double *M
     const double sc = ldexp(1.0, -s);
     for (int e = t; e < KK; e += blockDim.x) M0[e] *= sc;
     __syncthreads();
-    cta_matmul(K, M0, M0, M1);            // A2
-    cta_matmul(K, M1, M1, M2);            // A4
-    cta_matmul(K, M2, M1, M3);            // A6
+    cta_matmul(Kp, M0, M0, M1);            // A2
+    cta_matmul(Kp, M1, M1, M2);            // A4
+    cta_matmul(Kp, M2, M1, M3);            // A6
     // U = A [A6 (c13 A6 + c11 A4 + c9 A2) + c7 A6 + c5 A4 + c3 A2 + c1 I]
     for (int e = t; e < KK; e += blockDim.x) M4[e] = c[13] * M3[e] + c[11] * M2[e] + c[9] * M1[e];
     __syncthreads();
-    cta_matmul(K, M3, M4, M5);
-    for (int e = t; e < KK; e += blockDim.x) {
-        double v = M5[e] + c[7] * M3[e] + c[5] * M2[e] + c[3] * M1[e];
-        if (e % (K + 1) == 0) v += c[1];
-        M5[e] = v;
-    }
+    cta_matmul(Kp, M3, M4, M5);
+    for (int e = t; e < KK; e += blockDim.x) M5[e] = M5[e] + c[7] * M3[e] + c[5] * M2[e] + c[3] * M1[e];
     __syncthreads();
-    cta_matmul(K, M0, M5, M4);            // U in M4
+    for (int i = t; i < Kp; i += blockDim.x) M5[i * (Kp + 1)] += c[1];
+    __syncthreads();
+    cta_matmul(Kp, M0, M5, M4);            // U in M4
     // V = A6 (c12 A6 + c10 A4 + c8 A2) + c6 A6 + c4 A4 + c2 A2 + c0 I
     for (int e = t; e < KK; e += blockDim.x) M5[e] = c[12] * M3[e] + c[10] * M2[e] + c[8] * M1[e];
     __syncthreads();
-    cta_matmul(K, M3, M5, M0);            // A no longer needed
-    for (int e = t; e < KK; e += blockDim.x) {
-        double v = M0[e] + c[6] * M3[e] + c[4] * M2[e] + c[2] * M1[e];
-        if (e % (K + 1) == 0) v += c[0];
-        M0[e] = v;                        // V
-    }
+    cta_matmul(Kp, M3, M5, M0);            // A no longer needed
+    for (int e = t; e < KK; e += blockDim.x) M0[e] = M0[e] + c[6] * M3[e] + c[4] * M2[e] + c[2] * M1[e];
+    __syncthreads();
+    for (int i = t; i < Kp; i += blockDim.x) M0[i * (Kp + 1)] += c[0];   // V
     __syncthreads();
     // P = V + U (M1), Q = V - U (M2)
     for (int e = t; e < KK; e += blockDim.x) {
@@ -146,15 +152,19 @@ __device__ double *cta_expm(int K, double *M0, double *M1, double *M2, double *M
         M2[e] = v - u;
     }
     __syncthreads();
-    // Gauss-Jordan with partial pivoting: Q X = P, X overwrites P
+    // Gauss-Jordan with partial pivoting: Q X = P, X overwrites P (3 barriers per column).  Only the
+    // leading K x K block is eliminated: the padding block of Q and P is the identity and stays so.
     double *Q = M2, *P = M1;
+    const int rr = t % K, cstart = t / K, cstep = (int)blockDim.x / K;   // fixed row per thread
     for (int col = 0; col < K; col++) {
         if (t < 32) {
+            // pivot search on column col, and a snapshot of the column (pre-swap) in fcol
             double best = -1.0;
             int bi = col;
-            for (int r = col + t; r < K; r += 32) {
-                const double a = fabs(Q[r + (size_t)col * K]);
-                if (a > best) { best = a; bi = r; }
+            for (int r = t; r < K; r += 32) {
+                const double q = Q[r + (size_t)col * Kp];
+                fcol[r] = q;
+                if (r >= col && fabs(q) > best) { best = fabs(q); bi = r; }
             }
             for (int o = 16; o > 0; o >>= 1) {
                 const double ob = __shfl_xor_sync(0xffffffffu, best, o);
@@ -169,48 +179,42 @@ __device__ double *cta_expm(int K, double *M0, double *M1, double *M2, double *M
         __syncthreads();
         if (s_int[1]) { *status = 6; return P; }
         const int pr = s_int[0];
-        if (pr != col) {
-            for (int jc = t; jc < 2 * K; jc += blockDim.x) {
-                double *Mx = (jc < K) ? Q : P;
-                const int cc = (jc < K) ? jc : jc - K;
-                const double tmp = Mx[col + (size_t)cc * K];
-                Mx[col + (size_t)cc * K] = Mx[pr + (size_t)cc * K];
-                Mx[pr + (size_t)cc * K] = tmp;
-            }
+        const double rpiv = 1.0 / fcol[pr];
+        // swap rows col <-> pr; scale the new pivot row (Q right of the pivot, all of P) by 1/piv
+        for (int jc = t; jc < 2 * K; jc += blockDim.x) {
+            double *Mx = (jc < K) ? Q : P;
+            const int cc = (jc < K) ? jc : jc - K;
+            const double top = Mx[pr + (size_t)cc * Kp];
+            if (pr != col) Mx[pr + (size_t)cc * Kp] = Mx[col + (size_t)cc * Kp];
+            Mx[col + (size_t)cc * Kp] = (jc < K && cc <= col) ? top : top * rpiv;
         }
         __syncthreads();
-        // eliminate column col from every other row, using the unscaled pivot row
-        const double piv = Q[col + (size_t)col * K];
-        const int ncolq = K - col - 1;
-        const int width = ncolq + K;                   // Q columns col+1..K-1, then P columns
-        const int work = (K - 1) * width;
-        for (int w = t; w < work; w += blockDim.x) {
-            int r = w % (K - 1);
-            const int cc = w / (K - 1);
-            if (r >= col) r++;                          // skip the pivot row
-            const double f = Q[r + (size_t)col * K] / piv;
-            if (cc < ncolq) {
-                const int qc = col + 1 + cc;
-                Q[r + (size_t)qc * K] -= f * Q[col + (size_t)qc * K];
-            } else {
-                const int pc = cc - ncolq;
-                P[r + (size_t)pc * K] -= f * P[col + (size_t)pc * K];
+        // eliminate column col from every other row with the scaled pivot row
+        if (cstart < cstep) {
+            const double f = (rr == col) ? 0.0 : (rr == pr ? fcol[col] : fcol[rr]);
+            if (f != 0.0) {
+                const int ncolq = K - col - 1;
+                const int width = ncolq + K;
+                for (int cc = cstart; cc < width; cc += cstep) {
+                    if (cc < ncolq) {
+                        const int qc = col + 1 + cc;
+                        Q[rr + (size_t)qc * Kp] -= f * Q[col + (size_t)qc * Kp];
+                    } else {
+                        const int pc = cc - ncolq;
+                        P[rr + (size_t)pc * Kp] -= f * P[col + (size_t)pc * Kp];
+                    }
+                }
             }
-        }
-        __syncthreads();
-        // scale the pivot row (Q part right of the pivot is no longer needed except by later
-        // pivots' eliminations, which read row col's Q entries only for columns > col)
-        for (int jc = t; jc < width; jc += blockDim.x) {
-            if (jc < ncolq) Q[col + (size_t)(col + 1 + jc) * K] /= piv;
-            else P[col + (size_t)(jc - ncolq) * K] /= piv;
         }
         __syncthreads();
     }
     // squaring
     double *X = P, *T = M3;
     for (int q = 0; q < s; q++) {
-        cta_matmul(K, X, X, T);
-        double *tmp = X; X = T; T = tmp;
+        cta_matmul(Kp, X, X, T);
+        double *tmp = X;
+        X = T;
+        T = tmp;
     }
     return X;
 }
@@ -256,23 +260,28 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
         }
         return;
     }
-    const size_t KK = (size_t)K * K;
+    const int Kp = (K + 7) & ~7;                         // padded to the DMMA tile size
+    const size_t KK = (size_t)Kp * Kp;
     double *base = a.use_smem ? esm : a.scratch;
     double *M0 = base, *M1 = base + KK, *M2 = base + 2 * KK, *M3 = base + 3 * KK, *M4 = base + 4 * KK,
            *M5 = base + 5 * KK;
-    // build the matrix to exponentiate
+    __shared__ double fcol[EXPM_KMAX];
+    // build the matrix to exponentiate (zero padded to Kp)
+    for (size_t e = t; e < KK; e += blockDim.x) M0[e] = 0.0;
+    __syncthreads();
     if (a.mode == 1) {
-        for (size_t e = t; e < KK; e += blockDim.x) M0[e] = a.Ain[e];
+        for (size_t e = t; e < (size_t)K * K; e += blockDim.x) {
+            const int i = (int)(e % K), jc = (int)(e / K);
+            M0[i + (size_t)jc * Kp] = a.Ain[e];
+        }
     } else {
-        for (size_t e = t; e < KK; e += blockDim.x) M0[e] = 0.0;
-        __syncthreads();
         for (size_t e = t; e < (size_t)mu * mu; e += blockDim.x) {
             const int i = (int)(e % mu), jc = (int)(e / mu);
-            if (!a.tridiag || (i - jc <= 1 && jc - i <= 1)) M0[i + (size_t)jc * K] = a.tau * a.H[i + (size_t)jc * a.ldh];
+            if (!a.tridiag || (i - jc <= 1 && jc - i <= 1)) M0[i + (size_t)jc * Kp] = a.tau * a.H[i + (size_t)jc * a.ldh];
         }
         if (t == 0) {
-            M0[0 + (size_t)mu * K] = 1.0;
-            for (int i = 1; i <= a.p; i++) M0[(mu + i - 1) + (size_t)(mu + i) * K] = 1.0;
+            M0[0 + (size_t)mu * Kp] = 1.0;
+            for (int i = 1; i <= a.p; i++) M0[(mu + i - 1) + (size_t)(mu + i) * Kp] = 1.0;
         }
     }
     __syncthreads();
@@ -296,12 +305,15 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
     if (t == 0) s_status = 0;
     __syncthreads();
     int status = 0;
-    double *E = cta_expm(K, M0, M1, M2, M3, M4, M5, sred, s_int, &status);
+    double *E = cta_expm(K, Kp, M0, M1, M2, M3, M4, M5, sred, s_int, fcol, &status);
     if (t == 0 && status) s_status = status;
     __syncthreads();
     status = s_status;
     if (a.mode == 1) {
-        for (size_t e = t; e < KK; e += blockDim.x) a.Eout[e] = E[e];
+        for (size_t e = t; e < (size_t)K * K; e += blockDim.x) {
+            const int i = (int)(e % K), jc = (int)(e / K);
+            a.Eout[e] = E[i + (size_t)jc * Kp];
+        }
         if (t == 0) {
             AttemptResult r{};
             r.status = status; r.seq = a.seq;
@@ -313,8 +325,8 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
     const int cp1 = mu + a.p;
     if (a.mode == 2) {
         for (int i = t; i < mu; i += blockDim.x) {
-            a.phip_out[i] = E[i + (size_t)cp * K];
-            a.phip1_out[i] = E[i + (size_t)cp1 * K];
+            a.phip_out[i] = E[i + (size_t)cp * Kp];
+            a.phip1_out[i] = E[i + (size_t)cp1 * Kp];
         }
         if (t == 0) {
             AttemptResult r{};
@@ -329,13 +341,13 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
     const double h = corr ? a.H[mu + (size_t)(mu - 1) * a.ldh] : 0.0;
     double taup = 1.0;
     for (int j = 0; j < a.p; j++) taup *= a.tau;
-    const double phl = E[(mu - 1) + (size_t)cp1 * K];
-    for (int i = t; i < mu; i += blockDim.x) a.comb[i] = taup * beta * E[i + (size_t)cp * K] * a.sigma[i];
+    const double phl = E[(mu - 1) + (size_t)cp1 * Kp];
+    for (int i = t; i < mu; i += blockDim.x) a.comb[i] = taup * beta * E[i + (size_t)cp * Kp] * a.sigma[i];
     __shared__ int s_fin;
     if (t == 0) s_fin = 1;
     __syncthreads();
     for (int i = t; i < mu; i += blockDim.x)
-        if (!isfinite(E[i + (size_t)cp * K])) s_fin = 0;
+        if (!isfinite(E[i + (size_t)cp * Kp])) s_fin = 0;
     __syncthreads();
     if (t == 0) {
         a.comb[mu] = corr ? taup * beta * a.tau * h * phl * a.sigma[mu] : 0.0;

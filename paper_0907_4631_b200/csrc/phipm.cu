@@ -236,7 +236,8 @@ int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a, int cls)
 
 int launch_expm(phipm_ctx *c, ExpmArgs &a, int K)
 {
-    const size_t need = (size_t)6 * K * K * sizeof(double);
+    const int Kp = (K + 7) & ~7;
+    const size_t need = (size_t)6 * Kp * Kp * sizeof(double);
     a.use_smem = need <= c->expm_smem_limit;
     a.scratch = c->scratch;
     a.res = c->res_d;
@@ -896,7 +897,7 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     A((void **)&c->part, sizeof(double) * (size_t)c->pstride * (MAXD + 2));
     A((void **)&c->comb, sizeof(double) * (MAXD + 1));
     A((void **)&c->combd, sizeof(double) * (P_MAX_ABS + 1));
-    A((void **)&c->scratch, sizeof(double) * 6 * (size_t)c->kmax * c->kmax);
+    A((void **)&c->scratch, sizeof(double) * 6 * (size_t)((c->kmax + 7) & ~7) * ((c->kmax + 7) & ~7));
     A((void **)&c->raw, sizeof(double) * (MAXD + 2));
     A((void **)&c->counter, sizeof(unsigned) * 4);
     A((void **)&c->st, sizeof(DevState));

@@ -157,31 +157,63 @@ __device__ __forceinline__ double hx(const double *hb, const HaloPlan &h, int k,
     return hb[h.off[k] + (int)(g - h.start[k])];
 }
 
-// Stencil row, summed in ascending column order (z-, y-, x-, centre, x+, y+, z+) with separately
-// rounded products (no FMA): the same operations in the same order as a sequential CSR row sum,
-// so y is bit-exact with it.
-__device__ __forceinline__ double stencil_row(const StencilOp &S, const double *hb, const HaloPlan &h, int64_t r)
+// Per-tile neighbour base pointers into the halo buffer: x[g] of direction d is ptr_d[g]
+// (resolved once per tile, so the row loop does no dynamic indexing of the plan).
+struct HaloPtrs {
+    const double *c, *ym, *yp, *zm, *zp;
+};
+
+__device__ __forceinline__ HaloPtrs halo_ptrs(const double *hb, const HaloPlan &h)
+{
+    HaloPtrs P;
+    P.c = hb + h.off[0] - h.start[0];
+    P.ym = hb + h.off[h.ylo] - h.start[h.ylo];
+    P.yp = hb + h.off[h.yhi] - h.start[h.yhi];
+    P.zm = hb + h.off[h.zlo] - h.start[h.zlo];
+    P.zp = hb + h.off[h.zhi] - h.start[h.zhi];
+    return P;
+}
+
+// Stencil row r with grid coordinates (i, j, k), summed in ascending column order (z-, y-, x-,
+// centre, x+, y+, z+) with separately rounded products (no FMA): the same operations in the same
+// order as a sequential CSR row sum, so y is bit-exact with it.
+__device__ __forceinline__ double stencil_row(const StencilOp &S, const HaloPtrs &P, int64_t r, int i, int jj, int kk)
+{
+    const int64_t pl = (int64_t)S.nx * S.ny;
+    double s = 0.0;
+    if (S.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(S.c[5], P.zm[r - pl]));
+    if (S.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(S.c[3], P.ym[r - S.nx]));
+    if (i > 0) s = __dadd_rn(s, __dmul_rn(S.c[1], P.c[r - 1]));
+    s = __dadd_rn(s, __dmul_rn(S.c[0], P.c[r]));
+    if (i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[2], P.c[r + 1]));
+    if (S.dim >= 2 && jj < S.ny - 1) s = __dadd_rn(s, __dmul_rn(S.c[4], P.yp[r + S.nx]));
+    if (S.dim >= 3 && kk < S.nz - 1) s = __dadd_rn(s, __dmul_rn(S.c[6], P.zp[r + pl]));
+    return s;
+}
+
+// grid coordinates of row r (two 32-bit divisions)
+__device__ __forceinline__ void grid_ijk(const StencilOp &S, int64_t r, int &i, int &jj, int &kk)
 {
     const unsigned ur = (unsigned)r, unx = (unsigned)S.nx;
     const unsigned q = ur / unx;
-    const int i = (int)(ur - q * unx);
-    int jj = 0, kk = 0;
+    i = (int)(ur - q * unx);
+    jj = 0;
+    kk = 0;
     if (S.dim >= 2) {
         const unsigned uny = (unsigned)S.ny;
         const unsigned q2 = q / uny;
         jj = (int)(q - q2 * uny);
         kk = (int)q2;
     }
-    const int64_t pl = (int64_t)S.nx * S.ny;
-    double s = 0.0;
-    if (S.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(S.c[5], hx(hb, h, h.zlo, r - pl)));
-    if (S.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(S.c[3], hx(hb, h, h.ylo, r - S.nx)));
-    if (i > 0) s = __dadd_rn(s, __dmul_rn(S.c[1], hx(hb, h, 0, r - 1)));
-    s = __dadd_rn(s, __dmul_rn(S.c[0], hx(hb, h, 0, r)));
-    if (i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[2], hx(hb, h, 0, r + 1)));
-    if (S.dim >= 2 && jj < S.ny - 1) s = __dadd_rn(s, __dmul_rn(S.c[4], hx(hb, h, h.yhi, r + S.nx)));
-    if (S.dim >= 3 && kk < S.nz - 1) s = __dadd_rn(s, __dmul_rn(S.c[6], hx(hb, h, h.zhi, r + pl)));
-    return s;
+}
+
+// the row after (i, j, k)
+__device__ __forceinline__ void grid_next(const StencilOp &S, int &i, int &jj, int &kk)
+{
+    if (++i == S.nx) {
+        i = 0;
+        if (++jj == S.ny) { jj = 0; kk++; }
+    }
 }
 
 // CSR rows of a tile into ys: G = 2^glog lanes per row, U row groups in flight per lane (memory-
@@ -301,15 +333,20 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
             ht++;
             HaloPlan h;
             plan(r0, rows, h);
+            const HaloPtrs P = halo_ptrs(hbuf, h);
 #pragma unroll
             for (int p = 0; p < NP; p++) {
                 const int q = 2 * tid + 2 * SNT * p;
+                const int64_t r = r0 + q;
                 if constexpr (IS_ST) {
-                    y[p].x = q < rows ? stencil_row(op, hbuf, h, r0 + q) : 0.0;
-                    y[p].y = q + 1 < rows ? stencil_row(op, hbuf, h, r0 + q + 1) : 0.0;
+                    int i, jj, kk;
+                    grid_ijk(op, r, i, jj, kk);
+                    y[p].x = q < rows ? stencil_row(op, P, r, i, jj, kk) : 0.0;
+                    grid_next(op, i, jj, kk);
+                    y[p].y = q + 1 < rows ? stencil_row(op, P, r + 1, i, jj, kk) : 0.0;
                 } else {
-                    y[p].x = q < rows ? hx(hbuf, h, 0, r0 + q) : 0.0;
-                    y[p].y = q + 1 < rows ? hx(hbuf, h, 0, r0 + q + 1) : 0.0;
+                    y[p].x = q < rows ? P.c[r] : 0.0;
+                    y[p].y = q + 1 < rows ? P.c[r + 1] : 0.0;
                 }
             }
             __syncthreads();                               // halo consumed

@@ -205,29 +205,37 @@ def run_gpu(args):
         _, st = solve()
     torch.cuda.synchronize()
 
-    # ---- timed region (device time, CUDA events on the solve stream; L2 flushed between steps)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    ctx.reset_profile()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()
-            ev[i][0].record(stream)
-            _, st = solve(profile=True)
-            ev[i][1].record(stream)
+    def timed(profile):
+        """K solves; device time from CUDA events on the solve stream around each solve (L2 flushed
+        between steps, outside the events).  Returns (max-over-ranks ms, last stats, clocks)."""
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        ctx.reset_profile()
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    elapsed_ms = sum(a.elapsed_time(b) for a, b in ev)
-    prof = ctx.profile()
-    t_max = elapsed_ms
-    if world > 1:
-        t = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max = float(t.item())
+        with ClockSampler(local) as clk:
+            for i in range(args.steps):
+                flush.zero_()
+                ev[i][0].record(stream)
+                _, st_ = solve(profile=profile)
+                ev[i][1].record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = sum(a.elapsed_time(b) for a, b in ev)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, st_, clk.summary()
+
+    # ---- timed region 1: the headline (no per-kernel instrumentation: kernels chain with PDL)
+    t_max, st, clocks = timed(0)
     value = world * args.steps / (t_max / 1e3)
+    # ---- timed region 2: same steps with per-kernel CUDA events (roofline of the dominant kernel)
+    t_prof, st2, clocks2 = timed(1)
+    prof = ctx.profile()
 
     # ---- end to end through the host-buffer C-ABI entry point (pinned host memory)
     hu = [torch.from_numpy(x).pin_memory().numpy() for x in Pb.u]
@@ -282,7 +290,6 @@ def run_gpu(args):
                 "peak_source": peak_src}
 
     if rank == 0:
-        clocks = clk.summary()
         cpu = cpu_baseline(Pb) if not args.no_cpu_baseline else None
         launches_total = prof["launches"]
         line = {
@@ -299,6 +306,10 @@ def run_gpu(args):
             "arnoldi_step": {"achieved_gbs": arnoldi_gbs, "frac_of_8000": arnoldi_gbs / 8000.0,
                              "frac_of_measured": arnoldi_gbs / peak,
                              "ms_per_solve": krylov_ms / args.steps},
+            "profiled_region": {"ms_per_step": t_prof / args.steps, "value": world * args.steps / (t_prof / 1e3),
+                                "note": "second timed region with CUDA events around every kernel "
+                                        "(source of roofline / arnoldi_step / profile_ms_per_solve)",
+                                "clocks": clocks2},
             "cpu_baseline": cpu,
             "clocks": clocks,
             "stats": {"nsteps": st.nsteps, "nreject": st.nreject, "nspmv": st.nspmv, "nexpm": st.nexpm,

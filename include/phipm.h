@@ -75,7 +75,8 @@ typedef struct {
     int fixed_m;         /* 1: "phip" mode: m fixed to m_init, only tau adapts */
     int eq6_variant;     /* 0: Eq. (6) as printed; 1: log(eps/eps_old)/log(tau/tau_old) - 1 (R13) */
     int orth;            /* PHIPM_ORTH_* */
-    int profile;         /* 1: time every kernel class with CUDA events (phipm_get_profile) */
+    int profile;         /* 1: time every kernel class with CUDA events (phipm_get_profile);
+                            2: also record every launch (phipm_get_trace) */
 } phipm_opts;
 
 /* Statistics (the paper's stats(1..4), plus the Krylov dimension). */
@@ -104,6 +105,14 @@ typedef struct {
     int64_t n_spmv_dot, n_orth, n_expm, n_combine;
 } phipm_profile;
 
+/* One traced kernel launch (opts.profile = 2). */
+typedef struct {
+    int32_t cls;           /* 0 spmv_dot, 1 orth, 2 expm, 3 combine, 4 other */
+    int32_t ncols;         /* dot columns (spmv) or streamed vectors (axpy); K for expm */
+    double bytes;          /* algorithmic bytes */
+    double us;             /* device time (CUDA events) */
+} phipm_trace_rec;
+
 void phipm_default_opts(phipm_opts *opts);
 
 /* Create a context that can solve problems with n <= n_max, m_max <= m_max, p <= p_max.
@@ -115,6 +124,9 @@ const char *phipm_strerror(int status);
 const char *phipm_last_error(const phipm_ctx *ctx);
 int phipm_get_profile(const phipm_ctx *ctx, phipm_profile *out);
 void phipm_reset_profile(phipm_ctx *ctx);
+/* Copy up to max traced launches (oldest first) into out; *count = number recorded since the
+ * last phipm_reset_profile (the buffer keeps the first 65536). */
+int phipm_get_trace(const phipm_ctx *ctx, phipm_trace_rec *out, int max, int *count);
 
 /* w = phi_0(tA)u_0 + sum_k t^k phi_k(tA) u_k.  u: HOST array of p+1 DEVICE pointers, each length
  * A->n; w: DEVICE, length n (may alias u[0] only).  opts NULL = defaults.  stats may be NULL.

@@ -51,6 +51,10 @@ class _Stats(C.Structure):
                 ("m_last", C.c_int32), ("m_peak", C.c_int32), ("t_reached", C.c_double)]
 
 
+class _TraceRec(C.Structure):
+    _fields_ = [("cls", C.c_int32), ("ncols", C.c_int32), ("bytes", C.c_double), ("us", C.c_double)]
+
+
 class _Profile(C.Structure):
     _fields_ = [("ms_spmv_dot", C.c_double), ("ms_orth", C.c_double), ("ms_expm", C.c_double),
                 ("ms_combine", C.c_double), ("ms_other", C.c_double), ("bytes_spmv_dot", C.c_double),
@@ -113,6 +117,7 @@ def lib():
             "phipm_last_error": (C.c_char_p, [vp]),
             "phipm_get_profile": (i32, [vp, P(_Profile)]),
             "phipm_reset_profile": (None, [vp]),
+            "phipm_get_trace": (i32, [vp, P(_TraceRec), i32, P(i32)]),
             "phipm_solve_csr": (i32, [vp, d, P(_Csr), i32, P(vp), P(_Opts), vp, P(_Stats)]),
             "phipm_solve_stencil": (i32, [vp, d, P(_Stencil), i32, P(vp), P(_Opts), vp, P(_Stats)]),
             "phipm_reserve_host_csr": (i32, [vp, i64]),
@@ -139,7 +144,7 @@ def lib():
 
 EXPORTED = [
     "phipm_default_opts", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
-    "phipm_get_profile", "phipm_reset_profile", "phipm_solve_csr", "phipm_solve_stencil",
+    "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_solve_csr", "phipm_solve_stencil",
     "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_stencil_nnz",
     "phipm_csr_from_stencil", "phipm_spmv_csr", "phipm_spmv_stencil", "phipm_dot", "phipm_inf_norm_csr",
     "phipm_expm", "phipm_phi_pair", "phipm_krylov_csr", "phipm_krylov_stencil",
@@ -206,7 +211,7 @@ class Context:
 
     # ---------------------------------------------------------------- options / profile
     def opts(self, tol=1e-7, m_init=10, m_max=None, symmetric=False, fixed_m=False,
-             eq6_variant=False, orth=ORTH_CGS, profile=False) -> _Opts:
+             eq6_variant=False, orth=ORTH_CGS, profile=0) -> _Opts:
         o = _Opts()
         self._L.phipm_default_opts(C.byref(o))
         o.tol = tol
@@ -216,7 +221,7 @@ class Context:
         o.fixed_m = int(bool(fixed_m))
         o.eq6_variant = int(bool(eq6_variant))
         o.orth = int(orth)
-        o.profile = int(bool(profile))
+        o.profile = int(profile)
         return o
 
     def profile(self) -> dict:
@@ -226,6 +231,15 @@ class Context:
 
     def reset_profile(self):
         self._L.phipm_reset_profile(self._h)
+
+    def trace(self):
+        """Per-launch records (opts profile=2): list of (cls, ncols, bytes, us)."""
+        cnt = C.c_int()
+        self._check(self._L.phipm_get_trace(self._h, None, 0, C.byref(cnt)))
+        n = min(cnt.value, 65536)
+        buf = (_TraceRec * max(n, 1))()
+        self._check(self._L.phipm_get_trace(self._h, buf, n, C.byref(cnt)))
+        return [(r.cls, r.ncols, r.bytes, r.us) for r in buf[:n]]
 
     # ---------------------------------------------------------------- solves
     @staticmethod

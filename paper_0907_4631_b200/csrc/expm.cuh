@@ -16,7 +16,7 @@
 
 namespace phipm {
 
-constexpr int EXPM_NT = 512;
+constexpr int EXPM_NT = 1024;
 constexpr int EXPM_KMAX = 136;         // padded K bound (m_max + p_max + 1 <= 128 + 8)
 
 // result block read by the host controller (mapped pinned memory)
@@ -226,6 +226,7 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
     __shared__ int s_int[4];
     __shared__ int s_mu;
     const int t = threadIdx.x;
+    pdl_wait();
     int mu, K;
     if (a.mode == 1) {
         mu = 0;
@@ -275,9 +276,12 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
             M0[i + (size_t)jc * Kp] = a.Ain[e];
         }
     } else {
+        // tau H_mu into M0, |H_mu| into M1 (scratch for the unscaled 1-norm)
         for (size_t e = t; e < (size_t)mu * mu; e += blockDim.x) {
             const int i = (int)(e % mu), jc = (int)(e / mu);
-            if (!a.tridiag || (i - jc <= 1 && jc - i <= 1)) M0[i + (size_t)jc * Kp] = a.tau * a.H[i + (size_t)jc * a.ldh];
+            const double hv = (!a.tridiag || (i - jc <= 1 && jc - i <= 1)) ? a.H[i + (size_t)jc * a.ldh] : 0.0;
+            M0[i + (size_t)jc * Kp] = a.tau * hv;
+            M1[i + (size_t)jc * Kp] = fabs(hv);
         }
         if (t == 0) {
             M0[0 + (size_t)mu * Kp] = 1.0;
@@ -285,14 +289,13 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
         }
     }
     __syncthreads();
-    // ||H_mu||_1 (unscaled) for the cost model (R20)
+    // ||H_mu||_1 (unscaled) for the cost model (R20), from the shared copy
     double normH1 = 0.0;
     if (a.mode != 1) {
         double m = 0.0;
         for (int jc = t; jc < mu; jc += blockDim.x) {
             double s = 0.0;
-            const int i0 = a.tridiag ? max(jc - 1, 0) : 0, i1 = a.tridiag ? min(jc + 2, mu) : mu;
-            for (int i = i0; i < i1; i++) s += fabs(a.H[i + (size_t)jc * a.ldh]);
+            for (int i = 0; i < mu; i++) s += M1[i + (size_t)jc * Kp];
             m = fmax(m, s);
         }
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));

@@ -89,6 +89,8 @@ struct SpmvArgs {
     const double *V;             // dot columns V[:, d0 .. d0+nd-1] (nd = 0: none)
     int64_t ldv;
     int d0, nd;
+    int xcol;                    // dot column index (relative to d0) that equals x, or -1: its
+                                 // values are taken from the x tile already on chip
     int ynorm;                   // also reduce ||y||^2
     int fin, j;
     int check_brk;               // exit early if a breakdown happened earlier in this step
@@ -117,6 +119,14 @@ struct AxpyArgs {
 
 // ------------------------------------------------------------------------------------------
 // helpers
+
+// Programmatic Dependent Launch: wait for the predecessor grid (no-op without PDL), then let the
+// successor grid start launching.  Called before any access to data written by earlier kernels.
+__device__ __forceinline__ void pdl_wait()
+{
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 
 __device__ __forceinline__ double warp_sum(double v)
 {
@@ -152,14 +162,29 @@ __device__ __forceinline__ bool publish_partials(const Work &wk, const double *b
 }
 
 // Last block: out[v] = sum over blocks in a fixed order (deterministic), then reset the ticket.
+// Each lane issues 8 independent L2 loads per batch (fixed lane/slot assignment, fixed combine
+// order), so the tail costs about one L2 round trip per value instead of one per 32 blocks.
 __device__ __forceinline__ void final_reduce(const Work &wk, int nv, double *out)
 {
     __threadfence();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int nb = gridDim.x;
     for (int v = warp; v < nv; v += nw) {
         const double *pv = wk.part + (size_t)v * wk.pstride;
-        double s = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(pv + b);
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) acc[u] = 0.0;
+        for (int b0 = 0; b0 < nb; b0 += 256) {
+            double x[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int b = b0 + u * 32 + lane;
+                x[u] = (b < nb) ? __ldcg(pv + b) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) acc[u] += x[u];
+        }
+        double s = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
         s = warp_sum(s);
         if (lane == 0) out[v] = s;
     }

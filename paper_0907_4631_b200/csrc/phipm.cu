@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -30,6 +31,7 @@ enum ProfClass { PC_SPMV = 0, PC_ORTH, PC_EXPM, PC_COMBINE, PC_OTHER, PC_N };
 struct ProfRec {
     cudaEvent_t a, b;
     int cls;
+    int ncols;
     double bytes;
 };
 
@@ -59,6 +61,10 @@ struct phipm_ctx {
     int64_t nnz_cap = 0;
     // profiling
     bool prof = false;
+    bool trace = false;
+    bool pdl = true;
+    std::vector<phipm_trace_rec> tracebuf;
+    int64_t ntrace = 0;
     std::vector<ProfRec> pending;
     std::vector<cudaEvent_t> pool;
     phipm_profile acc{};
@@ -117,10 +123,11 @@ cudaEvent_t ev_get(phipm_ctx *c)
     return e;
 }
 
-void prof_begin(phipm_ctx *c, ProfRec &r, int cls, double bytes)
+void prof_begin(phipm_ctx *c, ProfRec &r, int cls, double bytes, int ncols = 0)
 {
     if (!c->prof) return;
     r.cls = cls;
+    r.ncols = ncols;
     r.bytes = bytes;
     r.a = ev_get(c);
     r.b = ev_get(c);
@@ -147,6 +154,10 @@ void prof_collect(phipm_ctx *c)
         case PC_COMBINE: c->acc.ms_combine += ms; c->acc.bytes_combine += r.bytes; c->acc.n_combine++; break;
         default: c->acc.ms_other += ms; break;
         }
+        if (c->trace) {
+            if (c->tracebuf.size() < 65536) c->tracebuf.push_back({r.cls, r.ncols, r.bytes, 1e3 * (double)ms});
+            c->ntrace++;
+        }
         c->pool.push_back(r.a);
         c->pool.push_back(r.b);
     }
@@ -163,6 +174,25 @@ int grid_for(phipm_ctx *c, int64_t units, int occ)
 
 // ---------------------------------------------------------------------------------------------
 // launches
+
+// Launch with Programmatic Dependent Launch allowed: the kernel's launch and prologue overlap the
+// previous kernel's tail; every kernel executes griddepcontrol.wait before touching data written
+// by its predecessor (kernels.cuh: pdl_wait).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(phipm_ctx *c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 // occupancy-limited grid for a streaming kernel (cached per kernel/smem)
 int stream_grid(phipm_ctx *c, const void *fn, size_t smem, int64_t ntiles)
@@ -183,8 +213,18 @@ int halo_cap_host(const Op &, int tile) { return tile; }
 template <>
 int halo_cap_host<StencilOp>(const StencilOp &S, int tile) { return halo_capacity(S.dim, S.nx, tile); }
 
-// rows per thread: 8 (TILE 2048) when there are enough tiles to fill the GPU, else 2 (TILE 512)
-int pick_rpt(phipm_ctx *c, int64_t n) { return n >= (int64_t)SNT * 8 * 2 * c->sm_count ? 8 : 2; }
+// rows per thread: 8 (TILE 2048) when there are enough tiles to fill the GPU, else 2 (TILE 512);
+// PHIPM_RPT=2|4|8 overrides (tuning experiments)
+int pick_rpt(phipm_ctx *c, int64_t n)
+{
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("PHIPM_RPT");
+        env = e ? atoi(e) : 0;
+    }
+    if (env == 2 || env == 4 || env == 8) return env;
+    return n >= (int64_t)SNT * 8 * 2 * c->sm_count ? 8 : 2;
+}
 
 template <class Op, int RPT>
 int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a)
@@ -194,7 +234,7 @@ int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a)
     const size_t smem = spmv_smem_bytes(halo_cap_host(op, TILE_), TILE_, a.nd);
     const void *fn = (const void *)spmv_stream_kernel<Op, RPT>;
     const int grid = std::min(stream_grid(c, fn, smem, ntiles), c->pstride);
-    spmv_stream_kernel<Op, RPT><<<grid, SNT, smem, c->stream>>>(op, a, make_work(c));
+    launch_k(c, spmv_stream_kernel<Op, RPT>, grid, SNT, smem, op, a, make_work(c));
     return PHIPM_OK;
 }
 
@@ -203,10 +243,15 @@ int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
 {
     SpmvArgs a = a0;
     if (a.ldx == 0) a.ldx = c->ldv;
+    if (std::is_same<Op, CsrOp>::value) a.xcol = -1;          // CSR gathers x: no on-chip tile
     ProfRec r;
-    const double bytes = bytes_op + 8.0 * (double)op.n * (a.nd + a.nz);
-    prof_begin(c, r, PC_SPMV, bytes);
-    if (pick_rpt(c, op.n) == 8) launch_spmv_t<Op, 8>(c, op, a);
+    // algorithmic bytes: operator pass + streamed dot columns (the x column is reused on chip) + z
+    const int nd_mem = a.nd - (a.xcol >= 0 && a.xcol < a.nd ? 1 : 0);
+    const double bytes = bytes_op + 8.0 * (double)op.n * (nd_mem + a.nz);
+    prof_begin(c, r, PC_SPMV, bytes, a.nd);
+    const int rpt = pick_rpt(c, op.n);
+    if (rpt == 8) launch_spmv_t<Op, 8>(c, op, a);
+    else if (rpt == 4) launch_spmv_t<Op, 4>(c, op, a);
     else launch_spmv_t<Op, 2>(c, op, a);
     prof_end(c, r);
     c->acc.launches++;
@@ -218,15 +263,20 @@ int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a, int cls)
 {
     ProfRec r;
     const double bytes = 8.0 * (double)n * (a.nc + a.ne + 1 + (a.a0h != 0.0 ? 1 : 0));
-    prof_begin(c, r, cls, bytes);
-    if (pick_rpt(c, n) == 8) {
+    prof_begin(c, r, cls, bytes, a.nc + a.ne + (a.a0h != 0.0 ? 1 : 0));
+    const int rpt = pick_rpt(c, n);
+    if (rpt == 8) {
         const int64_t ntiles = (n + SNT * 8 - 1) / (SNT * 8);
         const int grid = std::min(stream_grid(c, (const void *)axpy_stream_kernel<8>, 0, ntiles), c->pstride);
-        axpy_stream_kernel<8><<<grid, SNT, 0, c->stream>>>(n, a, make_work(c));
+        launch_k(c, axpy_stream_kernel<8>, grid, SNT, 0, n, a, make_work(c));
+    } else if (rpt == 4) {
+        const int64_t ntiles = (n + SNT * 4 - 1) / (SNT * 4);
+        const int grid = std::min(stream_grid(c, (const void *)axpy_stream_kernel<4>, 0, ntiles), c->pstride);
+        launch_k(c, axpy_stream_kernel<4>, grid, SNT, 0, n, a, make_work(c));
     } else {
         const int64_t ntiles = (n + SNT * 2 - 1) / (SNT * 2);
         const int grid = std::min(stream_grid(c, (const void *)axpy_stream_kernel<2>, 0, ntiles), c->pstride);
-        axpy_stream_kernel<2><<<grid, SNT, 0, c->stream>>>(n, a, make_work(c));
+        launch_k(c, axpy_stream_kernel<2>, grid, SNT, 0, n, a, make_work(c));
     }
     prof_end(c, r);
     c->acc.launches++;
@@ -243,8 +293,8 @@ int launch_expm(phipm_ctx *c, ExpmArgs &a, int K)
     a.res = c->res_d;
     a.seq = ++c->seq;
     ProfRec r;
-    prof_begin(c, r, PC_EXPM, 0.0);
-    expm_kernel<<<1, EXPM_NT, a.use_smem ? need : 0, c->stream>>>(a);
+    prof_begin(c, r, PC_EXPM, 0.0, K);
+    launch_k(c, expm_kernel, 1, EXPM_NT, a.use_smem ? need : 0, a);
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -270,6 +320,7 @@ SpmvArgs spmv0()
 {
     SpmvArgs a;
     memset(&a, 0, sizeof(a));
+    a.xcol = -1;
     return a;
 }
 
@@ -435,6 +486,7 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
             }
             s.d0 = j;
             s.nd = 1;
+            s.xcol = 0;                      // v_j is x
             s.fin = FIN_LANCZOS;
             u.c0 = j;
             u.nc = 1;
@@ -443,6 +495,7 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
             // Alg. 1 (classical Gram-Schmidt form): h = V_j^T w; w -= V_j h
             s.d0 = 0;
             s.nd = j + 1;
+            s.xcol = j;                      // v_j is x
             s.fin = FIN_ARNOLDI;
             u.c0 = 0;
             u.nc = j + 1;
@@ -821,7 +874,19 @@ int phipm_get_profile(const phipm_ctx *c, phipm_profile *out)
 
 void phipm_reset_profile(phipm_ctx *c)
 {
-    if (c) c->acc = phipm_profile{};
+    if (!c) return;
+    c->acc = phipm_profile{};
+    c->tracebuf.clear();
+    c->ntrace = 0;
+}
+
+int phipm_get_trace(const phipm_ctx *c, phipm_trace_rec *out, int max, int *count)
+{
+    if (!c || !count || (max > 0 && !out)) return PHIPM_EINVAL;
+    const int nrec = (int)std::min<size_t>(c->tracebuf.size(), (size_t)std::max(max, 0));
+    for (int i = 0; i < nrec; i++) out[i] = c->tracebuf[i];
+    *count = (int)c->ntrace;
+    return PHIPM_OK;
 }
 
 void phipm_destroy(phipm_ctx *c)
@@ -852,6 +917,10 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     c->p_max = p_max;
     c->ldv = (n_max + 31) / 32 * 32;
     c->kmax = m_max + p_max + 1;
+    {
+        const char *e = getenv("PHIPM_PDL");
+        c->pdl = !(e && e[0] == '0');
+    }
     cudaError_t e = cudaGetDevice(&c->dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->dev);
     if (e != cudaSuccess) {
@@ -864,6 +933,9 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         const int mx = 200 * 1024;
         cudaFuncSetAttribute(spmv_stream_kernel<StencilOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<StencilOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<StencilOp, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -926,6 +998,7 @@ int phipm_solve_stencil(phipm_ctx *c, double t, const phipm_stencil *S, int p, c
     rc = check_common(c, t, op.n, p, u, w, o);
     if (rc) return rc;
     c->prof = o.profile != 0;
+    c->trace = o.profile >= 2;
     return solve_impl(c, t, op, 16.0 * (double)op.n, stencil_nnz(op), stencil_infnorm(op), p, u, o, w, stats);
 }
 
@@ -940,6 +1013,7 @@ int phipm_solve_csr(phipm_ctx *c, double t, const phipm_csr *A, int p, const dou
     rc = check_common(c, t, op.n, p, u, w, o);
     if (rc) return rc;
     c->prof = o.profile != 0;
+    c->trace = o.profile >= 2;
     // ||A||_inf (a1 setup, once per call)
     const int grid = grid_for(c, (op.n + NT - 1) / NT, c->occ_axpy);
     ProfRec r;

@@ -151,46 +151,6 @@ __device__ __forceinline__ void halo_plan_ident(int64_t r0, int rows, int64_t ld
     seg_range(r0, r0 + rows, ldx, h.start[0], h.bytes[0]);
 }
 
-// x value at global index g from segment k of the halo buffer
-__device__ __forceinline__ double hx(const double *hb, const HaloPlan &h, int k, int64_t g)
-{
-    return hb[h.off[k] + (int)(g - h.start[k])];
-}
-
-// Per-tile neighbour base pointers into the halo buffer: x[g] of direction d is ptr_d[g]
-// (resolved once per tile, so the row loop does no dynamic indexing of the plan).
-struct HaloPtrs {
-    const double *c, *ym, *yp, *zm, *zp;
-};
-
-__device__ __forceinline__ HaloPtrs halo_ptrs(const double *hb, const HaloPlan &h)
-{
-    HaloPtrs P;
-    P.c = hb + h.off[0] - h.start[0];
-    P.ym = hb + h.off[h.ylo] - h.start[h.ylo];
-    P.yp = hb + h.off[h.yhi] - h.start[h.yhi];
-    P.zm = hb + h.off[h.zlo] - h.start[h.zlo];
-    P.zp = hb + h.off[h.zhi] - h.start[h.zhi];
-    return P;
-}
-
-// Stencil row r with grid coordinates (i, j, k), summed in ascending column order (z-, y-, x-,
-// centre, x+, y+, z+) with separately rounded products (no FMA): the same operations in the same
-// order as a sequential CSR row sum, so y is bit-exact with it.
-__device__ __forceinline__ double stencil_row(const StencilOp &S, const HaloPtrs &P, int64_t r, int i, int jj, int kk)
-{
-    const int64_t pl = (int64_t)S.nx * S.ny;
-    double s = 0.0;
-    if (S.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(S.c[5], P.zm[r - pl]));
-    if (S.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(S.c[3], P.ym[r - S.nx]));
-    if (i > 0) s = __dadd_rn(s, __dmul_rn(S.c[1], P.c[r - 1]));
-    s = __dadd_rn(s, __dmul_rn(S.c[0], P.c[r]));
-    if (i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[2], P.c[r + 1]));
-    if (S.dim >= 2 && jj < S.ny - 1) s = __dadd_rn(s, __dmul_rn(S.c[4], P.yp[r + S.nx]));
-    if (S.dim >= 3 && kk < S.nz - 1) s = __dadd_rn(s, __dmul_rn(S.c[6], P.zp[r + pl]));
-    return s;
-}
-
 // grid coordinates of row r (two 32-bit divisions)
 __device__ __forceinline__ void grid_ijk(const StencilOp &S, int64_t r, int &i, int &jj, int &kk)
 {
@@ -204,15 +164,6 @@ __device__ __forceinline__ void grid_ijk(const StencilOp &S, int64_t r, int &i, 
         const unsigned q2 = q / uny;
         jj = (int)(q - q2 * uny);
         kk = (int)q2;
-    }
-}
-
-// the row after (i, j, k)
-__device__ __forceinline__ void grid_next(const StencilOp &S, int &i, int &jj, int &kk)
-{
-    if (++i == S.nx) {
-        i = 0;
-        if (++jj == S.ny) { jj = 0; kk++; }
     }
 }
 
@@ -276,6 +227,7 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
     constexpr bool HALO = !std::is_same<Op, CsrOp>::value;
     extern __shared__ __align__(128) double sm[];
     __shared__ uint64_t hbar;
+    __shared__ int hofs[2][5];                            // tile-relative halo offsets per parity
     __shared__ double bsum[MAXD + 2];
     __shared__ double wsum[SNW];
     __shared__ int s_exit;
@@ -290,11 +242,15 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
         if constexpr (IS_ST) halo_plan(op, TILE_, r0, rows, a.ldx, h);
         else halo_plan_ident(r0, rows, a.ldx, h);
     };
-    auto issue_halo = [&](int64_t tl) {
+    auto issue_halo = [&](int64_t tl, uint32_t par) {
         const int64_t hr0 = tl * TILE_;
         const int hrows = (int)min((int64_t)TILE_, n - hr0);
         HaloPlan h;
         plan(hr0, hrows, h);
+        // x[hr0 + q + d] of direction k is hbuf[hofs[k] + q + d] (centre, y-, y+, z-, z+)
+        const int seg[5] = {0, h.ylo, h.yhi, h.zlo, h.zhi};
+#pragma unroll
+        for (int k = 0; k < 5; k++) hofs[par][k] = h.off[seg[k]] - (int)(h.start[seg[k]] - hr0);
         uint32_t tot = 0;
         for (int k = 0; k < h.nseg; k++) tot += h.bytes[k];
         const uint64_t pol = policy_evict_last();
@@ -303,13 +259,14 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
         for (int k = 0; k < h.nseg; k++)
             if (h.bytes[k]) tma_load_1d(hbuf + h.off[k], a.x + h.start[k], h.bytes[k], &hbar, pol);
     };
+    pdl_wait();
     if (tid == 0) {
         s_exit = a.check_brk ? (wk.st->brk >= 0) : 0;
         if constexpr (HALO) {
             if (!s_exit) {
                 mbar_init(&hbar, 1);
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-                if ((int64_t)blockIdx.x < ntiles) issue_halo(blockIdx.x);
+                if ((int64_t)blockIdx.x < ntiles) issue_halo(blockIdx.x, 0);
             }
         }
     }
@@ -326,32 +283,66 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t r0 = tile * TILE_;
         const int rows = (int)min((int64_t)TILE_, n - r0);
-        double2 y[NP];
-        // ---- phase 1: raw (A x) rows into registers
+        double2 y[NP], xr[NP];
+        // ---- phase 1: raw (A x) rows into registers (and x itself, for a dot with v_j = x)
         if constexpr (HALO) {
             mbar_wait(&hbar, ht & 1);
+            const int *ho = hofs[ht & 1];
             ht++;
-            HaloPlan h;
-            plan(r0, rows, h);
-            const HaloPtrs P = halo_ptrs(hbuf, h);
+            const double *pc = hbuf + ho[0];
+            if constexpr (IS_ST) {
+                const double *pym = hbuf + ho[1], *pyp = hbuf + ho[2], *pzm = hbuf + ho[3], *pzp = hbuf + ho[4];
+                const int nx = op.nx, ny = op.ny, pl = op.nx * op.ny;
+                const double c0 = op.c[0], cxm = op.c[1], cxp = op.c[2], cym = op.c[3], cyp = op.c[4],
+                             czm = op.c[5], czp = op.c[6];
+                // grid coordinates of this thread's first row, then stepped (no per-row division)
+                int i, jj, kk;
+                grid_ijk(op, r0 + 2 * tid, i, jj, kk);
+                auto step = [&](int d) {
+                    if (op.dim == 1) { i += d; return; }
+                    const int dj = d / nx;               // d is a compile-time constant below
+                    i += d - dj * nx;
+                    jj += dj;
+                    if (i >= nx) { i -= nx; jj++; }
+                    while (jj >= ny) { jj -= ny; kk++; }
+                };
+                // ascending column order, separately rounded products (bit-exact with a sequential
+                // CSR row sum)
+                auto row = [&](int q) -> double {
+                    double s = 0.0;
+                    if (op.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(czm, pzm[q - pl]));
+                    if (op.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(cym, pym[q - nx]));
+                    if (i > 0) s = __dadd_rn(s, __dmul_rn(cxm, pc[q - 1]));
+                    s = __dadd_rn(s, __dmul_rn(c0, pc[q]));
+                    if (i < nx - 1) s = __dadd_rn(s, __dmul_rn(cxp, pc[q + 1]));
+                    if (op.dim >= 2 && jj < ny - 1) s = __dadd_rn(s, __dmul_rn(cyp, pyp[q + nx]));
+                    if (op.dim >= 3 && kk < op.nz - 1) s = __dadd_rn(s, __dmul_rn(czp, pzp[q + pl]));
+                    return s;
+                };
 #pragma unroll
-            for (int p = 0; p < NP; p++) {
-                const int q = 2 * tid + 2 * SNT * p;
-                const int64_t r = r0 + q;
-                if constexpr (IS_ST) {
-                    int i, jj, kk;
-                    grid_ijk(op, r, i, jj, kk);
-                    y[p].x = q < rows ? stencil_row(op, P, r, i, jj, kk) : 0.0;
-                    grid_next(op, i, jj, kk);
-                    y[p].y = q + 1 < rows ? stencil_row(op, P, r + 1, i, jj, kk) : 0.0;
-                } else {
-                    y[p].x = q < rows ? P.c[r] : 0.0;
-                    y[p].y = q + 1 < rows ? P.c[r + 1] : 0.0;
+                for (int p = 0; p < NP; p++) {
+                    const int q = 2 * tid + 2 * SNT * p;
+                    xr[p].x = q < rows ? pc[q] : 0.0;
+                    xr[p].y = q + 1 < rows ? pc[q + 1] : 0.0;
+                    y[p].x = q < rows ? row(q) : 0.0;
+                    step(1);
+                    y[p].y = q + 1 < rows ? row(q + 1) : 0.0;
+                    if (p + 1 < NP) step(2 * SNT - 1);
+                }
+            } else {
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    const int q = 2 * tid + 2 * SNT * p;
+                    xr[p].x = q < rows ? pc[q] : 0.0;
+                    xr[p].y = q + 1 < rows ? pc[q + 1] : 0.0;
+                    y[p] = xr[p];
                 }
             }
             __syncthreads();                               // halo consumed
-            if (tid == 0 && tile + gridDim.x < ntiles) issue_halo(tile + gridDim.x);
+            if (tid == 0 && tile + gridDim.x < ntiles) issue_halo(tile + gridDim.x, ht & 1);
         } else {
+#pragma unroll
+            for (int p = 0; p < NP; p++) xr[p] = make_double2(0.0, 0.0);
             csr_tile(op, a.x, r0, rows, hbuf);
             __syncthreads();
 #pragma unroll
@@ -382,17 +373,31 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
             ysq = fma(y[p].x, y[p].x, ysq);
             ysq = fma(y[p].y, y[p].y, ysq);
         }
-        // ---- phase 3: d_k = V_k^T y over the tile, CU columns in flight
+        // ---- phase 3: d_k = V_k^T y over the tile, CU columns in flight; the column equal to x
+        //      (if any) is not re-read: its dot comes from the x tile values kept in registers
+        int xc = -1;
+        if constexpr (HALO) xc = a.xcol;
+        if (xc >= 0 && xc < a.nd) {
+            double d = 0.0;
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                d = fma(xr[p].x, y[p].x, d);
+                d = fma(xr[p].y, y[p].y, d);
+            }
+            d = warp_sum(d);
+            if (lane == 0) lacc[xc * SNW + warp] += d;
+        }
         for (int k0 = 0; k0 < a.nd; k0 += CU) {
             double2 v[CU][NP];
 #pragma unroll
             for (int u = 0; u < CU; u++) {
                 const int k = k0 + u;
+                const bool ld = k < a.nd && k != xc;
                 const double *vc = a.V + (int64_t)(a.d0 + (k < a.nd ? k : k0)) * a.ldv + r0;
 #pragma unroll
                 for (int p = 0; p < NP; p++) {
                     const int q = 2 * tid + 2 * SNT * p;
-                    v[u][p] = (k < a.nd && q < rows) ? ld_stream2(vc + q) : make_double2(0.0, 0.0);
+                    v[u][p] = (ld && q < rows) ? ld_stream2(vc + q) : make_double2(0.0, 0.0);
                 }
             }
 #pragma unroll
@@ -404,7 +409,7 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
                     d = fma(v[u][p].y, y[p].y, d);
                 }
                 d = warp_sum(d);
-                if (lane == 0 && k0 + u < a.nd) lacc[(k0 + u) * SNW + warp] += d;
+                if (lane == 0 && k0 + u < a.nd && k0 + u != xc) lacc[(k0 + u) * SNW + warp] += d;
             }
         }
     }
@@ -448,6 +453,7 @@ __global__ void __launch_bounds__(SNT, 4) axpy_stream_kernel(int64_t n, AxpyArgs
     __shared__ double wsum[SNW];
     __shared__ int s_exit;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_wait();
     if (tid == 0) s_exit = a.check_brk ? (wk.st->brk >= 0) : 0;
     const int nbase = (a.a0h != 0.0) ? 1 : 0;
     const int nitem = nbase + a.nc + a.ne;

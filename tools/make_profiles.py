@@ -1,0 +1,97 @@
+"""Turn raw gpurun_out/ ncu outputs into the committed summaries under profiles/<round>/."""
+import collections
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+from ncu_summary import summary  # noqa: E402
+
+rnd = sys.argv[1] if len(sys.argv) > 1 else "round1"
+src = os.path.join(ROOT, "gpurun_out")
+dst = os.path.join(ROOT, "profiles", rnd)
+os.makedirs(dst, exist_ok=True)
+
+
+def read_ncu_csv(path):
+    rows = list(csv.reader(open(path)))
+    hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hdr]
+    return [dict(zip(h, r)) for r in rows[hdr + 1:] if len(r) == len(h)]
+
+
+def short(k):
+    for key in ("spmv_stream_kernel", "axpy_stream_kernel", "expm_kernel", "maxabs_kernel", "csr_infnorm_kernel"):
+        if key in k:
+            return key + ("<Stencil>" if "StencilOp" in k else "<Csr>" if "CsrOp" in k else "")
+    return k[:40]
+
+
+# 1) launch list of the bench command: per-kernel share of the step
+p = os.path.join(src, "pf_launches_c3.csv")
+if os.path.exists(p):
+    d = read_ncu_csv(p)
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in d:
+        if r["Metric Name"] == "gpu__time_duration.sum":
+            k = short(r["Kernel Name"])
+            agg[k][0] += 1
+            unit = r["Metric Unit"]
+            agg[k][1] += float(r["Metric Value"].replace(",", "")) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0,
+                                                                       "usecond": 1.0, "ms": 1e3}.get(unit, 1e-3)
+    tot = sum(v[1] for v in agg.values())
+    with open(os.path.join(dst, "launches_c3_summary.txt"), "w") as f:
+        f.write("ncu --metrics gpu__time_duration.sum --clock-control none  python bench.py --steps 2 --warmup 1 "
+                "--no-cpu-baseline  (config c3; cold-cache, serialised launches: compare SHARES)\n")
+        f.write(f"{'kernel':34s} {'launches':>8s} {'total us':>10s} {'share':>7s}\n")
+        for k, (n, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
+            f.write(f"{k:34s} {n:8d} {us:10.1f} {100 * us / tot:6.1f}%\n")
+    os.system(f"cp {p} {dst}/launches_c3.csv")
+
+# 2) DRAM traffic per launch of each kernel class (one solve of c3)
+p = os.path.join(src, "pf_dram_c3.csv")
+traffic = {}
+if os.path.exists(p):
+    d = read_ncu_csv(p)
+    per = collections.defaultdict(dict)
+    for r in d:
+        unit = r["Metric Unit"]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "ns": 1e-3, "usecond": 1,
+                 "us": 1, "msecond": 1e3, "ms": 1e3}.get(unit, 1)
+        v = float(r["Metric Value"].replace(",", ""))
+        per[r["ID"]][r["Metric Name"]] = v * scale
+        per[r["ID"]]["kernel"] = short(r["Kernel Name"])
+    cls = collections.defaultdict(list)
+    for rid, m in per.items():
+        cls[m["kernel"]].append(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0))
+    with open(os.path.join(dst, "dram_traffic_c3.txt"), "w") as f:
+        f.write("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum  (one c3 solve)\n")
+        for k, v in cls.items():
+            f.write(f"{k:34s} launches {len(v):4d}  avg DRAM bytes/launch {sum(v) / len(v) / 1e6:9.2f} MB\n")
+    sp = cls.get("spmv_stream_kernel<Stencil>")
+    if sp:
+        traffic["c3"] = {"kernel_class": "spmv_dot", "dram_bytes_per_launch": sum(sp) / len(sp),
+                         "launches": len(sp), "source": f"profiles/{rnd}/dram_traffic_c3.txt"}
+    os.system(f"cp {p} {dst}/dram_c3.csv")
+if traffic:
+    json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+
+# 3) --set full summaries of the top kernels
+for name in ("pf_full_c3_spmv", "pf_full_c3_axpy"):
+    p = os.path.join(src, name + ".ncu-rep")
+    if os.path.exists(p):
+        with open(os.path.join(dst, name.replace("pf_", "") + ".txt"), "w") as f:
+            for d in summary(p):
+                f.write(f"=== {d['kernel']}\n")
+                for k, v in d.items():
+                    if k not in ("kernel", "stalls"):
+                        f.write(f"  {k:62s} {v[0]:>16s} {v[1]}\n")
+                f.write(f"  warp stall samples (%): {d['stalls']}\n")
+for extra in ("stream_roof.txt", "q_trace.txt", "rpt.txt"):
+    p = os.path.join(src, extra)
+    if os.path.exists(p):
+        os.system(f"cp {p} {dst}/")
+print("wrote", dst)

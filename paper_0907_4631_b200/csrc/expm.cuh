@@ -16,7 +16,7 @@
 
 namespace phipm {
 
-constexpr int EXPM_NT = 1024;
+constexpr int EXPM_NT = 512;
 constexpr int EXPM_KMAX = 136;         // padded K bound (m_max + p_max + 1 <= 128 + 8)
 
 // result block read by the host controller (mapped pinned memory)
@@ -50,43 +50,60 @@ struct ExpmArgs {
     double *phip_out, *phip1_out;   // mode 2
     AttemptResult *res;
     int seq;
+    long long *clk;    // optional phase timestamps (PHIPM_EXPM_CLOCKS)
 };
+
+// leading dimension of the K x K work matrices: Kp rounded up to 4 (mod 16) doubles, so the
+// 32 lanes of a DMMA fragment load (8 rows x 4 columns, or 4 rows x 8 columns) touch every bank
+// pair at most twice (256 B = 2 wavefronts, the minimum)
+__host__ __device__ inline int expm_ld(int Kp) { return Kp + ((4 - Kp % 16) + 16) % 16; }
 
 // C = A B for Kp x Kp column-major matrices (Kp a multiple of 8, zero padded) on the fp64 tensor
 // cores: each warp computes 8x8 output tiles with mma.sync.m8n8k4.f64 (SASS DMMA).
 // Fragment layouts (PTX ISA, m8n8k4 .f64): A row-major 8x4, a0 = A[lane/4][lane%4];
 // B column-major 4x8, b0 = B[lane%4][lane/4]; C 8x8, c_i = C[lane/4][2 (lane%4) + i].
-__device__ __forceinline__ void cta_matmul(int Kp, const double *A, const double *B, double *C)
+__device__ __forceinline__ void cta_matmul(int Kp, int ld, const double *A, const double *B, double *C)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int nt = Kp >> 3;
     const int ar = lane >> 2, ac = lane & 3;
     for (int t = warp; t < nt * nt; t += nw) {
         const int ti = t % nt, tj = t / nt;
-        const double *Ap = A + (ti * 8 + ar) + (size_t)ac * Kp;
-        const double *Bp = B + ac + (size_t)(tj * 8 + ar) * Kp;
-        double c0 = 0.0, c1 = 0.0;
-        for (int kk = 0; kk < Kp; kk += 4) {
-            const double a = Ap[(size_t)kk * Kp];
-            const double b = Bp[kk];
+        const double *Ap = A + (ti * 8 + ar) + (size_t)ac * ld;
+        const double *Bp = B + ac + (size_t)(tj * 8 + ar) * ld;
+        // two independent accumulator chains (even / odd k blocks), next fragments prefetched
+        double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+        double a0 = Ap[0], b0 = Bp[0], a1 = Ap[(size_t)4 * ld], b1 = Bp[4];
+        for (int kk = 0; kk < Kp; kk += 8) {
+            double na0 = 0.0, nb0 = 0.0, na1 = 0.0, nb1 = 0.0;
+            if (kk + 8 < Kp) {
+                na0 = Ap[(size_t)(kk + 8) * ld];
+                nb0 = Bp[kk + 8];
+                na1 = Ap[(size_t)(kk + 12) * ld];
+                nb1 = Bp[kk + 12];
+            }
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                          : "+d"(c0), "+d"(c1)
-                         : "d"(a), "d"(b));
+                         : "d"(a0), "d"(b0));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(d0), "+d"(d1)
+                         : "d"(a1), "d"(b1));
+            a0 = na0; b0 = nb0; a1 = na1; b1 = nb1;
         }
         const int row = ti * 8 + ar, col = tj * 8 + 2 * ac;
-        C[row + (size_t)col * Kp] = c0;
-        C[row + (size_t)(col + 1) * Kp] = c1;
+        C[row + (size_t)col * ld] = c0 + d0;
+        C[row + (size_t)(col + 1) * ld] = c1 + d1;
     }
     __syncthreads();
 }
 
-__device__ __forceinline__ double block_max_colsum(int K, const double *A, double *sred)
+__device__ __forceinline__ double block_max_colsum(int K, int ld, const double *A, double *sred)
 {
     // ||A||_1 = max_j sum_i |a_ij|
     double m = 0.0;
     for (int jc = threadIdx.x; jc < K; jc += blockDim.x) {
         double s = 0.0;
-        for (int i = 0; i < K; i++) s += fabs(A[i + (size_t)jc * K]);
+        for (int i = 0; i < K; i++) s += fabs(A[i + (size_t)jc * ld]);
         m = fmax(m, s);
     }
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -108,14 +125,16 @@ __device__ __forceinline__ void pade13(double *c)
 
 // exp(M0) -> returned pointer (one of the buffers); M0..M5 are Kp x Kp buffers (Kp = K rounded
 // up to a multiple of 8, padding zero: exp(blockdiag(A, 0)) = blockdiag(exp A, I)).  status 0/5/6
-__device__ double *cta_expm(int K, int Kp, double *M0, double *M1, double *M2, double *M3, double *M4, double *M5,
-                            double *sred, int *s_int, double *fcol, int *status)
+__device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, double *M2, double *M3, double *M4, double *M5,
+                            double *sred, int *s_int, double *fcol, int *status, long long *clk)
 {
-    const int KK = Kp * Kp, t = threadIdx.x;
+#define EXPM_CLK(i) \
+    if (clk && threadIdx.x == 0) clk[i] = clock64();
+    const int KK = ld * Kp, t = threadIdx.x;         // whole buffers (padding rows are never read)
     double c[14];
     pade13(c);
     // scaling: s = ceil_+(log2(||A||_1 / 5.37)) (theta_13 = 5.37 as printed, R26)
-    const double nrm = block_max_colsum(Kp, M0, sred);
+    const double nrm = block_max_colsum(Kp, ld, M0, sred);
     int s = 0;
     if (nrm > 0.0) {
         const double l = ceil(log2(nrm / 5.37));
@@ -125,25 +144,26 @@ __device__ double *cta_expm(int K, int Kp, double *M0, double *M1, double *M2, d
     const double sc = ldexp(1.0, -s);
     for (int e = t; e < KK; e += blockDim.x) M0[e] *= sc;
     __syncthreads();
-    cta_matmul(Kp, M0, M0, M1);            // A2
-    cta_matmul(Kp, M1, M1, M2);            // A4
-    cta_matmul(Kp, M2, M1, M3);            // A6
+    cta_matmul(Kp, ld, M0, M0, M1);            // A2
+    cta_matmul(Kp, ld, M1, M1, M2);            // A4
+    cta_matmul(Kp, ld, M2, M1, M3);            // A6
+    EXPM_CLK(2)
     // U = A [A6 (c13 A6 + c11 A4 + c9 A2) + c7 A6 + c5 A4 + c3 A2 + c1 I]
     for (int e = t; e < KK; e += blockDim.x) M4[e] = c[13] * M3[e] + c[11] * M2[e] + c[9] * M1[e];
     __syncthreads();
-    cta_matmul(Kp, M3, M4, M5);
+    cta_matmul(Kp, ld, M3, M4, M5);
     for (int e = t; e < KK; e += blockDim.x) M5[e] = M5[e] + c[7] * M3[e] + c[5] * M2[e] + c[3] * M1[e];
     __syncthreads();
-    for (int i = t; i < Kp; i += blockDim.x) M5[i * (Kp + 1)] += c[1];
+    for (int i = t; i < Kp; i += blockDim.x) M5[i * (ld + 1)] += c[1];
     __syncthreads();
-    cta_matmul(Kp, M0, M5, M4);            // U in M4
+    cta_matmul(Kp, ld, M0, M5, M4);            // U in M4
     // V = A6 (c12 A6 + c10 A4 + c8 A2) + c6 A6 + c4 A4 + c2 A2 + c0 I
     for (int e = t; e < KK; e += blockDim.x) M5[e] = c[12] * M3[e] + c[10] * M2[e] + c[8] * M1[e];
     __syncthreads();
-    cta_matmul(Kp, M3, M5, M0);            // A no longer needed
+    cta_matmul(Kp, ld, M3, M5, M0);            // A no longer needed
     for (int e = t; e < KK; e += blockDim.x) M0[e] = M0[e] + c[6] * M3[e] + c[4] * M2[e] + c[2] * M1[e];
     __syncthreads();
-    for (int i = t; i < Kp; i += blockDim.x) M0[i * (Kp + 1)] += c[0];   // V
+    for (int i = t; i < Kp; i += blockDim.x) M0[i * (ld + 1)] += c[0];   // V
     __syncthreads();
     // P = V + U (M1), Q = V - U (M2)
     for (int e = t; e < KK; e += blockDim.x) {
@@ -152,81 +172,129 @@ __device__ double *cta_expm(int K, int Kp, double *M0, double *M1, double *M2, d
         M2[e] = v - u;
     }
     __syncthreads();
-    // Gauss-Jordan with partial pivoting: Q X = P, X overwrites P (3 barriers per column).  Only the
-    // leading K x K block is eliminated: the padding block of Q and P is the identity and stays so.
+    EXPM_CLK(3)
+    // Gauss-Jordan with partial pivoting: Q X = P, implicit pivoting (no row interchanges; the
+    // pivot row of column c is prow[c]), ONE barrier per column: warp 0 updates the next pivot
+    // column first, searches its pivot among the unused rows and prepares the multipliers while
+    // the other warps eliminate the current column from the rest of [Q | P].
     double *Q = M2, *P = M1;
-    const int rr = t % K, cstart = t / K, cstep = (int)blockDim.x / K;   // fixed row per thread
+    int *prow = s_int + 8, *used = s_int + 8 + EXPM_KMAX;
+    double *fb = fcol;                                    // 2 x EXPM_KMAX multipliers
+    __shared__ int s_pr[2], s_bad;
+    __shared__ double s_rq[EXPM_KMAX];
+    const int warp = t >> 5, lane = t & 31;
+    for (int r = t; r < K; r += blockDim.x) used[r] = 0;
+    if (t == 0) s_bad = 0;
+    __syncthreads();
+    auto lookahead = [&](int c, int b) {                 // warp 0; column c of Q is final
+        double best = -1.0;
+        int bi = K;
+        for (int r = lane; r < K; r += 32)
+            if (!used[r]) {
+                const double a = fabs(Q[r + (size_t)c * ld]);
+                if (a > best) { best = a; bi = r; }
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (!(best >= 1e-300) || bi >= K) {
+            if (lane == 0) s_bad = 1;
+            return;
+        }
+        const double rp = 1.0 / Q[bi + (size_t)c * ld];
+        for (int r = lane; r < K; r += 32) fb[b * EXPM_KMAX + r] = (r == bi) ? 0.0 : Q[r + (size_t)c * ld] * rp;
+        __syncwarp();
+        if (lane == 0) {
+            s_pr[b] = bi;
+            used[bi] = 1;
+            prow[c] = bi;
+        }
+        __syncwarp();
+    };
+    if (warp == 0) lookahead(0, 0);
+    __syncthreads();
+    const int t2 = t - 32, n2 = (int)blockDim.x - 32;
+    const int er = t2 % K, eg = t2 / K, neg = n2 / K;     // elimination warps: fixed row, column group
     for (int col = 0; col < K; col++) {
-        if (t < 32) {
-            // pivot search on column col, and a snapshot of the column (pre-swap) in fcol
-            double best = -1.0;
-            int bi = col;
-            for (int r = t; r < K; r += 32) {
-                const double q = Q[r + (size_t)col * Kp];
-                fcol[r] = q;
-                if (r >= col && fabs(q) > best) { best = fabs(q); bi = r; }
+        if (s_bad) { *status = 6; return P; }
+        const int b = col & 1;
+        const int pr = s_pr[b];
+        const double *f = fb + b * EXPM_KMAX;
+        if (warp == 0) {
+            if (col + 1 < K) {
+                const int j = col + 1;
+                const double pv = Q[pr + (size_t)j * ld];
+                for (int r = lane; r < K; r += 32)
+                    if (r != pr) Q[r + (size_t)j * ld] -= f[r] * pv;
+                __syncwarp();
+                lookahead(col + 1, b ^ 1);
             }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-            }
-            if (t == 0) {
-                s_int[0] = bi;
-                s_int[1] = (best >= 1e-300) ? 0 : 1;
-            }
-        }
-        __syncthreads();
-        if (s_int[1]) { *status = 6; return P; }
-        const int pr = s_int[0];
-        const double rpiv = 1.0 / fcol[pr];
-        // swap rows col <-> pr; scale the new pivot row (Q right of the pivot, all of P) by 1/piv
-        for (int jc = t; jc < 2 * K; jc += blockDim.x) {
-            double *Mx = (jc < K) ? Q : P;
-            const int cc = (jc < K) ? jc : jc - K;
-            const double top = Mx[pr + (size_t)cc * Kp];
-            if (pr != col) Mx[pr + (size_t)cc * Kp] = Mx[col + (size_t)cc * Kp];
-            Mx[col + (size_t)cc * Kp] = (jc < K && cc <= col) ? top : top * rpiv;
-        }
-        __syncthreads();
-        // eliminate column col from every other row with the scaled pivot row
-        if (cstart < cstep) {
-            const double f = (rr == col) ? 0.0 : (rr == pr ? fcol[col] : fcol[rr]);
-            if (f != 0.0) {
-                const int ncolq = K - col - 1;
-                const int width = ncolq + K;
-                for (int cc = cstart; cc < width; cc += cstep) {
-                    if (cc < ncolq) {
-                        const int qc = col + 1 + cc;
-                        Q[rr + (size_t)qc * Kp] -= f * Q[col + (size_t)qc * Kp];
-                    } else {
-                        const int pc = cc - ncolq;
-                        P[rr + (size_t)pc * Kp] -= f * P[col + (size_t)pc * Kp];
+        } else if (eg < neg && er != pr) {
+            const double fr = f[er];
+            if (fr != 0.0) {
+                // columns: Q col+2 .. K-1 (nq of them), then P 0 .. K-1
+                const int nq = max(K - col - 2, 0);
+                const int total = nq + K;
+                for (int j0 = eg; j0 < total; j0 += 4 * neg) {
+                    double *dst[4];
+                    double pv[4], xv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int jj = j0 + u * neg;
+                        double *M = (jj < nq) ? Q : P;
+                        const int j = (jj < nq) ? col + 2 + jj : jj - nq;
+                        dst[u] = (jj < total) ? M + er + (size_t)j * ld : nullptr;
+                        pv[u] = (jj < total) ? M[pr + (size_t)j * ld] : 0.0;
+                        xv[u] = (jj < total) ? *dst[u] : 0.0;
                     }
+#pragma unroll
+                    for (int u = 0; u < 4; u++)
+                        if (dst[u]) *dst[u] = xv[u] - fr * pv[u];
                 }
             }
         }
         __syncthreads();
     }
+    // X[c, :] = P[prow(c), :] / Q[prow(c), c]   (the pivot row's diagonal value is final)
+    for (int c = t; c < K; c += blockDim.x) s_rq[c] = 1.0 / Q[prow[c] + (size_t)c * ld];
+    __syncthreads();
+    double *Xo = M3;
+    for (int e = t; e < K * K; e += blockDim.x) {
+        const int c = e % K, j = e / K;
+        Xo[c + (size_t)j * ld] = P[prow[c] + (size_t)j * ld] * s_rq[c];
+    }
+    // padding block of X: identity (Q and P were identity there)
+    for (int e = t; e < Kp * Kp; e += blockDim.x) {
+        const int c = e % Kp, j = e / Kp;
+        if (c >= K || j >= K) Xo[c + (size_t)j * ld] = (c == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    P = Xo;
+    EXPM_CLK(4)
     // squaring
-    double *X = P, *T = M3;
+    double *X = P, *T = M4;
     for (int q = 0; q < s; q++) {
-        cta_matmul(Kp, X, X, T);
+        cta_matmul(Kp, ld, X, X, T);
         double *tmp = X;
         X = T;
         T = tmp;
     }
+    EXPM_CLK(5)
     return X;
 }
 
+template <bool SMEM>
 __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
 {
     extern __shared__ double esm[];
     __shared__ double sred[EXPM_NT / 32];
-    __shared__ int s_int[4];
+    __shared__ int s_int[8 + 2 * EXPM_KMAX];
     __shared__ int s_mu;
     const int t = threadIdx.x;
     pdl_wait();
+    if (a.clk && t == 0) a.clk[0] = clock64();
     int mu, K;
     if (a.mode == 1) {
         mu = 0;
@@ -262,30 +330,31 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
         return;
     }
     const int Kp = (K + 7) & ~7;                         // padded to the DMMA tile size
-    const size_t KK = (size_t)Kp * Kp;
-    double *base = a.use_smem ? esm : a.scratch;
+    const int ld = expm_ld(Kp);                          // bank-conflict-free DMMA fragment loads
+    const size_t KK = (size_t)ld * Kp;
+    double *base = SMEM ? esm : a.scratch;          // compile-time address space (LDS/STS when SMEM)
     double *M0 = base, *M1 = base + KK, *M2 = base + 2 * KK, *M3 = base + 3 * KK, *M4 = base + 4 * KK,
            *M5 = base + 5 * KK;
-    __shared__ double fcol[EXPM_KMAX];
+    __shared__ double fcol[2 * EXPM_KMAX];
     // build the matrix to exponentiate (zero padded to Kp)
     for (size_t e = t; e < KK; e += blockDim.x) M0[e] = 0.0;
     __syncthreads();
     if (a.mode == 1) {
         for (size_t e = t; e < (size_t)K * K; e += blockDim.x) {
             const int i = (int)(e % K), jc = (int)(e / K);
-            M0[i + (size_t)jc * Kp] = a.Ain[e];
+            M0[i + (size_t)jc * ld] = a.Ain[e];
         }
     } else {
         // tau H_mu into M0, |H_mu| into M1 (scratch for the unscaled 1-norm)
         for (size_t e = t; e < (size_t)mu * mu; e += blockDim.x) {
             const int i = (int)(e % mu), jc = (int)(e / mu);
             const double hv = (!a.tridiag || (i - jc <= 1 && jc - i <= 1)) ? a.H[i + (size_t)jc * a.ldh] : 0.0;
-            M0[i + (size_t)jc * Kp] = a.tau * hv;
-            M1[i + (size_t)jc * Kp] = fabs(hv);
+            M0[i + (size_t)jc * ld] = a.tau * hv;
+            M1[i + (size_t)jc * ld] = fabs(hv);
         }
         if (t == 0) {
-            M0[0 + (size_t)mu * Kp] = 1.0;
-            for (int i = 1; i <= a.p; i++) M0[(mu + i - 1) + (size_t)(mu + i) * Kp] = 1.0;
+            M0[0 + (size_t)mu * ld] = 1.0;
+            for (int i = 1; i <= a.p; i++) M0[(mu + i - 1) + (size_t)(mu + i) * ld] = 1.0;
         }
     }
     __syncthreads();
@@ -295,7 +364,7 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
         double m = 0.0;
         for (int jc = t; jc < mu; jc += blockDim.x) {
             double s = 0.0;
-            for (int i = 0; i < mu; i++) s += M1[i + (size_t)jc * Kp];
+            for (int i = 0; i < mu; i++) s += M1[i + (size_t)jc * ld];
             m = fmax(m, s);
         }
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -307,15 +376,16 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
     __shared__ int s_status;
     if (t == 0) s_status = 0;
     __syncthreads();
+    if (a.clk && t == 0) a.clk[1] = clock64();
     int status = 0;
-    double *E = cta_expm(K, Kp, M0, M1, M2, M3, M4, M5, sred, s_int, fcol, &status);
+    double *E = cta_expm(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, s_int, fcol, &status, a.clk);
     if (t == 0 && status) s_status = status;
     __syncthreads();
     status = s_status;
     if (a.mode == 1) {
         for (size_t e = t; e < (size_t)K * K; e += blockDim.x) {
             const int i = (int)(e % K), jc = (int)(e / K);
-            a.Eout[e] = E[i + (size_t)jc * Kp];
+            a.Eout[e] = E[i + (size_t)jc * ld];
         }
         if (t == 0) {
             AttemptResult r{};
@@ -328,8 +398,8 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
     const int cp1 = mu + a.p;
     if (a.mode == 2) {
         for (int i = t; i < mu; i += blockDim.x) {
-            a.phip_out[i] = E[i + (size_t)cp * Kp];
-            a.phip1_out[i] = E[i + (size_t)cp1 * Kp];
+            a.phip_out[i] = E[i + (size_t)cp * ld];
+            a.phip1_out[i] = E[i + (size_t)cp1 * ld];
         }
         if (t == 0) {
             AttemptResult r{};
@@ -344,13 +414,13 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
     const double h = corr ? a.H[mu + (size_t)(mu - 1) * a.ldh] : 0.0;
     double taup = 1.0;
     for (int j = 0; j < a.p; j++) taup *= a.tau;
-    const double phl = E[(mu - 1) + (size_t)cp1 * Kp];
-    for (int i = t; i < mu; i += blockDim.x) a.comb[i] = taup * beta * E[i + (size_t)cp * Kp] * a.sigma[i];
+    const double phl = E[(mu - 1) + (size_t)cp1 * ld];
+    for (int i = t; i < mu; i += blockDim.x) a.comb[i] = taup * beta * E[i + (size_t)cp * ld] * a.sigma[i];
     __shared__ int s_fin;
     if (t == 0) s_fin = 1;
     __syncthreads();
     for (int i = t; i < mu; i += blockDim.x)
-        if (!isfinite(E[i + (size_t)cp * Kp])) s_fin = 0;
+        if (!isfinite(E[i + (size_t)cp * ld])) s_fin = 0;
     __syncthreads();
     if (t == 0) {
         a.comb[mu] = corr ? taup * beta * a.tau * h * phl * a.sigma[mu] : 0.0;
@@ -370,6 +440,7 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
         r.status = status ? status : ((s_fin && isfinite(eps) && isfinite(phl)) ? 0 : 5);
         r.seq = a.seq;
         *a.res = r;
+        if (a.clk) a.clk[6] = clock64();
     }
 }
 

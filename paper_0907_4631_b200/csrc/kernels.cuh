@@ -75,6 +75,13 @@ struct CsrOp {
     const int32_t *__restrict__ col;
     const double *__restrict__ val;
     int glog;              // log2(lanes per row)
+    // x-window mode (tile rows' columns within a band): per-tile [tlo, thi] column range for tiles
+    // of `wtile` rows; tiles whose range fits `wcap` doubles gather x from shared memory
+    const int32_t *__restrict__ tlo;
+    const int32_t *__restrict__ thi;
+    int wtile, wcap;
+    int ell;               // > 0: every row has exactly `ell` entries (row_ptr[r] = ell r), ell % 4 == 0,
+                           // ell <= 128: vectorised fast path (4 entries per lane)
 };
 
 struct SpmvArgs {
@@ -94,6 +101,7 @@ struct SpmvArgs {
     int ynorm;                   // also reduce ||y||^2
     int fin, j;
     int check_brk;               // exit early if a breakdown happened earlier in this step
+    int64_t rpc;                 // rows per CTA (balanced contiguous ranges; multiple of 32)
 };
 
 struct AxpyArgs {
@@ -115,6 +123,7 @@ struct AxpyArgs {
     int check_brk;
     double bthr;                 // breakdown threshold n eps ||A||_inf (FIN_NORM)
     int lanczos;                 // FIN_NORM: also store the symmetric entry and the coupling
+    int64_t rpc;                 // rows per CTA (balanced contiguous ranges; multiple of 32)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -330,6 +339,40 @@ __global__ void __launch_bounds__(NT) csr_infnorm_kernel(CsrOp A, Work wk)
     }
     __syncthreads();
     if (tid == 0) *wk.counter = 0u;
+}
+
+// Uniform row length check: flag[0] stays 0 iff row_ptr[r] == L r for all r <= n.
+__global__ void csr_uniform_check_kernel(int64_t n, const int32_t *__restrict__ rp, int L, int *flag)
+{
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= n; r += (int64_t)gridDim.x * blockDim.x)
+        if ((int64_t)rp[r] != (int64_t)L * r) atomicOr(flag, 1);
+}
+
+// Column range [min, max] of every tile of `tile` rows (one warp per tile); empty tile -> [0, -1].
+__global__ void csr_tile_range_kernel(int64_t n, const int32_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                      int tile, int32_t *tlo, int32_t *thi)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t ntiles = (n + tile - 1) / tile;
+    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < ntiles;
+         t += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const int64_t r0 = t * tile, r1 = min(n, r0 + tile);
+        const int e0 = rp[r0], e1 = rp[r1];
+        int lo = 0x7fffffff, hi = -1;
+        for (int e = e0 + lane; e < e1; e += 32) {
+            const int c = col[e];
+            lo = min(lo, c);
+            hi = max(hi, c);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            tlo[t] = hi >= 0 ? lo : 0;
+            thi[t] = hi;
+        }
+    }
 }
 
 // CSR of a stencil: every row independently, with the closed-form row pointer

@@ -52,7 +52,10 @@ struct phipm_ctx {
     double *part = nullptr, *comb = nullptr, *combd = nullptr, *scratch = nullptr, *raw = nullptr;
     unsigned *counter = nullptr;
     DevState *st = nullptr;
+    int32_t *tlo = nullptr, *thi = nullptr;                  // CSR per-tile column ranges
+    int64_t ntile_cap = 0;
     AttemptResult *res_h = nullptr, *res_d = nullptr;
+    long long *expm_clk_h = nullptr, *expm_clk_d = nullptr;   // PHIPM_EXPM_CLOCKS=1 debug timestamps
     double *raw_h = nullptr;                 // pinned staging for small readbacks
     // host-buffer solve staging
     double *hu = nullptr, *hw = nullptr;
@@ -213,6 +216,11 @@ int halo_cap_host(const Op &, int tile) { return tile; }
 template <>
 int halo_cap_host<StencilOp>(const StencilOp &S, int tile) { return halo_capacity(S.dim, S.nx, tile); }
 
+template <class Op>
+int csr_wcap(const Op &, int) { return 0; }
+template <>
+int csr_wcap<CsrOp>(const CsrOp &A, int tile) { return A.wtile == tile ? A.wcap : 0; }
+
 // rows per thread: 8 (TILE 2048) when there are enough tiles to fill the GPU, else 2 (TILE 512);
 // PHIPM_RPT=2|4|8 overrides (tuning experiments)
 int pick_rpt(phipm_ctx *c, int64_t n)
@@ -226,14 +234,26 @@ int pick_rpt(phipm_ctx *c, int64_t n)
     return n >= (int64_t)SNT * 8 * 2 * c->sm_count ? 8 : 2;
 }
 
+// balanced partition: every resident CTA slot gets one contiguous range of rpc rows (a multiple
+// of 32), processed in tiles of <= 256*RPT rows; small problems use fewer CTAs
+void balance(phipm_ctx *c, int64_t n, int slots, int &grid, int64_t &rpc)
+{
+    int64_t g = std::min<int64_t>(slots, (n + 31) / 32);
+    g = std::max<int64_t>(1, std::min<int64_t>(g, c->pstride));
+    rpc = ((n + g - 1) / g + 31) / 32 * 32;
+    grid = (int)((n + rpc - 1) / rpc);
+}
+
 template <class Op, int RPT>
-int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a)
+int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a0)
 {
     constexpr int TILE_ = SNT * RPT;
-    const int64_t ntiles = (op.n + TILE_ - 1) / TILE_;
-    const size_t smem = spmv_smem_bytes(halo_cap_host(op, TILE_), TILE_, a.nd);
+    SpmvArgs a = a0;
+    const size_t smem = spmv_smem_bytes(halo_cap_host(op, TILE_), TILE_, a.nd, csr_wcap(op, TILE_));
     const void *fn = (const void *)spmv_stream_kernel<Op, RPT>;
-    const int grid = std::min(stream_grid(c, fn, smem, ntiles), c->pstride);
+    const int slots = stream_grid(c, fn, smem, (int64_t)1 << 40);
+    int grid;
+    balance(c, op.n, slots, grid, a.rpc);
     launch_k(c, spmv_stream_kernel<Op, RPT>, grid, SNT, smem, op, a, make_work(c));
     return PHIPM_OK;
 }
@@ -249,7 +269,8 @@ int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
     const int nd_mem = a.nd - (a.xcol >= 0 && a.xcol < a.nd ? 1 : 0);
     const double bytes = bytes_op + 8.0 * (double)op.n * (nd_mem + a.nz);
     prof_begin(c, r, PC_SPMV, bytes, a.nd);
-    const int rpt = pick_rpt(c, op.n);
+    int rpt = pick_rpt(c, op.n);
+    if (csr_wcap(op, SNT * 8) > 0) rpt = 8;                  // CSR x-window mode uses 2048-row tiles
     if (rpt == 8) launch_spmv_t<Op, 8>(c, op, a);
     else if (rpt == 4) launch_spmv_t<Op, 4>(c, op, a);
     else launch_spmv_t<Op, 2>(c, op, a);
@@ -259,25 +280,25 @@ int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
     return PHIPM_OK;
 }
 
+template <int RPT>
+void launch_axpy_t(phipm_ctx *c, int64_t n, const AxpyArgs &a0)
+{
+    AxpyArgs a = a0;
+    const int slots = stream_grid(c, (const void *)axpy_stream_kernel<RPT>, 0, (int64_t)1 << 40);
+    int grid;
+    balance(c, n, slots, grid, a.rpc);
+    launch_k(c, axpy_stream_kernel<RPT>, grid, SNT, 0, n, a, make_work(c));
+}
+
 int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a, int cls)
 {
     ProfRec r;
     const double bytes = 8.0 * (double)n * (a.nc + a.ne + 1 + (a.a0h != 0.0 ? 1 : 0));
     prof_begin(c, r, cls, bytes, a.nc + a.ne + (a.a0h != 0.0 ? 1 : 0));
     const int rpt = pick_rpt(c, n);
-    if (rpt == 8) {
-        const int64_t ntiles = (n + SNT * 8 - 1) / (SNT * 8);
-        const int grid = std::min(stream_grid(c, (const void *)axpy_stream_kernel<8>, 0, ntiles), c->pstride);
-        launch_k(c, axpy_stream_kernel<8>, grid, SNT, 0, n, a, make_work(c));
-    } else if (rpt == 4) {
-        const int64_t ntiles = (n + SNT * 4 - 1) / (SNT * 4);
-        const int grid = std::min(stream_grid(c, (const void *)axpy_stream_kernel<4>, 0, ntiles), c->pstride);
-        launch_k(c, axpy_stream_kernel<4>, grid, SNT, 0, n, a, make_work(c));
-    } else {
-        const int64_t ntiles = (n + SNT * 2 - 1) / (SNT * 2);
-        const int grid = std::min(stream_grid(c, (const void *)axpy_stream_kernel<2>, 0, ntiles), c->pstride);
-        launch_k(c, axpy_stream_kernel<2>, grid, SNT, 0, n, a, make_work(c));
-    }
+    if (rpt == 8) launch_axpy_t<8>(c, n, a);
+    else if (rpt == 4) launch_axpy_t<4>(c, n, a);
+    else launch_axpy_t<2>(c, n, a);
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -287,14 +308,16 @@ int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a, int cls)
 int launch_expm(phipm_ctx *c, ExpmArgs &a, int K)
 {
     const int Kp = (K + 7) & ~7;
-    const size_t need = (size_t)6 * Kp * Kp * sizeof(double);
+    const size_t need = (size_t)6 * expm_ld(Kp) * Kp * sizeof(double);
     a.use_smem = need <= c->expm_smem_limit;
     a.scratch = c->scratch;
     a.res = c->res_d;
     a.seq = ++c->seq;
+    a.clk = c->expm_clk_d;
     ProfRec r;
     prof_begin(c, r, PC_EXPM, 0.0, K);
-    launch_k(c, expm_kernel, 1, EXPM_NT, a.use_smem ? need : 0, a);
+    if (a.use_smem) launch_k(c, expm_kernel<true>, 1, EXPM_NT, need, a);
+    else launch_k(c, expm_kernel<false>, 1, EXPM_NT, 0, a);
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -794,6 +817,61 @@ int make_csr(phipm_ctx *c, const phipm_csr *A, CsrOp &op)
     int glog = 0;
     while (glog < 5 && (double)(1 << (glog + 1)) <= mean) glog++;
     op.glog = glog;
+    op.tlo = op.thi = nullptr;
+    op.wtile = op.wcap = 0;
+    op.ell = 0;
+    return PHIPM_OK;
+}
+
+// CSR x-window mode: per-tile column ranges for 2048-row tiles (one pass over col); tiles whose
+// range fits CSR_WCAP doubles gather x from shared memory (stream.cuh)
+constexpr int CSR_WCAP = 10496;                             // 82 KB: band +-4096 around 2048 rows
+
+// Uniform row length (ELL-like CSR) detection: one pass over row_ptr; enables csr_tile_ell.
+int detect_csr_ell(phipm_ctx *c, CsrOp &op, int64_t nnz)
+{
+    op.ell = 0;
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("PHIPM_CSR_ELL");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (!env || op.n <= 0 || nnz % op.n) return PHIPM_OK;
+    const int64_t L = nnz / op.n;
+    if (L < 4 || L > 128 || (L % 4) || ((L / 4) & (L / 4 - 1))) return PHIPM_OK;   // L/4 a power of two
+    if (((uintptr_t)op.val & 15) || ((uintptr_t)op.col & 15)) return PHIPM_OK;
+    int *flag = reinterpret_cast<int *>(c->counter + 2);
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+    const int grid = (int)std::min<int64_t>((op.n + 256) / 256, (int64_t)c->sm_count * 8);
+    csr_uniform_check_kernel<<<grid, 256, 0, c->stream>>>(op.n, op.rp, (int)L, flag);
+    c->acc.launches++;
+    CK(cudaGetLastError());
+    int h = 1;
+    CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (h == 0) op.ell = (int)L;
+    return PHIPM_OK;
+}
+
+int enable_csr_window(phipm_ctx *c, CsrOp &op)
+{
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("PHIPM_CSR_WINDOW");
+        env = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (!env) return PHIPM_OK;                              // default off (measured slower, round 1)
+    const int tile = SNT * 8;
+    const int64_t ntiles = (op.n + tile - 1) / tile;
+    if (ntiles > c->ntile_cap || op.n < (int64_t)tile) return PHIPM_OK;   // small problems: global gathers
+    const int grid = (int)std::min<int64_t>((ntiles + 7) / 8, (int64_t)c->sm_count * 8);
+    csr_tile_range_kernel<<<grid, 256, 0, c->stream>>>(op.n, op.rp, op.col, tile, c->tlo, c->thi);
+    c->acc.launches++;
+    CK(cudaGetLastError());
+    op.tlo = c->tlo;
+    op.thi = c->thi;
+    op.wtile = tile;
+    op.wcap = CSR_WCAP;
     return PHIPM_OK;
 }
 
@@ -897,9 +975,10 @@ void phipm_destroy(phipm_ctx *c)
     for (auto e : c->pool) cudaEventDestroy(e);
     cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
     cudaFree(c->part); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
-    cudaFree(c->counter); cudaFree(c->st);
+    cudaFree(c->counter); cudaFree(c->st); cudaFree(c->tlo); cudaFree(c->thi);
     cudaFree(c->hu); cudaFree(c->hw); cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
     if (c->res_h) cudaFreeHost(c->res_h);
+    if (c->expm_clk_h) cudaFreeHost(c->expm_clk_h);
     if (c->raw_h) cudaFreeHost(c->raw_h);
     delete c;
 }
@@ -948,8 +1027,12 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     }
     int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
-    c->expm_smem_limit = (size_t)std::max(0, smem_optin - 4096);
-    cudaFuncSetAttribute(expm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->expm_smem_limit);
+    {
+        cudaFuncAttributes fa;
+        cudaFuncGetAttributes(&fa, expm_kernel<true>);
+        c->expm_smem_limit = (size_t)std::max(0, smem_optin - (int)fa.sharedSizeBytes - 1024);
+        cudaFuncSetAttribute(expm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->expm_smem_limit);
+    }
     cudaGetLastError();
 
     const size_t vbytes = (size_t)c->ldv * sizeof(double);
@@ -969,13 +1052,24 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     A((void **)&c->part, sizeof(double) * (size_t)c->pstride * (MAXD + 2));
     A((void **)&c->comb, sizeof(double) * (MAXD + 1));
     A((void **)&c->combd, sizeof(double) * (P_MAX_ABS + 1));
-    A((void **)&c->scratch, sizeof(double) * 6 * (size_t)((c->kmax + 7) & ~7) * ((c->kmax + 7) & ~7));
+    {
+        const int kp = (c->kmax + 7) & ~7;
+        A((void **)&c->scratch, sizeof(double) * 6 * (size_t)expm_ld(kp) * kp);
+    }
     A((void **)&c->raw, sizeof(double) * (MAXD + 2));
     A((void **)&c->counter, sizeof(unsigned) * 4);
     A((void **)&c->st, sizeof(DevState));
+    c->ntile_cap = n_max / 512 + 2;
+    A((void **)&c->tlo, sizeof(int32_t) * c->ntile_cap);
+    A((void **)&c->thi, sizeof(int32_t) * c->ntile_cap);
     if (ok && cudaHostAlloc((void **)&c->res_h, sizeof(AttemptResult), cudaHostAllocMapped) != cudaSuccess) ok = false;
     if (ok && cudaHostGetDevicePointer((void **)&c->res_d, c->res_h, 0) != cudaSuccess) ok = false;
     if (ok && cudaHostAlloc((void **)&c->raw_h, sizeof(double) * (MAXD + 2), cudaHostAllocDefault) != cudaSuccess) ok = false;
+    if (ok && getenv("PHIPM_EXPM_CLOCKS")) {
+        if (cudaHostAlloc((void **)&c->expm_clk_h, sizeof(long long) * 8, cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer((void **)&c->expm_clk_d, c->expm_clk_h, 0) != cudaSuccess)
+            ok = false;
+    }
     if (ok && cudaDeviceSynchronize() != cudaSuccess) ok = false;
     if (!ok) {
         cudaGetLastError();
@@ -1026,6 +1120,10 @@ int phipm_solve_csr(phipm_ctx *c, double t, const phipm_csr *A, int p, const dou
     rc = sync(c);
     if (rc) return rc;
     const double normA = c->raw_h[0];
+    rc = detect_csr_ell(c, op, A->nnz);
+    if (rc) return rc;
+    rc = enable_csr_window(c, op);
+    if (rc) return rc;
     return solve_impl(c, t, op, csr_bytes(op, A->nnz), A->nnz, normA, p, u, o, w, stats);
 }
 
@@ -1136,8 +1234,14 @@ int phipm_spmv_csr(phipm_ctx *c, const phipm_csr *A, const double *x, double *y)
     CsrOp op;
     int rc = make_csr(c, A, op);
     if (rc) return rc;
+    if (op.n > c->n_max) return set_err(c, PHIPM_EINVAL, "n > n_max");
+    CK(cudaMemcpyAsync(c->Y, x, op.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    rc = detect_csr_ell(c, op, A->nnz);
+    if (rc) return rc;
+    rc = enable_csr_window(c, op);
+    if (rc) return rc;
     SpmvArgs s = spmv0();
-    s.x = x;
+    s.x = c->Y;
     s.y = y;
     rc = launch_spmv(c, op, s, csr_bytes(op, A->nnz));
     if (rc) return rc;
@@ -1239,6 +1343,11 @@ int phipm_phi_pair(phipm_ctx *c, int mu, const double *H, int ldh, double tau, i
     if (rc) return rc;
     rc = sync(c);
     if (rc) return rc;
+    if (c->expm_clk_h) {
+        const long long *k = c->expm_clk_h;
+        fprintf(stderr, "expm K=%d cycles: build %lld | A2,A4,A6 %lld | U,V %lld | GJ %lld | squarings %lld | tail %lld\n",
+                mu + p + 1, k[1] - k[0], k[2] - k[1], k[3] - k[2], k[4] - k[3], k[5] - k[4], k[6] - k[5]);
+    }
     AttemptResult R;
     memcpy(&R, (const void *)c->res_h, sizeof(R));
     if (normH1) *normH1 = R.normH1;
@@ -1301,6 +1410,10 @@ int phipm_krylov_csr(phipm_ctx *c, const phipm_csr *A, const double *v, int m, c
     if (rc) return rc;
     double normA = 0.0;
     rc = phipm_inf_norm_csr(c, A, &normA);
+    if (rc) return rc;
+    rc = detect_csr_ell(c, op, A->nnz);
+    if (rc) return rc;
+    rc = enable_csr_window(c, op);
     if (rc) return rc;
     return krylov_export(c, op, csr_bytes(op, A->nnz), normA, v, m, opts, V, H, k, brk, beta);
 }

@@ -169,7 +169,12 @@ __device__ __forceinline__ void grid_ijk(const StencilOp &S, int64_t r, int &i, 
 
 // CSR rows of a tile into ys: G = 2^glog lanes per row, U row groups in flight per lane (memory-
 // level parallelism for the col -> x gather chain), rows longer than G strided, shuffle reduce.
-__device__ __forceinline__ void csr_tile(const CsrOp &A, const double *__restrict__ x, int64_t r0, int rows, double *ys)
+// WIN: x is gathered from the tile's x window in shared memory (xs[c - xs0]) instead of global
+// memory; `wait` is called once, after the first batch of row_ptr/col/val loads is in flight and
+// before the first x access (it waits for the window's TMA copy).
+template <bool WIN, class Wait>
+__device__ __forceinline__ void csr_tile(const CsrOp &A, const double *__restrict__ x, const double *xs, int64_t xs0,
+                                         int64_t r0, int rows, double *ys, Wait wait)
 {
     constexpr int U = 8;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -177,6 +182,11 @@ __device__ __forceinline__ void csr_tile(const CsrOp &A, const double *__restric
     const int rpw = 32 >> A.glog;
     const int sub = lane >> A.glog, li = lane & (G - 1);
     const int stride = SNW * rpw;
+    bool waited = false;
+    auto X = [&](int c) -> double {
+        if constexpr (WIN) return xs[c - xs0];
+        else return __ldg(x + c);
+    };
     for (int base = warp * rpw; base < rows; base += stride * U) {
         int q[U], e[U], e1[U];
         double acc[U];
@@ -195,24 +205,85 @@ __device__ __forceinline__ void csr_tile(const CsrOp &A, const double *__restric
             cc[u] = ok ? __ldg(A.col + e[u]) : 0;
             vv[u] = ok ? ldg_stream(A.val + e[u]) : 0.0;
         }
+        if (!waited) {
+            wait();
+            waited = true;
+        }
 #pragma unroll
-        for (int u = 0; u < U; u++) acc[u] = (e[u] < e1[u]) ? vv[u] * __ldg(x + cc[u]) : 0.0;
+        for (int u = 0; u < U; u++) acc[u] = (e[u] < e1[u]) ? vv[u] * X(cc[u]) : 0.0;
 #pragma unroll
         for (int u = 0; u < U; u++)
-            for (int f = e[u] + G; f < e1[u]; f += G) acc[u] = fma(ldg_stream(A.val + f), __ldg(x + __ldg(A.col + f)), acc[u]);
+            for (int f = e[u] + G; f < e1[u]; f += G) acc[u] = fma(ldg_stream(A.val + f), X(__ldg(A.col + f)), acc[u]);
 #pragma unroll
         for (int u = 0; u < U; u++) {
             for (int o = G >> 1; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
             if (q[u] < rows && li == 0) ys[q[u]] = acc[u];
         }
     }
+    if (!waited) wait();
 }
 
-// dynamic shared memory of spmv_stream (bytes): halo (or ys for CSR), then per-warp dot partials
-__host__ __device__ inline size_t spmv_smem_bytes(int halo_cap, int tile, int nd)
+// Uniform-row-length CSR (row_ptr[r] = L r, L % 4 == 0): G = L/4 lanes per row, each lane loads 4
+// consecutive entries with 16-B vector loads (val: 2 x double2, col: int4), U row groups in flight
+// per lane; products summed in entry order per lane, then a log2(G)-level shuffle tree.
+template <bool WIN>
+__device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__restrict__ x, const double *xs, int64_t xs0,
+                                             int64_t r0, int rows, double *ys)
+{
+    constexpr int U = 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int G = A.ell >> 2;                 // lanes per row (power of two, <= 32)
+    const int rpw = 32 / G;
+    const int sub = lane / G, li = lane - sub * G;
+    const int stride = SNW * rpw;
+    auto X = [&](int c) -> double {
+        if constexpr (WIN) return xs[c - xs0];
+        else return __ldg(x + c);
+    };
+    for (int base = warp * rpw; base < rows; base += stride * U) {
+        double2 va[U], vb[U];
+        int4 cc[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int q = base + u * stride + sub;
+            if (q < rows) {
+                const int64_t e = (r0 + q) * (int64_t)A.ell + 4 * li;
+                va[u] = ldg_stream2(A.val + e);
+                vb[u] = ldg_stream2(A.val + e + 2);
+                cc[u] = __ldg(reinterpret_cast<const int4 *>(A.col + e));
+            } else {
+                va[u] = vb[u] = make_double2(0.0, 0.0);
+                cc[u] = make_int4(0, 0, 0, 0);
+            }
+        }
+        double acc[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int q = base + u * stride + sub;
+            double t = 0.0;
+            if (q < rows) {
+                t = va[u].x * X(cc[u].x);
+                t = fma(va[u].y, X(cc[u].y), t);
+                t = fma(vb[u].x, X(cc[u].z), t);
+                t = fma(vb[u].y, X(cc[u].w), t);
+            }
+            acc[u] = t;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            for (int o = G >> 1; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+            const int q = base + u * stride + sub;
+            if (q < rows && li == 0) ys[q] = acc[u];
+        }
+    }
+}
+
+// dynamic shared memory of spmv_stream (bytes): halo (or ys for CSR), CSR x window, per-warp dot
+// partials
+__host__ __device__ inline size_t spmv_smem_bytes(int halo_cap, int tile, int nd, int wcap = 0)
 {
     const int h = halo_cap > 0 ? halo_cap : tile;
-    return ((size_t)((h + 15) & ~15) + (size_t)nd * SNW) * sizeof(double);
+    return ((size_t)((h + 15) & ~15) + (size_t)((wcap + 15) & ~15) + (size_t)nd * SNW) * sizeof(double);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -233,18 +304,40 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
     __shared__ int s_exit;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t n = op.n;
-    const int64_t ntiles = (n + TILE_ - 1) / TILE_;
+    const int64_t cs = (int64_t)blockIdx.x * a.rpc, ce = min(n, cs + a.rpc);   // this CTA's rows
     int hcap = TILE_;
     if constexpr (IS_ST) hcap = halo_capacity(op.dim, op.nx, TILE_);
+    int wcap = 0;
+    if constexpr (!HALO) wcap = (op.wtile == TILE_) ? op.wcap : 0;
     double *hbuf = sm;                                    // halo (stencil/ident) or ys (CSR)
-    double *lacc = sm + ((hcap + 15) & ~15);
+    double *xwin = sm + ((hcap + 15) & ~15);             // CSR x window (wcap doubles)
+    double *lacc = xwin + ((wcap + 15) & ~15);
+    __shared__ int64_t s_wstart[2];
+    // CSR: TMA the x window of tile tl (its [tlo, thi] column range) if it fits
+    auto issue_window = [&](int64_t wr0, int wrows, uint32_t par) {
+        if constexpr (!HALO) {
+            // union of the column ranges of the global wtile-row tiles covering [wr0, wr0 + wrows)
+            int lo = 0x7fffffff, hi = -1;
+            for (int64_t tl = wr0 / op.wtile; tl <= (wr0 + wrows - 1) / op.wtile; tl++) {
+                if (op.thi[tl] >= 0) {
+                    lo = min(lo, op.tlo[tl]);
+                    hi = max(hi, op.thi[tl]);
+                }
+            }
+            int64_t st = 0;
+            uint32_t by = 0;
+            if (hi >= lo && hi - lo + 4 <= wcap) seg_range(lo, (int64_t)hi + 1, a.ldx, st, by);
+            s_wstart[par] = by ? st : -1;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_expect_tx(&hbar, by);
+            if (by) tma_load_1d(xwin, a.x + st, by, &hbar, policy_evict_last());
+        }
+    };
     auto plan = [&](int64_t r0, int rows, HaloPlan &h) {
         if constexpr (IS_ST) halo_plan(op, TILE_, r0, rows, a.ldx, h);
         else halo_plan_ident(r0, rows, a.ldx, h);
     };
-    auto issue_halo = [&](int64_t tl, uint32_t par) {
-        const int64_t hr0 = tl * TILE_;
-        const int hrows = (int)min((int64_t)TILE_, n - hr0);
+    auto issue_halo = [&](int64_t hr0, int hrows, uint32_t par) {
         HaloPlan h;
         plan(hr0, hrows, h);
         // x[hr0 + q + d] of direction k is hbuf[hofs[k] + q + d] (centre, y-, y+, z-, z+)
@@ -266,7 +359,13 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
             if (!s_exit) {
                 mbar_init(&hbar, 1);
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-                if ((int64_t)blockIdx.x < ntiles) issue_halo(blockIdx.x, 0);
+                if (cs < ce) issue_halo(cs, (int)min((int64_t)TILE_, ce - cs), 0);
+            }
+        } else {
+            if (!s_exit && wcap > 0) {
+                mbar_init(&hbar, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                if (cs < ce) issue_window(cs, (int)min((int64_t)TILE_, ce - cs), 0);
             }
         }
     }
@@ -280,9 +379,9 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
 
     double ysq = 0.0;
     uint32_t ht = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t r0 = tile * TILE_;
-        const int rows = (int)min((int64_t)TILE_, n - r0);
+    for (int64_t r0 = cs; r0 < ce; r0 += TILE_) {
+        const int rows = (int)min((int64_t)TILE_, ce - r0);
+        const int64_t r1 = r0 + TILE_;                     // next tile of this CTA
         double2 y[NP], xr[NP];
         // ---- phase 1: raw (A x) rows into registers (and x itself, for a dot with v_j = x)
         if constexpr (HALO) {
@@ -339,12 +438,29 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
                 }
             }
             __syncthreads();                               // halo consumed
-            if (tid == 0 && tile + gridDim.x < ntiles) issue_halo(tile + gridDim.x, ht & 1);
+            if (tid == 0 && r1 < ce) issue_halo(r1, (int)min((int64_t)TILE_, ce - r1), ht & 1);
         } else {
 #pragma unroll
             for (int p = 0; p < NP; p++) xr[p] = make_double2(0.0, 0.0);
-            csr_tile(op, a.x, r0, rows, hbuf);
-            __syncthreads();
+            if (wcap > 0) {
+                const uint32_t par = ht & 1;
+                ht++;
+                // the window decision is uniform per tile; read it once the copy has landed
+                mbar_wait(&hbar, par);
+                const int64_t ws = s_wstart[par];
+                auto nowait = [] {};
+                if (op.ell) {
+                    if (ws >= 0) csr_tile_ell<true>(op, a.x, xwin, ws, r0, rows, hbuf);
+                    else csr_tile_ell<false>(op, a.x, xwin, 0, r0, rows, hbuf);
+                } else if (ws >= 0) csr_tile<true>(op, a.x, xwin, ws, r0, rows, hbuf, nowait);
+                else csr_tile<false>(op, a.x, xwin, 0, r0, rows, hbuf, nowait);
+                __syncthreads();                           // window consumed, ys complete
+                if (tid == 0 && r1 < ce) issue_window(r1, (int)min((int64_t)TILE_, ce - r1), ht & 1);
+            } else {
+                if (op.ell) csr_tile_ell<false>(op, a.x, xwin, 0, r0, rows, hbuf);
+                else csr_tile<false>(op, a.x, xwin, 0, r0, rows, hbuf, [] {});
+                __syncthreads();
+            }
 #pragma unroll
             for (int p = 0; p < NP; p++) {
                 const int q = 2 * tid + 2 * SNT * p;
@@ -476,11 +592,10 @@ __global__ void __launch_bounds__(SNT, 4) axpy_stream_kernel(int64_t n, AxpyArgs
     }
     __syncthreads();
     if (s_exit) return;
-    const int64_t ntiles = (n + TILE_ - 1) / TILE_;
+    const int64_t cs = (int64_t)blockIdx.x * a.rpc, ce = min(n, cs + a.rpc);   // this CTA's rows
     double nrm = 0.0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t r0 = tile * TILE_;
-        const int rows = (int)min((int64_t)TILE_, n - r0);
+    for (int64_t r0 = cs; r0 < ce; r0 += TILE_) {
+        const int rows = (int)min((int64_t)TILE_, ce - r0);
         double2 acc[NP];
 #pragma unroll
         for (int p = 0; p < NP; p++) acc[p] = make_double2(0.0, 0.0);

@@ -178,3 +178,17 @@ def test_breakdown(ctx, orc):
     Vo, Ho, ko, bo, _ = orc.krylov(Pb.csr, Pb.u[0], 40, symmetric=False)
     assert k <= 40
     assert bo == brk or k == 40
+
+
+@pytest.mark.parametrize("L,n", [(4, 3001), (8, 10_007), (32, 2049), (16, 4096)])
+def test_spmv_csr_uniform_rows(ctx, orc, L, n):
+    # uniform row length: exercises the vectorised (4 entries per lane) fast path
+    rng = np.random.default_rng(L * 7 + n)
+    col = np.sort(np.stack([rng.choice(n, L, replace=False) for _ in range(n)]), axis=1).astype(np.int32).ravel()
+    rp = (np.arange(n + 1, dtype=np.int64) * L).astype(np.int32)
+    val = rng.standard_normal(n * L)
+    x = rng.standard_normal(n)
+    y = ctx.spmv_csr((to_dev(rp), to_dev(col), to_dev(val)), to_dev(x)).cpu().numpy()
+    ref = orc.spmv((rp, col, val), x)
+    absAx = orc.spmv((rp, col, np.abs(val)), np.abs(x))
+    assert np.all(np.abs(y - ref) <= 1e-13 * absAx)

@@ -124,6 +124,8 @@ struct AxpyArgs {
     double bthr;                 // breakdown threshold n eps ||A||_inf (FIN_NORM)
     int lanczos;                 // FIN_NORM: also store the symmetric entry and the coupling
     int64_t rpc;                 // rows per CTA (balanced contiguous ranges; multiple of 32)
+    int rev;                     // stream the V columns in descending order (L2 ping-pong with the
+                                 // ascending dot pass of the SpMV kernel)
 };
 
 // ------------------------------------------------------------------------------------------

@@ -499,6 +499,7 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
         u.j = j;
         u.check_brk = 1;
         u.bthr = bthr;
+        u.rev = 1;
         if (symmetric) {
             // Alg. 2: w = A v_j - t_{j,j-1} v_{j-1}; t_jj = v_j^T w; w -= t_jj v_j
             if (j > 0) {

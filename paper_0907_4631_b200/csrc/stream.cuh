@@ -580,8 +580,9 @@ __global__ void __launch_bounds__(SNT, 4) axpy_stream_kernel(int64_t n, AxpyArgs
             c = a.a0h * (a.a0d ? *a.a0d : 1.0);
             p = a.base;
         } else if (k < nbase + a.nc) {
-            c = a.gsign * a.g[k - nbase];
-            p = a.V + (int64_t)(a.c0 + k - nbase) * a.ldv;
+            const int kc = a.rev ? (a.nc - 1 - (k - nbase)) : (k - nbase);
+            c = a.gsign * a.g[kc];
+            p = a.V + (int64_t)(a.c0 + kc) * a.ldv;
         } else {
             const int i = k - nbase - a.nc;
             c = a.ec[i] * (a.ecd ? a.ecd[i] : 1.0);

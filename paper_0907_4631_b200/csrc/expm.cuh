@@ -234,25 +234,23 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
         } else if (eg < neg && er != pr) {
             const double fr = f[er];
             if (fr != 0.0) {
-                // columns: Q col+2 .. K-1 (nq of them), then P 0 .. K-1
-                const int nq = max(K - col - 2, 0);
-                const int total = nq + K;
-                for (int j0 = eg; j0 < total; j0 += 4 * neg) {
-                    double *dst[4];
-                    double pv[4], xv[4];
-#pragma unroll
-                    for (int u = 0; u < 4; u++) {
-                        const int jj = j0 + u * neg;
-                        double *M = (jj < nq) ? Q : P;
-                        const int j = (jj < nq) ? col + 2 + jj : jj - nq;
-                        dst[u] = (jj < total) ? M + er + (size_t)j * ld : nullptr;
-                        pv[u] = (jj < total) ? M[pr + (size_t)j * ld] : 0.0;
-                        xv[u] = (jj < total) ? *dst[u] : 0.0;
+                // Q columns col+2 .. K-1 and P columns 0 .. K-1 owned by this thread's column group,
+                // four loads in flight before the stores
+                auto rank1 = [&](double *M, int j) {
+                    for (; j + 3 * neg < K; j += 4 * neg) {
+                        const double p0 = M[pr + (size_t)j * ld], p1 = M[pr + (size_t)(j + neg) * ld];
+                        const double p2 = M[pr + (size_t)(j + 2 * neg) * ld], p3 = M[pr + (size_t)(j + 3 * neg) * ld];
+                        const double x0 = M[er + (size_t)j * ld], x1 = M[er + (size_t)(j + neg) * ld];
+                        const double x2 = M[er + (size_t)(j + 2 * neg) * ld], x3 = M[er + (size_t)(j + 3 * neg) * ld];
+                        M[er + (size_t)j * ld] = x0 - fr * p0;
+                        M[er + (size_t)(j + neg) * ld] = x1 - fr * p1;
+                        M[er + (size_t)(j + 2 * neg) * ld] = x2 - fr * p2;
+                        M[er + (size_t)(j + 3 * neg) * ld] = x3 - fr * p3;
                     }
-#pragma unroll
-                    for (int u = 0; u < 4; u++)
-                        if (dst[u]) *dst[u] = xv[u] - fr * pv[u];
-                }
+                    for (; j < K; j += neg) M[er + (size_t)j * ld] -= fr * M[pr + (size_t)j * ld];
+                };
+                rank1(Q, col + 2 + eg);
+                rank1(P, eg);
             }
         }
         __syncthreads();

@@ -18,6 +18,7 @@
 #include "kernels.cuh"
 #include "expm.cuh"
 #include "stream.cuh"
+#include "small.cuh"
 
 using namespace phipm;
 
@@ -474,6 +475,25 @@ template <class Op>
 int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1, double bthr)
 {
     const int64_t n = op.n;
+    if (n <= SMALL_N && k1 > k0) {
+        // small problems: the whole extension in one single-CTA kernel (small.cuh)
+        SmallArgs sa;
+        sa.k0 = k0;
+        sa.k1 = k1;
+        sa.symmetric = symmetric ? 1 : 0;
+        sa.orth = orth;
+        sa.bthr = bthr;
+        double bytes = 0.0;
+        for (int j = k0; j < k1; j++)
+            bytes += bytes_op + 8.0 * (double)n * (symmetric ? 4.0 : 2.0 * j + 3.0);
+        ProfRec r;
+        prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
+        launch_k(c, krylov_small_kernel<Op>, 1, SMALL_NT, (size_t)n * sizeof(double), op, sa, make_work(c));
+        prof_end(c, r);
+        c->acc.launches++;
+        CK(cudaGetLastError());
+        return PHIPM_OK;
+    }
     for (int j = k0; j < k1; j++) {
         double *vj = c->V + (int64_t)j * c->ldv;
         double *vn = c->V + (int64_t)(j + 1) * c->ldv;
@@ -1016,6 +1036,8 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         cudaFuncSetAttribute(spmv_stream_kernel<StencilOp, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(krylov_small_kernel<StencilOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_N * 8);
+        cudaFuncSetAttribute(krylov_small_kernel<CsrOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_N * 8);
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);

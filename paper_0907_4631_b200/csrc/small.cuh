@@ -1,0 +1,173 @@
+// small.cuh — the whole Krylov extension k0 -> k1 (Algorithm 1 in CGS form / Algorithm 2) in ONE
+// single-CTA kernel, for small n (n <= SMALL_N).  At that size every step is latency-bound: two
+// grid-wide kernels per step cost far more in launch and reduction tails than the work itself,
+// while one CTA keeps y in shared memory and V in L2 and synchronises with block barriers only.
+// Arithmetic per step is the same as the streaming kernels (same unnormalised basis, sigma
+// scaling, finalize formulas), and rows are summed in ascending column order.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace phipm {
+
+constexpr int SMALL_N = 8192;
+constexpr int SMALL_NT = 1024;
+
+struct SmallArgs {
+    int k0, k1;          // extend the basis from k0 to k1 columns of H
+    int symmetric;       // Lanczos (Alg. 2) or Arnoldi (Alg. 1, CGS)
+    int orth;            // PHIPM_ORTH_CGS2: second CGS pass per step
+    double bthr;         // breakdown threshold
+};
+
+// (A x)_r, ascending column order with separately rounded products (= sequential CSR row sum)
+__device__ __forceinline__ double row_apply(const StencilOp &S, const double *__restrict__ x, int64_t r)
+{
+    const unsigned ur = (unsigned)r, unx = (unsigned)S.nx;
+    const unsigned q = ur / unx;
+    const int i = (int)(ur - q * unx);
+    int jj = 0, kk = 0;
+    if (S.dim >= 2) {
+        const unsigned uny = (unsigned)S.ny;
+        const unsigned q2 = q / uny;
+        jj = (int)(q - q2 * uny);
+        kk = (int)q2;
+    }
+    const int64_t pl = (int64_t)S.nx * S.ny;
+    double s = 0.0;
+    if (S.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(S.c[5], x[r - pl]));
+    if (S.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(S.c[3], x[r - S.nx]));
+    if (i > 0) s = __dadd_rn(s, __dmul_rn(S.c[1], x[r - 1]));
+    s = __dadd_rn(s, __dmul_rn(S.c[0], x[r]));
+    if (i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[2], x[r + 1]));
+    if (S.dim >= 2 && jj < S.ny - 1) s = __dadd_rn(s, __dmul_rn(S.c[4], x[r + S.nx]));
+    if (S.dim >= 3 && kk < S.nz - 1) s = __dadd_rn(s, __dmul_rn(S.c[6], x[r + pl]));
+    return s;
+}
+
+__device__ __forceinline__ double row_apply(const CsrOp &A, const double *__restrict__ x, int64_t r)
+{
+    double s = 0.0;
+    for (int e = A.rp[r]; e < A.rp[r + 1]; e++) s = __dadd_rn(s, __dmul_rn(A.val[e], x[A.col[e]]));
+    return s;
+}
+
+// block sum of one value per thread (all threads receive it)
+__device__ __forceinline__ double block_sum(double v, double *red)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < nw; w++) t += red[w];
+    return t;
+}
+
+template <class Op>
+__global__ void __launch_bounds__(SMALL_NT) krylov_small_kernel(Op op, SmallArgs a, Work wk)
+{
+    extern __shared__ double ys[];                      // n doubles (dynamic)
+    __shared__ double dres[MAXD + 2];
+    __shared__ double gs[MAXD + 2];
+    __shared__ double red[SMALL_NT / 32];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = SMALL_NT / 32;
+    const int n = (int)op.n;
+    pdl_wait();
+    for (int j = a.k0; j < a.k1; j++) {
+        if (wk.st->brk >= 0) break;                      // uniform: written before the last barrier
+        const double *vj = wk.V + (int64_t)j * wk.ldv;
+        const double sj = wk.sigma[j];
+        const double lz = (a.symmetric && j > 0) ? wk.st->lz : 0.0;
+        const double *vjm = (a.symmetric && j > 0) ? vj - wk.ldv : nullptr;
+        // y = sigma_j A v~_j  [- h_{j,j-1} sigma_{j-1} v~_{j-1}]
+        for (int r = t; r < n; r += SMALL_NT) {
+            double y = sj * row_apply(op, vj, r);
+            if (vjm) y = fma(-lz, vjm[r], y);
+            ys[r] = y;
+        }
+        __syncthreads();
+        // dot products with the basis columns (Arnoldi: 0..j, Lanczos: j), one warp per column
+        const int c0 = a.symmetric ? j : 0;
+        const int nd = j - c0 + 1;
+        for (int kk = warp; kk < nd; kk += nw) {
+            const double *vc = wk.V + (int64_t)(c0 + kk) * wk.ldv;
+            double d0 = 0.0, d1 = 0.0;
+            int r = lane;
+            for (; r + 32 < n; r += 64) {
+                d0 = fma(vc[r], ys[r], d0);
+                d1 = fma(vc[r + 32], ys[r + 32], d1);
+            }
+            if (r < n) d0 = fma(vc[r], ys[r], d0);
+            const double d = warp_sum(d0 + d1);
+            if (lane == 0) dres[kk] = d;
+        }
+        __syncthreads();
+        if (a.symmetric) {
+            if (t == 0) {
+                const double al = wk.sigma[j] * dres[0];
+                wk.H[j + (size_t)j * wk.ldh] = al;
+                gs[0] = al * wk.sigma[j];
+            }
+        } else {
+            for (int k = t; k < nd; k += SMALL_NT) {
+                const double h = wk.sigma[k] * dres[k];
+                wk.H[k + (size_t)j * wk.ldh] = h;
+                gs[k] = h * wk.sigma[k];
+            }
+        }
+        __syncthreads();
+        // v~_{j+1} = y - sum_k g_k v~_k, ||v~_{j+1}||^2
+        double *vn = wk.V + (int64_t)(j + 1) * wk.ldv;
+        double nrm = 0.0;
+        for (int r = t; r < n; r += SMALL_NT) {
+            double v = ys[r];
+#pragma unroll 8
+            for (int k = 0; k < nd; k++) v = fma(-gs[k], wk.V[r + (int64_t)(c0 + k) * wk.ldv], v);
+            vn[r] = v;
+            nrm = fma(v, v, nrm);
+        }
+        double tot = block_sum(nrm, red);
+        if (!a.symmetric && a.orth == 1) {
+            // CGS2: second pass on v~_{j+1}
+            __syncthreads();
+            for (int kk = warp; kk < nd; kk += nw) {
+                const double *vc = wk.V + (int64_t)kk * wk.ldv;
+                double d = 0.0;
+                for (int r = lane; r < n; r += 32) d = fma(vc[r], vn[r], d);
+                d = warp_sum(d);
+                if (lane == 0) dres[kk] = d;
+            }
+            __syncthreads();
+            for (int k = t; k < nd; k += SMALL_NT) {
+                const double c = wk.sigma[k] * dres[k];
+                wk.H[k + (size_t)j * wk.ldh] += c;
+                gs[k] = c * wk.sigma[k];
+            }
+            __syncthreads();
+            nrm = 0.0;
+            for (int r = t; r < n; r += SMALL_NT) {
+                double v = vn[r];
+                for (int k = 0; k < nd; k++) v = fma(-gs[k], wk.V[r + (int64_t)k * wk.ldv], v);
+                vn[r] = v;
+                nrm = fma(v, v, nrm);
+            }
+            tot = block_sum(nrm, red);
+        }
+        if (t == 0) {
+            const double h = sqrt(tot);
+            wk.H[(j + 1) + (size_t)j * wk.ldh] = h;
+            if (a.symmetric) {
+                if (j + 1 < wk.hcols) wk.H[j + (size_t)(j + 1) * wk.ldh] = h;
+                wk.st->lz = h * wk.sigma[j];
+            }
+            wk.sigma[j + 1] = 1.0 / h;
+            if (!isfinite(h)) { wk.st->nonfinite = 1; wk.st->brk = j + 1; }
+            else if (h <= a.bthr) wk.st->brk = j + 1;
+        }
+        __syncthreads();
+    }
+}
+
+} // namespace phipm

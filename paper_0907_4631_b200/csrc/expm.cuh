@@ -1,15 +1,14 @@
 // expm.cuh — single-CTA kernel for the small dense part of a phipm attempt (Sec. 3.1-3.2):
 //
 //   Hhat = [[tau H_mu, e1, 0], [0, 0, I_p], [0, 0, 0]]   (Eq. hathm P:368-377 with p+1)
-//   E = exp(Hhat) by the degree-13 Pade approximant with scaling and squaring (Eq. 8)
+//   E = exp(Hhat) by scaling and squaring (here with a Taylor polynomial, see cta_expm)
 //   phi_p(tau H)e1 = E[0:mu, mu+p-1] (p = 0: column 0), phi_{p+1}(tau H)e1 = E[0:mu, mu+p]
 //   eps = tau^p beta tau |h_{mu+1,mu} [phi_{p+1}]_mu|                 (Eq. errest with R9/R10)
 //   combine coefficients of Eq. (step)/(phipapprox2) for the assembly kernel.
 //
 // All K x K matrices (K <= m_max + p_max + 1) live in shared memory when 6 K^2 doubles fit,
-// otherwise in an L2-resident global scratch; generic addressing serves both.  The linear solve
-// (V - U) X = (V + U) uses Gauss-Jordan elimination with partial pivoting (parallel over the
-// CTA; the oracle uses LU with triangular solves — same pivoting, different operation order).
+// otherwise in an L2-resident global scratch; generic addressing serves both.  Every step of the
+// exponential is a K x K product on the fp64 tensor cores (DMMA) shared by all warps of the CTA.
 #pragma once
 
 #include "kernels.cuh"
@@ -58,11 +57,12 @@ struct ExpmArgs {
 // pair at most twice (256 B = 2 wavefronts, the minimum)
 __host__ __device__ inline int expm_ld(int Kp) { return Kp + ((4 - Kp % 16) + 16) % 16; }
 
-// C = A B for Kp x Kp column-major matrices (Kp a multiple of 8, zero padded) on the fp64 tensor
-// cores: each warp computes 8x8 output tiles with mma.sync.m8n8k4.f64 (SASS DMMA).
-// Fragment layouts (PTX ISA, m8n8k4 .f64): A row-major 8x4, a0 = A[lane/4][lane%4];
+// C = epi(row, col, (A B)[row, col]) for Kp x Kp column-major matrices (Kp a multiple of 8, zero
+// padded) on the fp64 tensor cores: each warp computes 8x8 output tiles with mma.sync.m8n8k4.f64
+// (SASS DMMA).  Fragment layouts (PTX ISA, m8n8k4 .f64): A row-major 8x4, a0 = A[lane/4][lane%4];
 // B column-major 4x8, b0 = B[lane%4][lane/4]; C 8x8, c_i = C[lane/4][2 (lane%4) + i].
-__device__ __forceinline__ void cta_matmul(int Kp, int ld, const double *A, const double *B, double *C)
+template <class Epi>
+__device__ __forceinline__ void cta_matmul_e(int Kp, int ld, const double *A, const double *B, double *C, Epi epi)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int nt = Kp >> 3;
@@ -91,188 +91,151 @@ __device__ __forceinline__ void cta_matmul(int Kp, int ld, const double *A, cons
             a0 = na0; b0 = nb0; a1 = na1; b1 = nb1;
         }
         const int row = ti * 8 + ar, col = tj * 8 + 2 * ac;
-        C[row + (size_t)col * ld] = c0 + d0;
-        C[row + (size_t)(col + 1) * ld] = c1 + d1;
+        C[row + (size_t)col * ld] = epi(row, col, c0 + d0);
+        C[row + (size_t)(col + 1) * ld] = epi(row, col + 1, c1 + d1);
     }
     __syncthreads();
 }
 
-__device__ __forceinline__ double block_max_colsum(int K, int ld, const double *A, double *sred)
+struct EpiNone {
+    __device__ double operator()(int, int, double v) const { return v; }
+};
+
+__device__ __forceinline__ void cta_matmul(int Kp, int ld, const double *A, const double *B, double *C)
 {
-    // ||A||_1 = max_j sum_i |a_ij|
-    double m = 0.0;
-    for (int jc = threadIdx.x; jc < K; jc += blockDim.x) {
-        double s = 0.0;
-        for (int i = 0; i < K; i++) s += fabs(A[i + (size_t)jc * ld]);
-        m = fmax(m, s);
-    }
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = m;
-    __syncthreads();
-    double r = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) r = fmax(r, sred[w]);
-    __syncthreads();
-    return r;
+    cta_matmul_e(Kp, ld, A, B, C, EpiNone{});
 }
 
-// Pade [13/13] coefficients c_j = (26-j)! 13! / (26! j! (13-j)!), c_0 = 1, via the ratio
-// c_{j+1}/c_j = (13-j)/((26-j)(j+1)).
-__device__ __forceinline__ void pade13(double *c)
-{
-    c[0] = 1.0;
-    for (int j = 0; j < 13; j++) c[j + 1] = c[j] * (double)(13 - j) / ((double)(26 - j) * (double)(j + 1));
-}
+// Paterson-Stockmeyer block B_k = c0 I + c1 A + c2 A^2 + c3 A^3 added in the product's epilogue
+struct EpiBlock {
+    const double *A1, *A2, *A3;
+    int ld;
+    double c0, c1, c2, c3;
+    __device__ double operator()(int r, int c, double v) const
+    {
+        const size_t e = r + (size_t)c * ld;
+        double b = c3 * A3[e];
+        b = fma(c2, A2[e], b);
+        b = fma(c1, A1[e], b);
+        if (r == c) b += c0;
+        return v + b;
+    }
+};
+
+// Taylor degrees evaluable from A, A^2, A^3, A^4 by Paterson-Stockmeyer (m = 4 r), the products
+// they cost including the three powers, and their backward-error thresholds theta_m: the largest
+// alpha with sum_{k>m} |c_k| alpha^(k-1) <= 2^-53 for h_m(x) = log(exp(-x) T_m(x)) = sum c_k x^k
+// (exact rational series, tools/taylor_theta.py).
+constexpr int TAYLOR_NDEG = 3;
+__device__ constexpr int TAYLOR_M[TAYLOR_NDEG] = {8, 12, 16};
+__device__ constexpr int TAYLOR_PROD[TAYLOR_NDEG] = {4, 5, 6};
+__device__ constexpr double TAYLOR_THETA[TAYLOR_NDEG] = {0.049912288711153226, 0.29961589138115802,
+                                                         0.78028742566265741};
+
+// Taylor coefficients 1/k!, k = 0..16, correctly rounded from the exact rationals
+__device__ constexpr double TAYLOR_INVFACT[17] = {
+    1.0, 1.0, 0.5, 0.16666666666666666, 0.041666666666666664, 0.008333333333333333, 0.001388888888888889,
+    0.0001984126984126984, 2.48015873015873e-05, 2.7557319223985893e-06, 2.755731922398589e-07,
+    2.505210838544172e-08, 2.08767569878681e-09, 1.6059043836821613e-10, 1.1470745597729725e-11,
+    7.647163731819816e-13, 4.779477332387385e-14};
 
 // exp(M0) -> returned pointer (one of the buffers); M0..M5 are Kp x Kp buffers (Kp = K rounded
-// up to a multiple of 8, padding zero: exp(blockdiag(A, 0)) = blockdiag(exp A, I)).  status 0/5/6
+// up to a multiple of 8, padding zero: exp(blockdiag(A, 0)) = blockdiag(exp A, I)).  status 0/5.
+//
+// Scaling and squaring with a truncated Taylor polynomial evaluated by Paterson-Stockmeyer, all
+// products on DMMA across the CTA.  The paper's MATLAB expm (and the oracle) uses the [13/13]
+// Pade approximant, whose linear solve (V - U) X = (V + U) is a chain of K dependent pivot steps
+// on one SM; the polynomial needs only matrix products.  Both approximate exp to unit-roundoff
+// backward error; the GPU's number of squarings is chosen from
+//   alpha = max(||A^3||_1^(1/3), ||A^4||_1^(1/4))  (>= the spectral growth; Al-Mohy & Higham's
+// alpha_3 bound, valid for m >= 5), which the nilpotent shift block of Hhat does not inflate.
 __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, double *M2, double *M3, double *M4, double *M5,
-                            double *sred, int *s_int, double *fcol, int *status, long long *clk)
+                            double *sred, int *status, long long *clk)
 {
 #define EXPM_CLK(i) \
     if (clk && threadIdx.x == 0) clk[i] = clock64();
+    (void)K;
     const int KK = ld * Kp, t = threadIdx.x;         // whole buffers (padding rows are never read)
-    double c[14];
-    pade13(c);
-    // scaling: s = ceil_+(log2(||A||_1 / 5.37)) (theta_13 = 5.37 as printed, R26)
-    const double nrm = block_max_colsum(Kp, ld, M0, sred);
-    int s = 0;
-    if (nrm > 0.0) {
-        const double l = ceil(log2(nrm / 5.37));
-        s = l > 0.0 ? (int)l : 0;
-    }
-    if (!isfinite(nrm)) { *status = 5; return M0; }
-    const double sc = ldexp(1.0, -s);
-    for (int e = t; e < KK; e += blockDim.x) M0[e] *= sc;
-    __syncthreads();
-    cta_matmul(Kp, ld, M0, M0, M1);            // A2
-    cta_matmul(Kp, ld, M1, M1, M2);            // A4
-    cta_matmul(Kp, ld, M2, M1, M3);            // A6
+    cta_matmul(Kp, ld, M0, M0, M1);            // A^2
+    cta_matmul(Kp, ld, M1, M0, M2);            // A^3
+    cta_matmul(Kp, ld, M1, M1, M3);            // A^4
     EXPM_CLK(2)
-    // U = A [A6 (c13 A6 + c11 A4 + c9 A2) + c7 A6 + c5 A4 + c3 A2 + c1 I]
-    for (int e = t; e < KK; e += blockDim.x) M4[e] = c[13] * M3[e] + c[11] * M2[e] + c[9] * M1[e];
-    __syncthreads();
-    cta_matmul(Kp, ld, M3, M4, M5);
-    for (int e = t; e < KK; e += blockDim.x) M5[e] = M5[e] + c[7] * M3[e] + c[5] * M2[e] + c[3] * M1[e];
-    __syncthreads();
-    for (int i = t; i < Kp; i += blockDim.x) M5[i * (ld + 1)] += c[1];
-    __syncthreads();
-    cta_matmul(Kp, ld, M0, M5, M4);            // U in M4
-    // V = A6 (c12 A6 + c10 A4 + c8 A2) + c6 A6 + c4 A4 + c2 A2 + c0 I
-    for (int e = t; e < KK; e += blockDim.x) M5[e] = c[12] * M3[e] + c[10] * M2[e] + c[8] * M1[e];
-    __syncthreads();
-    cta_matmul(Kp, ld, M3, M5, M0);            // A no longer needed
-    for (int e = t; e < KK; e += blockDim.x) M0[e] = M0[e] + c[6] * M3[e] + c[4] * M2[e] + c[2] * M1[e];
-    __syncthreads();
-    for (int i = t; i < Kp; i += blockDim.x) M0[i * (ld + 1)] += c[0];   // V
-    __syncthreads();
-    // P = V + U (M1), Q = V - U (M2)
-    for (int e = t; e < KK; e += blockDim.x) {
-        const double v = M0[e], u = M4[e];
-        M1[e] = v + u;
-        M2[e] = v - u;
+    // ||A||_1, ||A^3||_1, ||A^4||_1: one warp per column, then the max over columns
+    const int lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
+    double m1 = 0.0, m3 = 0.0, m4 = 0.0;
+    for (int jc = warp; jc < Kp; jc += nw) {
+        double s1 = 0.0, s3 = 0.0, s4 = 0.0;
+        for (int i = lane; i < Kp; i += 32) {
+            const size_t e = i + (size_t)jc * ld;
+            s1 += fabs(M0[e]);
+            s3 += fabs(M2[e]);
+            s4 += fabs(M3[e]);
+        }
+        s1 = warp_sum(s1);
+        s3 = warp_sum(s3);
+        s4 = warp_sum(s4);
+        m1 = fmax(m1, s1);
+        m3 = fmax(m3, s3);
+        m4 = fmax(m4, s4);
     }
+    if (lane == 0) { sred[warp] = m1; sred[warp + 16] = m3; sred[warp + 32] = m4; }
     __syncthreads();
-    EXPM_CLK(3)
-    // Gauss-Jordan with partial pivoting: Q X = P, implicit pivoting (no row interchanges; the
-    // pivot row of column c is prow[c]), ONE barrier per column: warp 0 updates the next pivot
-    // column first, searches its pivot among the unused rows and prepares the multipliers while
-    // the other warps eliminate the current column from the rest of [Q | P].
-    double *Q = M2, *P = M1;
-    int *prow = s_int + 8, *used = s_int + 8 + EXPM_KMAX;
-    double *fb = fcol;                                    // 2 x EXPM_KMAX multipliers
-    __shared__ int s_pr[2], s_bad;
-    __shared__ double s_rq[EXPM_KMAX];
-    const int warp = t >> 5, lane = t & 31;
-    for (int r = t; r < K; r += blockDim.x) used[r] = 0;
-    if (t == 0) s_bad = 0;
+    double nrm = 0.0, n3 = 0.0, n4 = 0.0;
+    for (int w = 0; w < nw; w++) { nrm = fmax(nrm, sred[w]); n3 = fmax(n3, sred[w + 16]); n4 = fmax(n4, sred[w + 32]); }
     __syncthreads();
-    auto lookahead = [&](int c, int b) {                 // warp 0; column c of Q is final
-        double best = -1.0;
-        int bi = K;
-        for (int r = lane; r < K; r += 32)
-            if (!used[r]) {
-                const double a = fabs(Q[r + (size_t)c * ld]);
-                if (a > best) { best = a; bi = r; }
-            }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    if (!isfinite(nrm)) { *status = 5; return M0; }
+    double alpha = fmax(cbrt(n3), sqrt(sqrt(n4)));
+    if (!isfinite(alpha) || alpha > nrm) alpha = nrm;      // overflowed powers: ||A|| bounds alpha
+    // degree and squarings: minimise products (powers + Horner) + squarings, smallest m on ties
+    int m = TAYLOR_M[0], s = 0, best = 1 << 30;
+    for (int d = 0; d < TAYLOR_NDEG; d++) {
+        int sd = 0;
+        if (alpha > TAYLOR_THETA[d]) {
+            const double l = ceil(log2(alpha / TAYLOR_THETA[d]));
+            sd = l > 0.0 ? (int)l : 0;
         }
-        if (!(best >= 1e-300) || bi >= K) {
-            if (lane == 0) s_bad = 1;
-            return;
-        }
-        const double rp = 1.0 / Q[bi + (size_t)c * ld];
-        for (int r = lane; r < K; r += 32) fb[b * EXPM_KMAX + r] = (r == bi) ? 0.0 : Q[r + (size_t)c * ld] * rp;
-        __syncwarp();
-        if (lane == 0) {
-            s_pr[b] = bi;
-            used[bi] = 1;
-            prow[c] = bi;
-        }
-        __syncwarp();
-    };
-    if (warp == 0) lookahead(0, 0);
-    __syncthreads();
-    const int t2 = t - 32, n2 = (int)blockDim.x - 32;
-    const int er = t2 % K, eg = t2 / K, neg = n2 / K;     // elimination warps: fixed row, column group
-    for (int col = 0; col < K; col++) {
-        if (s_bad) { *status = 6; return P; }
-        const int b = col & 1;
-        const int pr = s_pr[b];
-        const double *f = fb + b * EXPM_KMAX;
-        if (warp == 0) {
-            if (col + 1 < K) {
-                const int j = col + 1;
-                const double pv = Q[pr + (size_t)j * ld];
-                for (int r = lane; r < K; r += 32)
-                    if (r != pr) Q[r + (size_t)j * ld] -= f[r] * pv;
-                __syncwarp();
-                lookahead(col + 1, b ^ 1);
-            }
-        } else if (eg < neg && er != pr) {
-            const double fr = f[er];
-            if (fr != 0.0) {
-                // Q columns col+2 .. K-1 and P columns 0 .. K-1 owned by this thread's column group,
-                // four loads in flight before the stores
-                auto rank1 = [&](double *M, int j) {
-                    for (; j + 3 * neg < K; j += 4 * neg) {
-                        const double p0 = M[pr + (size_t)j * ld], p1 = M[pr + (size_t)(j + neg) * ld];
-                        const double p2 = M[pr + (size_t)(j + 2 * neg) * ld], p3 = M[pr + (size_t)(j + 3 * neg) * ld];
-                        const double x0 = M[er + (size_t)j * ld], x1 = M[er + (size_t)(j + neg) * ld];
-                        const double x2 = M[er + (size_t)(j + 2 * neg) * ld], x3 = M[er + (size_t)(j + 3 * neg) * ld];
-                        M[er + (size_t)j * ld] = x0 - fr * p0;
-                        M[er + (size_t)(j + neg) * ld] = x1 - fr * p1;
-                        M[er + (size_t)(j + 2 * neg) * ld] = x2 - fr * p2;
-                        M[er + (size_t)(j + 3 * neg) * ld] = x3 - fr * p3;
-                    }
-                    for (; j < K; j += neg) M[er + (size_t)j * ld] -= fr * M[pr + (size_t)j * ld];
-                };
-                rank1(Q, col + 2 + eg);
-                rank1(P, eg);
-            }
+        if (TAYLOR_PROD[d] + sd < best) { best = TAYLOR_PROD[d] + sd; m = TAYLOR_M[d]; s = sd; }
+    }
+    // scale the powers: (2^-s A)^k = 2^-sk A^k (exact)
+    if (s > 0) {
+        const double f1 = ldexp(1.0, -s), f2 = ldexp(1.0, -2 * s), f3 = ldexp(1.0, -3 * s), f4 = ldexp(1.0, -4 * s);
+        for (int e = t; e < KK; e += blockDim.x) {
+            M0[e] *= f1;
+            M1[e] *= f2;
+            M2[e] *= f3;
+            M3[e] *= f4;
         }
         __syncthreads();
     }
-    // X[c, :] = P[prow(c), :] / Q[prow(c), c]   (the pivot row's diagonal value is final)
-    for (int c = t; c < K; c += blockDim.x) s_rq[c] = 1.0 / Q[prow[c] + (size_t)c * ld];
-    __syncthreads();
-    double *Xo = M3;
-    for (int e = t; e < K * K; e += blockDim.x) {
-        const int c = e % K, j = e / K;
-        Xo[c + (size_t)j * ld] = P[prow[c] + (size_t)j * ld] * s_rq[c];
+    auto c = [](int k) { return TAYLOR_INVFACT[k]; };
+    // Horner in A^4: Y = B_{r-1} + c_m A^4;  Y <- Y A^4 + B_k, k = r-2 .. 0
+    const int r = m >> 2;
+    double *Y = M4, *Z = M5;
+    {
+        const int b = 4 * (r - 1);
+        const double cm = c(m), cb0 = c(b), cb1 = c(b + 1), cb2 = c(b + 2), cb3 = c(b + 3);
+        for (int e = t; e < KK; e += blockDim.x) {
+            double v = cm * M3[e];
+            v = fma(cb3, M2[e], v);
+            v = fma(cb2, M1[e], v);
+            v = fma(cb1, M0[e], v);
+            Y[e] = v;
+        }
+        __syncthreads();
+        for (int i = t; i < Kp; i += blockDim.x) Y[i * (ld + 1)] += cb0;
+        __syncthreads();
     }
-    // padding block of X: identity (Q and P were identity there)
-    for (int e = t; e < Kp * Kp; e += blockDim.x) {
-        const int c = e % Kp, j = e / Kp;
-        if (c >= K || j >= K) Xo[c + (size_t)j * ld] = (c == j) ? 1.0 : 0.0;
+    for (int k = r - 2; k >= 0; k--) {
+        const int b = 4 * k;
+        cta_matmul_e(Kp, ld, Y, M3, Z, EpiBlock{M0, M1, M2, ld, c(b), c(b + 1), c(b + 2), c(b + 3)});
+        double *tmp = Y;
+        Y = Z;
+        Z = tmp;
     }
-    __syncthreads();
-    P = Xo;
+    EXPM_CLK(3)
     EXPM_CLK(4)
-    // squaring
-    double *X = P, *T = M4;
+    // squaring (Z and M0 are free)
+    double *X = Y, *T = Z;
     for (int q = 0; q < s; q++) {
         cta_matmul(Kp, ld, X, X, T);
         double *tmp = X;
@@ -280,15 +243,15 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
         T = tmp;
     }
     EXPM_CLK(5)
+    if (clk && t == 0) clk[7] = ((long long)m << 16) | s;
     return X;
 }
 
 template <bool SMEM>
-__global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
+__global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
 {
     extern __shared__ double esm[];
-    __shared__ double sred[EXPM_NT / 32];
-    __shared__ int s_int[8 + 2 * EXPM_KMAX];
+    __shared__ double sred[3 * (EXPM_NT / 32)];
     __shared__ int s_mu;
     const int t = threadIdx.x;
     pdl_wait();
@@ -333,7 +296,6 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
     double *base = SMEM ? esm : a.scratch;          // compile-time address space (LDS/STS when SMEM)
     double *M0 = base, *M1 = base + KK, *M2 = base + 2 * KK, *M3 = base + 3 * KK, *M4 = base + 4 * KK,
            *M5 = base + 5 * KK;
-    __shared__ double fcol[2 * EXPM_KMAX];
     // build the matrix to exponentiate (zero padded to Kp)
     for (size_t e = t; e < KK; e += blockDim.x) M0[e] = 0.0;
     __syncthreads();
@@ -376,7 +338,7 @@ __global__ void __launch_bounds__(EXPM_NT) expm_kernel(ExpmArgs a)
     __syncthreads();
     if (a.clk && t == 0) a.clk[1] = clock64();
     int status = 0;
-    double *E = cta_expm(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, s_int, fcol, &status, a.clk);
+    double *E = cta_expm(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, &status, a.clk);
     if (t == 0 && status) s_status = status;
     __syncthreads();
     status = s_status;

@@ -1368,8 +1368,8 @@ int phipm_phi_pair(phipm_ctx *c, int mu, const double *H, int ldh, double tau, i
     if (rc) return rc;
     if (c->expm_clk_h) {
         const long long *k = c->expm_clk_h;
-        fprintf(stderr, "expm K=%d cycles: build %lld | A2,A4,A6 %lld | U,V %lld | GJ %lld | squarings %lld | tail %lld\n",
-                mu + p + 1, k[1] - k[0], k[2] - k[1], k[3] - k[2], k[4] - k[3], k[5] - k[4], k[6] - k[5]);
+        fprintf(stderr, "expm K=%d cycles: build %lld | A2,A3,A4 %lld | Horner %lld | squarings %lld | m=%lld s=%lld\n",
+                mu + p + 1, k[1] - k[0], k[2] - k[1], k[3] - k[2], k[5] - k[4], k[7] >> 16, k[7] & 0xffff);
     }
     AttemptResult R;
     memcpy(&R, (const void *)c->res_h, sizeof(R));

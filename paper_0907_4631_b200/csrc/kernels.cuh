@@ -102,6 +102,7 @@ struct SpmvArgs {
     int fin, j;
     int check_brk;               // exit early if a breakdown happened earlier in this step
     int64_t rpc;                 // rows per CTA (balanced contiguous ranges; multiple of 32)
+    unsigned long long *dbg;     // optional per-CTA %globaltimer stamps (PHIPM_KCLOCKS tool), 8 per CTA
 };
 
 struct AxpyArgs {
@@ -126,6 +127,7 @@ struct AxpyArgs {
     int64_t rpc;                 // rows per CTA (balanced contiguous ranges; multiple of 32)
     int rev;                     // stream the V columns in descending order (L2 ping-pong with the
                                  // ascending dot pass of the SpMV kernel)
+    unsigned long long *dbg;     // optional per-CTA %globaltimer stamps (PHIPM_KCLOCKS tool)
 };
 
 // ------------------------------------------------------------------------------------------
@@ -138,6 +140,15 @@ __device__ __forceinline__ void pdl_wait()
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define KSTAMP(i) \
+    if (a.dbg && threadIdx.x == 0) a.dbg[(size_t)blockIdx.x * 8 + (i)] = gtimer();
 
 __device__ __forceinline__ double warp_sum(double v)
 {
@@ -165,9 +176,15 @@ __device__ __forceinline__ bool publish_partials(const Work &wk, const double *b
 {
     __shared__ unsigned s_ticket;
     for (int v = threadIdx.x; v < nv; v += blockDim.x) wk.part[(size_t)v * wk.pstride + blockIdx.x] = bsum[v];
-    __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_ticket = atomicAdd(wk.counter, 1u);
+    // one acq_rel gpu-scope ticket after the CTA barrier: release orders every thread's partial
+    // (observed through the barrier) before the ticket; acquire, propagated by the next barrier,
+    // makes the other CTAs' partials visible to the last CTA.  No per-thread fences.
+    if (threadIdx.x == 0) {
+        unsigned tk;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(tk) : "l"(wk.counter) : "memory");
+        s_ticket = tk;
+    }
     __syncthreads();
     return s_ticket == gridDim.x - 1;
 }
@@ -177,7 +194,6 @@ __device__ __forceinline__ bool publish_partials(const Work &wk, const double *b
 // order), so the tail costs about one L2 round trip per value instead of one per 32 blocks.
 __device__ __forceinline__ void final_reduce(const Work &wk, int nv, double *out)
 {
-    __threadfence();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int nb = gridDim.x;
     for (int v = warp; v < nv; v += nw) {
@@ -298,7 +314,7 @@ __global__ void __launch_bounds__(NT) maxabs_kernel(int64_t n, MaxAbsArgs a, Wor
     }
     __syncthreads();
     if (!publish_partials(wk, bsum, a.nv)) return;
-    __threadfence();
+    // publish_partials acquired the other CTAs' partials
     for (int v = warp; v < a.nv; v += NWARP) {
         double m = 0.0;
         for (int b = lane; b < (int)gridDim.x; b += 32) m = fmax(m, __ldcg(wk.part + (size_t)v * wk.pstride + b));
@@ -332,7 +348,7 @@ __global__ void __launch_bounds__(NT) csr_infnorm_kernel(CsrOp A, Work wk)
     }
     __syncthreads();
     if (!publish_partials(wk, bsum, 1)) return;
-    __threadfence();
+    // publish_partials acquired the other CTAs' partials
     if (warp == 0) {
         double t = 0.0;
         for (int b = lane; b < (int)gridDim.x; b += 32) t = fmax(t, __ldcg(wk.part + b));

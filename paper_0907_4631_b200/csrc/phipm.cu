@@ -27,6 +27,8 @@ namespace {
 constexpr int P_MAX_ABS = 6;          // MAXZ bounds the epilogue vector count
 constexpr double EPS_MACH = 2.220446049250313080847e-16;
 
+constexpr int KCLK_MAXL = 512, KCLK_GRID = 1024;     // PHIPM_KCLOCKS capacity (launches, CTAs)
+
 enum ProfClass { PC_SPMV = 0, PC_ORTH, PC_EXPM, PC_COMBINE, PC_OTHER, PC_N };
 
 struct ProfRec {
@@ -45,7 +47,7 @@ struct phipm_ctx {
     int m_max = 0, p_max = 0, kmax = 0;
     int sm_count = 0, occ_spmv = 1, occ_axpy = 1;
     int pstride = 0;
-    size_t expm_smem_limit = 0, stream_smem_budget = 0;
+    size_t expm_smem_limit = 0, stream_smem_budget = 0, smem_optin = 0;
     struct OccEntry { const void *fn; size_t smem; int occ; };
     std::vector<OccEntry> occ_cache;
     // device workspace
@@ -57,6 +59,11 @@ struct phipm_ctx {
     int64_t ntile_cap = 0;
     AttemptResult *res_h = nullptr, *res_d = nullptr;
     long long *expm_clk_h = nullptr, *expm_clk_d = nullptr;   // PHIPM_EXPM_CLOCKS=1 debug timestamps
+    // PHIPM_KCLOCKS=<file>: per-CTA %globaltimer stamps of every streaming launch (measurement tool)
+    unsigned long long *kclk_d = nullptr;
+    struct KclkRec { int cls, grid, ncols; };
+    std::vector<KclkRec> kclk_recs;
+    const char *kclk_path = nullptr;
     double *raw_h = nullptr;                 // pinned staging for small readbacks
     // host-buffer solve staging
     double *hu = nullptr, *hw = nullptr;
@@ -222,7 +229,7 @@ int csr_wcap(const Op &, int) { return 0; }
 template <>
 int csr_wcap<CsrOp>(const CsrOp &A, int tile) { return A.wtile == tile ? A.wcap : 0; }
 
-// rows per thread: 8 (TILE 2048) when there are enough tiles to fill the GPU, else 2 (TILE 512);
+// rows per thread: 8 (TILE 8 SNT) when every CTA gets at least half a tile, else 2;
 // PHIPM_RPT=2|4|8 overrides (tuning experiments)
 int pick_rpt(phipm_ctx *c, int64_t n)
 {
@@ -232,7 +239,7 @@ int pick_rpt(phipm_ctx *c, int64_t n)
         env = e ? atoi(e) : 0;
     }
     if (env == 2 || env == 4 || env == 8) return env;
-    return n >= (int64_t)SNT * 8 * 2 * c->sm_count ? 8 : 2;
+    return n >= (int64_t)SNT * 8 * c->sm_count * SMINB / 2 ? 8 : 2;
 }
 
 // balanced partition: every resident CTA slot gets one contiguous range of rpc rows (a multiple
@@ -245,6 +252,14 @@ void balance(phipm_ctx *c, int64_t n, int slots, int &grid, int64_t &rpc)
     grid = (int)((n + rpc - 1) / rpc);
 }
 
+unsigned long long *kclk_slot(phipm_ctx *c, int cls, int grid, int ncols)
+{
+    if (!c->kclk_d || (int)c->kclk_recs.size() >= KCLK_MAXL || grid > KCLK_GRID) return nullptr;
+    unsigned long long *p = c->kclk_d + c->kclk_recs.size() * (size_t)KCLK_GRID * 8;
+    c->kclk_recs.push_back({cls, grid, ncols});
+    return p;
+}
+
 template <class Op, int RPT>
 int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a0)
 {
@@ -255,6 +270,7 @@ int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a0)
     const int slots = stream_grid(c, fn, smem, (int64_t)1 << 40);
     int grid;
     balance(c, op.n, slots, grid, a.rpc);
+    a.dbg = kclk_slot(c, PC_SPMV, grid, a.nd);
     launch_k(c, spmv_stream_kernel<Op, RPT>, grid, SNT, smem, op, a, make_work(c));
     return PHIPM_OK;
 }
@@ -271,7 +287,11 @@ int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
     const double bytes = bytes_op + 8.0 * (double)op.n * (nd_mem + a.nz);
     prof_begin(c, r, PC_SPMV, bytes, a.nd);
     int rpt = pick_rpt(c, op.n);
-    if (csr_wcap(op, SNT * 8) > 0) rpt = 8;                  // CSR x-window mode uses 2048-row tiles
+    if (csr_wcap(op, SNT * 8) > 0) rpt = 8;                  // CSR x-window mode uses 8 SNT-row tiles
+    // largest tile whose halo + dot accumulators fit in shared memory (3-D stencils, many dots)
+    while (rpt > 2 && spmv_smem_bytes(halo_cap_host(op, SNT * rpt), SNT * rpt, a.nd, csr_wcap(op, SNT * rpt)) >
+                          c->smem_optin)
+        rpt >>= 1;
     if (rpt == 8) launch_spmv_t<Op, 8>(c, op, a);
     else if (rpt == 4) launch_spmv_t<Op, 4>(c, op, a);
     else launch_spmv_t<Op, 2>(c, op, a);
@@ -288,6 +308,7 @@ void launch_axpy_t(phipm_ctx *c, int64_t n, const AxpyArgs &a0)
     const int slots = stream_grid(c, (const void *)axpy_stream_kernel<RPT>, 0, (int64_t)1 << 40);
     int grid;
     balance(c, n, slots, grid, a.rpc);
+    a.dbg = kclk_slot(c, PC_ORTH, grid, a.nc);
     launch_k(c, axpy_stream_kernel<RPT>, grid, SNT, 0, n, a, make_work(c));
 }
 
@@ -1000,6 +1021,24 @@ void phipm_destroy(phipm_ctx *c)
     cudaFree(c->hu); cudaFree(c->hw); cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
     if (c->res_h) cudaFreeHost(c->res_h);
     if (c->expm_clk_h) cudaFreeHost(c->expm_clk_h);
+    if (c->kclk_d) {
+        // dump: int32 count, then per launch int32 {cls, grid, ncols} and grid*8 uint64 stamps
+        FILE *f = fopen(c->kclk_path, "wb");
+        if (f) {
+            const int cnt = (int)c->kclk_recs.size();
+            fwrite(&cnt, 4, 1, f);
+            std::vector<unsigned long long> h((size_t)KCLK_GRID * 8);
+            for (int i = 0; i < cnt; i++) {
+                const auto &r = c->kclk_recs[i];
+                fwrite(&r, sizeof(r), 1, f);
+                cudaMemcpy(h.data(), c->kclk_d + (size_t)i * KCLK_GRID * 8, sizeof(unsigned long long) * r.grid * 8,
+                           cudaMemcpyDeviceToHost);
+                fwrite(h.data(), sizeof(unsigned long long), (size_t)r.grid * 8, f);
+            }
+            fclose(f);
+        }
+        cudaFree(c->kclk_d);
+    }
     if (c->raw_h) cudaFreeHost(c->raw_h);
     delete c;
 }
@@ -1030,7 +1069,10 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     }
     // streaming kernels: grid = min(tiles, occupancy x SMs); allow large dynamic smem (halo tiles)
     {
-        const int mx = 200 * 1024;
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+        const int mx = std::max(48 * 1024, optin - 8 * 1024);   // minus the kernels' static smem
+        c->smem_optin = (size_t)mx;
         cudaFuncSetAttribute(spmv_stream_kernel<StencilOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<StencilOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<StencilOp, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -1091,6 +1133,12 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     if (ok && getenv("PHIPM_EXPM_CLOCKS")) {
         if (cudaHostAlloc((void **)&c->expm_clk_h, sizeof(long long) * 8, cudaHostAllocMapped) != cudaSuccess ||
             cudaHostGetDevicePointer((void **)&c->expm_clk_d, c->expm_clk_h, 0) != cudaSuccess)
+            ok = false;
+    }
+    if (ok && getenv("PHIPM_KCLOCKS")) {
+        c->kclk_path = getenv("PHIPM_KCLOCKS");
+        if (cudaMalloc((void **)&c->kclk_d, sizeof(unsigned long long) * KCLK_MAXL * KCLK_GRID * 8) != cudaSuccess ||
+            cudaMemset(c->kclk_d, 0, sizeof(unsigned long long) * KCLK_MAXL * KCLK_GRID * 8) != cudaSuccess)
             ok = false;
     }
     if (ok && cudaDeviceSynchronize() != cudaSuccess) ok = false;

@@ -24,8 +24,13 @@
 
 namespace phipm {
 
-constexpr int SNT = 256;                // threads per CTA
+#ifndef PHIPM_SNT
+#define PHIPM_SNT 1024
+#endif
+constexpr int SNT = PHIPM_SNT;          // threads per CTA: one 1024-thread CTA per SM (fewer partials
+                                        // to reduce, less halo re-read per row than 4 x 256)
 constexpr int SNW = SNT / 32;
+constexpr int SMINB = 1024 / SNT;       // resident CTAs per SM the register budget is sized for
 constexpr int CU = 4;                   // columns in flight per thread
 constexpr int MAXITEM = MAXD + MAXZ + 2;
 
@@ -290,7 +295,7 @@ __host__ __device__ inline size_t spmv_smem_bytes(int halo_cap, int tile, int nd
 // spmv_stream
 
 template <class Op, int RPT>
-__global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, Work wk)
+__global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs a, Work wk)
 {
     constexpr int TILE_ = SNT * RPT;
     constexpr int NP = RPT / 2;                           // double2 pairs per thread
@@ -352,7 +357,9 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
         for (int k = 0; k < h.nseg; k++)
             if (h.bytes[k]) tma_load_1d(hbuf + h.off[k], a.x + h.start[k], h.bytes[k], &hbar, pol);
     };
+    KSTAMP(0)
     pdl_wait();
+    KSTAMP(1)
     if (tid == 0) {
         s_exit = a.check_brk ? (wk.st->brk >= 0) : 0;
         if constexpr (HALO) {
@@ -386,6 +393,7 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
         // ---- phase 1: raw (A x) rows into registers (and x itself, for a dot with v_j = x)
         if constexpr (HALO) {
             mbar_wait(&hbar, ht & 1);
+            if (r0 == cs) KSTAMP(2)
             const int *ho = hofs[ht & 1];
             ht++;
             const double *pc = hbuf + ho[0];
@@ -530,6 +538,7 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
         }
     }
     // ---- block totals (fixed order), grid reduction, finalize
+    KSTAMP(3)
     __syncthreads();
     for (int k = tid; k < a.nd; k += SNT) {
         double t = 0.0;
@@ -549,17 +558,21 @@ __global__ void __launch_bounds__(SNT, 4) spmv_stream_kernel(Op op, SpmvArgs a, 
     const int nv = a.nd + (a.ynorm ? 1 : 0);
     __syncthreads();
     if (nv == 0) return;
-    if (!publish_partials(wk, bsum, nv)) return;
+    const bool last = publish_partials(wk, bsum, nv);
+    KSTAMP(4)
+    if (!last) return;
     __shared__ double red[MAXD + 2];
     final_reduce(wk, nv, red);
+    KSTAMP(5)
     finalize(a.fin, a.j, a.nd, red, wk, 0.0, 0);
+    KSTAMP(6)
 }
 
 // ---------------------------------------------------------------------------------------------
 // axpy_stream
 
 template <int RPT>
-__global__ void __launch_bounds__(SNT, 4) axpy_stream_kernel(int64_t n, AxpyArgs a, Work wk)
+__global__ void __launch_bounds__(SNT, SMINB) axpy_stream_kernel(int64_t n, AxpyArgs a, Work wk)
 {
     constexpr int TILE_ = SNT * RPT;
     constexpr int NP = RPT / 2;
@@ -569,7 +582,9 @@ __global__ void __launch_bounds__(SNT, 4) axpy_stream_kernel(int64_t n, AxpyArgs
     __shared__ double wsum[SNW];
     __shared__ int s_exit;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    KSTAMP(0)
     pdl_wait();
+    KSTAMP(1)
     if (tid == 0) s_exit = a.check_brk ? (wk.st->brk >= 0) : 0;
     const int nbase = (a.a0h != 0.0) ? 1 : 0;
     const int nitem = nbase + a.nc + a.ne;
@@ -632,6 +647,7 @@ __global__ void __launch_bounds__(SNT, 4) axpy_stream_kernel(int64_t n, AxpyArgs
             if (q + 1 < rows) nrm = fma(acc[p].y, acc[p].y, nrm);
         }
     }
+    KSTAMP(3)
     if (!a.onorm) return;
     const double v = warp_sum(nrm);
     if (lane == 0) wsum[warp] = v;
@@ -642,10 +658,14 @@ __global__ void __launch_bounds__(SNT, 4) axpy_stream_kernel(int64_t n, AxpyArgs
         bsum[0] = t;
     }
     __syncthreads();
-    if (!publish_partials(wk, bsum, 1)) return;
+    const bool last = publish_partials(wk, bsum, 1);
+    KSTAMP(4)
+    if (!last) return;
     __shared__ double red[2];
     final_reduce(wk, 1, red);
+    KSTAMP(5)
     finalize(a.fin, a.j, 1, red, wk, a.bthr, a.lanczos);
+    KSTAMP(6)
 }
 
 } // namespace phipm

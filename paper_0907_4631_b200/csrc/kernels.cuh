@@ -82,6 +82,8 @@ struct CsrOp {
     int wtile, wcap;
     int ell;               // > 0: every row has exactly `ell` entries (row_ptr[r] = ell r), ell % 4 == 0,
                            // ell <= 128: vectorised fast path (4 entries per lane)
+    int ring;              // ell > 0 and every column within [r - blo, r + bhi]: x from a shared ring
+    int blo, bhi;          // band below / above the diagonal (even, >= 0)
 };
 
 struct SpmvArgs {
@@ -360,10 +362,30 @@ __global__ void __launch_bounds__(NT) csr_infnorm_kernel(CsrOp A, Work wk)
 }
 
 // Uniform row length check: flag[0] stays 0 iff row_ptr[r] == L r for all r <= n.
-__global__ void csr_uniform_check_kernel(int64_t n, const int32_t *__restrict__ rp, int L, int *flag)
+// Uniform row length check (flag[0] |= 1 if row_ptr[r] != L r for some r) and, assuming it holds,
+// the band: flag[1] = max(r - col), flag[2] = max(col - r) over all entries (entry e is in row e / L).
+__global__ void csr_uniform_check_kernel(int64_t n, const int32_t *__restrict__ rp, const int32_t *__restrict__ col,
+                                         int L, int *flag)
 {
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= n; r += (int64_t)gridDim.x * blockDim.x)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= n; r += stride)
         if ((int64_t)rp[r] != (int64_t)L * r) atomicOr(flag, 1);
+    int lo = 0, hi = 0;
+    const int64_t nnz = n * L;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += stride) {
+        const int64_t d = (int64_t)col[e] - e / L;
+        const int64_t cap = 0x3fffffff;
+        lo = max(lo, (int)(-d < cap ? -d : cap));
+        hi = max(hi, (int)(d < cap ? d : cap));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = max(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(flag + 1, lo);
+        atomicMax(flag + 2, hi);
+    }
 }
 
 // Column range [min, max] of every tile of `tile` rows (one warp per tile); empty tile -> [0, -1].

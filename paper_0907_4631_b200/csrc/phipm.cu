@@ -225,6 +225,22 @@ template <>
 int halo_cap_host<StencilOp>(const StencilOp &S, int tile) { return halo_capacity(S.dim, S.nx, tile); }
 
 template <class Op>
+int csr_ring(const Op &, int) { return 0; }
+template <>
+int csr_ring<CsrOp>(const CsrOp &A, int tile) { return A.ring && 2 * tile + A.blo + A.bhi <= XRING; }
+
+// the operator as one launch with `tile`-row tiles sees it (x ring only where it fits)
+template <class Op>
+Op launch_op(const Op &op, int) { return op; }
+template <>
+CsrOp launch_op<CsrOp>(const CsrOp &A, int tile)
+{
+    CsrOp o = A;
+    o.ring = csr_ring(A, tile);
+    return o;
+}
+
+template <class Op>
 int csr_wcap(const Op &, int) { return 0; }
 template <>
 int csr_wcap<CsrOp>(const CsrOp &A, int tile) { return A.wtile == tile ? A.wcap : 0; }
@@ -265,13 +281,14 @@ int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a0)
 {
     constexpr int TILE_ = SNT * RPT;
     SpmvArgs a = a0;
-    const size_t smem = spmv_smem_bytes(halo_cap_host(op, TILE_), TILE_, a.nd, csr_wcap(op, TILE_));
+    const Op lop = launch_op(op, TILE_);
+    const size_t smem = spmv_smem_bytes(halo_cap_host(op, TILE_), TILE_, a.nd, csr_wcap(op, TILE_), csr_ring(op, TILE_));
     const void *fn = (const void *)spmv_stream_kernel<Op, RPT>;
     const int slots = stream_grid(c, fn, smem, (int64_t)1 << 40);
     int grid;
     balance(c, op.n, slots, grid, a.rpc);
     a.dbg = kclk_slot(c, PC_SPMV, grid, a.nd);
-    launch_k(c, spmv_stream_kernel<Op, RPT>, grid, SNT, smem, op, a, make_work(c));
+    launch_k(c, spmv_stream_kernel<Op, RPT>, grid, SNT, smem, lop, a, make_work(c));
     return PHIPM_OK;
 }
 
@@ -289,9 +306,12 @@ int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
     int rpt = pick_rpt(c, op.n);
     if (csr_wcap(op, SNT * 8) > 0) rpt = 8;                  // CSR x-window mode uses 8 SNT-row tiles
     // largest tile whose halo + dot accumulators fit in shared memory (3-D stencils, many dots)
-    while (rpt > 2 && spmv_smem_bytes(halo_cap_host(op, SNT * rpt), SNT * rpt, a.nd, csr_wcap(op, SNT * rpt)) >
-                          c->smem_optin)
+    while (rpt > 2 && spmv_smem_bytes(halo_cap_host(op, SNT * rpt), SNT * rpt, a.nd, csr_wcap(op, SNT * rpt),
+                                      csr_ring(op, SNT * rpt)) > c->smem_optin)
         rpt >>= 1;
+    // x-ring CSR: the largest tile with 2 TILE + band <= XRING
+    if (csr_ring(op, SNT * 2))
+        while (rpt > 2 && !csr_ring(op, SNT * rpt)) rpt >>= 1;
     if (rpt == 8) launch_spmv_t<Op, 8>(c, op, a);
     else if (rpt == 4) launch_spmv_t<Op, 4>(c, op, a);
     else launch_spmv_t<Op, 2>(c, op, a);
@@ -862,6 +882,7 @@ int make_csr(phipm_ctx *c, const phipm_csr *A, CsrOp &op)
     op.tlo = op.thi = nullptr;
     op.wtile = op.wcap = 0;
     op.ell = 0;
+    op.ring = op.blo = op.bhi = 0;
     return PHIPM_OK;
 }
 
@@ -873,6 +894,7 @@ constexpr int CSR_WCAP = 10496;                             // 82 KB: band +-409
 int detect_csr_ell(phipm_ctx *c, CsrOp &op, int64_t nnz)
 {
     op.ell = 0;
+    op.ring = op.blo = op.bhi = 0;
     static int env = -1;
     if (env < 0) {
         const char *e = getenv("PHIPM_CSR_ELL");
@@ -882,16 +904,26 @@ int detect_csr_ell(phipm_ctx *c, CsrOp &op, int64_t nnz)
     const int64_t L = nnz / op.n;
     if (L < 4 || L > 128 || (L % 4) || ((L / 4) & (L / 4 - 1))) return PHIPM_OK;   // L/4 a power of two
     if (((uintptr_t)op.val & 15) || ((uintptr_t)op.col & 15)) return PHIPM_OK;
-    int *flag = reinterpret_cast<int *>(c->counter + 2);
-    CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+    int *flag = reinterpret_cast<int *>(c->raw);             // 3 ints of the raw scratch
+    CK(cudaMemsetAsync(flag, 0, 3 * sizeof(int), c->stream));
     const int grid = (int)std::min<int64_t>((op.n + 256) / 256, (int64_t)c->sm_count * 8);
-    csr_uniform_check_kernel<<<grid, 256, 0, c->stream>>>(op.n, op.rp, (int)L, flag);
+    csr_uniform_check_kernel<<<grid, 256, 0, c->stream>>>(op.n, op.rp, op.col, (int)L, flag);
     c->acc.launches++;
     CK(cudaGetLastError());
-    int h = 1;
-    CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    int h[3] = {1, 0, 0};
+    CK(cudaMemcpyAsync(h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    if (h == 0) op.ell = (int)L;
+    if (h[0] != 0) return PHIPM_OK;
+    op.ell = (int)L;
+    // banded: x from a shared-memory ring (PHIPM_CSR_RING=0 disables); bands rounded up to even
+    static int envr = -1;
+    if (envr < 0) {
+        const char *e = getenv("PHIPM_CSR_RING");
+        envr = (e && e[0] == '0') ? 0 : 1;
+    }
+    op.blo = (h[1] + 1) & ~1;
+    op.bhi = (h[2] + 1) & ~1;
+    op.ring = (envr && 2 * SNT * 2 + op.blo + op.bhi <= XRING) ? 1 : 0;
     return PHIPM_OK;
 }
 
@@ -902,7 +934,7 @@ int enable_csr_window(phipm_ctx *c, CsrOp &op)
         const char *e = getenv("PHIPM_CSR_WINDOW");
         env = (e && e[0] == '1') ? 1 : 0;
     }
-    if (!env) return PHIPM_OK;                              // default off (measured slower, round 1)
+    if (!env || op.ring) return PHIPM_OK;                  // default off (measured slower, round 1)
     const int tile = SNT * 8;
     const int64_t ntiles = (op.n + tile - 1) / tile;
     if (ntiles > c->ntile_cap || op.n < (int64_t)tile) return PHIPM_OK;   // small problems: global gathers

@@ -32,6 +32,9 @@ constexpr int SNT = PHIPM_SNT;          // threads per CTA: one 1024-thread CTA 
 constexpr int SNW = SNT / 32;
 constexpr int SMINB = 1024 / SNT;       // resident CTAs per SM the register budget is sized for
 constexpr int CU = 4;                   // columns in flight per thread
+// banded uniform-row CSR: x lives in a shared-memory ring of XRING doubles (x[c] at c mod XRING)
+// that slides with the CTA's row range; each tile's 1-D bulk copy brings in only the new chunk
+constexpr int XRING = 16384;
 constexpr int MAXITEM = MAXD + MAXZ + 2;
 
 // ---------------------------------------------------------------------------------------------
@@ -66,6 +69,13 @@ __device__ __forceinline__ uint64_t policy_evict_last()
 {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ uint64_t policy_evict_first()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
 
@@ -231,7 +241,9 @@ __device__ __forceinline__ void csr_tile(const CsrOp &A, const double *__restric
 // Uniform-row-length CSR (row_ptr[r] = L r, L % 4 == 0): G = L/4 lanes per row, each lane loads 4
 // consecutive entries with 16-B vector loads (val: 2 x double2, col: int4), U row groups in flight
 // per lane; products summed in entry order per lane, then a log2(G)-level shuffle tree.
-template <bool WIN>
+// XM: 0 gathers x from global memory, 1 from the tile's x window (xs[c - xs0]), 2 from the x ring
+// (xs[c mod XRING])
+template <int XM>
 __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__restrict__ x, const double *xs, int64_t xs0,
                                              int64_t r0, int rows, double *ys)
 {
@@ -242,7 +254,8 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
     const int sub = lane / G, li = lane - sub * G;
     const int stride = SNW * rpw;
     auto X = [&](int c) -> double {
-        if constexpr (WIN) return xs[c - xs0];
+        if constexpr (XM == 1) return xs[c - xs0];
+        else if constexpr (XM == 2) return xs[c & (XRING - 1)];
         else return __ldg(x + c);
     };
     for (int base = warp * rpw; base < rows; base += stride * U) {
@@ -285,10 +298,11 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
 
 // dynamic shared memory of spmv_stream (bytes): halo (or ys for CSR), CSR x window, per-warp dot
 // partials
-__host__ __device__ inline size_t spmv_smem_bytes(int halo_cap, int tile, int nd, int wcap = 0)
+__host__ __device__ inline size_t spmv_smem_bytes(int halo_cap, int tile, int nd, int wcap = 0, int ring = 0)
 {
     const int h = halo_cap > 0 ? halo_cap : tile;
-    return ((size_t)((h + 15) & ~15) + (size_t)((wcap + 15) & ~15) + (size_t)nd * SNW) * sizeof(double);
+    return ((size_t)((h + 15) & ~15) + (size_t)((wcap + 15) & ~15) + (size_t)(ring ? XRING : 0) +
+            (size_t)nd * SNW) * sizeof(double);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -314,9 +328,13 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
     if constexpr (IS_ST) hcap = halo_capacity(op.dim, op.nx, TILE_);
     int wcap = 0;
     if constexpr (!HALO) wcap = (op.wtile == TILE_) ? op.wcap : 0;
+    int ring = 0;
+    if constexpr (!HALO) ring = op.ring;
     double *hbuf = sm;                                    // halo (stencil/ident) or ys (CSR)
     double *xwin = sm + ((hcap + 15) & ~15);             // CSR x window (wcap doubles)
-    double *lacc = xwin + ((wcap + 15) & ~15);
+    double *xring = xwin + ((wcap + 15) & ~15);          // CSR x ring (XRING doubles)
+    double *lacc = xring + (ring ? XRING : 0);
+    __shared__ uint64_t rbar[2];                          // x ring: tile t's chunk on rbar[t & 1]
     __shared__ int64_t s_wstart[2];
     // CSR: TMA the x window of tile tl (its [tlo, thi] column range) if it fits
     auto issue_window = [&](int64_t wr0, int wrows, uint32_t par) {
@@ -336,6 +354,25 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive_expect_tx(&hbar, by);
             if (by) tma_load_1d(xwin, a.x + st, by, &hbar, policy_evict_last());
+        }
+    };
+    // x ring: copy x[lo, hi) (clamped to [0, ldx), even bounds) into ring slots lo mod XRING ..,
+    // split where the ring wraps; one mbarrier phase per call
+    auto issue_ring = [&](int64_t lo, int64_t hi, uint64_t *bar) {
+        int64_t st = 0;
+        uint32_t by = 0;
+        seg_range(lo, hi, a.ldx, st, by);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of the ring
+        mbar_arrive_expect_tx(bar, by);
+        const uint64_t pol = policy_evict_last();
+        int64_t c0 = st;
+        uint32_t left = by;
+        while (left) {
+            const int slot = (int)(c0 & (XRING - 1));
+            const uint32_t chunk = min(left, (uint32_t)(XRING - slot) * 8u);
+            tma_load_1d(xring + slot, a.x + c0, chunk, bar, pol);
+            c0 += chunk / 8;
+            left -= chunk;
         }
     };
     auto plan = [&](int64_t r0, int rows, HaloPlan &h) {
@@ -369,6 +406,12 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
                 if (cs < ce) issue_halo(cs, (int)min((int64_t)TILE_, ce - cs), 0);
             }
         } else {
+            if (!s_exit && ring) {
+                mbar_init(&rbar[0], 1);
+                mbar_init(&rbar[1], 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                if (cs < ce) issue_ring(cs - op.blo, cs + TILE_ + op.bhi, &rbar[0]);   // first tile's window
+            }
             if (!s_exit && wcap > 0) {
                 mbar_init(&hbar, 1);
                 asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -450,7 +493,18 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
         } else {
 #pragma unroll
             for (int p = 0; p < NP; p++) xr[p] = make_double2(0.0, 0.0);
-            if (wcap > 0) {
+            if (ring) {
+                // this tile needs x[r0 - blo, r0 + TILE + bhi): its new chunk was requested one tile
+                // ago (or in the prologue).  Request the next tile's chunk, whose ring slots held
+                // x[r0 - TILE - blo, r0 - blo) (previous tile only; its gathers are complete).  Two
+                // barriers: the one re-armed here was last waited on a tile ago, and every thread
+                // has passed that wait (tile-end barrier), so no waiter can miss a phase.
+                mbar_wait(&rbar[ht & 1], (ht >> 1) & 1);
+                if (tid == 0 && r1 < ce) issue_ring(r1 + op.bhi, r1 + TILE_ + op.bhi, &rbar[(ht + 1) & 1]);
+                ht++;
+                csr_tile_ell<2>(op, a.x, xring, 0, r0, rows, hbuf);
+                __syncthreads();                           // ring reads done, ys complete
+            } else if (wcap > 0) {
                 const uint32_t par = ht & 1;
                 ht++;
                 // the window decision is uniform per tile; read it once the copy has landed
@@ -458,14 +512,14 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
                 const int64_t ws = s_wstart[par];
                 auto nowait = [] {};
                 if (op.ell) {
-                    if (ws >= 0) csr_tile_ell<true>(op, a.x, xwin, ws, r0, rows, hbuf);
-                    else csr_tile_ell<false>(op, a.x, xwin, 0, r0, rows, hbuf);
+                    if (ws >= 0) csr_tile_ell<1>(op, a.x, xwin, ws, r0, rows, hbuf);
+                    else csr_tile_ell<0>(op, a.x, xwin, 0, r0, rows, hbuf);
                 } else if (ws >= 0) csr_tile<true>(op, a.x, xwin, ws, r0, rows, hbuf, nowait);
                 else csr_tile<false>(op, a.x, xwin, 0, r0, rows, hbuf, nowait);
                 __syncthreads();                           // window consumed, ys complete
                 if (tid == 0 && r1 < ce) issue_window(r1, (int)min((int64_t)TILE_, ce - r1), ht & 1);
             } else {
-                if (op.ell) csr_tile_ell<false>(op, a.x, xwin, 0, r0, rows, hbuf);
+                if (op.ell) csr_tile_ell<0>(op, a.x, xwin, 0, r0, rows, hbuf);
                 else csr_tile<false>(op, a.x, xwin, 0, r0, rows, hbuf, [] {});
                 __syncthreads();
             }

@@ -327,64 +327,80 @@ __global__ void __launch_bounds__(NT) maxabs_kernel(int64_t n, MaxAbsArgs a, Wor
     if (tid == 0) *wk.counter = 0u;
 }
 
-// ||A||_inf of a CSR matrix: rows summed sequentially in ascending column order (bit-exact with
-// a sequential reference), max over rows (exact).
-__global__ void __launch_bounds__(NT) csr_infnorm_kernel(CsrOp A, Work wk)
-{
-    __shared__ double wmax[NWARP];
-    __shared__ double bsum[1];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    double m = 0.0;
-    for (int64_t r = (int64_t)blockIdx.x * NT + tid; r < A.n; r += (int64_t)gridDim.x * NT) {
-        double s = 0.0;
-        for (int e = A.rp[r]; e < A.rp[r + 1]; e++) s = __dadd_rn(s, fabs(A.val[e]));
-        m = fmax(m, s);
-    }
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) wmax[warp] = m;
-    __syncthreads();
-    if (tid == 0) {
-        double t = 0.0;
-        for (int w = 0; w < NWARP; w++) t = fmax(t, wmax[w]);
-        bsum[0] = t;
-    }
-    __syncthreads();
-    if (!publish_partials(wk, bsum, 1)) return;
-    // publish_partials acquired the other CTAs' partials
-    if (warp == 0) {
-        double t = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) t = fmax(t, __ldcg(wk.part + b));
-        for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
-        if (lane == 0) wk.out_raw[0] = t;
-    }
-    __syncthreads();
-    if (tid == 0) *wk.counter = 0u;
-}
+// One pass over a CSR matrix (row_ptr, col, val), coalesced: each warp takes 32 consecutive rows,
+// copies their entries into shared memory (skewed: entry i at i + i/32, so that lanes walking rows
+// of equal length hit different banks) and each lane then walks its own row in order:
+//   ||A||_inf = max_r sum_e |a_re|   (summed sequentially in entry order: bit-exact with a
+//                                     sequential reference; the max is exact)
+//   uniform   = row_ptr[r] == L r for all r  (L = nnz / n, or -1)
+//   band      = max(r - col), max(col - r)
+// Rows of a group with more than CSRA_CAP entries are walked in global memory instead.
+constexpr int CSRA_CAP = 512;                  // staged entries per warp (32 rows of 16)
+constexpr int CSRA_NT = 128, CSRA_NW = CSRA_NT / 32;
+struct CsrAnalysis {
+    unsigned long long norm_bits;              // ||A||_inf (bits of a non-negative double)
+    int nonuniform, blo, bhi, pad;
+};
 
-// Uniform row length check: flag[0] stays 0 iff row_ptr[r] == L r for all r <= n.
-// Uniform row length check (flag[0] |= 1 if row_ptr[r] != L r for some r) and, assuming it holds,
-// the band: flag[1] = max(r - col), flag[2] = max(col - r) over all entries (entry e is in row e / L).
-__global__ void csr_uniform_check_kernel(int64_t n, const int32_t *__restrict__ rp, const int32_t *__restrict__ col,
-                                         int L, int *flag)
+__device__ __forceinline__ int clamp_band(int64_t d) { return d < 0 ? 0 : (d > 0x3fffffff ? 0x3fffffff : (int)d); }
+
+__global__ void __launch_bounds__(CSRA_NT) csr_analyze_kernel(CsrOp A, int L, CsrAnalysis *out)
 {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= n; r += stride)
-        if ((int64_t)rp[r] != (int64_t)L * r) atomicOr(flag, 1);
-    int lo = 0, hi = 0;
-    const int64_t nnz = n * L;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += stride) {
-        const int64_t d = (int64_t)col[e] - e / L;
-        const int64_t cap = 0x3fffffff;
-        lo = max(lo, (int)(-d < cap ? -d : cap));
-        hi = max(hi, (int)(d < cap ? d : cap));
+    constexpr int SK = CSRA_CAP + CSRA_CAP / 32;
+    __shared__ double sv[CSRA_NW][SK];
+    __shared__ int sc[CSRA_NW][SK];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n = A.n, ngroups = (n + 31) / 32;
+    double nrm = 0.0;
+    int bad = 0, blo = 0, bhi = 0;
+    for (int64_t g = (int64_t)blockIdx.x * CSRA_NW + warp; g < ngroups; g += (int64_t)gridDim.x * CSRA_NW) {
+        const int64_t r = g * 32 + lane;
+        const bool ok = r < n;
+        const int eb = ok ? A.rp[r] : 0, ee = ok ? A.rp[r + 1] : 0;
+        if (ok && L > 0 && ((int64_t)eb != (int64_t)L * r || (int64_t)ee != (int64_t)L * (r + 1))) bad = 1;
+        const int64_t rem = n - 1 - g * 32;
+        const int last = rem < 31 ? (int)rem : 31;
+        const int g0 = __shfl_sync(0xffffffffu, eb, 0), g1 = __shfl_sync(0xffffffffu, ee, last);
+        double s = 0.0;
+        int lo = 0, hi = 0;
+        if (g1 - g0 <= CSRA_CAP) {
+            for (int i = lane; i < g1 - g0; i += 32) {
+                const int k = i + (i >> 5);
+                sv[warp][k] = A.val[g0 + i];
+                sc[warp][k] = A.col[g0 + i];
+            }
+            __syncwarp();
+            for (int e = eb - g0; e < ee - g0; e++) {
+                const int k = e + (e >> 5);
+                s = __dadd_rn(s, fabs(sv[warp][k]));
+                const int64_t d = (int64_t)sc[warp][k] - r;
+                lo = max(lo, clamp_band(-d));
+                hi = max(hi, clamp_band(d));
+            }
+            __syncwarp();
+        } else {
+            for (int e = eb; e < ee; e++) {
+                s = __dadd_rn(s, fabs(A.val[e]));
+                const int64_t d = (int64_t)A.col[e] - r;
+                lo = max(lo, clamp_band(-d));
+                hi = max(hi, clamp_band(d));
+            }
+        }
+        nrm = fmax(nrm, s);
+        blo = max(blo, lo);
+        bhi = max(bhi, hi);
     }
     for (int o = 16; o > 0; o >>= 1) {
-        lo = max(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        blo = max(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+        bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
     }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMax(flag + 1, lo);
-        atomicMax(flag + 2, hi);
+    if (lane == 0) {
+        atomicMax(&out->norm_bits, (unsigned long long)__double_as_longlong(nrm));
+        if (bad) atomicOr(&out->nonuniform, 1);
+        atomicMax(&out->blo, blo);
+        atomicMax(&out->bhi, bhi);
     }
 }
 

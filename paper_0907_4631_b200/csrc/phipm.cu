@@ -890,40 +890,46 @@ int make_csr(phipm_ctx *c, const phipm_csr *A, CsrOp &op)
 // range fits CSR_WCAP doubles gather x from shared memory (stream.cuh)
 constexpr int CSR_WCAP = 10496;                             // 82 KB: band +-4096 around 2048 rows
 
-// Uniform row length (ELL-like CSR) detection: one pass over row_ptr; enables csr_tile_ell.
-int detect_csr_ell(phipm_ctx *c, CsrOp &op, int64_t nnz)
+// One analysis pass over a CSR matrix (csr_analyze_kernel): ||A||_inf (a1 setup, bit-exact), and
+// whether rows have a uniform length L (vectorised ELL path, PHIPM_CSR_ELL=0 disables) within a band
+// that fits the shared x ring (PHIPM_CSR_RING=0 disables).
+int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA)
 {
     op.ell = 0;
     op.ring = op.blo = op.bhi = 0;
-    static int env = -1;
-    if (env < 0) {
+    static int env_ell = -1, env_ring = -1;
+    if (env_ell < 0) {
         const char *e = getenv("PHIPM_CSR_ELL");
-        env = (e && e[0] == '0') ? 0 : 1;
+        env_ell = (e && e[0] == '0') ? 0 : 1;
+        e = getenv("PHIPM_CSR_RING");
+        env_ring = (e && e[0] == '0') ? 0 : 1;
     }
-    if (!env || op.n <= 0 || nnz % op.n) return PHIPM_OK;
-    const int64_t L = nnz / op.n;
-    if (L < 4 || L > 128 || (L % 4) || ((L / 4) & (L / 4 - 1))) return PHIPM_OK;   // L/4 a power of two
-    if (((uintptr_t)op.val & 15) || ((uintptr_t)op.col & 15)) return PHIPM_OK;
-    int *flag = reinterpret_cast<int *>(c->raw);             // 3 ints of the raw scratch
-    CK(cudaMemsetAsync(flag, 0, 3 * sizeof(int), c->stream));
-    const int grid = (int)std::min<int64_t>((op.n + 256) / 256, (int64_t)c->sm_count * 8);
-    csr_uniform_check_kernel<<<grid, 256, 0, c->stream>>>(op.n, op.rp, op.col, (int)L, flag);
+    if (op.n == 0) {
+        *normA = 0.0;
+        return PHIPM_OK;
+    }
+    const int64_t L = (nnz % op.n == 0 && nnz / op.n <= 128) ? nnz / op.n : -1;
+    CsrAnalysis *d = reinterpret_cast<CsrAnalysis *>(c->raw);
+    CK(cudaMemsetAsync(d, 0, sizeof(CsrAnalysis), c->stream));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((op.n + CSRA_NT - 1) / CSRA_NT, (int64_t)c->sm_count * 16));
+    ProfRec r;
+    prof_begin(c, r, PC_OTHER, 12.0 * (double)nnz + 4.0 * (double)(op.n + 1));
+    csr_analyze_kernel<<<grid, CSRA_NT, 0, c->stream>>>(op, (int)L, d);
+    prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
-    int h[3] = {1, 0, 0};
-    CK(cudaMemcpyAsync(h, flag, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    if (h[0] != 0) return PHIPM_OK;
+    CK(cudaMemcpyAsync(c->raw_h, d, sizeof(CsrAnalysis), cudaMemcpyDeviceToHost, c->stream));
+    int rc = sync(c);
+    if (rc) return rc;
+    CsrAnalysis h;
+    memcpy(&h, c->raw_h, sizeof(h));
+    memcpy(normA, &h.norm_bits, sizeof(double));
+    if (!env_ell || L < 4 || (L % 4) || ((L / 4) & (L / 4 - 1)) || h.nonuniform) return PHIPM_OK;
+    if (((uintptr_t)op.val & 15) || ((uintptr_t)op.col & 15)) return PHIPM_OK;
     op.ell = (int)L;
-    // banded: x from a shared-memory ring (PHIPM_CSR_RING=0 disables); bands rounded up to even
-    static int envr = -1;
-    if (envr < 0) {
-        const char *e = getenv("PHIPM_CSR_RING");
-        envr = (e && e[0] == '0') ? 0 : 1;
-    }
-    op.blo = (h[1] + 1) & ~1;
-    op.bhi = (h[2] + 1) & ~1;
-    op.ring = (envr && 2 * SNT * 2 + op.blo + op.bhi <= XRING) ? 1 : 0;
+    op.blo = (h.blo + 1) & ~1;
+    op.bhi = (h.bhi + 1) & ~1;
+    op.ring = (env_ring && 2 * SNT * 2 + op.blo + op.bhi <= XRING) ? 1 : 0;
     return PHIPM_OK;
 }
 
@@ -1211,19 +1217,9 @@ int phipm_solve_csr(phipm_ctx *c, double t, const phipm_csr *A, int p, const dou
     if (rc) return rc;
     c->prof = o.profile != 0;
     c->trace = o.profile >= 2;
-    // ||A||_inf (a1 setup, once per call)
-    const int grid = grid_for(c, (op.n + NT - 1) / NT, c->occ_axpy);
-    ProfRec r;
-    prof_begin(c, r, PC_OTHER, 0.0);
-    csr_infnorm_kernel<<<grid, NT, 0, c->stream>>>(op, make_work(c));
-    prof_end(c, r);
-    c->acc.launches++;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(c->raw_h, c->raw, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    rc = sync(c);
-    if (rc) return rc;
-    const double normA = c->raw_h[0];
-    rc = detect_csr_ell(c, op, A->nnz);
+    // ||A||_inf (a1 setup, once per call) and the operator's layout, one pass
+    double normA = 0.0;
+    rc = analyze_csr(c, op, A->nnz, &normA);
     if (rc) return rc;
     rc = enable_csr_window(c, op);
     if (rc) return rc;
@@ -1339,7 +1335,8 @@ int phipm_spmv_csr(phipm_ctx *c, const phipm_csr *A, const double *x, double *y)
     if (rc) return rc;
     if (op.n > c->n_max) return set_err(c, PHIPM_EINVAL, "n > n_max");
     CK(cudaMemcpyAsync(c->Y, x, op.n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    rc = detect_csr_ell(c, op, A->nnz);
+    double normA = 0.0;
+    rc = analyze_csr(c, op, A->nnz, &normA);
     if (rc) return rc;
     rc = enable_csr_window(c, op);
     if (rc) return rc;
@@ -1396,15 +1393,7 @@ int phipm_inf_norm_csr(phipm_ctx *c, const phipm_csr *A, double *result)
     CsrOp op;
     int rc = make_csr(c, A, op);
     if (rc) return rc;
-    const int grid = grid_for(c, (op.n + NT - 1) / NT, c->occ_axpy);
-    csr_infnorm_kernel<<<grid, NT, 0, c->stream>>>(op, make_work(c));
-    c->acc.launches++;
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(c->raw_h, c->raw, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    rc = sync(c);
-    if (rc) return rc;
-    *result = c->raw_h[0];
-    return PHIPM_OK;
+    return analyze_csr(c, op, A->nnz, result);
 }
 
 int phipm_expm(phipm_ctx *c, int K, const double *A, double *E)
@@ -1512,9 +1501,7 @@ int phipm_krylov_csr(phipm_ctx *c, const phipm_csr *A, const double *v, int m, c
     int rc = make_csr(c, A, op);
     if (rc) return rc;
     double normA = 0.0;
-    rc = phipm_inf_norm_csr(c, A, &normA);
-    if (rc) return rc;
-    rc = detect_csr_ell(c, op, A->nnz);
+    rc = analyze_csr(c, op, A->nnz, &normA);
     if (rc) return rc;
     rc = enable_csr_window(c, op);
     if (rc) return rc;

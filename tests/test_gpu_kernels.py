@@ -69,6 +69,27 @@ def test_spmv_csr_irregular_rows(ctx, orc):
     ref = orc.spmv((rp, col, val), x)
     absAx = orc.spmv((rp, col, np.abs(val)), np.abs(x))
     assert np.all(np.abs(y - ref) <= 1e-13 * absAx)
+    # the analysis pass: groups of 32 rows above and below the staging cap (512 entries)
+    assert ctx.inf_norm_csr((to_dev(rp), to_dev(col), to_dev(val))) == orc.inf_norm((rp, col, val))
+
+
+@pytest.mark.parametrize("n,L,band", [
+    (148 * 4096 * 3 + 77, 8, 2048),     # ring, several tiles per CTA, ragged tail
+    (600_011, 16, 4096),                 # band at the ring limit (2 TILE + 8192 = XRING)
+    (300_000, 4, 6143),                  # odd band (rounded up to even), 2048-row tiles
+    (200_000, 8, 7000),                  # band too wide for the ring: global gathers
+    (5_000, 16, 64),                     # small problem, one tile
+])
+def test_spmv_csr_banded_ring(ctx, orc, n, L, band):
+    rng = np.random.default_rng(n + L)
+    rp, col, val = W.random_banded_csr(rng, n, band, k_off=L - 1)
+    x = rng.standard_normal(n)
+    A = (to_dev(rp), to_dev(col), to_dev(val))
+    y = ctx.spmv_csr(A, to_dev(x)).cpu().numpy()
+    ref = orc.spmv((rp, col, val), x)
+    absAx = orc.spmv((rp, col, np.abs(val)), np.abs(x))
+    assert np.all(np.abs(y - ref) <= 1e-13 * absAx)
+    assert ctx.inf_norm_csr(A) == orc.inf_norm((rp, col, val))
 
 
 @pytest.mark.parametrize("n", [1, 31, 1024, 1025, 300_007, 4_194_304])
@@ -192,3 +213,4 @@ def test_spmv_csr_uniform_rows(ctx, orc, L, n):
     ref = orc.spmv((rp, col, val), x)
     absAx = orc.spmv((rp, col, np.abs(val)), np.abs(x))
     assert np.all(np.abs(y - ref) <= 1e-13 * absAx)
+    assert ctx.inf_norm_csr((to_dev(rp), to_dev(col), to_dev(val))) == orc.inf_norm((rp, col, val))

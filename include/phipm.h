@@ -65,8 +65,15 @@ typedef struct {
                                 arithmetic; the default) */
 #define PHIPM_ORTH_CGS2  1   /* CGS with one full re-orthogonalisation pass every step */
 
+/* Method for exp(Hhat) (Eq. 8: scaling and squaring).  Both reach unit-
+ * roundoff backward error; the oracle always uses Pade-13. */
+#define PHIPM_EXPM_TAYLOR  0 /* degree 8/12/16 Taylor by Paterson-Stockmeyer, all products on the
+                                fp64 tensor cores, squarings from ||A^k||^(1/k) (the default) */
+#define PHIPM_EXPM_PADE13  1 /* the paper's [13/13] Pade, theta_13 = 5.37, with a pivoted
+                                Gauss-Jordan solve (V - U) X = (V + U) */
+
 /* Options.  Defaults (phipm_default_opts): tol 1e-7, m_init 10 (Alg. 3),
- * m_max 100, symmetric 0, fixed_m 0, eq6_variant 0, orth CGS, profile 0. */
+ * m_max 100, symmetric 0, fixed_m 0, eq6_variant 0, orth CGS, profile 0, expm_method Taylor. */
 typedef struct {
     double tol;          /* Tol of Eq. (taunew) P:588-593 (absolute 2-norm error per unit time) */
     int m_init;          /* initial Krylov dimension m (Alg. 3) */
@@ -77,6 +84,7 @@ typedef struct {
     int orth;            /* PHIPM_ORTH_* */
     int profile;         /* 1: time every kernel class with CUDA events (phipm_get_profile);
                             2: also record every launch (phipm_get_trace) */
+    int expm_method;     /* PHIPM_EXPM_* */
 } phipm_opts;
 
 /* Statistics (the paper's stats(1..4), plus the Krylov dimension). */
@@ -114,6 +122,10 @@ typedef struct {
 } phipm_trace_rec;
 
 void phipm_default_opts(phipm_opts *opts);
+
+/* Method used by the kernel-level entry points phipm_expm and phipm_phi_pair (solves take
+ * opts.expm_method).  PHIPM_EINVAL for an unknown method. */
+int phipm_set_expm_method(phipm_ctx *ctx, int method);
 
 /* Create a context that can solve problems with n <= n_max, m_max <= m_max, p <= p_max.
  * Allocates the device workspace (Krylov basis (m_max+1) x n_max, w vectors, small matrices,

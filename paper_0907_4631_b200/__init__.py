@@ -22,6 +22,7 @@ __all__ = ["Context", "Stencil", "Stats", "Profile", "PhipmError", "lib", "LIB",
 
 OK, EINVAL, ENOMEM, ECUDA, ESTEP, ENONFINITE, ESINGULAR = 0, 1, 2, 3, 4, 5, 6
 ORTH_CGS, ORTH_CGS2 = 0, 1
+EXPM_TAYLOR, EXPM_PADE13 = 0, 1
 
 
 class PhipmError(RuntimeError):
@@ -43,7 +44,8 @@ class _Stencil(C.Structure):
 
 class _Opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("m_init", C.c_int), ("m_max", C.c_int), ("symmetric", C.c_int),
-                ("fixed_m", C.c_int), ("eq6_variant", C.c_int), ("orth", C.c_int), ("profile", C.c_int)]
+                ("fixed_m", C.c_int), ("eq6_variant", C.c_int), ("orth", C.c_int), ("profile", C.c_int),
+                ("expm_method", C.c_int)]
 
 
 class _Stats(C.Structure):
@@ -111,6 +113,7 @@ def lib():
         P = C.POINTER
         sig = {
             "phipm_default_opts": (None, [P(_Opts)]),
+            "phipm_set_expm_method": (i32, [vp, i32]),
             "phipm_create": (i32, [P(vp), i64, i32, i32, vp]),
             "phipm_destroy": (None, [vp]),
             "phipm_strerror": (C.c_char_p, [i32]),
@@ -143,7 +146,7 @@ def lib():
 
 
 EXPORTED = [
-    "phipm_default_opts", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
+    "phipm_default_opts", "phipm_set_expm_method", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
     "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_solve_csr", "phipm_solve_stencil",
     "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_stencil_nnz",
     "phipm_csr_from_stencil", "phipm_spmv_csr", "phipm_spmv_stencil", "phipm_dot", "phipm_inf_norm_csr",
@@ -211,7 +214,7 @@ class Context:
 
     # ---------------------------------------------------------------- options / profile
     def opts(self, tol=1e-7, m_init=10, m_max=None, symmetric=False, fixed_m=False,
-             eq6_variant=False, orth=ORTH_CGS, profile=0) -> _Opts:
+             eq6_variant=False, orth=ORTH_CGS, profile=0, expm_method=EXPM_TAYLOR) -> _Opts:
         o = _Opts()
         self._L.phipm_default_opts(C.byref(o))
         o.tol = tol
@@ -222,7 +225,12 @@ class Context:
         o.eq6_variant = int(bool(eq6_variant))
         o.orth = int(orth)
         o.profile = int(profile)
+        o.expm_method = int(expm_method)
         return o
+
+    def set_expm_method(self, method):
+        """Method of expm() / phi_pair() (solves take opts(expm_method=...))."""
+        self._check(self._L.phipm_set_expm_method(self._h, int(method)))
 
     def profile(self) -> dict:
         p = _Profile()

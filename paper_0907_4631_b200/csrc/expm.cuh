@@ -32,6 +32,7 @@ struct AttemptResult {
 
 struct ExpmArgs {
     int mode;          // 0: phipm attempt; 1: plain expm of Ain; 2: phi pair of H (mu = m)
+    int method;        // PHIPM_EXPM_TAYLOR (0) or PHIPM_EXPM_PADE13 (1)
     int m, p;          // requested Krylov dimension, phi order
     int tridiag;       // Lanczos: H is tridiagonal, read only the band
     double tau;
@@ -122,6 +123,198 @@ struct EpiBlock {
     }
 };
 
+// optional phase timestamps (PHIPM_EXPM_CLOCKS)
+#define EXPM_CLK(i) \
+    if (clk && threadIdx.x == 0) clk[i] = clock64();
+
+__device__ __forceinline__ double block_max_colsum(int K, int ld, const double *A, double *sred)
+{
+    // ||A||_1 = max_j sum_i |a_ij|
+    double m = 0.0;
+    for (int jc = threadIdx.x; jc < K; jc += blockDim.x) {
+        double s = 0.0;
+        for (int i = 0; i < K; i++) s += fabs(A[i + (size_t)jc * ld]);
+        m = fmax(m, s);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = m;
+    __syncthreads();
+    double r = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) r = fmax(r, sred[w]);
+    __syncthreads();
+    return r;
+}
+
+// Pade [13/13] coefficients c_j = (26-j)! 13! / (26! j! (13-j)!), c_0 = 1, via the ratio
+// c_{j+1}/c_j = (13-j)/((26-j)(j+1)).
+__device__ __forceinline__ void pade13(double *c)
+{
+    c[0] = 1.0;
+    for (int j = 0; j < 13; j++) c[j + 1] = c[j] * (double)(13 - j) / ((double)(26 - j) * (double)(j + 1));
+}
+
+// PHIPM_EXPM_PADE13: the paper's method: [13/13] Pade with s = ceil_+(log2(||A||_1 /
+// 5.37)) squarings; U, V from A^2, A^4, A^6 (6 DMMA products), then (V - U) X = (V + U) by
+// Gauss-Jordan with partial pivoting (implicit: no row interchanges, pivot row of column c is
+// prow[c]).  One barrier per column: warp 0 updates the next pivot column, searches its pivot and
+// prepares the multipliers while the other warps eliminate the current column.  K dependent pivot
+// steps on one SM: the latency the Taylor method avoids.  Returns exp(M0); status 0/5/6.
+__device__ double *cta_expm_pade(int K, int Kp, int ld, double *M0, double *M1, double *M2, double *M3, double *M4, double *M5,
+                            double *sred, int *s_int, double *fcol, int *status, long long *clk)
+{
+    const int KK = ld * Kp, t = threadIdx.x;         // whole buffers (padding rows are never read)
+    double c[14];
+    pade13(c);
+    // scaling: s = ceil_+(log2(||A||_1 / 5.37)) (theta_13 = 5.37 as printed, R26)
+    const double nrm = block_max_colsum(Kp, ld, M0, sred);
+    int s = 0;
+    if (nrm > 0.0) {
+        const double l = ceil(log2(nrm / 5.37));
+        s = l > 0.0 ? (int)l : 0;
+    }
+    if (!isfinite(nrm)) { *status = 5; return M0; }
+    const double sc = ldexp(1.0, -s);
+    for (int e = t; e < KK; e += blockDim.x) M0[e] *= sc;
+    __syncthreads();
+    cta_matmul(Kp, ld, M0, M0, M1);            // A2
+    cta_matmul(Kp, ld, M1, M1, M2);            // A4
+    cta_matmul(Kp, ld, M2, M1, M3);            // A6
+    EXPM_CLK(2)
+    // U = A [A6 (c13 A6 + c11 A4 + c9 A2) + c7 A6 + c5 A4 + c3 A2 + c1 I]
+    for (int e = t; e < KK; e += blockDim.x) M4[e] = c[13] * M3[e] + c[11] * M2[e] + c[9] * M1[e];
+    __syncthreads();
+    cta_matmul(Kp, ld, M3, M4, M5);
+    for (int e = t; e < KK; e += blockDim.x) M5[e] = M5[e] + c[7] * M3[e] + c[5] * M2[e] + c[3] * M1[e];
+    __syncthreads();
+    for (int i = t; i < Kp; i += blockDim.x) M5[i * (ld + 1)] += c[1];
+    __syncthreads();
+    cta_matmul(Kp, ld, M0, M5, M4);            // U in M4
+    // V = A6 (c12 A6 + c10 A4 + c8 A2) + c6 A6 + c4 A4 + c2 A2 + c0 I
+    for (int e = t; e < KK; e += blockDim.x) M5[e] = c[12] * M3[e] + c[10] * M2[e] + c[8] * M1[e];
+    __syncthreads();
+    cta_matmul(Kp, ld, M3, M5, M0);            // A no longer needed
+    for (int e = t; e < KK; e += blockDim.x) M0[e] = M0[e] + c[6] * M3[e] + c[4] * M2[e] + c[2] * M1[e];
+    __syncthreads();
+    for (int i = t; i < Kp; i += blockDim.x) M0[i * (ld + 1)] += c[0];   // V
+    __syncthreads();
+    // P = V + U (M1), Q = V - U (M2)
+    for (int e = t; e < KK; e += blockDim.x) {
+        const double v = M0[e], u = M4[e];
+        M1[e] = v + u;
+        M2[e] = v - u;
+    }
+    __syncthreads();
+    EXPM_CLK(3)
+    // Gauss-Jordan with partial pivoting: Q X = P, implicit pivoting (no row interchanges; the
+    // pivot row of column c is prow[c]), ONE barrier per column: warp 0 updates the next pivot
+    // column first, searches its pivot among the unused rows and prepares the multipliers while
+    // the other warps eliminate the current column from the rest of [Q | P].
+    double *Q = M2, *P = M1;
+    int *prow = s_int + 8, *used = s_int + 8 + EXPM_KMAX;
+    double *fb = fcol;                                    // 2 x EXPM_KMAX multipliers
+    __shared__ int s_pr[2], s_bad;
+    __shared__ double s_rq[EXPM_KMAX];
+    const int warp = t >> 5, lane = t & 31;
+    for (int r = t; r < K; r += blockDim.x) used[r] = 0;
+    if (t == 0) s_bad = 0;
+    __syncthreads();
+    auto lookahead = [&](int c, int b) {                 // warp 0; column c of Q is final
+        double best = -1.0;
+        int bi = K;
+        for (int r = lane; r < K; r += 32)
+            if (!used[r]) {
+                const double a = fabs(Q[r + (size_t)c * ld]);
+                if (a > best) { best = a; bi = r; }
+            }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (!(best >= 1e-300) || bi >= K) {
+            if (lane == 0) s_bad = 1;
+            return;
+        }
+        const double rp = 1.0 / Q[bi + (size_t)c * ld];
+        for (int r = lane; r < K; r += 32) fb[b * EXPM_KMAX + r] = (r == bi) ? 0.0 : Q[r + (size_t)c * ld] * rp;
+        __syncwarp();
+        if (lane == 0) {
+            s_pr[b] = bi;
+            used[bi] = 1;
+            prow[c] = bi;
+        }
+        __syncwarp();
+    };
+    if (warp == 0) lookahead(0, 0);
+    __syncthreads();
+    const int t2 = t - 32, n2 = (int)blockDim.x - 32;
+    const int er = t2 % K, eg = t2 / K, neg = n2 / K;     // elimination warps: fixed row, column group
+    for (int col = 0; col < K; col++) {
+        if (s_bad) { *status = 6; return P; }
+        const int b = col & 1;
+        const int pr = s_pr[b];
+        const double *f = fb + b * EXPM_KMAX;
+        if (warp == 0) {
+            if (col + 1 < K) {
+                const int j = col + 1;
+                const double pv = Q[pr + (size_t)j * ld];
+                for (int r = lane; r < K; r += 32)
+                    if (r != pr) Q[r + (size_t)j * ld] -= f[r] * pv;
+                __syncwarp();
+                lookahead(col + 1, b ^ 1);
+            }
+        } else if (eg < neg && er != pr) {
+            const double fr = f[er];
+            if (fr != 0.0) {
+                // Q columns col+2 .. K-1 and P columns 0 .. K-1 owned by this thread's column group,
+                // four loads in flight before the stores
+                auto rank1 = [&](double *M, int j) {
+                    for (; j + 3 * neg < K; j += 4 * neg) {
+                        const double p0 = M[pr + (size_t)j * ld], p1 = M[pr + (size_t)(j + neg) * ld];
+                        const double p2 = M[pr + (size_t)(j + 2 * neg) * ld], p3 = M[pr + (size_t)(j + 3 * neg) * ld];
+                        const double x0 = M[er + (size_t)j * ld], x1 = M[er + (size_t)(j + neg) * ld];
+                        const double x2 = M[er + (size_t)(j + 2 * neg) * ld], x3 = M[er + (size_t)(j + 3 * neg) * ld];
+                        M[er + (size_t)j * ld] = x0 - fr * p0;
+                        M[er + (size_t)(j + neg) * ld] = x1 - fr * p1;
+                        M[er + (size_t)(j + 2 * neg) * ld] = x2 - fr * p2;
+                        M[er + (size_t)(j + 3 * neg) * ld] = x3 - fr * p3;
+                    }
+                    for (; j < K; j += neg) M[er + (size_t)j * ld] -= fr * M[pr + (size_t)j * ld];
+                };
+                rank1(Q, col + 2 + eg);
+                rank1(P, eg);
+            }
+        }
+        __syncthreads();
+    }
+    // X[c, :] = P[prow(c), :] / Q[prow(c), c]   (the pivot row's diagonal value is final)
+    for (int c = t; c < K; c += blockDim.x) s_rq[c] = 1.0 / Q[prow[c] + (size_t)c * ld];
+    __syncthreads();
+    double *Xo = M3;
+    for (int e = t; e < K * K; e += blockDim.x) {
+        const int c = e % K, j = e / K;
+        Xo[c + (size_t)j * ld] = P[prow[c] + (size_t)j * ld] * s_rq[c];
+    }
+    // padding block of X: identity (Q and P were identity there)
+    for (int e = t; e < Kp * Kp; e += blockDim.x) {
+        const int c = e % Kp, j = e / Kp;
+        if (c >= K || j >= K) Xo[c + (size_t)j * ld] = (c == j) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    P = Xo;
+    EXPM_CLK(4)
+    // squaring
+    double *X = P, *T = M4;
+    for (int q = 0; q < s; q++) {
+        cta_matmul(Kp, ld, X, X, T);
+        double *tmp = X;
+        X = T;
+        T = tmp;
+    }
+    EXPM_CLK(5)
+    return X;
+}
+
 // Taylor degrees evaluable from A, A^2, A^3, A^4 by Paterson-Stockmeyer (m = 4 r), the products
 // they cost including the three powers, and their backward-error thresholds theta_m: the largest
 // alpha with sum_{k>m} |c_k| alpha^(k-1) <= 2^-53 for h_m(x) = log(exp(-x) T_m(x)) = sum c_k x^k
@@ -152,8 +345,6 @@ __device__ constexpr double TAYLOR_INVFACT[17] = {
 __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, double *M2, double *M3, double *M4, double *M5,
                             double *sred, int *status, long long *clk)
 {
-#define EXPM_CLK(i) \
-    if (clk && threadIdx.x == 0) clk[i] = clock64();
     (void)K;
     const int KK = ld * Kp, t = threadIdx.x;         // whole buffers (padding rows are never read)
     cta_matmul(Kp, ld, M0, M0, M1);            // A^2
@@ -252,6 +443,8 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
 {
     extern __shared__ double esm[];
     __shared__ double sred[3 * (EXPM_NT / 32)];
+    __shared__ int s_int[8 + 2 * EXPM_KMAX];           // Pade: pivot rows, used flags
+    __shared__ double fcol[2 * EXPM_KMAX];              // Pade: multipliers
     __shared__ int s_mu;
     const int t = threadIdx.x;
     pdl_wait();
@@ -338,7 +531,8 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
     __syncthreads();
     if (a.clk && t == 0) a.clk[1] = clock64();
     int status = 0;
-    double *E = cta_expm(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, &status, a.clk);
+    double *E = a.method == 1 ? cta_expm_pade(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, s_int, fcol, &status, a.clk)
+                              : cta_expm(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, &status, a.clk);
     if (t == 0 && status) s_status = status;
     __syncthreads();
     status = s_status;

@@ -80,6 +80,7 @@ struct phipm_ctx {
     std::vector<cudaEvent_t> pool;
     phipm_profile acc{};
     int seq = 0;
+    int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     char err[512] = {0};
 };
 
@@ -720,6 +721,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             ExpmArgs ea;
             memset(&ea, 0, sizeof(ea));
             ea.mode = 0;
+            ea.method = o.expm_method;
             ea.tridiag = P.symmetric ? 1 : 0;
             ea.m = m;
             ea.p = p;
@@ -975,6 +977,8 @@ int check_common(phipm_ctx *c, double t, int64_t n, int p, const double *const *
     if (!(o.tol > 0.0)) return set_err(c, PHIPM_EINVAL, "tol must be > 0");
     if (o.m_max > c->m_max) return set_err(c, PHIPM_EINVAL, "opts.m_max %d > context m_max %d", o.m_max, c->m_max);
     if (o.m_init < 1 || o.m_init > o.m_max) return set_err(c, PHIPM_EINVAL, "m_init must be in [1, m_max]");
+    if (o.expm_method != PHIPM_EXPM_TAYLOR && o.expm_method != PHIPM_EXPM_PADE13)
+        return set_err(c, PHIPM_EINVAL, "unknown expm_method %d", o.expm_method);
     if (o.orth != PHIPM_ORTH_CGS && o.orth != PHIPM_ORTH_CGS2) return set_err(c, PHIPM_EINVAL, "bad orth");
     return PHIPM_OK;
 }
@@ -994,6 +998,13 @@ phipm_opts resolve_opts(const phipm_opts *o)
 
 extern "C" {
 
+int phipm_set_expm_method(phipm_ctx *c, int method)
+{
+    if (!c || (method != PHIPM_EXPM_TAYLOR && method != PHIPM_EXPM_PADE13)) return PHIPM_EINVAL;
+    c->expm_method = method;
+    return PHIPM_OK;
+}
+
 void phipm_default_opts(phipm_opts *o)
 {
     if (!o) return;
@@ -1005,6 +1016,7 @@ void phipm_default_opts(phipm_opts *o)
     o->eq6_variant = 0;
     o->orth = PHIPM_ORTH_CGS;
     o->profile = 0;
+    o->expm_method = PHIPM_EXPM_TAYLOR;
 }
 
 const char *phipm_strerror(int s)
@@ -1402,6 +1414,7 @@ int phipm_expm(phipm_ctx *c, int K, const double *A, double *E)
     ExpmArgs a;
     memset(&a, 0, sizeof(a));
     a.mode = 1;
+    a.method = c->expm_method;
     a.K = K;
     a.Ain = A;
     a.Eout = E;
@@ -1424,6 +1437,7 @@ int phipm_phi_pair(phipm_ctx *c, int mu, const double *H, int ldh, double tau, i
     ExpmArgs a;
     memset(&a, 0, sizeof(a));
     a.mode = 2;
+    a.method = c->expm_method;
     a.m = mu;
     a.p = p;
     a.tau = tau;

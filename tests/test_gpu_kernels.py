@@ -102,9 +102,16 @@ def test_dot(ctx, orc, n):
     assert d == ctx.dot(to_dev(x), to_dev(y))
 
 
+@pytest.fixture(params=[0, 1], ids=["taylor", "pade13"])
+def method(request, ctx):
+    ctx.set_expm_method(request.param)
+    yield request.param
+    ctx.set_expm_method(0)
+
+
 @pytest.mark.parametrize("K,norm", [(1, 0.5), (2, 3.0), (16, 40.0), (43, 300.0), (68, 20.0), (69, 20.0),
                                     (105, 80.0)])
-def test_expm(ctx, orc, K, norm):
+def test_expm(ctx, orc, method, K, norm):
     import torch
     rng = np.random.default_rng(K)
     A = rng.standard_normal((K, K))
@@ -115,7 +122,7 @@ def test_expm(ctx, orc, K, norm):
     assert np.linalg.norm(E - R) <= 1e-12 * np.linalg.norm(R) * max(1.0, norm / 5)
 
 
-def test_expm_special(ctx):
+def test_expm_special(ctx, method):
     import torch
     Z = ctx.expm(torch.zeros((5, 5), dtype=torch.float64, device="cuda")).cpu().numpy()
     assert np.array_equal(Z, np.eye(5))
@@ -124,7 +131,7 @@ def test_expm_special(ctx):
 
 
 @pytest.mark.parametrize("mu,p,tau", [(1, 0, 1.0), (1, 3, 0.5), (10, 2, 0.3), (40, 4, 0.01), (64, 1, 0.02)])
-def test_phi_pair(ctx, orc, mu, p, tau):
+def test_phi_pair(ctx, orc, method, mu, p, tau):
     import torch
     rng = np.random.default_rng(mu * 10 + p)
     H = np.triu(rng.standard_normal((mu, mu)), -1) * 30.0
@@ -136,7 +143,7 @@ def test_phi_pair(ctx, orc, mu, p, tau):
     assert nh == pytest.approx(rnh, rel=1e-15)
 
 
-def test_phi_pair_closed_forms(ctx):
+def test_phi_pair_closed_forms(ctx, method):
     import torch
     for z in (-3.0, -1.0, 1.0, 3.0):
         a, b, _ = ctx.phi_pair(torch.tensor([[z]], dtype=torch.float64, device="cuda"), 1.0, 1)

@@ -54,6 +54,18 @@ def test_solve_parity_small(ctx, orc, name, path):
     assert relerr(wg, wo) <= parity_bound(Pb.tol), (sg, so)
 
 
+@pytest.mark.parametrize("name,path", [("c1_mini", "stencil"), ("c3_mini", "stencil"), ("c5_mini", "csr"),
+                                       ("c1", "csr"), ("c3_med", "stencil"), ("c5_med", "csr")])
+def test_solve_parity_pade13(ctx, orc, name, path):
+    # the paper's expm (Pade-13 + pivoted solve) on the GPU: same parity bar as the default Taylor
+    import paper_0907_4631_b200 as P
+    Pb = W.make(name)
+    wg, sg = run_gpu(ctx, Pb, path, expm_method=P.EXPM_PADE13)
+    wo, so = run_oracle(orc, Pb)
+    assert sg.t_reached == Pb.t
+    assert relerr(wg, wo) <= parity_bound(Pb.tol), (sg, so)
+
+
 FULL = [("c1", "csr"), ("c1", "stencil"), ("c2", "csr"), ("c2", "stencil"), ("c3", "stencil"),
         ("c4", "stencil"), ("c5", "csr")]
 

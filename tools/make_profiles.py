@@ -24,7 +24,8 @@ def read_ncu_csv(path):
 
 
 def short(k):
-    for key in ("spmv_stream_kernel", "axpy_stream_kernel", "expm_kernel", "maxabs_kernel", "csr_infnorm_kernel"):
+    for key in ("spmv_stream_kernel", "axpy_stream_kernel", "expm_kernel", "maxabs_kernel", "csr_analyze_kernel",
+                "krylov_small_kernel"):
         if key in k:
             return key + ("<Stencil>" if "StencilOp" in k else "<Csr>" if "CsrOp" in k else "")
     return k[:40]
@@ -51,10 +52,12 @@ if os.path.exists(p):
             f.write(f"{k:34s} {n:8d} {us:10.1f} {100 * us / tot:6.1f}%\n")
     os.system(f"cp {p} {dst}/launches_c3.csv")
 
-# 2) DRAM traffic per launch of each kernel class (one solve of c3)
-p = os.path.join(src, "pf_dram_c3.csv")
+# 2) DRAM traffic per launch of each kernel class (exactly one solve: ncu --profile-from-start off)
 traffic = {}
-if os.path.exists(p):
+for cfg in ("c3", "c4", "c5"):
+    p = os.path.join(src, f"pf_dram_{cfg}.csv")
+    if not os.path.exists(p):
+        continue
     d = read_ncu_csv(p)
     per = collections.defaultdict(dict)
     for r in d:
@@ -66,21 +69,26 @@ if os.path.exists(p):
         per[r["ID"]]["kernel"] = short(r["Kernel Name"])
     cls = collections.defaultdict(list)
     for rid, m in per.items():
-        cls[m["kernel"]].append(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0))
-    with open(os.path.join(dst, "dram_traffic_c3.txt"), "w") as f:
-        f.write("ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum  (one c3 solve)\n")
-        for k, v in cls.items():
-            f.write(f"{k:34s} launches {len(v):4d}  avg DRAM bytes/launch {sum(v) / len(v) / 1e6:9.2f} MB\n")
-    sp = cls.get("spmv_stream_kernel<Stencil>")
+        cls[m["kernel"]].append((m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0),
+                                 m.get("gpu__time_duration.sum", 0)))
+    with open(os.path.join(dst, f"dram_traffic_{cfg}.txt"), "w") as f:
+        f.write(f"ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
+                f"gpu__time_duration.sum  (exactly one {cfg} solve; cold-cache serialised launches)\n")
+        for k, v in sorted(cls.items(), key=lambda x: -sum(t for _, t in x[1])):
+            by = [b for b, _ in v]
+            us = [t for _, t in v]
+            f.write(f"{k:34s} launches {len(v):4d}  avg DRAM bytes/launch {sum(by) / len(by) / 1e6:9.2f} MB"
+                    f"  avg {sum(us) / len(us):8.1f} us  total {sum(us):9.1f} us\n")
+    sp = [b for b, _ in cls.get("spmv_stream_kernel<Stencil>", []) or cls.get("spmv_stream_kernel<Csr>", [])]
     if sp:
-        traffic["c3"] = {"kernel_class": "spmv_dot", "dram_bytes_per_launch": sum(sp) / len(sp),
-                         "launches": len(sp), "source": f"profiles/{rnd}/dram_traffic_c3.txt"}
-    os.system(f"cp {p} {dst}/dram_c3.csv")
+        traffic[cfg] = {"kernel_class": "spmv_dot", "dram_bytes_per_launch": sum(sp) / len(sp),
+                        "launches": len(sp), "source": f"profiles/{rnd}/dram_traffic_{cfg}.txt"}
+    os.system(f"cp {p} {dst}/dram_{cfg}.csv")
 if traffic:
     json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
 
 # 3) --set full summaries of the top kernels
-for name in ("pf_full_c3_spmv", "pf_full_c3_axpy"):
+for name in ("pf_full_c3_spmv", "pf_full_c3_axpy", "pf_full_c4_spmv", "pf_full_c5_spmv", "pf_full_c3_expm"):
     p = os.path.join(src, name + ".ncu-rep")
     if os.path.exists(p):
         with open(os.path.join(dst, name.replace("pf_", "") + ".txt"), "w") as f:
@@ -90,6 +98,16 @@ for name in ("pf_full_c3_spmv", "pf_full_c3_axpy"):
                     if k not in ("kernel", "stalls"):
                         f.write(f"  {k:62s} {v[0]:>16s} {v[1]}\n")
                 f.write(f"  warp stall samples (%): {d['stalls']}\n")
+# 4) bench lines and in-kernel timelines
+for cfg in ("c1", "c2", "c3", "c4", "c5"):
+    p = os.path.join(src, f"pf_bench_{cfg}.json.log")
+    if os.path.exists(p):
+        lines = [x for x in open(p) if x.startswith("{")]
+        if lines:
+            open(os.path.join(dst, f"bench_{cfg}.json"), "w").write(lines[-1])
+    p = os.path.join(src, f"kclock_{cfg}.txt")
+    if os.path.exists(p):
+        os.system(f"cp {p} {dst}/")
 for extra in ("stream_roof.txt", "q_trace.txt", "rpt.txt"):
     p = os.path.join(src, extra)
     if os.path.exists(p):

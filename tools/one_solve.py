@@ -13,16 +13,23 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--solves", type=int, default=2)
 ap.add_argument("--orth", type=int, default=0)
+ap.add_argument("--profile-last", action="store_true",
+                help="wrap only the last solve in cudaProfilerStart/Stop (ncu --profile-from-start off)")
 a = ap.parse_args()
 Pb = W.make(a.config)
 P.build()
 ctx = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1))
 u = [torch.from_numpy(x).cuda() for x in Pb.u]
 for i in range(a.solves):
+    if a.profile_last and i == a.solves - 1:
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
     if Pb.stencil is not None:
         w, s = ctx.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), u, tol=Pb.tol, symmetric=Pb.symmetric, orth=a.orth)
     else:
         A = tuple(torch.from_numpy(x).cuda() for x in Pb.csr)
         w, s = ctx.solve_csr(Pb.t, A, u, tol=Pb.tol, symmetric=Pb.symmetric, orth=a.orth)
 torch.cuda.synchronize()
+if a.profile_last:
+    torch.cuda.cudart().cudaProfilerStop()
 print(a.config, s)

@@ -438,13 +438,15 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
     return X;
 }
 
-template <bool SMEM>
+// PADE: method PHIPM_EXPM_PADE13 (separate instantiations keep each kernel's code small: the
+// kernel runs cold, after the streaming kernels, once per attempt)
+template <bool SMEM, bool PADE>
 __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
 {
     extern __shared__ double esm[];
     __shared__ double sred[3 * (EXPM_NT / 32)];
-    __shared__ int s_int[8 + 2 * EXPM_KMAX];           // Pade: pivot rows, used flags
-    __shared__ double fcol[2 * EXPM_KMAX];              // Pade: multipliers
+    __shared__ int s_int[PADE ? 8 + 2 * EXPM_KMAX : 1];     // Pade: pivot rows, used flags
+    __shared__ double fcol[PADE ? 2 * EXPM_KMAX : 1];       // Pade: multipliers
     __shared__ int s_mu;
     const int t = threadIdx.x;
     pdl_wait();
@@ -531,8 +533,9 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
     __syncthreads();
     if (a.clk && t == 0) a.clk[1] = clock64();
     int status = 0;
-    double *E = a.method == 1 ? cta_expm_pade(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, s_int, fcol, &status, a.clk)
-                              : cta_expm(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, &status, a.clk);
+    double *E;
+    if constexpr (PADE) E = cta_expm_pade(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, s_int, fcol, &status, a.clk);
+    else E = cta_expm(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, &status, a.clk);
     if (t == 0 && status) s_status = status;
     __syncthreads();
     status = s_status;
@@ -591,7 +594,7 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
         r.h = h;
         r.mu = mu;
         r.brk = brk;
-        r.status = status ? status : ((s_fin && isfinite(eps) && isfinite(phl)) ? 0 : 5);
+        r.status = a.st->aborted ? 3 : status ? status : ((s_fin && isfinite(eps) && isfinite(phl)) ? 0 : 5);
         r.seq = a.seq;
         *a.res = r;
         if (a.clk) a.clk[6] = clock64();

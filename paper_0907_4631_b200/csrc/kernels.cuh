@@ -46,6 +46,7 @@ struct DevState {
     double lz;         // Lanczos: h_{j+1,j} sigma_j, the coefficient of v~_j in step j+1
     int brk;           // -1: no breakdown; otherwise the number of valid H columns
     int nonfinite;     // a non-finite norm was met
+    int aborted;       // the persistent Krylov kernel timed out waiting for a grid phase
 };
 
 // pointers into the context workspace, shared by all kernels of a solve

@@ -1,0 +1,292 @@
+// persist.cuh — the whole Krylov extension k0 -> k1 of a stencil operator in ONE cooperative kernel
+// (Alg. 1 in CGS form / Alg. 2), one 1024-thread CTA per SM, for n > SMALL_N.
+//
+// Per step j the two-kernel path (spmv_stream + axpy_stream) pays two launch boundaries and the
+// y round trip through L2.  Here every CTA keeps the y of its contiguous row range in shared
+// memory between the SpMV phase and the update phase, and each phase ends in a grid reduction:
+//   phase A  y = sigma_j A v~_j [- lz v~_{j-1}] (halo tiles by TMA), d_k = v~_k^T y, ||y||^2
+//   phase B  v~_{j+1} = y - sum_k g_k v~_k (columns in descending order), ||v~_{j+1}||^2
+// Phase end: every CTA publishes its partials and takes an acq_rel ticket; the CTA with the last
+// ticket sums the partials in the fixed block order (final_reduce, identical to the two-kernel
+// path), runs the same finalize (H, g, sigma, breakdown) and releases a phase flag the others
+// wait on with ld.acquire.  Co-residency of all CTAs is guaranteed by the cooperative launch;
+// a CTA that waits longer than timeout_ns sets an abort flag (every waiter then exits and the
+// solve reports PHIPM_ECUDA) instead of hanging the GPU.
+// The arithmetic per row, per thread, per warp and per block is that of spmv_stream/axpy_stream.
+#pragma once
+
+#include "stream.cuh"
+
+namespace phipm {
+
+struct PersistArgs {
+    int k0, k1;
+    int symmetric;
+    double bthr;
+    int64_t rpc;                   // rows per CTA (balanced contiguous ranges, multiple of 32)
+    unsigned *flag;                // last completed phase (released by the reducing CTA)
+    unsigned *abort;               // set by a CTA that timed out
+    unsigned long long timeout_ns;
+    unsigned long long *dbg;       // optional (PHIPM_KCLOCKS): per phase, per CTA: body end, release seen
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v)
+{
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// L2-coherent 16-B load (columns written earlier in this same kernel must not come from the
+// non-coherent read-only path)
+__device__ __forceinline__ double2 ld_cg2(const double *p)
+{
+    double2 r;
+    asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+
+// End of a grid phase: publish, reduce in the last CTA, release / acquire the phase flag.
+// Returns false if the kernel must exit (abort).
+__device__ __forceinline__ bool phase_end(const Work &wk, const double *bsum, int nv, unsigned phase,
+                                          const PersistArgs &a, int fin, int j, int nd, int lanczos, double *red)
+{
+    __shared__ int s_ok;
+    if (a.dbg && threadIdx.x == 0) a.dbg[((size_t)(phase - 1) * gridDim.x + blockIdx.x) * 2] = gtimer();
+    const bool last = publish_partials(wk, bsum, nv);
+    if (last) {
+        final_reduce(wk, nv, red);                      // resets the ticket counter
+        finalize(fin, j, nd, red, wk, a.bthr, lanczos);
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_u32(a.flag, phase);
+    }
+    if (threadIdx.x == 0) {
+        int ok = 1;
+        if (!last) {
+            const unsigned long long t0 = gtimer();
+            while (ld_acquire_u32(a.flag) < phase) {
+                if (*(volatile unsigned *)a.abort) { ok = 0; break; }
+                if (gtimer() - t0 > a.timeout_ns) {
+                    atomicExch(a.abort, 1u);
+                    wk.st->aborted = 1;
+                    ok = 0;
+                    break;
+                }
+            }
+        }
+        // the other CTAs' generic-proxy writes (acquired above) before this thread's TMA reads
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        s_ok = ok;
+        if (a.dbg) a.dbg[((size_t)(phase - 1) * gridDim.x + blockIdx.x) * 2 + 1] = gtimer();
+    }
+    __syncthreads();
+    return s_ok != 0;
+}
+
+// dynamic shared memory (bytes): halo tile, y of the CTA's rows, per-warp dot partials
+__host__ __device__ inline size_t persist_smem_bytes(int halo_cap, int64_t rpc, int ndmax)
+{
+    return ((size_t)((halo_cap + 15) & ~15) + (size_t)((rpc + 15) & ~(int64_t)15) + (size_t)ndmax * SNW) *
+           sizeof(double);
+}
+
+template <int RPT>
+__global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, PersistArgs a, Work wk)
+{
+    constexpr int TILE_ = SNT * RPT;
+    constexpr int NP = RPT / 2;
+    extern __shared__ __align__(128) double sm[];
+    __shared__ uint64_t hbar;
+    __shared__ int hofs[2][5];
+    __shared__ double bsum[MAXD + 2];
+    __shared__ double red[MAXD + 2];
+    __shared__ double wsum[SNW];
+    __shared__ double gco[MAXD + 2];
+    __shared__ int s_stop;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t n = op.n;
+    const int64_t cs = (int64_t)blockIdx.x * a.rpc, ce = min(n, cs + a.rpc);
+    const int hcap = halo_capacity(op.dim, op.nx, TILE_);
+    double *hbuf = sm;
+    double *ys = sm + ((hcap + 15) & ~15);
+    double *lacc = ys + ((a.rpc + 15) & ~(int64_t)15);
+    const int64_t ldv = wk.ldv;
+    if (tid == 0) {
+        mbar_init(&hbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t ht = 0;
+    unsigned phase = 0;
+    for (int j = a.k0; j < a.k1; j++) {
+        if (tid == 0) s_stop = __ldcg(&wk.st->brk) >= 0;
+        __syncthreads();
+        if (s_stop) break;
+        const double *x = wk.V + (int64_t)j * ldv;
+        const double sj = __ldcg(wk.sigma + j);
+        const bool lanc = a.symmetric != 0;
+        const double *zv = (lanc && j > 0) ? x - ldv : nullptr;
+        const double lz = zv ? __ldcg(&wk.st->lz) : 0.0;
+        const int c0 = lanc ? j : 0;
+        const int nd = j - c0 + 1;                         // dot columns c0..j; column j is x
+
+        // ---------------- phase A: y = sigma_j A x [- lz v~_{j-1}], dots, ||y||^2
+        if (tid == 0 && cs < ce) issue_halo_tile<TILE_>(op, hbuf, x, ldv, cs, (int)min((int64_t)TILE_, ce - cs),
+                                                        hofs[ht & 1], &hbar);
+        for (int i = tid; i < nd * SNW; i += SNT) lacc[i] = 0.0;
+        __syncthreads();
+        double ysq = 0.0;
+        for (int64_t r0 = cs; r0 < ce; r0 += TILE_) {
+            const int rows = (int)min((int64_t)TILE_, ce - r0);
+            const int64_t r1 = r0 + TILE_;
+            double2 y[NP], xr[NP];
+            mbar_wait(&hbar, ht & 1);
+            const int *ho = hofs[ht & 1];
+            ht++;
+            stencil_tile<NP>(op, hbuf, ho, r0, rows, tid, y, xr);
+            __syncthreads();                               // halo consumed
+            if (tid == 0 && r1 < ce)
+                issue_halo_tile<TILE_>(op, hbuf, x, ldv, r1, (int)min((int64_t)TILE_, ce - r1), hofs[ht & 1], &hbar);
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                const int q = 2 * tid + 2 * SNT * p;
+                const int64_t r = r0 + q;
+                y[p].x *= sj;
+                y[p].y *= sj;
+                if (zv) {
+                    if (q < rows) y[p].x = fma(-lz, __ldcg(zv + r), y[p].x);
+                    if (q + 1 < rows) y[p].y = fma(-lz, __ldcg(zv + r + 1), y[p].y);
+                }
+                double *yp = ys + (r - cs);
+                if (q + 1 < rows) *reinterpret_cast<double2 *>(yp) = y[p];
+                else if (q < rows) yp[0] = y[p].x;
+                ysq = fma(y[p].x, y[p].x, ysq);
+                ysq = fma(y[p].y, y[p].y, ysq);
+            }
+            // dot with v~_j = x from the tile values in registers
+            {
+                double d = 0.0;
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    d = fma(xr[p].x, y[p].x, d);
+                    d = fma(xr[p].y, y[p].y, d);
+                }
+                d = warp_sum(d);
+                if (lane == 0) lacc[(nd - 1) * SNW + warp] += d;
+            }
+            // Arnoldi: the other columns 0..j-1, CU in flight, ascending
+            for (int k0 = 0; k0 < nd - 1; k0 += CU) {
+                double2 v[CU][NP];
+#pragma unroll
+                for (int u = 0; u < CU; u++) {
+                    const int k = k0 + u;
+                    const bool ld = k < nd - 1;
+                    const double *vc = wk.V + (int64_t)(c0 + (ld ? k : k0)) * ldv + r0;
+#pragma unroll
+                    for (int p = 0; p < NP; p++) {
+                        const int q = 2 * tid + 2 * SNT * p;
+                        v[u][p] = (ld && q < rows) ? ld_cg2(vc + q) : make_double2(0.0, 0.0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < CU; u++) {
+                    double d = 0.0;
+#pragma unroll
+                    for (int p = 0; p < NP; p++) {
+                        d = fma(v[u][p].x, y[p].x, d);
+                        d = fma(v[u][p].y, y[p].y, d);
+                    }
+                    d = warp_sum(d);
+                    if (lane == 0 && k0 + u < nd - 1) lacc[(k0 + u) * SNW + warp] += d;
+                }
+            }
+        }
+        __syncthreads();
+        for (int k = tid; k < nd; k += SNT) {
+            double t = 0.0;
+            for (int w = 0; w < SNW; w++) t += lacc[k * SNW + w];
+            bsum[k] = t;
+        }
+        {
+            const double v = warp_sum(ysq);
+            if (lane == 0) wsum[warp] = v;
+            __syncthreads();
+            if (tid == 0) {
+                double t = 0.0;
+                for (int w = 0; w < SNW; w++) t += wsum[w];
+                bsum[nd] = t;
+            }
+        }
+        __syncthreads();
+        if (!phase_end(wk, bsum, nd + 1, ++phase, a, lanc ? FIN_LANCZOS : FIN_ARNOLDI, j, nd, 0, red)) return;
+
+        // ---------------- phase B: v~_{j+1} = y - sum_k g_k v~_k, ||v~_{j+1}||^2
+        for (int k = tid; k < nd; k += SNT) gco[k] = -__ldcg(wk.g + k);
+        __syncthreads();
+        double *vn = wk.V + (int64_t)(j + 1) * ldv;
+        double nrm = 0.0;
+        for (int64_t r0 = cs; r0 < ce; r0 += TILE_) {
+            const int rows = (int)min((int64_t)TILE_, ce - r0);
+            double2 acc[NP];
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                const int q = 2 * tid + 2 * SNT * p;
+                const double *yp = ys + (r0 - cs) + q;
+                acc[p] = q + 1 < rows ? *reinterpret_cast<const double2 *>(yp)
+                                      : make_double2(q < rows ? yp[0] : 0.0, 0.0);
+            }
+            for (int i0 = 0; i0 < nd; i0 += CU) {
+                double2 v[CU][NP];
+#pragma unroll
+                for (int u = 0; u < CU; u++) {
+                    const int it = i0 + u;
+                    const int kc = nd - 1 - (it < nd ? it : i0);     // descending columns
+                    const double *vc = wk.V + (int64_t)(c0 + kc) * ldv + r0;
+#pragma unroll
+                    for (int p = 0; p < NP; p++) {
+                        const int q = 2 * tid + 2 * SNT * p;
+                        v[u][p] = (it < nd && q < rows) ? ld_cg2(vc + q) : make_double2(0.0, 0.0);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < CU; u++) {
+                    const int it = i0 + u;
+                    const double cf = it < nd ? gco[nd - 1 - it] : 0.0;
+#pragma unroll
+                    for (int p = 0; p < NP; p++) {
+                        acc[p].x = fma(cf, v[u][p].x, acc[p].x);
+                        acc[p].y = fma(cf, v[u][p].y, acc[p].y);
+                    }
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                const int q = 2 * tid + 2 * SNT * p;
+                double *o = vn + r0 + q;
+                if (q + 1 < rows) *reinterpret_cast<double2 *>(o) = acc[p];
+                else if (q < rows) o[0] = acc[p].x;
+                if (q < rows) nrm = fma(acc[p].x, acc[p].x, nrm);
+                if (q + 1 < rows) nrm = fma(acc[p].y, acc[p].y, nrm);
+            }
+        }
+        {
+            const double v = warp_sum(nrm);
+            if (lane == 0) wsum[warp] = v;
+            __syncthreads();
+            if (tid == 0) {
+                double t = 0.0;
+                for (int w = 0; w < SNW; w++) t += wsum[w];
+                bsum[0] = t;
+            }
+            __syncthreads();
+        }
+        if (!phase_end(wk, bsum, 1, ++phase, a, FIN_NORM, j, 1, lanc ? 1 : 0, red)) return;
+    }
+}
+
+} // namespace phipm

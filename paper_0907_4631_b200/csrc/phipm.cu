@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "phipm.h"
@@ -19,6 +20,7 @@
 #include "expm.cuh"
 #include "stream.cuh"
 #include "small.cuh"
+#include "persist.cuh"
 
 using namespace phipm;
 
@@ -28,6 +30,7 @@ constexpr int P_MAX_ABS = 6;          // MAXZ bounds the epilogue vector count
 constexpr double EPS_MACH = 2.220446049250313080847e-16;
 
 constexpr int KCLK_MAXL = 512, KCLK_GRID = 1024;     // PHIPM_KCLOCKS capacity (launches, CTAs)
+constexpr size_t PCLK_CAP = (size_t)1 << 22;           // persistent-kernel stamps (u64)
 
 enum ProfClass { PC_SPMV = 0, PC_ORTH, PC_EXPM, PC_COMBINE, PC_OTHER, PC_N };
 
@@ -64,6 +67,10 @@ struct phipm_ctx {
     struct KclkRec { int cls, grid, ncols; };
     std::vector<KclkRec> kclk_recs;
     const char *kclk_path = nullptr;
+    unsigned long long *pclk_d = nullptr;            // persistent kernel phase stamps
+    struct PclkRec { int grid, steps; long long off; };
+    std::vector<PclkRec> pclk_recs;
+    size_t pclk_used = 0;
     double *raw_h = nullptr;                 // pinned staging for small readbacks
     // host-buffer solve staging
     double *hu = nullptr, *hw = nullptr;
@@ -201,6 +208,23 @@ cudaError_t launch_k(phipm_ctx *c, void (*kern)(KArgs...), dim3 grid, dim3 block
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// Cooperative launch (all CTAs co-resident, or the launch fails): no PDL, plain stream order.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_coop(phipm_ctx *c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, args...);
@@ -359,8 +383,13 @@ int launch_expm(phipm_ctx *c, ExpmArgs &a, int K)
     a.clk = c->expm_clk_d;
     ProfRec r;
     prof_begin(c, r, PC_EXPM, 0.0, K);
-    if (a.use_smem) launch_k(c, expm_kernel<true>, 1, EXPM_NT, need, a);
-    else launch_k(c, expm_kernel<false>, 1, EXPM_NT, 0, a);
+    if (a.method == PHIPM_EXPM_PADE13) {
+        if (a.use_smem) launch_k(c, expm_kernel<true, true>, 1, EXPM_NT, need, a);
+        else launch_k(c, expm_kernel<false, true>, 1, EXPM_NT, 0, a);
+    } else {
+        if (a.use_smem) launch_k(c, expm_kernel<true, false>, 1, EXPM_NT, need, a);
+        else launch_k(c, expm_kernel<false, false>, 1, EXPM_NT, 0, a);
+    }
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -513,6 +542,86 @@ double tau0(double normA, double b_inf, double tol, double mbar)
 // ---------------------------------------------------------------------------------------------
 // Krylov extension: steps j = k0 .. k1-1 (0-based), all on the device
 
+// The whole extension k0 -> k1 in one cooperative kernel (persist.cuh) when the operator is a
+// stencil and the CTA's y, halo tile and dot partials fit in shared memory (PHIPM_PERSIST=0
+// disables).  Returns true if it launched (rc = status).
+template <class Op>
+bool launch_persist(phipm_ctx *, const Op &, double, bool, int, int, double, int &) { return false; }
+
+template <int RPT>
+bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, int k1, double bthr, double bytes,
+                     int &rc)
+{
+    constexpr int TILE_ = SNT * RPT;
+    int grid;
+    int64_t rpc;
+    balance(c, op.n, c->sm_count, grid, rpc);
+    const int ndmax = symmetric ? 1 : k1;
+    const size_t smem = persist_smem_bytes(halo_capacity(op.dim, op.nx, TILE_), rpc, ndmax);
+    if (smem > c->smem_optin || ndmax + 1 > MAXD + 2) return false;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, krylov_persist_kernel<RPT>, SNT, smem) != cudaSuccess ||
+        occ < 1 || grid > occ * c->sm_count) {
+        cudaGetLastError();
+        return false;
+    }
+    PersistArgs a;
+    a.k0 = k0;
+    a.k1 = k1;
+    a.symmetric = symmetric ? 1 : 0;
+    a.bthr = bthr;
+    a.rpc = rpc;
+    a.flag = c->counter + 2;
+    a.abort = c->counter + 3;
+    a.timeout_ns = 2000000000ull;
+    // PHIPM_KCLOCKS: 2 stamps per CTA per phase (2 phases per step), separate buffer
+    a.dbg = nullptr;
+    const size_t need = (size_t)2 * (k1 - k0) * grid * 2;
+    if (c->pclk_d && c->pclk_used + need <= PCLK_CAP) {
+        a.dbg = c->pclk_d + c->pclk_used;
+        c->pclk_recs.push_back({grid, k1 - k0, (long long)c->pclk_used});
+        c->pclk_used += need;
+    }
+    rc = PHIPM_OK;
+    if (cudaMemsetAsync(c->counter + 2, 0, 2 * sizeof(unsigned), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(&c->st->aborted, 0, sizeof(int), c->stream) != cudaSuccess) {
+        rc = set_err(c, PHIPM_ECUDA, "persist: memset failed");
+        return true;
+    }
+    ProfRec r;
+    prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
+    const cudaError_t e = launch_coop(c, krylov_persist_kernel<RPT>, grid, SNT, smem, op, a, make_work(c));
+    prof_end(c, r);
+    c->acc.launches++;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;                                      // fall back to the two-kernel path
+    }
+    return true;
+}
+
+template <>
+bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_op, bool symmetric, int k0, int k1,
+                               double bthr, int &rc)
+{
+    // PHIPM_PERSIST: 0 off, 1 (default) for n <= 2^19, where the measured per-step saving of a grid
+    // phase over a kernel boundary outweighs the smaller tiles (c2 +8 %; c3 -6 %, c4 +-0 at full
+    // size, profiles/round1), 2 always
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("PHIPM_PERSIST");
+        env = e ? atoi(e) : 1;
+    }
+    if (env == 0 || op.n <= SMALL_N || (env == 1 && op.n > ((int64_t)1 << 19))) return false;
+    double bytes = 0.0;
+    const double n = (double)op.n;
+    for (int j = k0; j < k1; j++) bytes += bytes_op + 8.0 * n * (symmetric ? 4.0 : 2.0 * j + 3.0);
+    // largest tile that fits (halo + the CTA's y + dot partials); RPT = 8 would spill
+    if (op.n >= (int64_t)SNT * 4 * c->sm_count / 2 && try_persist_rpt<4>(c, op, symmetric, k0, k1, bthr, bytes, rc))
+        return true;
+    return try_persist_rpt<2>(c, op, symmetric, k0, k1, bthr, bytes, rc);
+}
+
 template <class Op>
 int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1, double bthr)
 {
@@ -535,6 +644,10 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
         c->acc.launches++;
         CK(cudaGetLastError());
         return PHIPM_OK;
+    }
+    if (k1 > k0 && orth != PHIPM_ORTH_CGS2) {
+        int rc = PHIPM_OK;
+        if (launch_persist(c, op, bytes_op, symmetric, k0, k1, bthr, rc)) return rc;
     }
     for (int j = k0; j < k1; j++) {
         double *vj = c->V + (int64_t)j * c->ldv;
@@ -747,6 +860,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             if (R.brk >= 0 && R.brk < k) kb = k;
             S.nspmv += kb - k;
             k = kb;
+            if (R.status == 3) return finish(set_err(c, PHIPM_ECUDA, "persistent Krylov kernel: grid phase timed out"));
             if (R.status == 5) return finish(set_err(c, PHIPM_ENONFINITE, "non-finite value in the Krylov step"));
             if (R.status == 6) return finish(set_err(c, PHIPM_ESINGULAR, "singular Pade denominator"));
             mu = R.mu;
@@ -1088,6 +1202,24 @@ void phipm_destroy(phipm_ctx *c)
             fclose(f);
         }
         cudaFree(c->kclk_d);
+        if (c->pclk_d) {
+            std::string pp = std::string(c->kclk_path) + ".p";
+            FILE *g = fopen(pp.c_str(), "wb");
+            if (g) {
+                const int cnt = (int)c->pclk_recs.size();
+                fwrite(&cnt, 4, 1, g);
+                for (const auto &r : c->pclk_recs) {
+                    const size_t nst = (size_t)2 * r.steps * r.grid * 2;
+                    std::vector<unsigned long long> h(nst);
+                    cudaMemcpy(h.data(), c->pclk_d + r.off, nst * 8, cudaMemcpyDeviceToHost);
+                    int hd[2] = {r.grid, r.steps};
+                    fwrite(hd, 4, 2, g);
+                    fwrite(h.data(), 8, nst, g);
+                }
+                fclose(g);
+            }
+            cudaFree(c->pclk_d);
+        }
     }
     if (c->raw_h) cudaFreeHost(c->raw_h);
     delete c;
@@ -1134,6 +1266,8 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(krylov_persist_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(krylov_persist_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, maxabs_kernel, NT, 0);
         c->occ_axpy = std::max(1, occ);
@@ -1144,9 +1278,10 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
     {
         cudaFuncAttributes fa;
-        cudaFuncGetAttributes(&fa, expm_kernel<true>);
+        cudaFuncGetAttributes(&fa, expm_kernel<true, true>);     // the larger static smem of the two
         c->expm_smem_limit = (size_t)std::max(0, smem_optin - (int)fa.sharedSizeBytes - 1024);
-        cudaFuncSetAttribute(expm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->expm_smem_limit);
+        cudaFuncSetAttribute(expm_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->expm_smem_limit);
+        cudaFuncSetAttribute(expm_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->expm_smem_limit);
     }
     cudaGetLastError();
 
@@ -1187,7 +1322,9 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     }
     if (ok && getenv("PHIPM_KCLOCKS")) {
         c->kclk_path = getenv("PHIPM_KCLOCKS");
-        if (cudaMalloc((void **)&c->kclk_d, sizeof(unsigned long long) * KCLK_MAXL * KCLK_GRID * 8) != cudaSuccess ||
+        if (cudaMalloc((void **)&c->pclk_d, sizeof(unsigned long long) * PCLK_CAP) != cudaSuccess ||
+            cudaMemset(c->pclk_d, 0, sizeof(unsigned long long) * PCLK_CAP) != cudaSuccess ||
+            cudaMalloc((void **)&c->kclk_d, sizeof(unsigned long long) * KCLK_MAXL * KCLK_GRID * 8) != cudaSuccess ||
             cudaMemset(c->kclk_d, 0, sizeof(unsigned long long) * KCLK_MAXL * KCLK_GRID * 8) != cudaSuccess)
             ok = false;
     }
@@ -1490,6 +1627,7 @@ static int krylov_export(phipm_ctx *c, const Op &op, double bytes_op, double nor
     CK(cudaMemcpyAsync(&ds, c->st, sizeof(ds), cudaMemcpyDeviceToHost, c->stream));
     rc = sync(c);
     if (rc) return rc;
+    if (ds.aborted) return set_err(c, PHIPM_ECUDA, "persistent Krylov kernel: grid phase timed out");
     const int kk = (ds.brk >= 0) ? std::min(ds.brk, m) : m;
     const int ncols = (ds.brk >= 0) ? kk : m + 1;
     dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)std::max(ncols, 1));

@@ -296,6 +296,117 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
     }
 }
 
+// Issue the 1-D TMA copies of one stencil tile's halo x[hr0 - nx(ny), hr0 + hrows + nx(ny)) (thread
+// 0 only): ho receives the tile-relative offsets of the centre, y-, y+, z-, z+ segments in hbuf.
+template <int TILE_>
+__device__ __forceinline__ void issue_halo_tile(const StencilOp &op, double *hbuf, const double *x, int64_t ldx,
+                                                int64_t hr0, int hrows, int *ho, uint64_t *bar)
+{
+    HaloPlan h;
+    halo_plan(op, TILE_, hr0, hrows, ldx, h);
+    const int seg[5] = {0, h.ylo, h.yhi, h.zlo, h.zhi};
+#pragma unroll
+    for (int k = 0; k < 5; k++) ho[k] = h.off[seg[k]] - (int)(h.start[seg[k]] - hr0);
+    uint32_t tot = 0;
+    for (int k = 0; k < h.nseg; k++) tot += h.bytes[k];
+    const uint64_t pol = policy_evict_last();
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of hbuf
+    mbar_arrive_expect_tx(bar, tot);
+    for (int k = 0; k < h.nseg; k++)
+        if (h.bytes[k]) tma_load_1d(hbuf + h.off[k], x + h.start[k], h.bytes[k], bar, pol);
+}
+
+// The raw rows (A x)_r of one stencil tile from its halo in shared memory (ho: tile-relative
+// offsets of the centre, y-, y+, z-, z+ segments), for this thread's NP row pairs
+// q = 2 tid + 2 SNT p, and the x values themselves (xr, for a dot with v_j = x).  Ascending column
+// order with separately rounded products: bit-exact with a sequential CSR row sum.
+// DIM is a template parameter; a pair of rows whose 2 DIM neighbours all lie inside the grid takes
+// a branch-free path (the same operations in the same order), boundary pairs test each term.
+template <int NP, int DIM>
+__device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double *hbuf, const int *ho, int64_t r0,
+                                               int rows, int tid, double2 (&y)[NP], double2 (&xr)[NP])
+{
+    const double *pc = hbuf + ho[0];
+    const double *pym = hbuf + ho[1], *pyp = hbuf + ho[2], *pzm = hbuf + ho[3], *pzp = hbuf + ho[4];
+    const int nx = op.nx, ny = op.ny, nz = op.nz, pl = op.nx * op.ny;
+    const double c0 = op.c[0], cxm = op.c[1], cxp = op.c[2], cym = op.c[3], cyp = op.c[4],
+                 czm = op.c[5], czp = op.c[6];
+    // grid coordinates of this thread's first row; later pairs are 2 SNT rows further on
+    int i, jj = 0, kk = 0;
+    {
+        const unsigned ur = (unsigned)(r0 + 2 * tid), unx = (unsigned)nx;
+        const unsigned qy = ur / unx;
+        i = (int)(ur - qy * unx);
+        if (DIM >= 2) {
+            const unsigned q2 = qy / (unsigned)ny;
+            jj = (int)(qy - q2 * (unsigned)ny);
+            kk = (int)q2;
+        }
+    }
+    int di = 2 * SNT, dj = 0;                             // 2 SNT = dj nx + di
+    if (DIM >= 2) {
+        dj = (2 * SNT) / nx;
+        di = 2 * SNT - dj * nx;
+    }
+    // one term of the ascending-column sum, taken only where the neighbour exists: every lane
+    // executes the same instructions (a warp spans boundary and interior rows, so per-row branches
+    // would run both paths); absent neighbours read a clamped in-buffer index and are discarded
+    auto term = [&](double s, bool on, double c, const double *nb, int q) -> double {
+        const double v = *(on ? nb : pc + q);              // pc[q] (this row's own x) is always in the buffer
+        const double t = __dadd_rn(s, __dmul_rn(c, v));
+        return on ? t : s;
+    };
+    // v: the row exists (rows past the tile end compute row 0 with every neighbour off)
+    auto row = [&](bool v, int q, int ii, int j2, int k2) -> double {
+        double s = 0.0;
+        if (DIM >= 3) s = term(s, v && k2 > 0, czm, pzm + (q - pl), q);
+        if (DIM >= 2) s = term(s, v && j2 > 0, cym, pym + (q - nx), q);
+        s = term(s, v && ii > 0, cxm, pc + (q - 1), q);
+        s = __dadd_rn(s, __dmul_rn(c0, pc[q]));
+        s = term(s, v && ii < nx - 1, cxp, pc + (q + 1), q);
+        if (DIM >= 2) s = term(s, v && j2 < ny - 1, cyp, pyp + (q + nx), q);
+        if (DIM >= 3) s = term(s, v && k2 < nz - 1, czp, pzp + (q + pl), q);
+        return s;
+    };
+#pragma unroll
+    for (int p = 0; p < NP; p++) {
+        const int q = 2 * tid + 2 * SNT * p;
+        // second row of the pair: one step along x (wrapping to the next line / plane)
+        int i1 = i + 1, j1 = jj, k1 = kk;
+        if (i1 == nx) {
+            i1 = 0;
+            if (DIM >= 2) {
+                j1++;
+                if (j1 == ny) { j1 = 0; k1++; }
+            }
+        }
+        const bool v0 = q < rows, v1 = q + 1 < rows;
+        const int qa = v0 ? q : 0, qb = v1 ? q + 1 : 0;     // rows past the tile: any valid index
+        xr[p].x = v0 ? pc[qa] : 0.0;
+        xr[p].y = v1 ? pc[qb] : 0.0;
+        const double ya = row(v0, qa, i, jj, kk), yb = row(v1, qb, i1, j1, k1);
+        y[p].x = v0 ? ya : 0.0;
+        y[p].y = v1 ? yb : 0.0;
+        if (p + 1 < NP) {
+            i += di;
+            if (DIM >= 2) {
+                jj += dj;
+                if (i >= nx) { i -= nx; jj++; }
+                while (jj >= ny) { jj -= ny; kk++; }
+            }
+        }
+    }
+}
+
+template <int NP>
+__device__ __forceinline__ void stencil_tile(const StencilOp &op, const double *hbuf, const int *ho, int64_t r0, int rows,
+                                             int tid, double2 (&y)[NP], double2 (&xr)[NP])
+{
+    if (op.dim == 3) stencil_tile_d<NP, 3>(op, hbuf, ho, r0, rows, tid, y, xr);
+    else if (op.dim == 2) stencil_tile_d<NP, 2>(op, hbuf, ho, r0, rows, tid, y, xr);
+    else stencil_tile_d<NP, 1>(op, hbuf, ho, r0, rows, tid, y, xr);
+}
+
 // dynamic shared memory of spmv_stream (bytes): halo (or ys for CSR), CSR x window, per-warp dot
 // partials
 __host__ __device__ inline size_t spmv_smem_bytes(int halo_cap, int tile, int nd, int wcap = 0, int ring = 0)
@@ -441,44 +552,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
             ht++;
             const double *pc = hbuf + ho[0];
             if constexpr (IS_ST) {
-                const double *pym = hbuf + ho[1], *pyp = hbuf + ho[2], *pzm = hbuf + ho[3], *pzp = hbuf + ho[4];
-                const int nx = op.nx, ny = op.ny, pl = op.nx * op.ny;
-                const double c0 = op.c[0], cxm = op.c[1], cxp = op.c[2], cym = op.c[3], cyp = op.c[4],
-                             czm = op.c[5], czp = op.c[6];
-                // grid coordinates of this thread's first row, then stepped (no per-row division)
-                int i, jj, kk;
-                grid_ijk(op, r0 + 2 * tid, i, jj, kk);
-                auto step = [&](int d) {
-                    if (op.dim == 1) { i += d; return; }
-                    const int dj = d / nx;               // d is a compile-time constant below
-                    i += d - dj * nx;
-                    jj += dj;
-                    if (i >= nx) { i -= nx; jj++; }
-                    while (jj >= ny) { jj -= ny; kk++; }
-                };
-                // ascending column order, separately rounded products (bit-exact with a sequential
-                // CSR row sum)
-                auto row = [&](int q) -> double {
-                    double s = 0.0;
-                    if (op.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(czm, pzm[q - pl]));
-                    if (op.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(cym, pym[q - nx]));
-                    if (i > 0) s = __dadd_rn(s, __dmul_rn(cxm, pc[q - 1]));
-                    s = __dadd_rn(s, __dmul_rn(c0, pc[q]));
-                    if (i < nx - 1) s = __dadd_rn(s, __dmul_rn(cxp, pc[q + 1]));
-                    if (op.dim >= 2 && jj < ny - 1) s = __dadd_rn(s, __dmul_rn(cyp, pyp[q + nx]));
-                    if (op.dim >= 3 && kk < op.nz - 1) s = __dadd_rn(s, __dmul_rn(czp, pzp[q + pl]));
-                    return s;
-                };
-#pragma unroll
-                for (int p = 0; p < NP; p++) {
-                    const int q = 2 * tid + 2 * SNT * p;
-                    xr[p].x = q < rows ? pc[q] : 0.0;
-                    xr[p].y = q + 1 < rows ? pc[q + 1] : 0.0;
-                    y[p].x = q < rows ? row(q) : 0.0;
-                    step(1);
-                    y[p].y = q + 1 < rows ? row(q + 1) : 0.0;
-                    if (p + 1 < NP) step(2 * SNT - 1);
-                }
+                stencil_tile<NP>(op, hbuf, ho, r0, rows, tid, y, xr);
             } else {
 #pragma unroll
                 for (int p = 0; p < NP; p++) {

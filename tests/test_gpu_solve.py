@@ -209,5 +209,39 @@ def test_profile_counts(ctx):
     w, s = run_gpu(ctx, Pb, "stencil", profile=True)
     prof = ctx.profile()
     assert prof["n_expm"] == s.nexpm
-    assert prof["n_spmv_dot"] == s.nspmv          # one fused SpMV launch per product
+    # launches of the SpMV class: one per product (two-kernel path) or one per Krylov extension
+    # plus the w-recurrence products (persistent kernel, n <= 2^19)
+    assert 0 < prof["n_spmv_dot"] <= s.nspmv
     assert prof["ms_spmv_dot"] > 0 and prof["bytes_spmv_dot"] > 0
+
+
+PERSIST_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+import workloads as W, oracle
+import paper_0907_4631_b200 as P
+from gpu_common import to_dev, stencil_of, parity_bound, relerr
+name = sys.argv[1]
+Pb = W.make(name)
+ctx = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1))
+w, s = ctx.solve_stencil(Pb.t, stencil_of(Pb), [to_dev(x) for x in Pb.u], tol=Pb.tol, symmetric=Pb.symmetric,
+                         m_init=Pb.m_init)
+wo, so, _ = oracle.solve(Pb)
+e = relerr(w.cpu().numpy(), wo)
+print("RELERR", e, "BOUND", parity_bound(Pb.tol), s)
+sys.exit(0 if e <= parity_bound(Pb.tol) and s.t_reached == Pb.t else 1)
+"""
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c2_med"])
+def test_persistent_kernel_forced(name):
+    # PHIPM_PERSIST=2 forces the cooperative whole-extension kernel (several tiles per CTA at full
+    # size); the environment is read once per process, hence the subprocess
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PHIPM_PERSIST="2")
+    r = subprocess.run([sys.executable, "-c", PERSIST_SCRIPT, name], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]

@@ -70,3 +70,26 @@ for i, (cls, grid, ncols, st) in enumerate(recs):
         nxt1 = recs[i + 1][3][:, 1].min() - t00
         line += f"  next entry {(nxt - e) / 1e3:+6.1f} pdl-release {(nxt1 - e) / 1e3:+6.1f}"
     print(line)
+
+# persistent Krylov kernel: per phase, body end (max over CTAs) -> flag seen (max over CTAs)
+pp = path + ".p"
+if os.path.exists(pp):
+    with open(pp, "rb") as f:
+        cnt = struct.unpack("i", f.read(4))[0]
+        for li in range(cnt):
+            grid, steps = struct.unpack("ii", f.read(8))
+            st = np.frombuffer(f.read(8 * 2 * steps * grid * 2), dtype=np.uint64).astype(np.int64)
+            st = st.reshape(2 * steps, grid, 2)
+            valid = st[:, :, 1].max(axis=1) > 0
+            st = st[valid]
+            t0 = st[0, :, 0].min()
+            print(f"persistent launch {li}: grid {grid}, {steps} steps, {len(st)} phases")
+            print("  phase  body(min/med/max end, us rel. prev release)   sync(max body end -> last release seen)  period")
+            prev = None
+            for ph in range(len(st)):
+                be, rs = st[ph, :, 0], st[ph, :, 1]
+                base = prev if prev is not None else be.min()
+                print(f"  {ph:3d} {'A' if ph % 2 == 0 else 'B'}  {(be.min() - base) / 1e3:7.2f} {(np.median(be) - base) / 1e3:7.2f} "
+                      f"{(be.max() - base) / 1e3:7.2f}   {(rs.max() - be.max()) / 1e3:7.2f}   "
+                      f"{(rs.max() - base) / 1e3:7.2f}")
+                prev = rs.max()

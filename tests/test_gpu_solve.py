@@ -120,6 +120,18 @@ def test_cgs2_and_fixed_m(ctx, orc):
     assert relerr(wg, wo) <= parity_bound(Pb.tol)
 
 
+@pytest.mark.parametrize("name,path", [("c2_med", "stencil"), ("c3_med", "stencil"), ("c4_med", "stencil"),
+                                       ("c5_med", "csr"), ("c1", "csr")])
+def test_fixed_m_phip_parity(ctx, orc, name, path):
+    # NEXT-1: the paper's phip mode (m fixed, only tau adapts) vs the oracle in the same mode
+    Pb = W.make(name)
+    wo, so = run_oracle(orc, Pb, m_init=30, fixed_m=True)
+    wg, sg = run_gpu(ctx, Pb, path, m_init=30, fixed_m=True)
+    assert sg.t_reached == Pb.t
+    assert sg.m_peak <= 30
+    assert relerr(wg, wo) <= parity_bound(Pb.tol), (sg, so)
+
+
 def test_eq6_variant(ctx, orc):
     Pb = W.make("c1")
     wo, so = run_oracle(orc, Pb, eq6_variant=True)

@@ -161,6 +161,20 @@ int phipm_solve_stencil_host(phipm_ctx *ctx, double t, const phipm_stencil *S, i
                              const double *const *host_u, const phipm_opts *opts, double *host_w,
                              phipm_stats *stats);
 
+/* Batch of nb INDEPENDENT solves (e.g. the stages of an exponential integrator), run
+ * concurrently on one GPU: solve b uses context ctx[b] (its own workspace and stream) and one
+ * native host thread, so the host-side controllers of different problems overlap.  Problem b:
+ * operator A[b] / S[b], time t[b], p[b], input vectors u[b][0..p[b]] (DEVICE), output w[b]
+ * (DEVICE), opts (shared, NULL = defaults), stats[b] (may be NULL).  The contexts must be distinct.
+ * Returns PHIPM_OK if every solve succeeded, else the first non-zero status; status[b] (may be
+ * NULL) receives each problem's own status. */
+int phipm_solve_csr_batch(phipm_ctx *const *ctx, int nb, const double *t, const phipm_csr *A, const int *p,
+                          const double *const *const *u, const phipm_opts *opts, double *const *w,
+                          phipm_stats *stats, int *status);
+int phipm_solve_stencil_batch(phipm_ctx *const *ctx, int nb, const double *t, const phipm_stencil *S,
+                              const int *p, const double *const *const *u, const phipm_opts *opts,
+                              double *const *w, phipm_stats *stats, int *status);
+
 /* ---- kernel-level entry points (parity tests; all DEVICE pointers unless stated) ---- */
 
 /* structural nonzeros of the stencil's CSR form (N_A of Eq. 4); -1 on a bad descriptor */

@@ -126,6 +126,10 @@ def lib():
             "phipm_reserve_host_csr": (i32, [vp, i64]),
             "phipm_solve_csr_host": (i32, [vp, d, P(_Csr), i32, P(vp), P(_Opts), vp, P(_Stats)]),
             "phipm_solve_stencil_host": (i32, [vp, d, P(_Stencil), i32, P(vp), P(_Opts), vp, P(_Stats)]),
+            "phipm_solve_csr_batch": (i32, [P(vp), i32, P(d), P(_Csr), P(i32), P(vp), P(_Opts), P(vp), P(_Stats),
+                                            P(i32)]),
+            "phipm_solve_stencil_batch": (i32, [P(vp), i32, P(d), P(_Stencil), P(i32), P(vp), P(_Opts), P(vp),
+                                                P(_Stats), P(i32)]),
             "phipm_stencil_nnz": (i64, [P(_Stencil)]),
             "phipm_csr_from_stencil": (i32, [vp, P(_Stencil), vp, vp, vp]),
             "phipm_spmv_csr": (i32, [vp, P(_Csr), vp, vp]),
@@ -148,7 +152,8 @@ def lib():
 EXPORTED = [
     "phipm_default_opts", "phipm_set_expm_method", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
     "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_solve_csr", "phipm_solve_stencil",
-    "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_stencil_nnz",
+    "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_solve_csr_batch",
+    "phipm_solve_stencil_batch", "phipm_stencil_nnz",
     "phipm_csr_from_stencil", "phipm_spmv_csr", "phipm_spmv_stencil", "phipm_dot", "phipm_inf_norm_csr",
     "phipm_expm", "phipm_phi_pair", "phipm_krylov_csr", "phipm_krylov_stencil",
 ]
@@ -380,3 +385,42 @@ class Context:
                                           _f64(Hcm), C.byref(k), C.byref(brk), C.byref(beta))
         self._check(st)
         return Vcm.t(), Hcm.t(), k.value, bool(brk.value), beta.value
+
+
+def solve_batch(ctxs: Sequence["Context"], t, ops, us: Sequence[Sequence], outs=None, **kw):
+    """nb independent solves run concurrently (phipm_solve_csr_batch / phipm_solve_stencil_batch):
+    problem b on context ctxs[b] (distinct contexts: each has its own workspace and stream) with one
+    native host thread.  t: scalar or per-problem list; ops: one operator for all or a list (each a
+    Stencil, or a (row_ptr, col, val) CUDA tuple; all of one kind); us[b]: the p_b+1 input vectors.
+    Returns (outputs, stats list); raises PhipmError with the first failing status."""
+    torch = _torch()
+    nb = len(ctxs)
+    if nb == 0:
+        return [], []
+    L = ctxs[0]._L
+    ops = list(ops) if isinstance(ops, (list, tuple)) and len(ops) == nb and not (
+        len(ops) == 3 and hasattr(ops[0], "numel") and not isinstance(ops[0], Stencil)) else [ops] * nb
+    ts = list(t) if isinstance(t, (list, tuple)) else [t] * nb
+    stencil = isinstance(ops[0], Stencil)
+    n = [o.n if stencil else o[0].numel() - 1 for o in ops]
+    outs = outs if outs is not None else [torch.empty(n[b], dtype=torch.float64, device=us[b][0].device)
+                                          for b in range(nb)]
+    o = ctxs[0].opts(**kw)
+    hs = (C.c_void_p * nb)(*[c._h for c in ctxs])
+    tt = (C.c_double * nb)(*[float(x) for x in ts])
+    pp = (C.c_int * nb)(*[len(u) - 1 for u in us])
+    uarrs = [ctxs[b]._uptrs(us[b]) for b in range(nb)]
+    ua = (C.c_void_p * nb)(*[C.cast(a, C.c_void_p) for a in uarrs])
+    wa = (C.c_void_p * nb)(*[_f64(w) for w in outs])
+    st = (_Stats * nb)()
+    status = (C.c_int * nb)()
+    if stencil:
+        ss = (_Stencil * nb)(*[op._c() for op in ops])
+        rc = L.phipm_solve_stencil_batch(hs, nb, tt, ss, pp, ua, C.byref(o), wa, st, status)
+    else:
+        cs = (_Csr * nb)(*[ctxs[b]._csr(ops[b]) for b in range(nb)])
+        rc = L.phipm_solve_csr_batch(hs, nb, tt, cs, pp, ua, C.byref(o), wa, st, status)
+    if rc != OK:
+        bad = next((b for b in range(nb) if status[b] != OK), 0)
+        ctxs[bad]._check(status[bad] if status[bad] != OK else rc)
+    return outs, [Stats(*[getattr(x, k) for k, _ in _Stats._fields_]) for x in st]

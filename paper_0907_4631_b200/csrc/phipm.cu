@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "phipm.h"
@@ -1107,6 +1108,28 @@ phipm_opts resolve_opts(const phipm_opts *o)
 
 } // namespace
 
+// Run nb solves concurrently, one native thread each (phipm_solve_*_batch).
+template <class F>
+static int run_batch(phipm_ctx *const *ctx, int nb, int *status, F solve_one)
+{
+    if (nb == 0) return PHIPM_OK;
+    if (!ctx || nb < 0) return PHIPM_EINVAL;
+    for (int b = 0; b < nb; b++)
+        for (int b2 = 0; b2 < b; b2++)
+            if (!ctx[b] || ctx[b] == ctx[b2]) return PHIPM_EINVAL;   // one context per problem
+    std::vector<int> st((size_t)nb, PHIPM_OK);
+    std::vector<std::thread> th;
+    th.reserve((size_t)nb);
+    for (int b = 0; b < nb; b++) th.emplace_back([&, b] { st[b] = solve_one(b); });
+    for (auto &x : th) x.join();
+    int rc = PHIPM_OK;
+    for (int b = 0; b < nb; b++) {
+        if (status) status[b] = st[b];
+        if (rc == PHIPM_OK && st[b] != PHIPM_OK) rc = st[b];
+    }
+    return rc;
+}
+
 // =============================================================================================
 // C ABI
 
@@ -1373,6 +1396,26 @@ int phipm_solve_csr(phipm_ctx *c, double t, const phipm_csr *A, int p, const dou
     rc = enable_csr_window(c, op);
     if (rc) return rc;
     return solve_impl(c, t, op, csr_bytes(op, A->nnz), A->nnz, normA, p, u, o, w, stats);
+}
+
+int phipm_solve_csr_batch(phipm_ctx *const *ctx, int nb, const double *t, const phipm_csr *A, const int *p,
+                          const double *const *const *u, const phipm_opts *opts, double *const *w,
+                          phipm_stats *stats, int *status)
+{
+    if (nb > 0 && (!t || !A || !p || !u || !w)) return PHIPM_EINVAL;
+    return run_batch(ctx, nb, status, [&](int b) {
+        return phipm_solve_csr(ctx[b], t[b], &A[b], p[b], u[b], opts, w[b], stats ? &stats[b] : nullptr);
+    });
+}
+
+int phipm_solve_stencil_batch(phipm_ctx *const *ctx, int nb, const double *t, const phipm_stencil *S,
+                              const int *p, const double *const *const *u, const phipm_opts *opts,
+                              double *const *w, phipm_stats *stats, int *status)
+{
+    if (nb > 0 && (!t || !S || !p || !u || !w)) return PHIPM_EINVAL;
+    return run_batch(ctx, nb, status, [&](int b) {
+        return phipm_solve_stencil(ctx[b], t[b], &S[b], p[b], u[b], opts, w[b], stats ? &stats[b] : nullptr);
+    });
 }
 
 int phipm_reserve_host_csr(phipm_ctx *c, int64_t nnz_max)

@@ -59,6 +59,16 @@ def test_pure_host_entry_points(libpath):
     assert L.phipm_stencil_nnz(ctypes.byref(S3._c())) == 7 * 128 ** 3 - 2 * 3 * 128 ** 2
     bad = P.Stencil(4, 2, 2, 2, (1,) * 7)
     assert L.phipm_stencil_nnz(ctypes.byref(bad._c())) == -1
+    assert o.expm_method == 0 and L.phipm_set_expm_method(None, 0) == 1      # EINVAL, no context
+    # batch entry points validate before touching a GPU: nb = 0 is a no-op, a null context EINVAL
+    assert L.phipm_solve_stencil_batch(None, 0, None, None, None, None, None, None, None, None) == 0
+    hs = (ctypes.c_void_p * 2)(None, None)
+    tt = (ctypes.c_double * 2)(1.0, 1.0)
+    pp = (ctypes.c_int * 2)(0, 0)
+    ss = (P._Stencil * 2)(S1._c(), S1._c())
+    ua = (ctypes.c_void_p * 2)(None, None)
+    wa = (ctypes.c_void_p * 2)(None, None)
+    assert L.phipm_solve_stencil_batch(hs, 2, tt, ss, pp, ua, None, wa, None, None) == 1
     # create without a GPU fails cleanly (no abort)
     h = ctypes.c_void_p()
     import torch

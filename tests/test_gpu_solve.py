@@ -257,3 +257,34 @@ def test_persistent_kernel_forced(name):
     r = subprocess.run([sys.executable, "-c", PERSIST_SCRIPT, name], cwd=root, env=env, capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_batch_matches_single_solves():
+    # phipm_solve_stencil_batch / _csr_batch: nb independent problems on nb contexts and native
+    # threads; each output equals the single solve bit for bit (deterministic kernels per stream)
+    import torch
+    import paper_0907_4631_b200 as P
+    Pb = W.make("c1_mini")
+    S = stencil_of(Pb)
+    ts = [Pb.t, 0.5 * Pb.t, 2 * Pb.t, Pb.t]
+    us = [[to_dev(x) for x in Pb.u], [to_dev(x) for x in Pb.u[:2]], [to_dev(x) for x in Pb.u], [to_dev(Pb.u[0])]]
+    ctxs = [P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=4, stream=torch.cuda.Stream()) for _ in ts]
+    kw = dict(tol=Pb.tol, symmetric=Pb.symmetric)
+    outs, stats = P.solve_batch(ctxs, ts, S, us, **kw)
+    torch.cuda.synchronize()
+    one = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=4)
+    for b in range(len(ts)):
+        w, s = one.solve_stencil(ts[b], S, us[b], **kw)
+        assert torch.equal(w, outs[b]) and s.nspmv == stats[b].nspmv
+    # CSR operands
+    A = tuple(to_dev(a) for a in W.make("c5_mini").csr)
+    P5 = W.make("c5_mini")
+    u5 = [to_dev(x) for x in P5.u]
+    ctx5 = [P.Context(n_max=P5.n, m_max=P5.m_max, p_max=4, stream=torch.cuda.Stream()) for _ in range(3)]
+    outs5, _ = P.solve_batch(ctx5, P5.t, A, [u5] * 3, tol=P5.tol)
+    ref = P.Context(n_max=P5.n, m_max=P5.m_max, p_max=4).solve_csr(P5.t, A, u5, tol=P5.tol)[0]
+    for o in outs5:
+        assert torch.equal(o, ref)
+    # distinct contexts are required
+    with pytest.raises(P.PhipmError):
+        P.solve_batch([ctxs[0], ctxs[0]], Pb.t, S, [us[0], us[0]], **kw)

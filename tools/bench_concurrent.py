@@ -25,13 +25,16 @@ ap.add_argument("--config", default="c1")
 ap.add_argument("--ks", default="1,2,4,8,16,32")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--out", default=None)
+ap.add_argument("--api", default="threads", choices=["threads", "batch"],
+                help="threads: one Python thread per context; batch: one phipm_solve_*_batch call (native threads)")
 a = ap.parse_args()
 P.build()
 Pb = W.make(a.config)
 u = [torch.from_numpy(x).cuda() for x in Pb.u]
 A = tuple(torch.from_numpy(x).cuda() for x in Pb.csr) if Pb.csr is not None else None
 torch.cuda.synchronize()
-lines = [f"NEXT-3: K concurrent independent solves of {a.config} (n={Pb.n}), one context + stream + host thread each"]
+lines = [f"NEXT-3: K concurrent independent solves of {a.config} (n={Pb.n}), one context + stream each; "
+         f"api={a.api} ({'one phipm_solve_*_batch call per round, native threads' if a.api == 'batch' else 'one Python thread per context'})"]
 base = None
 for K in [int(k) for k in a.ks.split(",")]:
     ctxs = [P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), stream=torch.cuda.Stream()) for _ in range(K)]
@@ -46,15 +49,25 @@ for K in [int(k) for k in a.ks.split(",")]:
                 c.solve_csr(Pb.t, A, u, out=outs[i], tol=Pb.tol, symmetric=Pb.symmetric)
         c.stream.synchronize()
 
+    def batch(reps):
+        op = P.Stencil.of(Pb.stencil) if Pb.stencil is not None else A
+        for _ in range(reps):
+            P.solve_batch(ctxs, Pb.t, op, [u] * K, outs=outs, tol=Pb.tol, symmetric=Pb.symmetric)
+        for c in ctxs:
+            c.stream.synchronize()
+
     for i in range(K):                                      # warm-up
         work(i, 2)
     torch.cuda.synchronize()
-    ths = [threading.Thread(target=work, args=(i, a.reps)) for i in range(K)]
     t0 = time.perf_counter()
-    for t in ths:
-        t.start()
-    for t in ths:
-        t.join()
+    if a.api == "batch":
+        batch(a.reps)
+    else:
+        ths = [threading.Thread(target=work, args=(i, a.reps)) for i in range(K)]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     rate = K * a.reps / dt

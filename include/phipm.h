@@ -54,10 +54,15 @@ typedef struct {
 /* Constant-coefficient stencil on an nx*ny*nz grid with zero Dirichlet data (neighbours outside
  * the grid are 0).  Row r = i + nx*(j + ny*k).  dim in {1,2,3}: dim=1 uses c_center,c_xm,c_xp
  * (ny = nz = 1); dim=2 adds c_ym,c_yp (nz = 1); dim=3 adds c_zm,c_zp.  Unused coefficients are
- * ignored.  (A 3-point 1-D, 5-point 2-D or 7-point 3-D operator; BASELINE.json configs c1-c4.) */
+ * ignored.  (A 3-point 1-D, 5-point 2-D or 7-point 3-D operator; BASELINE.json configs c1-c4.)
+ * points = 9 (dim = 2 only, e.g. the 9-point Laplacian of the paper's gr_30_30,
+ * P:1224-1232) adds the four corner neighbours c_xmym (i-1, j-1), c_xpym (i+1, j-1), c_xmyp
+ * (i-1, j+1), c_xpyp (i+1, j+1); any other value of points selects the 2 dim + 1 point form. */
 typedef struct {
     int dim, nx, ny, nz;
     double c_center, c_xm, c_xp, c_ym, c_yp, c_zm, c_zp;
+    double c_xmym, c_xpym, c_xmyp, c_xpyp;
+    int points;
 } phipm_stencil;
 
 /* Orthogonalisation of the Arnoldi step (ignored for symmetric = 1, which runs Lanczos, Alg. 2) */
@@ -174,6 +179,14 @@ int phipm_solve_csr_batch(phipm_ctx *const *ctx, int nb, const double *t, const 
 int phipm_solve_stencil_batch(phipm_ctx *const *ctx, int nb, const double *t, const phipm_stencil *S,
                               const int *p, const double *const *const *u, const phipm_opts *opts,
                               double *const *w, phipm_stats *stats, int *status);
+
+/* Matrix Market ingestion (HOST, no GPU needed): "%%MatrixMarket matrix coordinate {real|integer|pattern}
+ * {general|symmetric|skew-symmetric}", square, 1-based indices.  Result: CSR with columns ascending
+ * in each row, duplicate entries summed in file order, symmetric / skew-symmetric storage expanded.
+ * Call with row_ptr = col = val = NULL to get n and nnz; then again with caller-allocated HOST
+ * arrays row_ptr[n+1], col[nnz], val[nnz].  PHIPM_EINVAL on a missing file, an unsupported or
+ * malformed header, a non-square matrix, out-of-range indices or nnz >= 2^31. */
+int phipm_mm_read(const char *path, int64_t *n, int64_t *nnz, int32_t *row_ptr, int32_t *col, double *val);
 
 /* ---- kernel-level entry points (parity tests; all DEVICE pointers unless stated) ---- */
 

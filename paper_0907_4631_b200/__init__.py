@@ -39,7 +39,9 @@ class _Csr(C.Structure):
 class _Stencil(C.Structure):
     _fields_ = [("dim", C.c_int), ("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
                 ("c_center", C.c_double), ("c_xm", C.c_double), ("c_xp", C.c_double),
-                ("c_ym", C.c_double), ("c_yp", C.c_double), ("c_zm", C.c_double), ("c_zp", C.c_double)]
+                ("c_ym", C.c_double), ("c_yp", C.c_double), ("c_zm", C.c_double), ("c_zp", C.c_double),
+                ("c_xmym", C.c_double), ("c_xpym", C.c_double), ("c_xmyp", C.c_double), ("c_xpyp", C.c_double),
+                ("points", C.c_int)]
 
 
 class _Opts(C.Structure):
@@ -67,19 +69,23 @@ class _Profile(C.Structure):
 
 @dataclasses.dataclass(frozen=True)
 class Stencil:
-    """phipm_stencil: coeffs = (c_center, c_xm, c_xp, c_ym, c_yp, c_zm, c_zp)."""
+    """phipm_stencil: coeffs = (c_center, c_xm, c_xp, c_ym, c_yp, c_zm, c_zp); points = 9 (dim 2) adds the
+    corners = (c_xmym, c_xpym, c_xmyp, c_xpyp)."""
     dim: int
     nx: int
     ny: int
     nz: int
     coeffs: Tuple[float, ...]
+    corners: Tuple[float, ...] = (0.0, 0.0, 0.0, 0.0)
+    points: int = 0
 
     @property
     def n(self) -> int:
         return self.nx * self.ny * self.nz
 
     def _c(self) -> _Stencil:
-        return _Stencil(self.dim, self.nx, self.ny, self.nz, *[float(x) for x in self.coeffs])
+        return _Stencil(self.dim, self.nx, self.ny, self.nz, *[float(x) for x in self.coeffs],
+                        *[float(x) for x in self.corners], int(self.points))
 
     @classmethod
     def of(cls, s) -> "Stencil":
@@ -114,6 +120,7 @@ def lib():
         sig = {
             "phipm_default_opts": (None, [P(_Opts)]),
             "phipm_set_expm_method": (i32, [vp, i32]),
+            "phipm_mm_read": (i32, [C.c_char_p, P(i64), P(i64), vp, vp, vp]),
             "phipm_create": (i32, [P(vp), i64, i32, i32, vp]),
             "phipm_destroy": (None, [vp]),
             "phipm_strerror": (C.c_char_p, [i32]),
@@ -150,7 +157,7 @@ def lib():
 
 
 EXPORTED = [
-    "phipm_default_opts", "phipm_set_expm_method", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
+    "phipm_default_opts", "phipm_set_expm_method", "phipm_mm_read", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
     "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_solve_csr", "phipm_solve_stencil",
     "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_solve_csr_batch",
     "phipm_solve_stencil_batch", "phipm_stencil_nnz",
@@ -424,3 +431,22 @@ def solve_batch(ctxs: Sequence["Context"], t, ops, us: Sequence[Sequence], outs=
         bad = next((b for b in range(nb) if status[b] != OK), 0)
         ctxs[bad]._check(status[bad] if status[bad] != OK else rc)
     return outs, [Stats(*[getattr(x, k) for k, _ in _Stats._fields_]) for x in st]
+
+
+def read_matrix_market(path: str):
+    """Matrix Market file -> host CSR (row_ptr int32, col int32, val float64) numpy arrays, via
+    phipm_mm_read (columns ascending per row, duplicates summed, symmetric storage expanded)."""
+    import numpy as np
+    L = lib()
+    n, nnz = C.c_int64(), C.c_int64()
+    st = L.phipm_mm_read(os.fsencode(path), C.byref(n), C.byref(nnz), None, None, None)
+    if st != OK:
+        raise PhipmError(st, f"cannot read Matrix Market file {path}")
+    rp = np.empty(n.value + 1, dtype=np.int32)
+    col = np.empty(max(nnz.value, 1), dtype=np.int32)
+    val = np.empty(max(nnz.value, 1), dtype=np.float64)
+    st = L.phipm_mm_read(os.fsencode(path), C.byref(n), C.byref(nnz), rp.ctypes.data, col.ctypes.data,
+                         val.ctypes.data)
+    if st != OK:
+        raise PhipmError(st, f"cannot read Matrix Market file {path}")
+    return rp, col[: nnz.value], val[: nnz.value]

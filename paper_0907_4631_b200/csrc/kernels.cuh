@@ -67,7 +67,8 @@ struct Work {
 struct StencilOp {
     int dim, nx, ny, nz;
     int64_t n;
-    double c[7];           // center, xm, xp, ym, yp, zm, zp
+    double c[11];          // center, xm, xp, ym, yp, zm, zp, xmym, xpym, xmyp, xpyp
+    int diag;              // 2-D 9-point: the four corner neighbours (c[7..10]) exist
 };
 
 struct CsrOp {
@@ -450,11 +451,34 @@ __global__ void __launch_bounds__(NT) csr_from_stencil_kernel(StencilOp S, int32
             miss += (r < pl ? r : pl);                              // z- missing (k==0)
             miss += (r > n - pl ? r - (n - pl) : 0);                // z+ missing (k==nz-1)
         }
-        const int64_t e0 = (2 * S.dim + 1) * r - miss;
+        int64_t e0 = (2 * S.dim + 1) * r - miss;
+        if (S.diag) {
+            // 9-point: row (i, j) holds (1 + [j>0] + [j<ny-1]) (1 + [i>0] + [i<nx-1]) entries; a full
+            // x-line sums to 3 nx - 2 per y-factor, the first i rows of a line to 3 i - [i > 0]
+            const int64_t ny = S.ny, jr = r / nx, ir = r - jr * nx;
+            auto yf = [&](int64_t j) { return 1 + (j > 0) + (j < ny - 1); };
+            int64_t full = 0;                              // sum of y-factors of lines 0 .. jr-1
+            if (jr > 0) full = 3 * jr - 1 - (jr > ny - 1 ? 1 : 0);
+            e0 = full * (3 * nx - 2) + (jr < ny ? yf(jr) * (3 * ir - (ir > 0 ? 1 : 0)) : 0);
+        }
         rp[r] = (int32_t)e0;
         if (r == n) break;
         const int64_t i = r % nx, jj = (r / nx) % S.ny, kk = r / pl;
         int64_t e = e0;
+        if (S.diag) {
+            // ascending columns: (i-1,j-1) (i,j-1) (i+1,j-1) (i-1,j) (i,j) (i+1,j) (i-1,j+1) (i,j+1) (i+1,j+1)
+            const double cy[3][3] = {{S.c[7], S.c[3], S.c[8]}, {S.c[1], S.c[0], S.c[2]}, {S.c[9], S.c[4], S.c[10]}};
+            for (int dy = -1; dy <= 1; dy++) {
+                if ((dy < 0 && jj == 0) || (dy > 0 && jj == S.ny - 1)) continue;
+                for (int dx = -1; dx <= 1; dx++) {
+                    if ((dx < 0 && i == 0) || (dx > 0 && i == nx - 1)) continue;
+                    col[e] = (int32_t)(r + dy * nx + dx);
+                    val[e] = cy[dy + 1][dx + 1];
+                    e++;
+                }
+            }
+            continue;
+        }
         if (S.dim >= 3 && kk > 0) { col[e] = (int32_t)(r - pl); val[e] = S.c[5]; e++; }
         if (S.dim >= 2 && jj > 0) { col[e] = (int32_t)(r - nx); val[e] = S.c[3]; e++; }
         if (i > 0) { col[e] = (int32_t)(r - 1); val[e] = S.c[1]; e++; }

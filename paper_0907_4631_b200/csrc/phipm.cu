@@ -934,16 +934,21 @@ int make_stencil(phipm_ctx *c, const phipm_stencil *S, StencilOp &op)
     op.nz = S->nz;
     op.n = (int64_t)S->nx * S->ny * S->nz;
     if (op.n >= ((int64_t)1 << 31)) return set_err(c, PHIPM_EINVAL, "stencil too large");
-    const double cc[7] = {S->c_center, S->c_xm, S->c_xp, S->c_ym, S->c_yp, S->c_zm, S->c_zp};
-    for (int i = 0; i < 7; i++) op.c[i] = cc[i];
+    const double cc[11] = {S->c_center, S->c_xm, S->c_xp, S->c_ym, S->c_yp, S->c_zm, S->c_zp,
+                           S->c_xmym, S->c_xpym, S->c_xmyp, S->c_xpyp};
+    for (int i = 0; i < 11; i++) op.c[i] = cc[i];
     if (S->dim < 3) op.c[5] = op.c[6] = 0.0;
     if (S->dim < 2) op.c[3] = op.c[4] = 0.0;
+    if (S->points == 9 && S->dim != 2) return set_err(c, PHIPM_EINVAL, "stencil: points = 9 needs dim = 2");
+    op.diag = S->points == 9 ? 1 : 0;
+    if (!op.diag) op.c[7] = op.c[8] = op.c[9] = op.c[10] = 0.0;
     return PHIPM_OK;
 }
 
 int64_t stencil_nnz(const StencilOp &s)
 {
     const int64_t nx = s.nx, ny = s.ny, nz = s.nz, n = s.n;
+    if (s.diag) return (3 * nx - 2) * (3 * ny - 2);             // 9-point: (3nx-2)(3ny-2)
     int64_t nnz = n + 2 * (n - ny * nz);                       // x neighbours: 2(nx-1) per line
     if (s.dim >= 2) nnz += 2 * (n - nx * nz);
     if (s.dim >= 3) nnz += 2 * (n - nx * ny);
@@ -970,13 +975,19 @@ double stencil_infnorm(const StencilOp &s)
     for (int a = 0; a < cz; a++)
         for (int b = 0; b < cy; b++)
             for (int d = 0; d < cx; d++) {
+                // ascending column order of the CSR row (9-point corners around the y-neighbours)
+                const bool dg = s.diag != 0;
                 double t = 0.0;
                 if (s.dim >= 3 && zl[a]) t = t + std::fabs(s.c[5]);
+                if (dg && yl[b] && xl[d]) t = t + std::fabs(s.c[7]);
                 if (s.dim >= 2 && yl[b]) t = t + std::fabs(s.c[3]);
+                if (dg && yl[b] && xh[d]) t = t + std::fabs(s.c[8]);
                 if (xl[d]) t = t + std::fabs(s.c[1]);
                 t = t + std::fabs(s.c[0]);
                 if (xh[d]) t = t + std::fabs(s.c[2]);
+                if (dg && yh[b] && xl[d]) t = t + std::fabs(s.c[9]);
                 if (s.dim >= 2 && yh[b]) t = t + std::fabs(s.c[4]);
+                if (dg && yh[b] && xh[d]) t = t + std::fabs(s.c[10]);
                 if (s.dim >= 3 && zh[a]) t = t + std::fabs(s.c[6]);
                 best = std::max(best, t);
             }

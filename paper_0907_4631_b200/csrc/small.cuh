@@ -34,13 +34,18 @@ __device__ __forceinline__ double row_apply(const StencilOp &S, const double *__
         kk = (int)q2;
     }
     const int64_t pl = (int64_t)S.nx * S.ny;
+    const bool dg = S.diag != 0;
     double s = 0.0;
     if (S.dim >= 3 && kk > 0) s = __dadd_rn(s, __dmul_rn(S.c[5], x[r - pl]));
+    if (dg && jj > 0 && i > 0) s = __dadd_rn(s, __dmul_rn(S.c[7], x[r - S.nx - 1]));
     if (S.dim >= 2 && jj > 0) s = __dadd_rn(s, __dmul_rn(S.c[3], x[r - S.nx]));
+    if (dg && jj > 0 && i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[8], x[r - S.nx + 1]));
     if (i > 0) s = __dadd_rn(s, __dmul_rn(S.c[1], x[r - 1]));
     s = __dadd_rn(s, __dmul_rn(S.c[0], x[r]));
     if (i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[2], x[r + 1]));
+    if (dg && jj < S.ny - 1 && i > 0) s = __dadd_rn(s, __dmul_rn(S.c[9], x[r + S.nx - 1]));
     if (S.dim >= 2 && jj < S.ny - 1) s = __dadd_rn(s, __dmul_rn(S.c[4], x[r + S.nx]));
+    if (dg && jj < S.ny - 1 && i < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[10], x[r + S.nx + 1]));
     if (S.dim >= 3 && kk < S.nz - 1) s = __dadd_rn(s, __dmul_rn(S.c[6], x[r + pl]));
     return s;
 }

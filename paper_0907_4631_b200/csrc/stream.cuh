@@ -117,7 +117,7 @@ __host__ __device__ inline bool halo_union(int nx, int tile) { return nx <= tile
 __host__ __device__ inline int halo_capacity(int dim, int nx, int tile)
 {
     if (dim == 1) return tile + 4;
-    int c = halo_union(nx, tile) ? tile + 2 * nx + 4 : 3 * (tile + 4);
+    int c = halo_union(nx, tile) ? tile + 2 * nx + 8 : 3 * (tile + 8);     // (+-1 for 9-point corners)
     if (dim == 3) c += 2 * (tile + 4);
     return c;
 }
@@ -143,11 +143,13 @@ __device__ __forceinline__ void halo_plan(const StencilOp &S, int tile, int64_t 
         add(r0 - 1, r0 + rows + 1, tile + 4);
         h.ylo = h.yhi = 0;
     } else if (halo_union(S.nx, tile)) {
-        h.ylo = h.yhi = add(r0 - S.nx, r0 + rows + S.nx, tile + 2 * S.nx + 4);
+        const int d = S.diag ? 1 : 0;                       // corner neighbours x[r -+ nx -+ 1]
+        h.ylo = h.yhi = add(r0 - S.nx - d, r0 + rows + S.nx + d, tile + 2 * S.nx + 8);
     } else {
-        add(r0 - 1, r0 + rows + 1, tile + 4);
-        h.ylo = add(r0 - S.nx, r0 - S.nx + rows, tile + 4);
-        h.yhi = add(r0 + S.nx, r0 + S.nx + rows, tile + 4);
+        const int d = S.diag ? 1 : 0;
+        add(r0 - 1, r0 + rows + 1, tile + 8);
+        h.ylo = add(r0 - S.nx - d, r0 - S.nx + rows + d, tile + 8);
+        h.yhi = add(r0 + S.nx - d, r0 + S.nx + rows + d, tile + 8);
     }
     h.zlo = h.zhi = 0;
     if (S.dim == 3) {
@@ -322,7 +324,7 @@ __device__ __forceinline__ void issue_halo_tile(const StencilOp &op, double *hbu
 // order with separately rounded products: bit-exact with a sequential CSR row sum.
 // DIM is a template parameter; a pair of rows whose 2 DIM neighbours all lie inside the grid takes
 // a branch-free path (the same operations in the same order), boundary pairs test each term.
-template <int NP, int DIM>
+template <int NP, int DIM, bool DG = false>
 __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double *hbuf, const int *ho, int64_t r0,
                                                int rows, int tid, double2 (&y)[NP], double2 (&xr)[NP])
 {
@@ -331,6 +333,7 @@ __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double
     const int nx = op.nx, ny = op.ny, nz = op.nz, pl = op.nx * op.ny;
     const double c0 = op.c[0], cxm = op.c[1], cxp = op.c[2], cym = op.c[3], cyp = op.c[4],
                  czm = op.c[5], czp = op.c[6];
+    const double cmm = op.c[7], cpm = op.c[8], cmp = op.c[9], cpp = op.c[10];   // 9-point corners
     // grid coordinates of this thread's first row; later pairs are 2 SNT rows further on
     int i, jj = 0, kk = 0;
     {
@@ -360,11 +363,15 @@ __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double
     auto row = [&](bool v, int q, int ii, int j2, int k2) -> double {
         double s = 0.0;
         if (DIM >= 3) s = term(s, v && k2 > 0, czm, pzm + (q - pl), q);
+        if (DG) s = term(s, v && j2 > 0 && ii > 0, cmm, pym + (q - nx - 1), q);
         if (DIM >= 2) s = term(s, v && j2 > 0, cym, pym + (q - nx), q);
+        if (DG) s = term(s, v && j2 > 0 && ii < nx - 1, cpm, pym + (q - nx + 1), q);
         s = term(s, v && ii > 0, cxm, pc + (q - 1), q);
         s = __dadd_rn(s, __dmul_rn(c0, pc[q]));
         s = term(s, v && ii < nx - 1, cxp, pc + (q + 1), q);
+        if (DG) s = term(s, v && j2 < ny - 1 && ii > 0, cmp, pyp + (q + nx - 1), q);
         if (DIM >= 2) s = term(s, v && j2 < ny - 1, cyp, pyp + (q + nx), q);
+        if (DG) s = term(s, v && j2 < ny - 1 && ii < nx - 1, cpp, pyp + (q + nx + 1), q);
         if (DIM >= 3) s = term(s, v && k2 < nz - 1, czp, pzp + (q + pl), q);
         return s;
     };
@@ -403,6 +410,7 @@ __device__ __forceinline__ void stencil_tile(const StencilOp &op, const double *
                                              int tid, double2 (&y)[NP], double2 (&xr)[NP])
 {
     if (op.dim == 3) stencil_tile_d<NP, 3>(op, hbuf, ho, r0, rows, tid, y, xr);
+    else if (op.dim == 2 && op.diag) stencil_tile_d<NP, 2, true>(op, hbuf, ho, r0, rows, tid, y, xr);
     else if (op.dim == 2) stencil_tile_d<NP, 2>(op, hbuf, ho, r0, rows, tid, y, xr);
     else stencil_tile_d<NP, 1>(op, hbuf, ho, r0, rows, tid, y, xr);
 }

@@ -164,6 +164,35 @@ def cpu_baseline(Pb, budget_s=15.0):
             "sample": f"{n_done} full solve(s) of the same {Pb.name} workload, single thread, {t_tot:.1f} s"}
 
 
+# ---- multi-rank host logic (replicas only: independent problems, no data-path collective) ----
+
+GENERATORS = {"c1": W.c1, "c2": W.c2, "c3": W.c3, "c4": W.c4, "c5": W.c5}
+
+
+def replica_problem(config, rank):
+    """Rank r solves its own instance of the config: same shapes and distributions, seed + 1000 r."""
+    Pb = W.CONFIGS[config]()
+    if rank:
+        Pb = GENERATORS[config](seed=Pb.seed + 1000 * rank)
+    return Pb
+
+
+def max_over_ranks(x, world, device):
+    """The slowest rank's time (all_reduce MAX of one scalar; the only collective the bench uses)."""
+    if world <= 1:
+        return float(x)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_rate(world, steps, t_ms):
+    """Whole-job solves/s: every rank completed `steps` solves within the max-over-ranks time."""
+    return world * steps / (t_ms / 1e3)
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -179,10 +208,7 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
 
     # replica inputs: same shapes/distributions, seed offset by rank (independent problems)
-    base = W.CONFIGS[args.config]
-    Pb = base()
-    if rank:
-        Pb = {"c1": W.c1, "c2": W.c2, "c3": W.c3, "c4": W.c4, "c5": W.c5}[args.config](seed=Pb.seed + 1000 * rank)
+    Pb = replica_problem(args.config, rank)
     u = [torch.from_numpy(x).to(dev) for x in Pb.u]
     stream = torch.cuda.current_stream(dev)
     ctx = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), stream=stream)
@@ -223,16 +249,12 @@ def run_gpu(args):
             torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ms = sum(a.elapsed_time(b) for a, b in ev)
-        if world > 1:
-            t = torch.tensor([ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+        ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), world, dev)
         return ms, st_, clk.summary()
 
     # ---- timed region 1: the headline (no per-kernel instrumentation: kernels chain with PDL)
     t_max, st, clocks = timed(0)
-    value = world * args.steps / (t_max / 1e3)
+    value = aggregate_rate(world, args.steps, t_max)
     # ---- timed region 2: same steps with per-kernel CUDA events (roofline of the dominant kernel)
     t_prof, st2, clocks2 = timed(1)
     prof = ctx.profile()
@@ -261,11 +283,8 @@ def run_gpu(args):
         b.record(stream)
         b.synchronize()
         e2e_ms += a.elapsed_time(b)
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_val = world * args.steps / (e2e_ms / 1e3)
+    e2e_ms = max_over_ranks(e2e_ms, world, dev)
+    e2e_val = aggregate_rate(world, args.steps, e2e_ms)
     h2d = sum(x.nbytes for x in Pb.u) + h2d_A
     d2h = Pb.n * 8
 
@@ -306,7 +325,7 @@ def run_gpu(args):
             "arnoldi_step": {"achieved_gbs": arnoldi_gbs, "frac_of_8000": arnoldi_gbs / 8000.0,
                              "frac_of_measured": arnoldi_gbs / peak,
                              "ms_per_solve": krylov_ms / args.steps},
-            "profiled_region": {"ms_per_step": t_prof / args.steps, "value": world * args.steps / (t_prof / 1e3),
+            "profiled_region": {"ms_per_step": t_prof / args.steps, "value": aggregate_rate(world, args.steps, t_prof),
                                 "note": "second timed region with CUDA events around every kernel "
                                         "(source of roofline / arnoldi_step / profile_ms_per_solve)",
                                 "clocks": clocks2},

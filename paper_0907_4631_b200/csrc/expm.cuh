@@ -65,35 +65,53 @@ __host__ __device__ inline int expm_ld(int Kp) { return Kp + ((4 - Kp % 16) + 16
 template <class Epi>
 __device__ __forceinline__ void cta_matmul_e(int Kp, int ld, const double *A, const double *B, double *C, Epi epi)
 {
+    // each warp computes a 2 x 2 block of 8x8 tiles (16 x 16 outputs): per k-step it loads two A
+    // and two B fragments for four DMMAs, half the shared-memory fragment traffic of one tile at a
+    // time (fragment loads, not the DMMA rate, bound the product)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int nt = Kp >> 3;
+    const int nt = Kp >> 3, nb = (nt + 1) >> 1;          // tiles per side, 2x2 blocks per side
     const int ar = lane >> 2, ac = lane & 3;
-    for (int t = warp; t < nt * nt; t += nw) {
-        const int ti = t % nt, tj = t / nt;
-        const double *Ap = A + (ti * 8 + ar) + (size_t)ac * ld;
-        const double *Bp = B + ac + (size_t)(tj * 8 + ar) * ld;
-        // two independent accumulator chains (even / odd k blocks), next fragments prefetched
-        double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
-        double a0 = Ap[0], b0 = Bp[0], a1 = Ap[(size_t)4 * ld], b1 = Bp[4];
-        for (int kk = 0; kk < Kp; kk += 8) {
-            double na0 = 0.0, nb0 = 0.0, na1 = 0.0, nb1 = 0.0;
-            if (kk + 8 < Kp) {
-                na0 = Ap[(size_t)(kk + 8) * ld];
-                nb0 = Bp[kk + 8];
-                na1 = Ap[(size_t)(kk + 12) * ld];
-                nb1 = Bp[kk + 12];
+    for (int bI = warp; bI < nb * nb; bI += nw) {
+        const int bi = bI % nb, bj = bI / nb;
+        const int ti0 = 2 * bi, tj0 = 2 * bj;
+        const bool ri = ti0 + 1 < nt, rj = tj0 + 1 < nt;   // second tile row / column exists
+        const double *A0 = A + (ti0 * 8 + ar) + (size_t)ac * ld;
+        const double *A1 = ri ? A0 + 8 : A0;
+        const double *B0 = B + ac + (size_t)(tj0 * 8 + ar) * ld;
+        const double *B1 = rj ? B0 + (size_t)8 * ld : B0;
+        double c[2][2][2];
+#pragma unroll
+        for (int x = 0; x < 2; x++)
+#pragma unroll
+            for (int y = 0; y < 2; y++) c[x][y][0] = c[x][y][1] = 0.0;
+        double a0 = A0[0], a1 = A1[0], b0 = B0[0], b1 = B1[0];
+        for (int k = 0; k < Kp; k += 4) {
+            double na0 = 0.0, na1 = 0.0, nb0 = 0.0, nb1 = 0.0;
+            if (k + 4 < Kp) {
+                na0 = A0[(size_t)(k + 4) * ld];
+                na1 = A1[(size_t)(k + 4) * ld];
+                nb0 = B0[k + 4];
+                nb1 = B1[k + 4];
             }
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(c0), "+d"(c1)
-                         : "d"(a0), "d"(b0));
+                         : "+d"(c[0][0][0]), "+d"(c[0][0][1]) : "d"(a0), "d"(b0));
             asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(d0), "+d"(d1)
-                         : "d"(a1), "d"(b1));
-            a0 = na0; b0 = nb0; a1 = na1; b1 = nb1;
+                         : "+d"(c[0][1][0]), "+d"(c[0][1][1]) : "d"(a0), "d"(b1));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(c[1][0][0]), "+d"(c[1][0][1]) : "d"(a1), "d"(b0));
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(c[1][1][0]), "+d"(c[1][1][1]) : "d"(a1), "d"(b1));
+            a0 = na0; a1 = na1; b0 = nb0; b1 = nb1;
         }
-        const int row = ti * 8 + ar, col = tj * 8 + 2 * ac;
-        C[row + (size_t)col * ld] = epi(row, col, c0 + d0);
-        C[row + (size_t)(col + 1) * ld] = epi(row, col + 1, c1 + d1);
+#pragma unroll
+        for (int x = 0; x < 2; x++)
+#pragma unroll
+            for (int y = 0; y < 2; y++) {
+                if ((x && !ri) || (y && !rj)) continue;
+                const int row = (ti0 + x) * 8 + ar, col = (tj0 + y) * 8 + 2 * ac;
+                C[row + (size_t)col * ld] = epi(row, col, c[x][y][0]);
+                C[row + (size_t)(col + 1) * ld] = epi(row, col + 1, c[x][y][1]);
+            }
     }
     __syncthreads();
 }

@@ -3,15 +3,16 @@
 //
 // Per step j the two-kernel path (spmv_stream + axpy_stream) pays two launch boundaries and the
 // y round trip through L2.  Here every CTA keeps the y of its contiguous row range in shared
-// memory between the SpMV phase and the update phase, and each phase ends in a grid reduction:
+// memory between the SpMV phase and the update phase, and each phase ends in a grid all-reduce:
 //   phase A  y = sigma_j A v~_j [- lz v~_{j-1}] (halo tiles by TMA), d_k = v~_k^T y, ||y||^2
 //   phase B  v~_{j+1} = y - sum_k g_k v~_k (columns in descending order), ||v~_{j+1}||^2
-// Phase end: every CTA publishes its partials and takes an acq_rel ticket; the CTA with the last
-// ticket sums the partials in the fixed block order (final_reduce, identical to the two-kernel
-// path), runs the same finalize (H, g, sigma, breakdown) and releases a phase flag the others
-// wait on with ld.acquire.  Co-residency of all CTAs is guaranteed by the cooperative launch;
-// a CTA that waits longer than timeout_ns sets an abort flag (every waiter then exits and the
-// solve reports PHIPM_ECUDA) instead of hanging the GPU.
+// Phase end: every CTA publishes its partials, arrives on a monotonic counter (release) and, once
+// all CTAs arrived (acquire), sums the partials itself in the fixed block order, so every CTA holds
+// bit-identical totals and derives H, g, sigma and the breakdown decision locally; CTA 0 writes
+// them to global memory for the exponential.  (A last-CTA reduction + flag release costs 3.3-4.5
+// us per phase; the all-reduce 1.5 us, tools/kclock.py.)  Co-residency of all CTAs is guaranteed by
+// the cooperative launch; a CTA that waits longer than timeout_ns sets an abort flag (every waiter
+// then exits and the solve reports PHIPM_ECUDA) instead of hanging the GPU.
 // The arithmetic per row, per thread, per warp and per block is that of spmv_stream/axpy_stream.
 #pragma once
 
@@ -24,7 +25,7 @@ struct PersistArgs {
     int symmetric;
     double bthr;
     int64_t rpc;                   // rows per CTA (balanced contiguous ranges, multiple of 32)
-    unsigned *flag;                // last completed phase (released by the reducing CTA)
+    unsigned *flag;                // arrival counter (CTAs x phases, monotonic within a launch)
     unsigned *abort;               // set by a CTA that timed out
     unsigned long long timeout_ns;
     unsigned long long *dbg;       // optional (PHIPM_KCLOCKS): per phase, per CTA: body end, release seen
@@ -51,32 +52,32 @@ __device__ __forceinline__ double2 ld_cg2(const double *p)
     return r;
 }
 
-// End of a grid phase: publish, reduce in the last CTA, release / acquire the phase flag.
-// Returns false if the kernel must exit (abort).
-__device__ __forceinline__ bool phase_end(const Work &wk, const double *bsum, int nv, unsigned phase,
-                                          const PersistArgs &a, int fin, int j, int nd, int lanczos, double *red)
+// End of a grid phase as an all-reduce: every CTA writes its nv partials (buffer = phase parity,
+// so a fast CTA's next partials never overwrite ones a slow CTA is still summing), arrives on the
+// monotonic counter (release), waits until all gridDim.x CTAs of this phase arrived (acquire), and
+// then sums the partials itself in block order: every CTA obtains bit-identical totals in red[]
+// without a serialising last-CTA reduction and flag round trip.  Returns false on abort.
+__device__ __forceinline__ bool phase_allreduce(const Work &wk, const double *bsum, int nv, unsigned phase,
+                                                const PersistArgs &a, double *red)
 {
     __shared__ int s_ok;
+    const int nb = gridDim.x;
+    const size_t half = (size_t)(phase & 1) * nb;
     if (a.dbg && threadIdx.x == 0) a.dbg[((size_t)(phase - 1) * gridDim.x + blockIdx.x) * 2] = gtimer();
-    const bool last = publish_partials(wk, bsum, nv);
-    if (last) {
-        final_reduce(wk, nv, red);                      // resets the ticket counter
-        finalize(fin, j, nd, red, wk, a.bthr, lanczos);
-        __syncthreads();
-        if (threadIdx.x == 0) st_release_u32(a.flag, phase);
-    }
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) wk.part[(size_t)v * wk.pstride + half + blockIdx.x] = bsum[v];
+    __syncthreads();
     if (threadIdx.x == 0) {
         int ok = 1;
-        if (!last) {
-            const unsigned long long t0 = gtimer();
-            while (ld_acquire_u32(a.flag) < phase) {
-                if (*(volatile unsigned *)a.abort) { ok = 0; break; }
-                if (gtimer() - t0 > a.timeout_ns) {
-                    atomicExch(a.abort, 1u);
-                    wk.st->aborted = 1;
-                    ok = 0;
-                    break;
-                }
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.flag) : "memory");
+        const unsigned target = phase * (unsigned)nb;
+        const unsigned long long t0 = gtimer();
+        while (ld_acquire_u32(a.flag) < target) {
+            if (*(volatile unsigned *)a.abort) { ok = 0; break; }
+            if (gtimer() - t0 > a.timeout_ns) {
+                atomicExch(a.abort, 1u);
+                wk.st->aborted = 1;
+                ok = 0;
+                break;
             }
         }
         // the other CTAs' generic-proxy writes (acquired above) before this thread's TMA reads
@@ -85,7 +86,30 @@ __device__ __forceinline__ bool phase_end(const Work &wk, const double *bsum, in
         if (a.dbg) a.dbg[((size_t)(phase - 1) * gridDim.x + blockIdx.x) * 2 + 1] = gtimer();
     }
     __syncthreads();
-    return s_ok != 0;
+    if (!s_ok) return false;
+    // fixed-order sum of the nb partials of each value (one warp per value, 8 loads in flight per lane)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int v = warp; v < nv; v += nw) {
+        const double *pv = wk.part + (size_t)v * wk.pstride + half;
+        double acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) acc[u] = 0.0;
+        for (int b0 = 0; b0 < nb; b0 += 256) {
+            double x[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int b = b0 + u * 32 + lane;
+                x[u] = (b < nb) ? __ldcg(pv + b) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) acc[u] += x[u];
+        }
+        double t = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+        t = warp_sum(t);
+        if (lane == 0) red[v] = t;
+    }
+    __syncthreads();
+    return true;
 }
 
 // dynamic shared memory (bytes): halo tile, y of the CTA's rows, per-warp dot partials
@@ -123,15 +147,23 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
     __syncthreads();
     uint32_t ht = 0;
     unsigned phase = 0;
+    // state carried between steps in shared memory (every CTA derives it from identical totals;
+    // CTA 0 also writes it to global memory for the exponential and the next extension)
+    __shared__ double s_sig, s_lz;
+    if (tid == 0) {
+        s_stop = __ldcg(&wk.st->brk) >= 0;
+        s_sig = __ldcg(wk.sigma + a.k0);
+        s_lz = __ldcg(&wk.st->lz);
+    }
+    __syncthreads();
+    const bool lead = blockIdx.x == 0;
     for (int j = a.k0; j < a.k1; j++) {
-        if (tid == 0) s_stop = __ldcg(&wk.st->brk) >= 0;
-        __syncthreads();
-        if (s_stop) break;
+        if (s_stop) break;                                 // breakdown (same decision in every CTA)
         const double *x = wk.V + (int64_t)j * ldv;
-        const double sj = __ldcg(wk.sigma + j);
+        const double sj = s_sig;                           // sigma_j, local copy
         const bool lanc = a.symmetric != 0;
         const double *zv = (lanc && j > 0) ? x - ldv : nullptr;
-        const double lz = zv ? __ldcg(&wk.st->lz) : 0.0;
+        const double lz = zv ? s_lz : 0.0;
         const int c0 = lanc ? j : 0;
         const int nd = j - c0 + 1;                         // dot columns c0..j; column j is x
 
@@ -223,11 +255,33 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
             }
         }
         __syncthreads();
-        if (!phase_end(wk, bsum, nd + 1, ++phase, a, lanc ? FIN_LANCZOS : FIN_ARNOLDI, j, nd, 0, red)) return;
+        if (!phase_allreduce(wk, bsum, nd + 1, ++phase, a, red)) return;
+        // finalize (FIN_ARNOLDI / FIN_LANCZOS): h_k = sigma_k d_k, g_k = h_k sigma_k
+        if (lanc) {
+            if (tid == 0) {
+                const double al = sj * red[0];
+                gco[0] = -(al * sj);
+                if (lead) {
+                    wk.H[j + (size_t)j * wk.ldh] = al;
+                    wk.g[0] = al * sj;
+                    wk.st->wnorm2 = red[1];
+                }
+            }
+        } else {
+            for (int k = tid; k < nd; k += SNT) {
+                const double sk = (k == j) ? sj : __ldcg(wk.sigma + k);
+                const double h = sk * red[k];
+                gco[k] = -(h * sk);
+                if (lead) {
+                    wk.H[k + (size_t)j * wk.ldh] = h;
+                    wk.g[k] = h * sk;
+                }
+            }
+            if (lead && tid == 0) wk.st->wnorm2 = red[nd];
+        }
+        __syncthreads();
 
         // ---------------- phase B: v~_{j+1} = y - sum_k g_k v~_k, ||v~_{j+1}||^2
-        for (int k = tid; k < nd; k += SNT) gco[k] = -__ldcg(wk.g + k);
-        __syncthreads();
         double *vn = wk.V + (int64_t)(j + 1) * ldv;
         double nrm = 0.0;
         for (int64_t r0 = cs; r0 < ce; r0 += TILE_) {
@@ -285,7 +339,30 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
             }
             __syncthreads();
         }
-        if (!phase_end(wk, bsum, 1, ++phase, a, FIN_NORM, j, 1, lanc ? 1 : 0, red)) return;
+        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red)) return;
+        // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown
+        if (tid == 0) {
+            const double h = sqrt(red[0]);
+            const double sn = 1.0 / h;
+            const double lzn = h * sj;
+            int brk = -1, nonfin = 0;
+            if (!isfinite(h)) { nonfin = 1; brk = j + 1; }
+            else if (h <= a.bthr) brk = j + 1;
+            s_sig = sn;
+            s_lz = lzn;
+            s_stop = brk >= 0;
+            if (lead) {
+                wk.H[(j + 1) + (size_t)j * wk.ldh] = h;
+                if (lanc) {
+                    if (j + 1 < wk.hcols) wk.H[j + (size_t)(j + 1) * wk.ldh] = h;
+                    wk.st->lz = lzn;
+                }
+                wk.sigma[j + 1] = sn;
+                if (nonfin) wk.st->nonfinite = 1;
+                if (brk >= 0) wk.st->brk = brk;
+            }
+        }
+        __syncthreads();
     }
 }
 

@@ -605,15 +605,16 @@ template <>
 bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_op, bool symmetric, int k0, int k1,
                                double bthr, int &rc)
 {
-    // PHIPM_PERSIST: 0 off, 1 (default) for n <= 2^19, where the measured per-step saving of a grid
-    // phase over a kernel boundary outweighs the smaller tiles (c2 +8 %; c3 -6 %, c4 +-0 at full
-    // size, profiles/round1), 2 always
+    // PHIPM_PERSIST: 0 off, 1 (default) auto, 2 always.  Auto: n <= 2^19, or a Lanczos extension of
+    // any size; measured with the all-reduce phase end (profiles/round1): c2 +17 %, c4 +3.6 %, while
+    // c3 (Arnoldi, n = 1M) is even with the two-kernel path, whose PDL overlap it loses
     static int env = -1;
     if (env < 0) {
         const char *e = getenv("PHIPM_PERSIST");
         env = e ? atoi(e) : 1;
     }
-    if (env == 0 || op.n <= SMALL_N || (env == 1 && op.n > ((int64_t)1 << 19))) return false;
+    if (env == 0 || op.n <= SMALL_N) return false;
+    if (env == 1 && op.n > ((int64_t)1 << 19) && !symmetric) return false;
     double bytes = 0.0;
     const double n = (double)op.n;
     for (int j = k0; j < k1; j++) bytes += bytes_op + 8.0 * n * (symmetric ? 4.0 : 2.0 * j + 3.0);

@@ -190,11 +190,14 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
                 const int64_t r = r0 + q;
                 y[p].x *= sj;
                 y[p].y *= sj;
-                if (zv) {
-                    if (q < rows) y[p].x = fma(-lz, __ldcg(zv + r), y[p].x);
-                    if (q + 1 < rows) y[p].y = fma(-lz, __ldcg(zv + r + 1), y[p].y);
-                }
                 double *yp = ys + (r - cs);
+                if (zv) {
+                    // Lanczos: after the first step of this launch, v~_{j-1} of this thread's rows is
+                    // in shared memory (kept by phase B of the previous step), not re-read from HBM
+                    const bool zs = j > a.k0;
+                    if (q < rows) y[p].x = fma(-lz, zs ? yp[0] : __ldcg(zv + r), y[p].x);
+                    if (q + 1 < rows) y[p].y = fma(-lz, zs ? yp[1] : __ldcg(zv + r + 1), y[p].y);
+                }
                 if (q + 1 < rows) *reinterpret_cast<double2 *>(yp) = y[p];
                 else if (q < rows) yp[0] = y[p].x;
                 ysq = fma(y[p].x, y[p].x, ysq);
@@ -294,6 +297,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
                 acc[p] = q + 1 < rows ? *reinterpret_cast<const double2 *>(yp)
                                       : make_double2(q < rows ? yp[0] : 0.0, 0.0);
             }
+            double2 vkeep[NP];                             // Lanczos: v~_j of these rows, for the next step
             for (int i0 = 0; i0 < nd; i0 += CU) {
                 double2 v[CU][NP];
 #pragma unroll
@@ -316,6 +320,20 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
                         acc[p].x = fma(cf, v[u][p].x, acc[p].x);
                         acc[p].y = fma(cf, v[u][p].y, acc[p].y);
                     }
+                }
+                if (i0 == 0) {
+#pragma unroll
+                    for (int p = 0; p < NP; p++) vkeep[p] = v[0][p];
+                }
+            }
+            if (lanc) {
+                // y of these rows is consumed: keep v~_j (column j, the only Lanczos column) instead
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    const int q = 2 * tid + 2 * SNT * p;
+                    double *yp = ys + (r0 - cs) + q;
+                    if (q + 1 < rows) *reinterpret_cast<double2 *>(yp) = vkeep[p];
+                    else if (q < rows) yp[0] = vkeep[p].x;
                 }
             }
 #pragma unroll

@@ -23,6 +23,13 @@ struct SmallArgs {
 // (A x)_r, ascending column order with separately rounded products (= sequential CSR row sum)
 __device__ __forceinline__ double row_apply(const StencilOp &S, const double *__restrict__ x, int64_t r)
 {
+    if (S.dim == 1) {                                    // no grid coordinates to recover
+        double s = 0.0;
+        if (r > 0) s = __dadd_rn(s, __dmul_rn(S.c[1], x[r - 1]));
+        s = __dadd_rn(s, __dmul_rn(S.c[0], x[r]));
+        if (r < S.nx - 1) s = __dadd_rn(s, __dmul_rn(S.c[2], x[r + 1]));
+        return s;
+    }
     const unsigned ur = (unsigned)r, unx = (unsigned)S.nx;
     const unsigned q = ur / unx;
     const int i = (int)(ur - q * unx);
@@ -57,7 +64,8 @@ __device__ __forceinline__ double row_apply(const CsrOp &A, const double *__rest
     return s;
 }
 
-// block sum of one value per thread (all threads receive it)
+// block sum of one value per thread (all threads receive the same total: a warp shuffle tree over
+// the warp totals, identical in every warp)
 __device__ __forceinline__ double block_sum(double v, double *red)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -65,9 +73,7 @@ __device__ __forceinline__ double block_sum(double v, double *red)
     __syncthreads();
     if (lane == 0) red[warp] = v;
     __syncthreads();
-    double t = 0.0;
-    for (int w = 0; w < nw; w++) t += red[w];
-    return t;
+    return warp_sum(lane < nw ? red[lane] : 0.0);
 }
 
 template <class Op>
@@ -77,11 +83,64 @@ __global__ void __launch_bounds__(SMALL_NT) krylov_small_kernel(Op op, SmallArgs
     __shared__ double dres[MAXD + 2];
     __shared__ double gs[MAXD + 2];
     __shared__ double red[SMALL_NT / 32];
+    __shared__ int s_brk;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = SMALL_NT / 32;
     const int n = (int)op.n;
     pdl_wait();
+    if (t == 0) s_brk = wk.st->brk;
+    __syncthreads();
+    if (a.symmetric && n <= SMALL_NT) {
+        // Lanczos with one row per thread: every reduction is a block sum whose total every thread
+        // receives, so alpha, g, h, sigma and the breakdown test are computed by all threads alike
+        // (no single-thread stage between barriers); thread 0 writes them for the host / expm
+        double sj = wk.sigma[a.k0];
+        double lz = wk.st->lz;
+        int brk = s_brk;
+        for (int j = a.k0; j < a.k1 && brk < 0; j++) {
+            const double *vj = wk.V + (int64_t)j * wk.ldv;
+            const double *vjm = j > 0 ? vj - wk.ldv : nullptr;
+            double y = 0.0, xv = 0.0, zv = 0.0;
+            if (t < n) {
+                y = sj * row_apply(op, vj, t);
+                xv = vj[t];
+                if (vjm) {
+                    zv = vjm[t];
+                    y = fma(-lz, zv, y);
+                }
+            }
+            const double d = block_sum(xv * y, red);
+            const double al = sj * d;                      // t_jj = sigma_j v~_j^T y
+            const double g = al * sj;
+            double w = 0.0;
+            if (t < n) {
+                w = fma(-g, xv, y);                        // v~_{j+1} = y - g v~_j
+                wk.V[(int64_t)(j + 1) * wk.ldv + t] = w;
+            }
+            const double tot = block_sum(w * w, red);
+            const double h = sqrt(tot);
+            const double sn = 1.0 / h;
+            const double lzn = h * sj;
+            int b = -1;
+            if (!isfinite(h)) b = j + 1;
+            else if (h <= a.bthr) b = j + 1;
+            if (t == 0) {
+                wk.H[j + (size_t)j * wk.ldh] = al;
+                wk.g[0] = g;
+                wk.H[(j + 1) + (size_t)j * wk.ldh] = h;
+                if (j + 1 < wk.hcols) wk.H[j + (size_t)(j + 1) * wk.ldh] = h;
+                wk.st->lz = lzn;
+                wk.sigma[j + 1] = sn;
+                if (!isfinite(h)) wk.st->nonfinite = 1;
+                if (b >= 0) wk.st->brk = b;
+            }
+            sj = sn;
+            lz = lzn;
+            brk = b;
+        }
+        return;
+    }
     for (int j = a.k0; j < a.k1; j++) {
-        if (wk.st->brk >= 0) break;                      // uniform: written before the last barrier
+        if (s_brk >= 0) break;                           // uniform: written before the last barrier
         const double *vj = wk.V + (int64_t)j * wk.ldv;
         const double sj = wk.sigma[j];
         const double lz = (a.symmetric && j > 0) ? wk.st->lz : 0.0;
@@ -168,8 +227,8 @@ __global__ void __launch_bounds__(SMALL_NT) krylov_small_kernel(Op op, SmallArgs
                 wk.st->lz = h * wk.sigma[j];
             }
             wk.sigma[j + 1] = 1.0 / h;
-            if (!isfinite(h)) { wk.st->nonfinite = 1; wk.st->brk = j + 1; }
-            else if (h <= a.bthr) wk.st->brk = j + 1;
+            if (!isfinite(h)) { wk.st->nonfinite = 1; wk.st->brk = j + 1; s_brk = j + 1; }
+            else if (h <= a.bthr) { wk.st->brk = j + 1; s_brk = j + 1; }
         }
         __syncthreads();
     }

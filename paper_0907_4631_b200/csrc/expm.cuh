@@ -387,24 +387,50 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
         m3 = fmax(m3, s3);
         m4 = fmax(m4, s4);
     }
+    EXPM_CLK(8)
     if (lane == 0) { sred[warp] = m1; sred[warp + 16] = m3; sred[warp + 32] = m4; }
     __syncthreads();
-    double nrm = 0.0, n3 = 0.0, n4 = 0.0;
-    for (int w = 0; w < nw; w++) { nrm = fmax(nrm, sred[w]); n3 = fmax(n3, sred[w + 16]); n4 = fmax(n4, sred[w + 32]); }
+    EXPM_CLK(9)
+    // max over the warps by a shuffle tree (identical in every warp)
+    auto wmax = [&](double v) {
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        return v;
+    };
+    const double nrm = wmax(lane < nw ? sred[lane] : 0.0);
+    const double n3 = wmax(lane < nw ? sred[lane + 16] : 0.0);
+    const double n4 = wmax(lane < nw ? sred[lane + 32] : 0.0);
     __syncthreads();
     if (!isfinite(nrm)) { *status = 5; return M0; }
-    double alpha = fmax(cbrt(n3), sqrt(sqrt(n4)));
-    if (!isfinite(alpha) || alpha > nrm) alpha = nrm;      // overflowed powers: ||A|| bounds alpha
-    // degree and squarings: minimise products (powers + Horner) + squarings, smallest m on ties
+    // alpha = min(max(||A^3||^(1/3), ||A^4||^(1/4)), ||A||) <= T  <=>  (n3 <= T^3 and n4 <= T^4) or
+    // nrm <= T: the smallest s with alpha <= theta_d 2^s from exact comparisons (no cbrt / log2),
+    // starting a little below a single-precision estimate
+    auto fits = [&](double T) { return (n3 <= T * T * T && n4 <= (T * T) * (T * T)) || nrm <= T; };
+    const float l3 = n3 > 0.0 ? __log2f((float)n3) * (1.0f / 3.0f) : -1e30f;
+    const float l4 = n4 > 0.0 ? __log2f((float)n4) * 0.25f : -1e30f;
+    const float la = fminf(fmaxf(l3, l4), nrm > 0.0 ? __log2f((float)nrm) : -1e30f);   // ~log2 alpha
+    EXPM_CLK(10)
+    // degree and squarings: minimise products (powers + Horner) + squarings, smallest m on ties.
+    // theta 2^s by adding s to the exponent field (exact; theta is normal, s <= 1000)
+    auto pow2 = [](double th, int sd) {
+        return __longlong_as_double(__double_as_longlong(th) + ((long long)sd << 52));
+    };
     int m = TAYLOR_M[0], s = 0, best = 1 << 30;
+#pragma unroll
     for (int d = 0; d < TAYLOR_NDEG; d++) {
+        const double th = TAYLOR_THETA[d];
         int sd = 0;
-        if (alpha > TAYLOR_THETA[d]) {
-            const double l = ceil(log2(alpha / TAYLOR_THETA[d]));
-            sd = l > 0.0 ? (int)l : 0;
+        if (!fits(th)) {
+            sd = min(1000, max(1, (int)(la - __log2f((float)th))));   // estimate, then exact fix-up
+            if (sd > 1 && fits(pow2(th, sd - 1))) {
+                sd--;
+                while (sd > 1 && fits(pow2(th, sd - 1))) sd--;
+            } else {
+                while (sd < 1000 && !fits(pow2(th, sd))) sd++;
+            }
         }
         if (TAYLOR_PROD[d] + sd < best) { best = TAYLOR_PROD[d] + sd; m = TAYLOR_M[d]; s = sd; }
     }
+    EXPM_CLK(11)
     // scale the powers: (2^-s A)^k = 2^-sk A^k (exact)
     if (s > 0) {
         const double f1 = ldexp(1.0, -s), f2 = ldexp(1.0, -2 * s), f3 = ldexp(1.0, -3 * s), f4 = ldexp(1.0, -4 * s);
@@ -417,6 +443,7 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
         __syncthreads();
     }
     auto c = [](int k) { return TAYLOR_INVFACT[k]; };
+    EXPM_CLK(4)
     // Horner in A^4: Y = B_{r-1} + c_m A^4;  Y <- Y A^4 + B_k, k = r-2 .. 0
     const int r = m >> 2;
     double *Y = M4, *Z = M5;
@@ -442,7 +469,6 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
         Z = tmp;
     }
     EXPM_CLK(3)
-    EXPM_CLK(4)
     // squaring (Z and M0 are free)
     double *X = Y, *T = Z;
     for (int q = 0; q < s; q++) {
@@ -468,7 +494,14 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
     __shared__ int s_mu;
     const int t = threadIdx.x;
     pdl_wait();
-    if (a.clk && t == 0) a.clk[0] = clock64();
+    // phase stamps go to shared memory (a store to host-mapped memory followed by a barrier would
+    // stall and distort the phases); copied out to a.clk once at the end
+    __shared__ long long s_clk[16];
+    long long *clk = a.clk ? s_clk : nullptr;
+    if (clk && t == 0) {
+        for (int i = 0; i < 16; i++) s_clk[i] = 0;
+        clk[0] = clock64();
+    }
     int mu, K;
     if (a.mode == 1) {
         mu = 0;
@@ -549,11 +582,13 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
     __shared__ int s_status;
     if (t == 0) s_status = 0;
     __syncthreads();
-    if (a.clk && t == 0) a.clk[1] = clock64();
+    if (clk && t == 0) clk[1] = clock64();
     int status = 0;
     double *E;
-    if constexpr (PADE) E = cta_expm_pade(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, s_int, fcol, &status, a.clk);
-    else E = cta_expm(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, &status, a.clk);
+    if constexpr (PADE) E = cta_expm_pade(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, s_int, fcol, &status, clk);
+    else E = cta_expm(K, Kp, ld, M0, M1, M2, M3, M4, M5, sred, &status, clk);
+    if (clk && t == 0)
+        for (int i = 0; i < 16; i++) a.clk[i] = s_clk[i];
     if (t == 0 && status) s_status = status;
     __syncthreads();
     status = s_status;
@@ -615,7 +650,7 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
         r.status = a.st->aborted ? 3 : status ? status : ((s_fin && isfinite(eps) && isfinite(phl)) ? 0 : 5);
         r.seq = a.seq;
         *a.res = r;
-        if (a.clk) a.clk[6] = clock64();
+        if (a.clk) a.clk[6] = clock64();                 // (after the copy above: epilogue end)
     }
 }
 

@@ -1351,7 +1351,7 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     if (ok && cudaHostGetDevicePointer((void **)&c->res_d, c->res_h, 0) != cudaSuccess) ok = false;
     if (ok && cudaHostAlloc((void **)&c->raw_h, sizeof(double) * (MAXD + 2), cudaHostAllocDefault) != cudaSuccess) ok = false;
     if (ok && getenv("PHIPM_EXPM_CLOCKS")) {
-        if (cudaHostAlloc((void **)&c->expm_clk_h, sizeof(long long) * 8, cudaHostAllocMapped) != cudaSuccess ||
+        if (cudaHostAlloc((void **)&c->expm_clk_h, sizeof(long long) * 16, cudaHostAllocMapped) != cudaSuccess ||
             cudaHostGetDevicePointer((void **)&c->expm_clk_d, c->expm_clk_h, 0) != cudaSuccess)
             ok = false;
     }
@@ -1643,8 +1643,12 @@ int phipm_phi_pair(phipm_ctx *c, int mu, const double *H, int ldh, double tau, i
     if (rc) return rc;
     if (c->expm_clk_h) {
         const long long *k = c->expm_clk_h;
-        fprintf(stderr, "expm K=%d cycles: build %lld | A2,A3,A4 %lld | Horner %lld | squarings %lld | m=%lld s=%lld\n",
-                mu + p + 1, k[1] - k[0], k[2] - k[1], k[3] - k[2], k[5] - k[4], k[7] >> 16, k[7] & 0xffff);
+        fprintf(stderr, "expm K=%d cycles: build %lld | A2,A3,A4 %lld | norms,alpha,scale %lld | Horner %lld | "
+                        "squarings %lld | m=%lld s=%lld\n",
+                mu + p + 1, k[1] - k[0], k[2] - k[1], k[4] - k[2], k[3] - k[4], k[5] - k[3], k[7] >> 16,
+                k[7] & 0xffff);
+        fprintf(stderr, "  prep: norm loop %lld | sred+sync %lld | warp max %lld | degree %lld | scale %lld\n",
+                k[8] - k[2], k[9] - k[8], k[10] - k[9], k[11] - k[10], k[4] - k[11]);
     }
     AttemptResult R;
     memcpy(&R, (const void *)c->res_h, sizeof(R));

@@ -23,5 +23,7 @@ full c3 axpy_stream 18 c3_axpy
 full c4 spmv_stream 6 c4_spmv
 full c5 spmv_stream 6 c5_spmv
 full c3 expm_kernel 3 c3_expm
+full c4 krylov_persist 0 c4_persist
+full c1 krylov_small 10 c1_small
 for c in c2 c3 c4 c5; do timeout 200 python tools/kclock.py $c > $O/kclock_$c.txt 2>&1; done
 ls -la $O/pf_* | tail -30

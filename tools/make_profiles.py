@@ -25,7 +25,7 @@ def read_ncu_csv(path):
 
 def short(k):
     for key in ("spmv_stream_kernel", "axpy_stream_kernel", "expm_kernel", "maxabs_kernel", "csr_analyze_kernel",
-                "krylov_small_kernel"):
+                "krylov_small_kernel", "krylov_persist_kernel"):
         if key in k:
             return key + ("<Stencil>" if "StencilOp" in k else "<Csr>" if "CsrOp" in k else "")
     return k[:40]
@@ -79,7 +79,10 @@ for cfg in ("c3", "c4", "c5"):
             us = [t for _, t in v]
             f.write(f"{k:34s} launches {len(v):4d}  avg DRAM bytes/launch {sum(by) / len(by) / 1e6:9.2f} MB"
                     f"  avg {sum(us) / len(us):8.1f} us  total {sum(us):9.1f} us\n")
-    sp = [b for b, _ in cls.get("spmv_stream_kernel<Stencil>", []) or cls.get("spmv_stream_kernel<Csr>", [])]
+    # the bench's "spmv_dot" class: SpMV launches plus whole-extension Krylov kernels (persistent /
+    # single-CTA), so the per-launch average matches bench.py's algorithmic_bytes_per_launch
+    sp = [b for k in cls if k.startswith(("spmv_stream_kernel", "krylov_persist_kernel", "krylov_small_kernel"))
+          for b, _ in cls[k]]
     if sp:
         traffic[cfg] = {"kernel_class": "spmv_dot", "dram_bytes_per_launch": sum(sp) / len(sp),
                         "launches": len(sp), "source": f"profiles/{rnd}/dram_traffic_{cfg}.txt"}
@@ -88,7 +91,8 @@ if traffic:
     json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
 
 # 3) --set full summaries of the top kernels
-for name in ("pf_full_c3_spmv", "pf_full_c3_axpy", "pf_full_c4_spmv", "pf_full_c5_spmv", "pf_full_c3_expm"):
+for name in ("pf_full_c3_spmv", "pf_full_c3_axpy", "pf_full_c4_spmv", "pf_full_c4_persist", "pf_full_c5_spmv",
+             "pf_full_c3_expm", "pf_full_c1_small"):
     p = os.path.join(src, name + ".ncu-rep")
     if os.path.exists(p):
         with open(os.path.join(dst, name.replace("pf_", "") + ".txt"), "w") as f:

@@ -69,6 +69,7 @@ struct StencilOp {
     int64_t n;
     double c[11];          // center, xm, xp, ym, yp, zm, zp, xmym, xpym, xmyp, xpyp
     int diag;              // 2-D 9-point: the four corner neighbours (c[7..10]) exist
+    int sdi, sdj;          // dim >= 2: 2 SNT rows = sdj grid lines + sdi points (host-computed)
 };
 
 struct CsrOp {

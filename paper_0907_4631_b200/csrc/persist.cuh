@@ -157,6 +157,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
     }
     __syncthreads();
     const bool lead = blockIdx.x == 0;
+    const int3 gc0 = grid_coords(op, cs + 2 * tid);       // grid coordinates of this thread's first row
     for (int j = a.k0; j < a.k1; j++) {
         if (s_stop) break;                                 // breakdown (same decision in every CTA)
         const double *x = wk.V + (int64_t)j * ldv;
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
         for (int i = tid; i < nd * SNW; i += SNT) lacc[i] = 0.0;
         __syncthreads();
         double ysq = 0.0;
+        int3 gcoord = gc0;
         for (int64_t r0 = cs; r0 < ce; r0 += TILE_) {
             const int rows = (int)min((int64_t)TILE_, ce - r0);
             const int64_t r1 = r0 + TILE_;
@@ -180,7 +182,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
             mbar_wait(&hbar, ht & 1);
             const int *ho = hofs[ht & 1];
             ht++;
-            stencil_tile<NP>(op, hbuf, ho, r0, rows, tid, y, xr);
+            stencil_tile<NP>(op, hbuf, ho, r0, rows, tid, y, xr, &gcoord);
             __syncthreads();                               // halo consumed
             if (tid == 0 && r1 < ce)
                 issue_halo_tile<TILE_>(op, hbuf, x, ldv, r1, (int)min((int64_t)TILE_, ce - r1), hofs[ht & 1], &hbar);
@@ -298,7 +300,22 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
                                       : make_double2(q < rows ? yp[0] : 0.0, 0.0);
             }
             double2 vkeep[NP];                             // Lanczos: v~_j of these rows, for the next step
-            for (int i0 = 0; i0 < nd; i0 += CU) {
+            if (lanc) {
+                // one column (v~_j): no batching arithmetic
+                const double cf = gco[0];
+                const double *vc = wk.V + (int64_t)c0 * ldv + r0;
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    const int q = 2 * tid + 2 * SNT * p;
+                    vkeep[p] = q < rows ? ld_cg2(vc + q) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    acc[p].x = fma(cf, vkeep[p].x, acc[p].x);
+                    acc[p].y = fma(cf, vkeep[p].y, acc[p].y);
+                }
+            }
+            for (int i0 = 0; !lanc && i0 < nd; i0 += CU) {
                 double2 v[CU][NP];
 #pragma unroll
                 for (int u = 0; u < CU; u++) {
@@ -320,10 +337,6 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
                         acc[p].x = fma(cf, v[u][p].x, acc[p].x);
                         acc[p].y = fma(cf, v[u][p].y, acc[p].y);
                     }
-                }
-                if (i0 == 0) {
-#pragma unroll
-                    for (int p = 0; p < NP; p++) vkeep[p] = v[0][p];
                 }
             }
             if (lanc) {

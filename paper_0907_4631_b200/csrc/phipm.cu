@@ -942,6 +942,8 @@ int make_stencil(phipm_ctx *c, const phipm_stencil *S, StencilOp &op)
     if (S->dim < 2) op.c[3] = op.c[4] = 0.0;
     if (S->points == 9 && S->dim != 2) return set_err(c, PHIPM_EINVAL, "stencil: points = 9 needs dim = 2");
     op.diag = S->points == 9 ? 1 : 0;
+    op.sdj = S->dim >= 2 ? (2 * SNT) / S->nx : 0;          // 2 SNT rows = sdj lines + sdi points
+    op.sdi = S->dim >= 2 ? 2 * SNT - op.sdj * S->nx : 2 * SNT;
     if (!op.diag) op.c[7] = op.c[8] = op.c[9] = op.c[10] = 0.0;
     return PHIPM_OK;
 }

@@ -324,9 +324,12 @@ __device__ __forceinline__ void issue_halo_tile(const StencilOp &op, double *hbu
 // order with separately rounded products: bit-exact with a sequential CSR row sum.
 // DIM is a template parameter; a pair of rows whose 2 DIM neighbours all lie inside the grid takes
 // a branch-free path (the same operations in the same order), boundary pairs test each term.
+// gc (optional): grid coordinates (i, j, k) of row r0 + 2 tid on entry, of the next tile's row
+// r0 + TILE + 2 tid on return (callers walking consecutive tiles avoid the per-tile divisions)
 template <int NP, int DIM, bool DG = false>
 __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double *hbuf, const int *ho, int64_t r0,
-                                               int rows, int tid, double2 (&y)[NP], double2 (&xr)[NP])
+                                               int rows, int tid, double2 (&y)[NP], double2 (&xr)[NP],
+                                               int3 *gc = nullptr)
 {
     const double *pc = hbuf + ho[0];
     const double *pym = hbuf + ho[1], *pyp = hbuf + ho[2], *pzm = hbuf + ho[3], *pzp = hbuf + ho[4];
@@ -336,7 +339,11 @@ __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double
     const double cmm = op.c[7], cpm = op.c[8], cmp = op.c[9], cpp = op.c[10];   // 9-point corners
     // grid coordinates of this thread's first row; later pairs are 2 SNT rows further on
     int i, jj = 0, kk = 0;
-    {
+    if (gc) {
+        i = gc->x;
+        jj = gc->y;
+        kk = gc->z;
+    } else {
         const unsigned ur = (unsigned)(r0 + 2 * tid), unx = (unsigned)nx;
         const unsigned qy = ur / unx;
         i = (int)(ur - qy * unx);
@@ -346,11 +353,7 @@ __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double
             kk = (int)q2;
         }
     }
-    int di = 2 * SNT, dj = 0;                             // 2 SNT = dj nx + di
-    if (DIM >= 2) {
-        dj = (2 * SNT) / nx;
-        di = 2 * SNT - dj * nx;
-    }
+    const int di = DIM >= 2 ? op.sdi : 2 * SNT, dj = DIM >= 2 ? op.sdj : 0;   // 2 SNT = dj nx + di
     // one term of the ascending-column sum, taken only where the neighbour exists: every lane
     // executes the same instructions (a warp spans boundary and interior rows, so per-row branches
     // would run both paths); absent neighbours read a clamped in-buffer index and are discarded
@@ -394,7 +397,7 @@ __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double
         const double ya = row(v0, qa, i, jj, kk), yb = row(v1, qb, i1, j1, k1);
         y[p].x = v0 ? ya : 0.0;
         y[p].y = v1 ? yb : 0.0;
-        if (p + 1 < NP) {
+        if (p + 1 < NP || gc) {
             i += di;
             if (DIM >= 2) {
                 jj += dj;
@@ -403,16 +406,31 @@ __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double
             }
         }
     }
+    if (gc) *gc = make_int3(i, jj, kk);
+}
+
+// grid coordinates of row r (divisions; once per kernel for callers that pass gc above)
+__device__ __forceinline__ int3 grid_coords(const StencilOp &op, int64_t r)
+{
+    const unsigned ur = (unsigned)r, unx = (unsigned)op.nx;
+    const unsigned qy = ur / unx;
+    int3 g = make_int3((int)(ur - qy * unx), 0, 0);
+    if (op.dim >= 2) {
+        const unsigned q2 = qy / (unsigned)op.ny;
+        g.y = (int)(qy - q2 * (unsigned)op.ny);
+        g.z = (int)q2;
+    }
+    return g;
 }
 
 template <int NP>
 __device__ __forceinline__ void stencil_tile(const StencilOp &op, const double *hbuf, const int *ho, int64_t r0, int rows,
-                                             int tid, double2 (&y)[NP], double2 (&xr)[NP])
+                                             int tid, double2 (&y)[NP], double2 (&xr)[NP], int3 *gc = nullptr)
 {
-    if (op.dim == 3) stencil_tile_d<NP, 3>(op, hbuf, ho, r0, rows, tid, y, xr);
-    else if (op.dim == 2 && op.diag) stencil_tile_d<NP, 2, true>(op, hbuf, ho, r0, rows, tid, y, xr);
-    else if (op.dim == 2) stencil_tile_d<NP, 2>(op, hbuf, ho, r0, rows, tid, y, xr);
-    else stencil_tile_d<NP, 1>(op, hbuf, ho, r0, rows, tid, y, xr);
+    if (op.dim == 3) stencil_tile_d<NP, 3>(op, hbuf, ho, r0, rows, tid, y, xr, gc);
+    else if (op.dim == 2 && op.diag) stencil_tile_d<NP, 2, true>(op, hbuf, ho, r0, rows, tid, y, xr, gc);
+    else if (op.dim == 2) stencil_tile_d<NP, 2>(op, hbuf, ho, r0, rows, tid, y, xr, gc);
+    else stencil_tile_d<NP, 1>(op, hbuf, ho, r0, rows, tid, y, xr, gc);
 }
 
 // dynamic shared memory of spmv_stream (bytes): halo (or ys for CSR), CSR x window, per-warp dot
@@ -548,6 +566,8 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
 
     double ysq = 0.0;
     uint32_t ht = 0;
+    int3 gcoord = make_int3(0, 0, 0);                      // stencil: grid coordinates of row r0 + 2 tid
+    if constexpr (IS_ST) gcoord = grid_coords(op, cs + 2 * tid);
     for (int64_t r0 = cs; r0 < ce; r0 += TILE_) {
         const int rows = (int)min((int64_t)TILE_, ce - r0);
         const int64_t r1 = r0 + TILE_;                     // next tile of this CTA
@@ -560,7 +580,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
             ht++;
             const double *pc = hbuf + ho[0];
             if constexpr (IS_ST) {
-                stencil_tile<NP>(op, hbuf, ho, r0, rows, tid, y, xr);
+                stencil_tile<NP>(op, hbuf, ho, r0, rows, tid, y, xr, &gcoord);
             } else {
 #pragma unroll
                 for (int p = 0; p < NP; p++) {

@@ -556,7 +556,16 @@ bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, 
     constexpr int TILE_ = SNT * RPT;
     int grid;
     int64_t rpc;
-    balance(c, op.n, c->sm_count, grid, rpc);
+    // CTAs: at most one per SM, and (PHIPM_PERSIST_MINROWS, default TILE/2) enough rows each that the
+    // threads are busy: small problems then also reduce fewer partials per phase
+    static int env_rows = -1;
+    if (env_rows < 0) {
+        const char *e = getenv("PHIPM_PERSIST_MINROWS");
+        env_rows = e ? std::max(32, atoi(e)) : 0;
+    }
+    const int64_t minrows = env_rows ? env_rows : TILE_ / 2;
+    const int slots = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (op.n + minrows - 1) / minrows));
+    balance(c, op.n, slots, grid, rpc);
     const int ndmax = symmetric ? 1 : k1;
     const size_t smem = persist_smem_bytes(halo_capacity(op.dim, op.nx, TILE_), rpc, ndmax);
     if (smem > c->smem_optin || ndmax + 1 > MAXD + 2) return false;

@@ -37,6 +37,8 @@ enum Fin : int {
     FIN_NORM = 4,          // ||v~_{j+1}||^2 -> h_{j+1,j}, sigma_{j+1}, breakdown, Lanczos coupling
     FIN_REORTH = 5,        // CGS2 second pass dots: c_k = sigma_k d_k ; H(k,j) += c_k ; g_k = c_k sigma_k
     FIN_RAW = 6,           // copy the sums to out_raw (kernel-level parity entry points)
+    FIN_ARNOLDI_LAG = 7,   // lagged normalisation: raw dots D_k = v~_k^T A v~_j (k=0..j), ||A v~_j||^2 and
+                           // ||v~_j||^2 -> h_{j,j-1}, sigma_j, breakdown; H(k,j) = sigma_k sigma_j D_k
 };
 
 // device-resident scalars of the current time step
@@ -108,6 +110,8 @@ struct SpmvArgs {
     int check_brk;               // exit early if a breakdown happened earlier in this step
     int64_t rpc;                 // rows per CTA (balanced contiguous ranges; multiple of 32)
     unsigned long long *dbg;     // optional per-CTA %globaltimer stamps (PHIPM_KCLOCKS tool), 8 per CTA
+    int xnorm;                   // also reduce ||x||^2 (after ||y||^2), for FIN_ARNOLDI_LAG
+    double bthr;                 // breakdown threshold (FIN_ARNOLDI_LAG)
 };
 
 struct AxpyArgs {
@@ -237,6 +241,34 @@ __device__ void finalize(int fin, int j, int nd, const double *red, const Work &
         }
         if (t == 0) wk.st->wnorm2 = red[nd];
         break;
+    case FIN_ARNOLDI_LAG: {
+        // red[0..nd-1] raw dots, red[nd] ||A x||^2, red[nd+1] ||x||^2 with x = v~_j (j >= 1)
+        __shared__ double s_sj;
+        __shared__ int s_ok;
+        if (t == 0) {
+            const double hh = sqrt(red[nd + 1]);
+            const double sj = 1.0 / hh;
+            wk.H[j + (size_t)(j - 1) * wk.ldh] = hh;
+            wk.sigma[j] = sj;
+            int ok = 1;
+            if (!isfinite(hh)) { wk.st->nonfinite = 1; wk.st->brk = j; ok = 0; }
+            else if (hh <= bthr) { wk.st->brk = j; ok = 0; }
+            if (ok) wk.st->wnorm2 = red[nd] * sj * sj;
+            s_sj = sj;
+            s_ok = ok;
+        }
+        __syncthreads();
+        if (s_ok) {
+            const double sj = s_sj;
+            for (int k = t; k < nd; k += blockDim.x) {
+                const double sk = (k == j) ? sj : wk.sigma[k];
+                const double h = sk * (sj * red[k]);
+                wk.H[k + (size_t)j * wk.ldh] = h;
+                wk.g[k] = h * sk;
+            }
+        }
+        break;
+    }
     case FIN_LANCZOS:
         if (t == 0) {
             double a = wk.sigma[j] * red[0];

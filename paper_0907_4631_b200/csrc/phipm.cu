@@ -660,9 +660,21 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
         int rc = PHIPM_OK;
         if (launch_persist(c, op, bytes_op, symmetric, k0, k1, bthr, rc)) return rc;
     }
+    // Arnoldi (CGS): lagged normalisation (PHIPM_LAG=0 disables).  Step j > k0's SpMV works on the raw
+    // v~_j and also reduces ||v~_j||^2 (free: the x tile is on chip), its finalize derives sigma_j and
+    // h_{j,j-1}; so the update passes need no grid reduction except the extension's last one, which
+    // provides h_{k1,k1-1} and sigma_{k1} for the exponential.
+    static int env_lag = -1;
+    if (env_lag < 0) {
+        const char *e = getenv("PHIPM_LAG");
+        env_lag = (e && e[0] == '0') ? 0 : 1;
+    }
+    // (stencils only: a CSR SpMV would have to re-read its own x rows for the norm; c5 measured even)
+    const bool lag = env_lag && !symmetric && orth == PHIPM_ORTH_CGS && std::is_same<Op, StencilOp>::value;
     for (int j = k0; j < k1; j++) {
         double *vj = c->V + (int64_t)j * c->ldv;
         double *vn = c->V + (int64_t)(j + 1) * c->ldv;
+        const bool lag_j = lag && j > k0;                   // sigma_j still unknown at this SpMV
         SpmvArgs s = spmv0();
         s.x = vj;
         s.xscale = c->sigma + j;
@@ -709,6 +721,17 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
             s.fin = FIN_ARNOLDI;
             u.c0 = 0;
             u.nc = j + 1;
+            if (lag_j) {
+                s.xscale = nullptr;          // raw A v~_j; sigma_j is applied in the finalize / update
+                s.xnorm = 1;
+                s.bthr = bthr;
+                s.fin = FIN_ARNOLDI_LAG;
+                u.a0d = c->sigma + j;
+            }
+            if (lag && j + 1 < k1) {         // the next SpMV reduces ||v~_{j+1}||^2
+                u.onorm = 0;
+                u.fin = FIN_NONE;
+            }
         }
         int rc = launch_spmv(c, op, s, bytes_op);
         if (rc) return rc;

@@ -564,7 +564,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
     __syncthreads();
     if (s_exit) return;
 
-    double ysq = 0.0;
+    double ysq = 0.0, xsq = 0.0;
     uint32_t ht = 0;
     int3 gcoord = make_int3(0, 0, 0);                      // stencil: grid coordinates of row r0 + 2 tid
     if constexpr (IS_ST) gcoord = grid_coords(op, cs + 2 * tid);
@@ -655,6 +655,18 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
         }
         // ---- phase 3: d_k = V_k^T y over the tile, CU columns in flight; the column equal to x
         //      (if any) is not re-read: its dot comes from the x tile values kept in registers
+        if (a.xnorm) {
+            // ||x||^2 over the tile: x values in registers (halo operators) or this thread's own rows
+#pragma unroll
+            for (int p = 0; p < NP; p++) {
+                const int q = 2 * tid + 2 * SNT * p;
+                double2 xv = xr[p];
+                if constexpr (!HALO)
+                    xv = q + 1 < rows ? ld_stream2(a.x + r0 + q) : make_double2(q < rows ? a.x[r0 + q] : 0.0, 0.0);
+                xsq = fma(xv.x, xv.x, xsq);
+                xsq = fma(xv.y, xv.y, xsq);
+            }
+        }
         int xc = -1;
         if constexpr (HALO) xc = a.xcol;
         if (xc >= 0 && xc < a.nd) {
@@ -711,7 +723,18 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
             bsum[a.nd] = t;
         }
     }
-    const int nv = a.nd + (a.ynorm ? 1 : 0);
+    if (a.xnorm) {
+        __syncthreads();
+        const double v = warp_sum(xsq);
+        if (lane == 0) wsum[warp] = v;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < SNW; w++) t += wsum[w];
+            bsum[a.nd + (a.ynorm ? 1 : 0)] = t;
+        }
+    }
+    const int nv = a.nd + (a.ynorm ? 1 : 0) + (a.xnorm ? 1 : 0);
     __syncthreads();
     if (nv == 0) return;
     const bool last = publish_partials(wk, bsum, nv);
@@ -720,7 +743,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
     __shared__ double red[MAXD + 2];
     final_reduce(wk, nv, red);
     KSTAMP(5)
-    finalize(a.fin, a.j, a.nd, red, wk, 0.0, 0);
+    finalize(a.fin, a.j, a.nd, red, wk, a.bthr, 0);
     KSTAMP(6)
 }
 

@@ -309,12 +309,14 @@ int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a0)
     SpmvArgs a = a0;
     const Op lop = launch_op(op, TILE_);
     const size_t smem = spmv_smem_bytes(halo_cap_host(op, TILE_), TILE_, a.nd, csr_wcap(op, TILE_), csr_ring(op, TILE_));
-    const void *fn = (const void *)spmv_stream_kernel<Op, RPT>;
+    const bool ringk = csr_ring(op, TILE_) != 0;           // CsrOp only: the x-ring instantiation
+    const void *fn = ringk ? (const void *)spmv_stream_kernel<Op, RPT, 2> : (const void *)spmv_stream_kernel<Op, RPT>;
     const int slots = stream_grid(c, fn, smem, (int64_t)1 << 40);
     int grid;
     balance(c, op.n, slots, grid, a.rpc);
     a.dbg = kclk_slot(c, PC_SPMV, grid, a.nd);
-    launch_k(c, spmv_stream_kernel<Op, RPT>, grid, SNT, smem, lop, a, make_work(c));
+    if (ringk) launch_k(c, spmv_stream_kernel<Op, RPT, 2>, grid, SNT, smem, lop, a, make_work(c));
+    else launch_k(c, spmv_stream_kernel<Op, RPT>, grid, SNT, smem, lop, a, make_work(c));
     return PHIPM_OK;
 }
 
@@ -1333,6 +1335,9 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         cudaFuncSetAttribute(krylov_small_kernel<CsrOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_N * 8);
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(krylov_persist_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);

@@ -445,7 +445,9 @@ __host__ __device__ inline size_t spmv_smem_bytes(int halo_cap, int tile, int nd
 // ---------------------------------------------------------------------------------------------
 // spmv_stream
 
-template <class Op, int RPT>
+// CM = 2: the banded uniform-row CSR path with the x ring only (its own instantiation: its register
+// budget is not shared with the other CSR paths); CM = 0: every other path
+template <class Op, int RPT, int CM = 0>
 __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs a, Work wk)
 {
     constexpr int TILE_ = SNT * RPT;
@@ -595,7 +597,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
         } else {
 #pragma unroll
             for (int p = 0; p < NP; p++) xr[p] = make_double2(0.0, 0.0);
-            if (ring) {
+            if constexpr (CM == 2) {
                 // this tile needs x[r0 - blo, r0 + TILE + bhi): its new chunk was requested one tile
                 // ago (or in the prologue).  Request the next tile's chunk, whose ring slots held
                 // x[r0 - TILE - blo, r0 - blo) (previous tile only; its gathers are complete).  Two
@@ -606,24 +608,26 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
                 ht++;
                 csr_tile_ell<2>(op, a.x, xring, 0, r0, rows, hbuf);
                 __syncthreads();                           // ring reads done, ys complete
-            } else if (wcap > 0) {
-                const uint32_t par = ht & 1;
-                ht++;
-                // the window decision is uniform per tile; read it once the copy has landed
-                mbar_wait(&hbar, par);
-                const int64_t ws = s_wstart[par];
-                auto nowait = [] {};
-                if (op.ell) {
-                    if (ws >= 0) csr_tile_ell<1>(op, a.x, xwin, ws, r0, rows, hbuf);
-                    else csr_tile_ell<0>(op, a.x, xwin, 0, r0, rows, hbuf);
-                } else if (ws >= 0) csr_tile<true>(op, a.x, xwin, ws, r0, rows, hbuf, nowait);
-                else csr_tile<false>(op, a.x, xwin, 0, r0, rows, hbuf, nowait);
-                __syncthreads();                           // window consumed, ys complete
-                if (tid == 0 && r1 < ce) issue_window(r1, (int)min((int64_t)TILE_, ce - r1), ht & 1);
             } else {
-                if (op.ell) csr_tile_ell<0>(op, a.x, xwin, 0, r0, rows, hbuf);
-                else csr_tile<false>(op, a.x, xwin, 0, r0, rows, hbuf, [] {});
-                __syncthreads();
+                if (wcap > 0) {
+                    const uint32_t par = ht & 1;
+                    ht++;
+                    // the window decision is uniform per tile; read it once the copy has landed
+                    mbar_wait(&hbar, par);
+                    const int64_t ws = s_wstart[par];
+                    auto nowait = [] {};
+                    if (op.ell) {
+                        if (ws >= 0) csr_tile_ell<1>(op, a.x, xwin, ws, r0, rows, hbuf);
+                        else csr_tile_ell<0>(op, a.x, xwin, 0, r0, rows, hbuf);
+                    } else if (ws >= 0) csr_tile<true>(op, a.x, xwin, ws, r0, rows, hbuf, nowait);
+                    else csr_tile<false>(op, a.x, xwin, 0, r0, rows, hbuf, nowait);
+                    __syncthreads();                           // window consumed, ys complete
+                    if (tid == 0 && r1 < ce) issue_window(r1, (int)min((int64_t)TILE_, ce - r1), ht & 1);
+                } else {
+                    if (op.ell) csr_tile_ell<0>(op, a.x, xwin, 0, r0, rows, hbuf);
+                    else csr_tile<false>(op, a.x, xwin, 0, r0, rows, hbuf, [] {});
+                    __syncthreads();
+                }
             }
 #pragma unroll
             for (int p = 0; p < NP; p++) {

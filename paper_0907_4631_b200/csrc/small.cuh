@@ -64,6 +64,17 @@ __device__ __forceinline__ double row_apply(const CsrOp &A, const double *__rest
     return s;
 }
 
+// block sum with one barrier: the caller alternates two scratch arrays, so the array written here
+// was last read two sums ago, before the barrier of the sum in between
+__device__ __forceinline__ double block_sum1(double v, double *red)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    return warp_sum(lane < nw ? red[lane] : 0.0);
+}
+
 // block sum of one value per thread (all threads receive the same total: a warp shuffle tree over
 // the warp totals, identical in every warp)
 __device__ __forceinline__ double block_sum(double v, double *red)
@@ -83,6 +94,7 @@ __global__ void __launch_bounds__(SMALL_NT) krylov_small_kernel(Op op, SmallArgs
     __shared__ double dres[MAXD + 2];
     __shared__ double gs[MAXD + 2];
     __shared__ double red[SMALL_NT / 32];
+    __shared__ double red2[SMALL_NT / 32];
     __shared__ int s_brk;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5, nw = SMALL_NT / 32;
     const int n = (int)op.n;
@@ -92,31 +104,37 @@ __global__ void __launch_bounds__(SMALL_NT) krylov_small_kernel(Op op, SmallArgs
     if (a.symmetric && n <= SMALL_NT) {
         // Lanczos with one row per thread: every reduction is a block sum whose total every thread
         // receives, so alpha, g, h, sigma and the breakdown test are computed by all threads alike
-        // (no single-thread stage between barriers); thread 0 writes them for the host / expm
+        // (no single-thread stage between barriers); thread 0 writes them for the host / expm.
+        // v~_j lives in shared memory (the SpMV's neighbour reads are shared-memory loads, not L2
+        // round trips on a vector written a step ago) and v~_{j-1} of this thread's row in a register.
+        extern __shared__ double vs[];                   // n doubles: v~_j
         double sj = wk.sigma[a.k0];
         double lz = wk.st->lz;
         int brk = s_brk;
+        double zv = 0.0;
+        if (t < n) {
+            vs[t] = wk.V[(int64_t)a.k0 * wk.ldv + t];
+            if (a.k0 > 0) zv = wk.V[(int64_t)(a.k0 - 1) * wk.ldv + t];
+        }
+        __syncthreads();
         for (int j = a.k0; j < a.k1 && brk < 0; j++) {
-            const double *vj = wk.V + (int64_t)j * wk.ldv;
-            const double *vjm = j > 0 ? vj - wk.ldv : nullptr;
-            double y = 0.0, xv = 0.0, zv = 0.0;
+            double y = 0.0, xv = 0.0;
             if (t < n) {
-                y = sj * row_apply(op, vj, t);
-                xv = vj[t];
-                if (vjm) {
-                    zv = vjm[t];
-                    y = fma(-lz, zv, y);
-                }
+                y = sj * row_apply(op, vs, t);
+                xv = vs[t];
+                if (j > 0) y = fma(-lz, zv, y);
             }
-            const double d = block_sum(xv * y, red);
+            const double d = block_sum1(xv * y, red);
             const double al = sj * d;                      // t_jj = sigma_j v~_j^T y
             const double g = al * sj;
             double w = 0.0;
             if (t < n) {
                 w = fma(-g, xv, y);                        // v~_{j+1} = y - g v~_j
                 wk.V[(int64_t)(j + 1) * wk.ldv + t] = w;
+                vs[t] = w;                                 // every thread has read vs (block sum above)
             }
-            const double tot = block_sum(w * w, red);
+            zv = xv;
+            const double tot = block_sum1(w * w, red2);
             const double h = sqrt(tot);
             const double sn = 1.0 / h;
             const double lzn = h * sj;

@@ -331,6 +331,14 @@ int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
     const int nd_mem = a.nd - (a.xcol >= 0 && a.xcol < a.nd ? 1 : 0);
     const double bytes = bytes_op + 8.0 * (double)op.n * (nd_mem + a.nz);
     prof_begin(c, r, PC_SPMV, bytes, a.nd);
+    if (op.n <= SMALL_N && a.nd <= MAXD && !a.xnorm) {
+        // small vectors: one CTA, no grid reduction (small.cuh)
+        launch_k(c, spmv_small_kernel<Op>, 1, SMALL_NT, 0, op, a, make_work(c));
+        prof_end(c, r);
+        c->acc.launches++;
+        CK(cudaGetLastError());
+        return PHIPM_OK;
+    }
     int rpt = pick_rpt(c, op.n);
     if (csr_wcap(op, SNT * 8) > 0) rpt = 8;                  // CSR x-window mode uses 8 SNT-row tiles
     // largest tile whose halo + dot accumulators fit in shared memory (3-D stencils, many dots)
@@ -365,6 +373,13 @@ int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a, int cls)
     ProfRec r;
     const double bytes = 8.0 * (double)n * (a.nc + a.ne + 1 + (a.a0h != 0.0 ? 1 : 0));
     prof_begin(c, r, cls, bytes, a.nc + a.ne + (a.a0h != 0.0 ? 1 : 0));
+    if (n <= SMALL_N) {
+        launch_k(c, axpy_small_kernel, 1, SMALL_NT, 0, n, a, make_work(c));   // one CTA (small.cuh)
+        prof_end(c, r);
+        c->acc.launches++;
+        CK(cudaGetLastError());
+        return PHIPM_OK;
+    }
     const int rpt = pick_rpt(c, n);
     if (rpt == 8) launch_axpy_t<8>(c, n, a);
     else if (rpt == 4) launch_axpy_t<4>(c, n, a);

@@ -64,6 +64,8 @@ __device__ __forceinline__ double row_apply(const CsrOp &A, const double *__rest
     return s;
 }
 
+__device__ __forceinline__ double row_apply(const IdentOp &, const double *__restrict__ x, int64_t r) { return x[r]; }
+
 // block sum with one barrier: the caller alternates two scratch arrays, so the array written here
 // was last read two sums ago, before the barrier of the sum in between
 __device__ __forceinline__ double block_sum1(double v, double *red)
@@ -250,6 +252,146 @@ __global__ void __launch_bounds__(SMALL_NT) krylov_small_kernel(Op op, SmallArgs
         }
         __syncthreads();
     }
+}
+
+// ---------------------------------------------------------------------------------------------
+// One-CTA versions of the two generic streaming kernels for n <= SMALL_N (w-recurrence, seed,
+// combine, kernel-level entry points): no grid reduction, no halo copies.  Per row the arithmetic
+// is that of spmv_stream / axpy_stream (same operand order, same FMA chains; stencil rows bit-exact
+// with a sequential CSR sum); block sums replace the grid reduction and feed the same finalize().
+
+constexpr int SMALL_NR = SMALL_N / SMALL_NT;          // rows per thread (r = t + i SMALL_NT)
+constexpr int SMALL_NW = SMALL_NT / 32;
+
+// d_k = sum_r V[r, c0 + k] x_r for k < nd into dres (fixed order: rows per thread, warp shuffle
+// tree, warps in order); each thread issues the loads of 8 columns at once
+__device__ __forceinline__ void small_dots(const double *V, int64_t ldv, int c0, int nd, int n,
+                                           const double (&x)[SMALL_NR], double *wpart, double *dres)
+{
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    for (int k0 = 0; k0 < nd; k0 += 8) {
+        double d[8];
+#pragma unroll
+        for (int u = 0; u < 8; u++) d[u] = 0.0;
+#pragma unroll
+        for (int i = 0; i < SMALL_NR; i++) {
+            const int r = t + i * SMALL_NT;
+            if (r < n) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) v[u] = (k0 + u < nd) ? V[r + (int64_t)(c0 + k0 + u) * ldv] : 0.0;
+#pragma unroll
+                for (int u = 0; u < 8; u++) d[u] = fma(v[u], x[i], d[u]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; u++) {
+            const double w = warp_sum(d[u]);
+            if (lane == 0 && k0 + u < nd) wpart[(k0 + u) * SMALL_NW + warp] = w;
+        }
+    }
+    __syncthreads();
+    for (int k = t; k < nd; k += SMALL_NT) {
+        double s = 0.0;
+        for (int w = 0; w < SMALL_NW; w++) s += wpart[k * SMALL_NW + w];
+        dres[k] = s;
+    }
+    __syncthreads();
+}
+
+template <class Op>
+__global__ void __launch_bounds__(SMALL_NT) spmv_small_kernel(Op op, SpmvArgs a, Work wk)
+{
+    __shared__ double wpart[(MAXD + 2) * SMALL_NW];
+    __shared__ double red[MAXD + 2];
+    __shared__ double wsum[SMALL_NW];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n = (int)op.n;
+    pdl_wait();
+    if (a.check_brk && wk.st->brk >= 0) return;            // uniform
+    const double sc = a.xscale ? *a.xscale : 1.0;
+    double y[SMALL_NR];
+    double ysq = 0.0;
+#pragma unroll
+    for (int i = 0; i < SMALL_NR; i++) {
+        const int r = t + i * SMALL_NT;
+        double v = 0.0;
+        if (r < n) {
+            v = row_apply(op, a.x, r) * sc;
+            for (int l = 0; l < a.nz; l++) v = fma(a.zc[l] * (a.zcd[l] ? *a.zcd[l] : 1.0), a.z[l][r], v);
+            if (a.y) a.y[r] = v;
+            ysq = fma(v, v, ysq);
+        }
+        y[i] = v;
+    }
+    if (a.nd > 0) small_dots(a.V, a.ldv, a.d0, a.nd, n, y, wpart, red);
+    if (a.ynorm) {
+        const double v = warp_sum(ysq);
+        if (lane == 0) wsum[warp] = v;
+        __syncthreads();
+        if (t == 0) {
+            double s = 0.0;
+            for (int w = 0; w < SMALL_NW; w++) s += wsum[w];
+            red[a.nd] = s;
+        }
+    }
+    __syncthreads();
+    if (a.nd + (a.ynorm ? 1 : 0) == 0) return;
+    finalize(a.fin, a.j, a.nd, red, wk, a.bthr, 0);
+}
+
+__global__ void __launch_bounds__(SMALL_NT) axpy_small_kernel(int64_t n64, AxpyArgs a, Work wk)
+{
+    __shared__ double coef[MAXD + MAXZ + 2];
+    __shared__ const double *src[MAXD + MAXZ + 2];
+    __shared__ double red[2];
+    __shared__ double wsum[SMALL_NW];
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int n = (int)n64;
+    pdl_wait();
+    if (a.check_brk && wk.st->brk >= 0) return;            // uniform
+    const int nbase = (a.a0h != 0.0) ? 1 : 0;
+    const int nitem = nbase + a.nc + a.ne;
+    for (int k = t; k < nitem; k += SMALL_NT) {            // same item order as axpy_stream
+        double c;
+        const double *p;
+        if (k < nbase) {
+            c = a.a0h * (a.a0d ? *a.a0d : 1.0);
+            p = a.base;
+        } else if (k < nbase + a.nc) {
+            const int kc = a.rev ? (a.nc - 1 - (k - nbase)) : (k - nbase);
+            c = a.gsign * a.g[kc];
+            p = a.V + (int64_t)(a.c0 + kc) * a.ldv;
+        } else {
+            const int i = k - nbase - a.nc;
+            c = a.ec[i] * (a.ecd ? a.ecd[i] : 1.0);
+            p = a.e[i];
+        }
+        coef[k] = c;
+        src[k] = p;
+    }
+    __syncthreads();
+    double nrm = 0.0;
+#pragma unroll
+    for (int i = 0; i < SMALL_NR; i++) {
+        const int r = t + i * SMALL_NT;
+        if (r >= n) continue;
+        double acc = 0.0;
+        for (int k = 0; k < nitem; k++) acc = fma(coef[k], src[k][r], acc);
+        a.out[r] = acc;
+        nrm = fma(acc, acc, nrm);
+    }
+    if (!a.onorm) return;
+    const double v = warp_sum(nrm);
+    if (lane == 0) wsum[warp] = v;
+    __syncthreads();
+    if (t == 0) {
+        double s = 0.0;
+        for (int w = 0; w < SMALL_NW; w++) s += wsum[w];
+        red[0] = s;
+    }
+    __syncthreads();
+    finalize(a.fin, a.j, 1, red, wk, a.bthr, a.lanczos);
 }
 
 } // namespace phipm

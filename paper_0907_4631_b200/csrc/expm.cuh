@@ -648,8 +648,12 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
         r.mu = mu;
         r.brk = brk;
         r.status = a.st->aborted ? 3 : status ? status : ((s_fin && isfinite(eps) && isfinite(phl)) ? 0 : 5);
-        r.seq = a.seq;
+        // publish to the host (mapped pinned memory): the fields, a system-scope fence, then the
+        // sequence number the host spins on, so it can act before the kernel has even retired
+        r.seq = -1;
         *a.res = r;
+        __threadfence_system();
+        *(volatile int *)&a.res->seq = a.seq;
         if (a.clk) a.clk[6] = clock64();                 // (after the copy above: epilogue end)
     }
 }

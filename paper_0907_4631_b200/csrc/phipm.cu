@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -418,6 +420,29 @@ int sync(phipm_ctx *c)
 {
     CK(cudaStreamSynchronize(c->stream));
     if (c->prof) prof_collect(c);
+    return PHIPM_OK;
+}
+
+// Wait for the attempt result of the exponential just enqueued: spin on the sequence number its
+// epilogue publishes last (after a system-scope fence) in mapped pinned memory, instead of a stream
+// synchronisation.  The controller only needs that block; every later kernel is stream-ordered.
+// Profiling (events to collect) and anything slower than 2 s (e.g. a fault: the stream reports it)
+// fall back to cudaStreamSynchronize.
+int wait_attempt(phipm_ctx *c)
+{
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("PHIPM_SPIN");
+        env = (e && e[0] == '0') ? 0 : 1;
+    }
+    if (c->prof || !env) return sync(c);
+    const volatile int *seqp = &reinterpret_cast<volatile AttemptResult *>(c->res_h)->seq;
+    const auto t0 = std::chrono::steady_clock::now();
+    unsigned spins = 0;
+    while (*seqp != c->seq) {
+        if ((++spins & 1023) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) return sync(c);
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
     return PHIPM_OK;
 }
 
@@ -898,7 +923,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             ea.combd = c->combd;
             int rc = launch_expm(c, ea, m + p + 1);
             if (rc) return finish(rc);
-            rc = sync(c);
+            rc = wait_attempt(c);
             if (rc) return finish(rc);
             AttemptResult R;
     memcpy(&R, (const void *)c->res_h, sizeof(R));

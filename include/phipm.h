@@ -211,7 +211,8 @@ int phipm_phi_pair(phipm_ctx *ctx, int mu, const double *H, int ldh, double tau,
                    double *phip, double *phip1, double *normH1);
 /* Krylov basis from seed v (Alg. 1 via CGS per opts->orth, or Alg. 2 if symmetric): V device
  * n x (m+1) column-major (ld n, normalised columns), H device (m+1) x m column-major; *k (HOST)
- * columns of H built, *brk (HOST) 1 on breakdown, *beta (HOST) = ||v||. */
+ * columns of H built, *brk (HOST) 1 on breakdown, *beta (HOST) = ||v||.  V = H = NULL builds the
+ * basis in the context workspace without exporting it (the Arnoldi-step microbenchmark). */
 int phipm_krylov_csr(phipm_ctx *ctx, const phipm_csr *A, const double *v, int m,
                      const phipm_opts *opts, double *V, double *H, int *k, int *brk, double *beta);
 int phipm_krylov_stencil(phipm_ctx *ctx, const phipm_stencil *S, const double *v, int m,

@@ -376,21 +376,28 @@ class Context:
                                            C.byref(nh)))
         return a, b, nh.value
 
-    def krylov(self, A, v, m: int, symmetric=False, orth=ORTH_CGS):
-        """A: Stencil or CSR tuple of CUDA tensors.  Returns (V n x (m+1), H (m+1) x m, k, brk, beta)."""
+    def krylov(self, A, v, m: int, symmetric=False, orth=ORTH_CGS, build_only=False):
+        """A: Stencil or CSR tuple of CUDA tensors.  Returns (V n x (m+1), H (m+1) x m, k, brk, beta);
+        build_only: build the basis in the workspace without exporting V, H (returns None, None, ...)."""
         torch = _torch()
         n = v.numel()
-        Vcm = torch.zeros((m + 1, n), dtype=torch.float64, device=v.device)      # column-major n x (m+1)
-        Hcm = torch.zeros((m, m + 1), dtype=torch.float64, device=v.device)      # column-major (m+1) x m
+        if build_only:
+            Vp = Hp = None
+        else:
+            Vcm = torch.zeros((m + 1, n), dtype=torch.float64, device=v.device)      # column-major n x (m+1)
+            Hcm = torch.zeros((m, m + 1), dtype=torch.float64, device=v.device)      # column-major (m+1) x m
+            Vp, Hp = _f64(Vcm), _f64(Hcm)
         k, brk, beta = C.c_int(), C.c_int(), C.c_double()
         o = self.opts(symmetric=symmetric, orth=orth)
         if isinstance(A, Stencil):
-            st = self._L.phipm_krylov_stencil(self._h, C.byref(A._c()), _f64(v), m, C.byref(o), _f64(Vcm),
-                                              _f64(Hcm), C.byref(k), C.byref(brk), C.byref(beta))
+            st = self._L.phipm_krylov_stencil(self._h, C.byref(A._c()), _f64(v), m, C.byref(o), Vp, Hp,
+                                              C.byref(k), C.byref(brk), C.byref(beta))
         else:
-            st = self._L.phipm_krylov_csr(self._h, C.byref(self._csr(A)), _f64(v), m, C.byref(o), _f64(Vcm),
-                                          _f64(Hcm), C.byref(k), C.byref(brk), C.byref(beta))
+            st = self._L.phipm_krylov_csr(self._h, C.byref(self._csr(A)), _f64(v), m, C.byref(o), Vp, Hp,
+                                          C.byref(k), C.byref(brk), C.byref(beta))
         self._check(st)
+        if build_only:
+            return None, None, k.value, bool(brk.value), beta.value
         return Vcm.t(), Hcm.t(), k.value, bool(brk.value), beta.value
 
 

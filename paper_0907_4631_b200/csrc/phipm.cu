@@ -1744,7 +1744,7 @@ static int krylov_export(phipm_ctx *c, const Op &op, double bytes_op, double nor
                          const phipm_opts *opts, double *V, double *H, int *k, int *brk, double *beta)
 {
     phipm_opts o = resolve_opts(opts);
-    if (!v || !V || !H || m < 1 || m > c->m_max) return set_err(c, PHIPM_EINVAL, "krylov: bad args");
+    if (!v || (!V) != (!H) || m < 1 || m > c->m_max) return set_err(c, PHIPM_EINVAL, "krylov: bad args");
     const int64_t n = op.n;
     if (n > c->n_max) return set_err(c, PHIPM_EINVAL, "krylov: n > n_max");
     CK(cudaMemsetAsync(c->H, 0, sizeof(double) * (c->m_max + 1) * c->m_max, c->stream));
@@ -1767,6 +1767,12 @@ static int krylov_export(phipm_ctx *c, const Op &op, double bytes_op, double nor
     if (rc) return rc;
     if (ds.aborted) return set_err(c, PHIPM_ECUDA, "persistent Krylov kernel: grid phase timed out");
     const int kk = (ds.brk >= 0) ? std::min(ds.brk, m) : m;
+    if (!V) {                                             // build only (no export): timing
+        *k = kk;
+        *brk = ds.brk >= 0 ? 1 : 0;
+        *beta = ds.beta;
+        return PHIPM_OK;
+    }
     const int ncols = (ds.brk >= 0) ? kk : m + 1;
     dim3 grid((unsigned)std::min<int64_t>((n + 255) / 256, 1024), (unsigned)std::max(ncols, 1));
     if (ncols > 0) scale_columns_kernel<<<grid, 256, 0, c->stream>>>(n, ncols, c->V, c->ldv, c->sigma, V, n);

@@ -202,6 +202,10 @@ int phipm_spmv_stencil(phipm_ctx *ctx, const phipm_stencil *S, const double *x, 
 /* *result (HOST) = x^T y, deterministic grid reduction */
 int phipm_dot(phipm_ctx *ctx, int64_t n, const double *x, const double *y, double *result);
 /* *result (HOST) = ||A||_inf */
+/* ||A||_inf of a stencil operator (HOST arithmetic, no GPU): the closed form over the grid's boundary
+ * classes, each row summed in ascending column order (bit-exact with the CSR form's sequential sum);
+ * -1 on a bad descriptor. */
+double phipm_inf_norm_stencil(const phipm_stencil *S);
 int phipm_inf_norm_csr(phipm_ctx *ctx, const phipm_csr *A, double *result);
 /* E = exp(A), K x K column-major (Pade-13 scaling and squaring), K <= m_max + p_max + 1 */
 int phipm_expm(phipm_ctx *ctx, int K, const double *A, double *E);

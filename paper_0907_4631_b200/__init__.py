@@ -138,6 +138,7 @@ def lib():
             "phipm_solve_stencil_batch": (i32, [P(vp), i32, P(d), P(_Stencil), P(i32), P(vp), P(_Opts), P(vp),
                                                 P(_Stats), P(i32)]),
             "phipm_stencil_nnz": (i64, [P(_Stencil)]),
+            "phipm_inf_norm_stencil": (d, [P(_Stencil)]),
             "phipm_csr_from_stencil": (i32, [vp, P(_Stencil), vp, vp, vp]),
             "phipm_spmv_csr": (i32, [vp, P(_Csr), vp, vp]),
             "phipm_spmv_stencil": (i32, [vp, P(_Stencil), vp, vp]),
@@ -160,7 +161,7 @@ EXPORTED = [
     "phipm_default_opts", "phipm_set_expm_method", "phipm_mm_read", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
     "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_solve_csr", "phipm_solve_stencil",
     "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_solve_csr_batch",
-    "phipm_solve_stencil_batch", "phipm_stencil_nnz",
+    "phipm_solve_stencil_batch", "phipm_stencil_nnz", "phipm_inf_norm_stencil",
     "phipm_csr_from_stencil", "phipm_spmv_csr", "phipm_spmv_stencil", "phipm_dot", "phipm_inf_norm_csr",
     "phipm_expm", "phipm_phi_pair", "phipm_krylov_csr", "phipm_krylov_stencil",
 ]
@@ -438,6 +439,11 @@ def solve_batch(ctxs: Sequence["Context"], t, ops, us: Sequence[Sequence], outs=
         bad = next((b for b in range(nb) if status[b] != OK), 0)
         ctxs[bad]._check(status[bad] if status[bad] != OK else rc)
     return outs, [Stats(*[getattr(x, k) for k, _ in _Stats._fields_]) for x in st]
+
+
+def inf_norm_stencil(S: "Stencil") -> float:
+    """||A||_inf of a stencil operator (host closed form, bit-exact with the CSR row sums)."""
+    return float(lib().phipm_inf_norm_stencil(C.byref(S._c())))
 
 
 def read_matrix_market(path: str):

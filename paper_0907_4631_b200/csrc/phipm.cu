@@ -1590,6 +1590,13 @@ int phipm_solve_stencil_host(phipm_ctx *c, double t, const phipm_stencil *S, int
 
 // ---- kernel-level entry points ----
 
+double phipm_inf_norm_stencil(const phipm_stencil *S)
+{
+    StencilOp op;
+    if (make_stencil(nullptr, S, op) != PHIPM_OK) return -1.0;
+    return stencil_infnorm(op);
+}
+
 int64_t phipm_stencil_nnz(const phipm_stencil *S)
 {
     StencilOp op;

@@ -20,10 +20,12 @@ full() {  # config kernel-regex skip name
 }
 full c3 spmv_stream 20 c3_spmv
 full c3 axpy_stream 18 c3_axpy
-full c4 spmv_stream 6 c4_spmv
 full c5 spmv_stream 6 c5_spmv
 full c3 expm_kernel 3 c3_expm
 full c4 krylov_persist 0 c4_persist
 full c1 krylov_small 10 c1_small
 for c in c2 c3 c4 c5; do timeout 200 python tools/kclock.py $c > $O/kclock_$c.txt 2>&1; done
-ls -la $O/pf_* | tail -30
+# summarise here and drop the raw reports: gpurun copies back at most 64 MiB of gpurun_out/
+python tools/make_profiles.py round1 $O/round1_profiles > $O/make_profiles.log 2>&1
+rm -f $O/*.ncu-rep $O/*.bin $O/*.bin.p
+ls -la $O | tail -40

@@ -12,7 +12,11 @@ from ncu_summary import summary  # noqa: E402
 
 rnd = sys.argv[1] if len(sys.argv) > 1 else "round1"
 src = os.path.join(ROOT, "gpurun_out")
-dst = os.path.join(ROOT, "profiles", rnd)
+# argv[2] (optional): output directory (on the GPU box: a directory under gpurun_out, which is what
+# gpurun copies back); profiles/ncu_traffic.json then goes there too
+dst = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", rnd)
+TRAFFIC = os.path.join(dst, "ncu_traffic.json") if len(sys.argv) > 2 else os.path.join(ROOT, "profiles",
+                                                                                        "ncu_traffic.json")
 os.makedirs(dst, exist_ok=True)
 
 
@@ -45,7 +49,7 @@ if os.path.exists(p):
                                                                        "usecond": 1.0, "ms": 1e3}.get(unit, 1e-3)
     tot = sum(v[1] for v in agg.values())
     with open(os.path.join(dst, "launches_c3_summary.txt"), "w") as f:
-        f.write("ncu --metrics gpu__time_duration.sum --clock-control none  python bench.py --steps 2 --warmup 1 "
+        f.write("ncu --metrics gpu__time_duration.sum --clock-control none  python bench.py --steps 2 --warmup 3 "
                 "--no-cpu-baseline  (config c3; cold-cache, serialised launches: compare SHARES)\n")
         f.write(f"{'kernel':34s} {'launches':>8s} {'total us':>10s} {'share':>7s}\n")
         for k, (n, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
@@ -88,10 +92,10 @@ for cfg in ("c3", "c4", "c5"):
                         "launches": len(sp), "source": f"profiles/{rnd}/dram_traffic_{cfg}.txt"}
     os.system(f"cp {p} {dst}/dram_{cfg}.csv")
 if traffic:
-    json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+    json.dump(traffic, open(TRAFFIC, "w"), indent=1)
 
 # 3) --set full summaries of the top kernels
-for name in ("pf_full_c3_spmv", "pf_full_c3_axpy", "pf_full_c4_spmv", "pf_full_c4_persist", "pf_full_c5_spmv",
+for name in ("pf_full_c3_spmv", "pf_full_c3_axpy", "pf_full_c4_persist", "pf_full_c5_spmv",
              "pf_full_c3_expm", "pf_full_c1_small"):
     p = os.path.join(src, name + ".ncu-rep")
     if os.path.exists(p):

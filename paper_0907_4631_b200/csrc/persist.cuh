@@ -119,7 +119,9 @@ __host__ __device__ inline size_t persist_smem_bytes(int halo_cap, int64_t rpc, 
            sizeof(double);
 }
 
-template <int RPT>
+// LANC: Lanczos (symmetric) or Arnoldi; DIM: 1, 2, 3 or 4 (= 2-D 9-point) -- compile-time, so each
+// instantiation carries only its own stencil and orthogonalisation code (registers, no spills)
+template <int RPT, bool LANC, int DIM>
 __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, PersistArgs a, Work wk)
 {
     constexpr int TILE_ = SNT * RPT;
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
         if (s_stop) break;                                 // breakdown (same decision in every CTA)
         const double *x = wk.V + (int64_t)j * ldv;
         const double sj = s_sig;                           // sigma_j, local copy
-        const bool lanc = a.symmetric != 0;
+        constexpr bool lanc = LANC;
         const double *zv = (lanc && j > 0) ? x - ldv : nullptr;
         const double lz = zv ? s_lz : 0.0;
         const int c0 = lanc ? j : 0;
@@ -182,7 +184,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
             mbar_wait(&hbar, ht & 1);
             const int *ho = hofs[ht & 1];
             ht++;
-            stencil_tile<NP>(op, hbuf, ho, r0, rows, tid, y, xr, &gcoord);
+            stencil_tile_d<NP, (DIM == 4 ? 2 : DIM), (DIM == 4)>(op, hbuf, ho, r0, rows, tid, y, xr, &gcoord);
             __syncthreads();                               // halo consumed
             if (tid == 0 && r1 < ce)
                 issue_halo_tile<TILE_>(op, hbuf, x, ldv, r1, (int)min((int64_t)TILE_, ce - r1), hofs[ht & 1], &hbar);
@@ -262,7 +264,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
         __syncthreads();
         if (!phase_allreduce(wk, bsum, nd + 1, ++phase, a, red)) return;
         // finalize (FIN_ARNOLDI / FIN_LANCZOS): h_k = sigma_k d_k, g_k = h_k sigma_k
-        if (lanc) {
+        if constexpr (LANC) {
             if (tid == 0) {
                 const double al = sj * red[0];
                 gco[0] = -(al * sj);

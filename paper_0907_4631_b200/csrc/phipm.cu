@@ -591,11 +591,45 @@ double tau0(double normA, double b_inf, double tol, double mbar)
 template <class Op>
 bool launch_persist(phipm_ctx *, const Op &, double, bool, int, int, double, int &) { return false; }
 
+using PersistFn = void (*)(StencilOp, PersistArgs, Work);
+
+template <int RPT, bool LANC>
+PersistFn persist_fn_l(int dimc)
+{
+    switch (dimc) {
+    case 1: return krylov_persist_kernel<RPT, LANC, 1>;
+    case 2: return krylov_persist_kernel<RPT, LANC, 2>;
+    case 3: return krylov_persist_kernel<RPT, LANC, 3>;
+    default: return krylov_persist_kernel<RPT, LANC, 4>;
+    }
+}
+
+// the instantiation for this operator (dimension class: 1, 2, 3, or 4 = 2-D 9-point) and method
+template <int RPT>
+PersistFn persist_fn(const StencilOp &op, bool symmetric)
+{
+    const int dimc = (op.dim == 2 && op.diag) ? 4 : op.dim;
+    return symmetric ? persist_fn_l<RPT, true>(dimc) : persist_fn_l<RPT, false>(dimc);
+}
+
+template <int RPT>
+void persist_set_smem(int mx)
+{
+    for (int d = 1; d <= 4; d++)
+        for (int l = 0; l < 2; l++) {
+            StencilOp op{};
+            op.dim = d == 4 ? 2 : d;
+            op.diag = d == 4;
+            cudaFuncSetAttribute(persist_fn<RPT>(op, l != 0), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        }
+}
+
 template <int RPT>
 bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, int k1, double bthr, double bytes,
                      int &rc)
 {
     constexpr int TILE_ = SNT * RPT;
+    const PersistFn kfn = persist_fn<RPT>(op, symmetric);
     int grid;
     int64_t rpc;
     // CTAs: at most one per SM, and (PHIPM_PERSIST_MINROWS, default TILE/2) enough rows each that the
@@ -612,7 +646,7 @@ bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, 
     const size_t smem = persist_smem_bytes(halo_capacity(op.dim, op.nx, TILE_), rpc, ndmax);
     if (smem > c->smem_optin || ndmax + 1 > MAXD + 2) return false;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, krylov_persist_kernel<RPT>, SNT, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, SNT, smem) != cudaSuccess ||
         occ < 1 || grid > occ * c->sm_count) {
         cudaGetLastError();
         return false;
@@ -642,7 +676,7 @@ bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, 
     }
     ProfRec r;
     prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
-    const cudaError_t e = launch_coop(c, krylov_persist_kernel<RPT>, grid, SNT, smem, op, a, make_work(c));
+    const cudaError_t e = launch_coop(c, kfn, grid, SNT, smem, op, a, make_work(c));
     prof_end(c, r);
     c->acc.launches++;
     if (e != cudaSuccess) {
@@ -1380,8 +1414,8 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(krylov_persist_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-        cudaFuncSetAttribute(krylov_persist_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        persist_set_smem<4>(mx);
+        persist_set_smem<2>(mx);
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, maxabs_kernel, NT, 0);
         c->occ_axpy = std::max(1, occ);

@@ -378,9 +378,60 @@ __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double
         if (DIM >= 3) s = term(s, v && k2 < nz - 1, czp, pzp + (q + pl), q);
         return s;
     };
+    // Fast pair path (nx even, 5/7-point or 1-D): both rows of a pair lie on one x-line at (i, i+1),
+    // i even, and every halo segment offset is even, so the 2 DIM + 1 values each row reads come
+    // from 16-B shared loads; when every pair of the warp is y/z-interior (warp-uniform branch) only
+    // row a's x- and row b's x+ neighbour can be absent, and an absent value is replaced by 0 before
+    // its product: s + c 0 = s exactly (s starts at +0 and can never become -0), so the sums are
+    // bit-identical with the per-term path below.
+    const bool fastok = !DG && (DIM == 1 || (nx & 1) == 0);
 #pragma unroll
     for (int p = 0; p < NP; p++) {
         const int q = 2 * tid + 2 * SNT * p;
+        const bool v0 = q < rows, v1 = q + 1 < rows;
+        // which of the z-, z+, y-, y+ neighbours the pair has (bits 0..3); the fast path needs the
+        // same set for every lane, so a boundary plane or line is skipped by a uniform branch
+        int nbm = 0;
+        if (DIM >= 2) nbm |= (jj > 0 ? 4 : 0) | (jj < ny - 1 ? 8 : 0);
+        if (DIM >= 3) nbm |= (kk > 0 ? 1 : 0) | (kk < nz - 1 ? 2 : 0);
+        const int nbm0 = __shfl_sync(0xffffffffu, nbm, 0);
+        bool inner = v1 && nbm == nbm0;
+        if (DIM == 1) inner = inner && i > 0 && i + 2 < nx;           // 1-D: every neighbour present
+        if (fastok && __all_sync(0xffffffffu, inner)) {
+            auto ld2 = [](const double *a) { return *reinterpret_cast<const double2 *>(a); };
+            const double2 xl = ld2(pc + q - 2), xc = ld2(pc + q), xh = ld2(pc + q + 2);
+            const double am = (DIM == 1 || i > 0) ? xl.y : 0.0;        // x- of row a
+            const double bp = (DIM == 1 || i + 2 < nx) ? xh.x : 0.0;   // x+ of row b
+            double sa = 0.0, sb = 0.0;
+            if (DIM >= 3 && (nbm0 & 1)) {
+                const double2 zm = ld2(pzm + (q - pl));
+                sa = __dadd_rn(sa, __dmul_rn(czm, zm.x));
+                sb = __dadd_rn(sb, __dmul_rn(czm, zm.y));
+            }
+            if (DIM >= 2 && (nbm0 & 4)) {
+                const double2 ym = ld2(pym + (q - nx));
+                sa = __dadd_rn(sa, __dmul_rn(cym, ym.x));
+                sb = __dadd_rn(sb, __dmul_rn(cym, ym.y));
+            }
+            sa = __dadd_rn(sa, __dmul_rn(cxm, am));
+            sb = __dadd_rn(sb, __dmul_rn(cxm, xc.x));
+            sa = __dadd_rn(sa, __dmul_rn(c0, xc.x));
+            sb = __dadd_rn(sb, __dmul_rn(c0, xc.y));
+            sa = __dadd_rn(sa, __dmul_rn(cxp, xc.y));
+            sb = __dadd_rn(sb, __dmul_rn(cxp, bp));
+            if (DIM >= 2 && (nbm0 & 8)) {
+                const double2 yp = ld2(pyp + (q + nx));
+                sa = __dadd_rn(sa, __dmul_rn(cyp, yp.x));
+                sb = __dadd_rn(sb, __dmul_rn(cyp, yp.y));
+            }
+            if (DIM >= 3 && (nbm0 & 2)) {
+                const double2 zp = ld2(pzp + (q + pl));
+                sa = __dadd_rn(sa, __dmul_rn(czp, zp.x));
+                sb = __dadd_rn(sb, __dmul_rn(czp, zp.y));
+            }
+            xr[p] = xc;
+            y[p] = make_double2(sa, sb);
+        } else {
         // second row of the pair: one step along x (wrapping to the next line / plane)
         int i1 = i + 1, j1 = jj, k1 = kk;
         if (i1 == nx) {
@@ -390,13 +441,13 @@ __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double
                 if (j1 == ny) { j1 = 0; k1++; }
             }
         }
-        const bool v0 = q < rows, v1 = q + 1 < rows;
         const int qa = v0 ? q : 0, qb = v1 ? q + 1 : 0;     // rows past the tile: any valid index
         xr[p].x = v0 ? pc[qa] : 0.0;
         xr[p].y = v1 ? pc[qb] : 0.0;
         const double ya = row(v0, qa, i, jj, kk), yb = row(v1, qb, i1, j1, k1);
         y[p].x = v0 ? ya : 0.0;
         y[p].y = v1 ? yb : 0.0;
+        }
         if (p + 1 < NP || gc) {
             i += di;
             if (DIM >= 2) {

@@ -24,6 +24,7 @@
 #include "stream.cuh"
 #include "small.cuh"
 #include "persist.cuh"
+#include "persist_tm.cuh"
 
 using namespace phipm;
 
@@ -686,6 +687,75 @@ bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, 
     return true;
 }
 
+PersistFn persist_tm_fn(const StencilOp &op)
+{
+    switch ((op.dim == 2 && op.diag) ? 4 : op.dim) {
+    case 1: return krylov_persist_tm_kernel<1>;
+    case 2: return krylov_persist_tm_kernel<2>;
+    case 3: return krylov_persist_tm_kernel<3>;
+    default: return krylov_persist_tm_kernel<4>;
+    }
+}
+
+// Lanczos with the CTA's y / v~_j in tensor memory and double-buffered halo tiles (persist_tm.cuh),
+// when every CTA's rows fit the 8 pair slots per thread (PHIPM_TMEM=0 disables)
+bool try_persist_tm(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bthr, double bytes, int &rc)
+{
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("PHIPM_TMEM");
+        env = e ? atoi(e) : 1;
+    }
+    if (!env) return false;
+    constexpr int TILE_ = SNT * 4;
+    int grid;
+    int64_t rpc;
+    const int slots = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (op.n + TILE_ / 2 - 1) / (TILE_ / 2)));
+    balance(c, op.n, slots, grid, rpc);
+    if ((rpc + TILE_ - 1) / TILE_ * 2 > TM_PAIRS) return false;
+    const size_t smem = persist_tm_smem_bytes(halo_capacity(op.dim, op.nx, TILE_));
+    if (smem > c->smem_optin) return false;
+    const PersistFn kfn = persist_tm_fn(op);
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, SNT, smem) != cudaSuccess || occ < 1 ||
+        grid > occ * c->sm_count) {
+        cudaGetLastError();
+        return false;
+    }
+    PersistArgs a;
+    a.k0 = k0;
+    a.k1 = k1;
+    a.symmetric = 1;
+    a.bthr = bthr;
+    a.rpc = rpc;
+    a.flag = c->counter + 2;
+    a.abort = c->counter + 3;
+    a.timeout_ns = 2000000000ull;
+    a.dbg = nullptr;
+    const size_t need = (size_t)2 * (k1 - k0) * grid * 2;
+    if (c->pclk_d && c->pclk_used + need <= PCLK_CAP) {
+        a.dbg = c->pclk_d + c->pclk_used;
+        c->pclk_recs.push_back({grid, k1 - k0, (long long)c->pclk_used});
+        c->pclk_used += need;
+    }
+    rc = PHIPM_OK;
+    if (cudaMemsetAsync(c->counter + 2, 0, 2 * sizeof(unsigned), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(&c->st->aborted, 0, sizeof(int), c->stream) != cudaSuccess) {
+        rc = set_err(c, PHIPM_ECUDA, "persist: memset failed");
+        return true;
+    }
+    ProfRec r;
+    prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
+    const cudaError_t e = launch_coop(c, kfn, grid, SNT, smem, op, a, make_work(c));
+    prof_end(c, r);
+    c->acc.launches++;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+
 template <>
 bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_op, bool symmetric, int k0, int k1,
                                double bthr, int &rc)
@@ -703,6 +773,9 @@ bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_o
     double bytes = 0.0;
     const double n = (double)op.n;
     for (int j = k0; j < k1; j++) bytes += bytes_op + 8.0 * n * (symmetric ? 4.0 : 2.0 * j + 3.0);
+    // (small grids keep the 2048-row tiles: a 4096-row tile would leave half a CTA's threads idle)
+    if (symmetric && op.n >= (int64_t)SNT * 4 * c->sm_count / 2 && try_persist_tm(c, op, k0, k1, bthr, bytes, rc))
+        return true;
     // largest tile that fits (halo + the CTA's y + dot partials); RPT = 8 would spill
     if (op.n >= (int64_t)SNT * 4 * c->sm_count / 2 && try_persist_rpt<4>(c, op, symmetric, k0, k1, bthr, bytes, rc))
         return true;
@@ -1414,6 +1487,12 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        for (int d = 1; d <= 4; d++) {
+            StencilOp op{};
+            op.dim = d == 4 ? 2 : d;
+            op.diag = d == 4;
+            cudaFuncSetAttribute(persist_tm_fn(op), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        }
         persist_set_smem<4>(mx);
         persist_set_smem<2>(mx);
         int occ = 1;

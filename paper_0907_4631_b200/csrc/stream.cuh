@@ -397,7 +397,11 @@ __device__ __forceinline__ void stencil_tile_d(const StencilOp &op, const double
         const int nbm0 = __shfl_sync(0xffffffffu, nbm, 0);
         bool inner = v1 && nbm == nbm0;
         if (DIM == 1) inner = inner && i > 0 && i + 2 < nx;           // 1-D: every neighbour present
-        if (fastok && __all_sync(0xffffffffu, inner)) {
+        if (!__any_sync(0xffffffffu, v0)) {
+            // the whole warp's rows lie past the tile end (last, partial tile)
+            xr[p] = make_double2(0.0, 0.0);
+            y[p] = make_double2(0.0, 0.0);
+        } else if (fastok && __all_sync(0xffffffffu, inner)) {
             auto ld2 = [](const double *a) { return *reinterpret_cast<const double2 *>(a); };
             const double2 xl = ld2(pc + q - 2), xc = ld2(pc + q), xh = ld2(pc + q + 2);
             const double am = (DIM == 1 || i > 0) ? xl.y : 0.0;        // x- of row a

@@ -71,7 +71,10 @@ __device__ __forceinline__ bool phase_allreduce(const Work &wk, const double *bs
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.flag) : "memory");
         const unsigned target = phase * (unsigned)nb;
         const unsigned long long t0 = gtimer();
-        while (ld_acquire_u32(a.flag) < target) {
+        // the abort flag and the clock are looked at every 16th poll only: a volatile load per
+        // iteration doubles the poll period (two dependent L2 round trips)
+        for (unsigned it = 1; ld_acquire_u32(a.flag) < target; it++) {
+            if (it & 15) continue;
             if (*(volatile unsigned *)a.abort) { ok = 0; break; }
             if (gtimer() - t0 > a.timeout_ns) {
                 atomicExch(a.abort, 1u);

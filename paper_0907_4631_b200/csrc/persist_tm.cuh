@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
     static_assert(NP == 2, "TMEM slots are moved two pairs (8 columns) at a time");
     extern __shared__ __align__(128) double sm[];
     __shared__ uint64_t hbar[2];
-    __shared__ int hofs[2][5];
+    __shared__ TilePlan tplan[TM_PAIRS / 2];
     __shared__ double bsum[2];
     __shared__ double red[MAXD + 2];
     __shared__ double wsum[SNW];
@@ -119,6 +119,11 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
         s_sig = __ldcg(wk.sigma + a.k0);
         s_lz = __ldcg(&wk.st->lz);
     }
+    if (tid < TM_PAIRS / 2) {
+        const int64_t ru = cs + (int64_t)tid * TILE_;
+        if (ru < ce) tile_plan<TILE_>(op, ldv, ru, (int)min((int64_t)TILE_, ce - ru), tplan[tid]);
+    }
+    const uint64_t pol = policy_evict_last();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -142,9 +147,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
             for (int u = 0; u < 2; u++) {
                 const int64_t ru = cs + (int64_t)u * TILE_;
                 const uint32_t g = ht + u;
-                if (ru < ce)
-                    issue_halo_tile<TILE_>(op, sm + (g & 1) * hstride, x, ldv, ru, (int)min((int64_t)TILE_, ce - ru),
-                                           hofs[g & 1], &hbar[g & 1]);
+                if (ru < ce) issue_planned_tile(tplan[u], sm + (g & 1) * hstride, x, &hbar[g & 1], pol);
             }
         double ysq = 0.0, dot = 0.0;
         int3 gcoord = gc0;
@@ -166,11 +169,10 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
             double *hb = sm + (g & 1) * hstride;
             double2 y[NP], xr[NP];
             mbar_wait(&hbar[g & 1], (g >> 1) & 1);
-            stencil_tile_d<NP, (DIM == 4 ? 2 : DIM), (DIM == 4)>(op, hb, hofs[g & 1], r0, rows, tid, y, xr, &gcoord);
+            stencil_tile_d<NP, (DIM == 4 ? 2 : DIM), (DIM == 4)>(op, hb, tplan[t].ho, r0, rows, tid, y, xr, &gcoord);
             __syncthreads();                               // halo buffer g & 1 consumed
             if (tid == 0 && r0 + 2 * TILE_ < ce)
-                issue_halo_tile<TILE_>(op, hb, x, ldv, r0 + 2 * TILE_, (int)min((int64_t)TILE_, ce - r0 - 2 * TILE_),
-                                       hofs[g & 1], &hbar[g & 1]);
+                issue_planned_tile(tplan[t + 2], hb, x, &hbar[g & 1], pol);
 #pragma unroll
             for (int p = 0; p < NP; p++) {
                 const int q = 2 * tid + 2 * SNT * p;

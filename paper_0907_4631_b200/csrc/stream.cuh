@@ -318,6 +318,48 @@ __device__ __forceinline__ void issue_halo_tile(const StencilOp &op, double *hbu
         if (h.bytes[k]) tma_load_1d(hbuf + h.off[k], x + h.start[k], h.bytes[k], bar, pol);
 }
 
+// A tile's halo plan, computed once per kernel (the segments' offsets relative to the source vector
+// do not change from one Krylov column to the next): issuing a tile is then one expect_tx and
+// nseg bulk copies, instead of the 64-bit plan arithmetic (local-memory arrays) on the issuing
+// thread while its warp waits.
+struct TilePlan {
+    int64_t start[5];
+    uint32_t bytes[5];
+    int off[5];
+    int ho[5];                       // tile-relative offsets of the centre, y-, y+, z-, z+ segments
+    int nseg;
+    uint32_t tot;
+};
+
+template <int TILE_>
+__device__ __forceinline__ void tile_plan(const StencilOp &op, int64_t ldx, int64_t hr0, int hrows, TilePlan &tp)
+{
+    HaloPlan h;
+    halo_plan(op, TILE_, hr0, hrows, ldx, h);
+    const int seg[5] = {0, h.ylo, h.yhi, h.zlo, h.zhi};
+    uint32_t tot = 0;
+#pragma unroll
+    for (int k = 0; k < 5; k++) {
+        tp.ho[k] = h.off[seg[k]] - (int)(h.start[seg[k]] - hr0);
+        tp.start[k] = h.start[k];
+        tp.bytes[k] = k < h.nseg ? h.bytes[k] : 0u;
+        tp.off[k] = h.off[k];
+        tot += tp.bytes[k];
+    }
+    tp.nseg = h.nseg;
+    tp.tot = tot;
+}
+
+// issue a planned tile's bulk copies of vector x into hbuf (one thread)
+__device__ __forceinline__ void issue_planned_tile(const TilePlan &tp, double *hbuf, const double *x, uint64_t *bar,
+                                                   uint64_t pol)
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of hbuf
+    mbar_arrive_expect_tx(bar, tp.tot);
+    for (int k = 0; k < tp.nseg; k++)
+        if (tp.bytes[k]) tma_load_1d(hbuf + tp.off[k], x + tp.start[k], tp.bytes[k], bar, pol);
+}
+
 // The raw rows (A x)_r of one stencil tile from its halo in shared memory (ho: tile-relative
 // offsets of the centre, y-, y+, z-, z+ segments), for this thread's NP row pairs
 // q = 2 tid + 2 SNT p, and the x values themselves (xr, for a dot with v_j = x).  Ascending column

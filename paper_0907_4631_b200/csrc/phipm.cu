@@ -61,6 +61,7 @@ struct phipm_ctx {
     double *V = nullptr, *W = nullptr, *Y = nullptr, *U = nullptr, *H = nullptr, *sigma = nullptr, *g = nullptr;
     double *part = nullptr, *comb = nullptr, *combd = nullptr, *scratch = nullptr, *raw = nullptr;
     unsigned *counter = nullptr;
+    cudaEvent_t ev_binf = nullptr;                   // ||u_0||_inf readback of a solve
     DevState *st = nullptr;
     int32_t *tlo = nullptr, *thi = nullptr;                  // CSR per-tile column ranges
     int64_t ntile_cap = 0;
@@ -926,12 +927,9 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         int rc = sync(c);
         return finish(rc);
     }
-    // b_inf of Eq. (tau_0) = ||u_0||_inf, or the first nonzero ||u_k||_inf (R7); all zero -> w = 0.
-    // u_0 alone first: the other p vectors are only read when u_0 = 0 (c4: 17 MB instead of 84 MB)
-    for (int k0 = 0; k0 <= p;) {
+    auto enqueue_maxabs = [&](int k0, int k1) {
         MaxAbsArgs ma;
         memset(&ma, 0, sizeof(ma));
-        const int k1 = k0 == 0 ? 1 : p + 1;
         ma.nv = k1 - k0;
         for (int k = k0; k < k1; k++) ma.x[k - k0] = u[k];
         const int grid = grid_for(c, (n + NT - 1) / NT, c->occ_axpy);
@@ -939,46 +937,10 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         c->acc.launches++;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(c->raw_h + k0, c->raw, ma.nv * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        int rc = sync(c);
-        if (rc) return finish(rc);
-        if (c->raw_h[0] != 0.0) {
-            for (int k = 1; k <= p; k++) c->raw_h[k] = 0.0;     // not read (b_inf is u_0's)
-            break;
-        }
-        k0 = k1;
-    }
-    double b_inf = 0.0;
-    for (int k = 0; k <= p && b_inf == 0.0; k++) b_inf = c->raw_h[k];
-    if (b_inf == 0.0) {
-        CK(cudaMemsetAsync(w, 0, n * sizeof(double), c->stream));
-        S.t_reached = t_end;
-        return finish(sync(c));
-    }
-    if (!std::isfinite(b_inf)) return finish(set_err(c, PHIPM_ENONFINITE, "non-finite input vector"));
-
-    Problem P;
-    P.p = p;
-    P.n = n;
-    P.NA = NA;
-    P.symmetric = o.symmetric != 0;
-    P.m_max = (int)std::min<int64_t>(o.m_max, n);
-    P.fixed_m = o.fixed_m != 0;
-    P.eq6_variant = o.eq6_variant != 0;
-    int m = std::min(o.m_init, P.m_max);
-    const double mbar = 0.5 * ((double)o.m_init + (double)P.m_max);
-    double tau = (normA == 0.0) ? t_end : std::min(t_end, tau0(normA, b_inf, o.tol, mbar));
-    if (!(tau > 0.0)) tau = t_end;
-    const double bthr = (double)n * EPS_MACH * normA;
-
-    // the running solution u_k lives in the padded workspace vector U (TMA-readable)
-    double *ucur = c->U;
-    CK(cudaMemsetAsync(c->H, 0, sizeof(double) * (c->m_max + 1) * c->m_max, c->stream));
-    CK(cudaMemcpyAsync(ucur, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    double tk = 0.0;
-    S.m_peak = m;
-    while (tk < t_end) {
-        if (tau > t_end - tk) tau = t_end - tk;
-        // Eq. (wrecurrence): w_0 = u_k, w_j = A w_{j-1} + sum_l t_k^l/l! u_{j+l}; w_p -> V[:,0]
+        return PHIPM_OK;
+    };
+    // Eq. (wrecurrence): w_0 = u_k, w_j = A w_{j-1} + sum_l t_k^l/l! u_{j+l}; w_p -> V[:,0]
+    auto enqueue_wrec = [&](double tk, const double *ucur) {
         if (p == 0) {
             AxpyArgs a = axpy0();
             a.out = c->V;
@@ -988,8 +950,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             a.ldv = c->ldv;
             a.onorm = 1;
             a.fin = FIN_SEED;
-            int rc = launch_axpy(c, n, a, PC_OTHER);
-            if (rc) return finish(rc);
+            return launch_axpy(c, n, a, PC_OTHER);
         }
         for (int j = 1; j <= p; j++) {
             SpmvArgs s = spmv0();
@@ -1009,8 +970,84 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             s.ynorm = (j == p);
             s.fin = (j == p) ? FIN_SEED : FIN_NONE;
             int rc = launch_spmv(c, op, s, bytes_op);
+            if (rc) return rc;
+        }
+        return PHIPM_OK;
+    };
+
+    Problem P;
+    P.p = p;
+    P.n = n;
+    P.NA = NA;
+    P.symmetric = o.symmetric != 0;
+    P.m_max = (int)std::min<int64_t>(o.m_max, n);
+    P.fixed_m = o.fixed_m != 0;
+    P.eq6_variant = o.eq6_variant != 0;
+    int m = std::min(o.m_init, P.m_max);
+    const double mbar = 0.5 * ((double)o.m_init + (double)P.m_max);
+    const double bthr = (double)n * EPS_MACH * normA;
+
+    // b_inf of Eq. (tau_0) = ||u_0||_inf, or the first nonzero ||u_k||_inf (R7); all zero -> w = 0.
+    // ||u_0||_inf is read back through an event, and the first step's w-recurrence and initial
+    // Krylov extension -- which do not depend on it: tau enters only the exponential -- are
+    // enqueued before the host waits for it.  The other u_k are only read when u_0 = 0.
+    {
+        int rc = enqueue_maxabs(0, 1);
+        if (rc) return finish(rc);
+        CK(cudaEventRecord(c->ev_binf, c->stream));
+    }
+    // the running solution u_k lives in the padded workspace vector U (TMA-readable)
+    double *ucur = c->U;
+    CK(cudaMemsetAsync(c->H, 0, sizeof(double) * (c->m_max + 1) * c->m_max, c->stream));
+    CK(cudaMemcpyAsync(ucur, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    int enq = 0;                      // Krylov columns already enqueued for the current step
+    {
+        int rc = enqueue_wrec(0.0, ucur);
+        if (rc) return finish(rc);
+        if (m > 0) {
+            rc = enqueue_krylov(c, op, bytes_op, P.symmetric, o.orth, 0, m, bthr);
+            if (rc) return finish(rc);
+            enq = m;
+        }
+    }
+    CK(cudaEventSynchronize(c->ev_binf));
+    double b_inf = c->raw_h[0];
+    if (b_inf == 0.0) {
+        {
+            int rc = sync(c);
             if (rc) return finish(rc);
         }
+        if (p > 0) {
+            int rc = enqueue_maxabs(1, p + 1);
+            if (rc) return finish(rc);
+            rc = sync(c);
+            if (rc) return finish(rc);
+        }
+        for (int k = 1; k <= p && b_inf == 0.0; k++) b_inf = c->raw_h[k];
+        if (b_inf == 0.0) {
+            CK(cudaMemsetAsync(w, 0, n * sizeof(double), c->stream));
+            S.t_reached = t_end;
+            return finish(sync(c));
+        }
+    }
+    if (!std::isfinite(b_inf)) {
+        sync(c);
+        return finish(set_err(c, PHIPM_ENONFINITE, "non-finite input vector"));
+    }
+    double tau = (normA == 0.0) ? t_end : std::min(t_end, tau0(normA, b_inf, o.tol, mbar));
+    if (!(tau > 0.0)) tau = t_end;
+
+    double tk = 0.0;
+    S.m_peak = m;
+    bool first = true;
+    while (tk < t_end) {
+        if (tau > t_end - tk) tau = t_end - tk;
+        if (!first) {
+            enq = 0;
+            int rc = enqueue_wrec(tk, ucur);
+            if (rc) return finish(rc);
+        }
+        first = false;
         S.nspmv += p;
         int k = 0;
         bool brk = false;
@@ -1021,9 +1058,10 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         bool corr = false;
         for (;;) {
             attempts++;
-            if (k < m && !brk) {
-                int rc = enqueue_krylov(c, op, bytes_op, P.symmetric, o.orth, k, m, bthr);
+            if (std::max(k, enq) < m && !brk) {
+                int rc = enqueue_krylov(c, op, bytes_op, P.symmetric, o.orth, std::max(k, enq), m, bthr);
                 if (rc) return finish(rc);
+                enq = m;
             }
             ExpmArgs ea;
             memset(&ea, 0, sizeof(ea));
@@ -1079,9 +1117,10 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             }
         }
         // Eq. (step): u_{k+1} = sum_{i<=mu} comb_i v~_i + sum_{j<p} tau^j/j! w_j  (w_0 = u_k in place)
+        const bool last = tau_used >= t_end - tk;
         {
             AxpyArgs a = axpy0();
-            a.out = ucur;
+            a.out = last ? w : ucur;           // the last step writes the caller's w directly
             a.base = ucur;
             a.a0h = (p >= 1) ? 1.0 : 0.0;
             a.a0d = (p >= 1) ? c->combd : nullptr;
@@ -1100,13 +1139,12 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             int rc = launch_axpy(c, n, a, PC_COMBINE);
             if (rc) return finish(rc);
         }
-        if (tau_used >= t_end - tk) tk = t_end;
+        if (last) tk = t_end;
         else tk += tau_used;
         S.nsteps++;
         S.m_last = m_used;
         S.t_reached = tk;
     }
-    CK(cudaMemcpyAsync(w, ucur, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
     int rc = sync(c);
     return finish(rc);
 }
@@ -1408,6 +1446,7 @@ void phipm_destroy(phipm_ctx *c)
     cudaStreamSynchronize(c->stream);
     for (auto &r : c->pending) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
+    if (c->ev_binf) cudaEventDestroy(c->ev_binf);
     cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
     cudaFree(c->part); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
     cudaFree(c->counter); cudaFree(c->st); cudaFree(c->tlo); cudaFree(c->thi);
@@ -1546,6 +1585,7 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     }
     A((void **)&c->raw, sizeof(double) * (MAXD + 2));
     A((void **)&c->counter, sizeof(unsigned) * 4);
+    if (ok && cudaEventCreateWithFlags(&c->ev_binf, cudaEventDisableTiming) != cudaSuccess) ok = false;
     A((void **)&c->st, sizeof(DevState));
     c->ntile_cap = n_max / 512 + 2;
     A((void **)&c->tlo, sizeof(int32_t) * c->ntile_cap);

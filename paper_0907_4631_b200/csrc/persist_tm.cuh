@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
     extern __shared__ __align__(128) double sm[];
     __shared__ uint64_t hbar[2];
     __shared__ TilePlan tplan[TM_PAIRS / 2];
+    __shared__ unsigned hcons[2];                      // warps done with each halo buffer (monotonic)
     __shared__ double bsum[2];
     __shared__ double red[MAXD + 2];
     __shared__ double wsum[SNW];
@@ -119,6 +120,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
         s_sig = __ldcg(wk.sigma + a.k0);
         s_lz = __ldcg(&wk.st->lz);
     }
+    if (tid < 2) hcons[tid] = 0;
     if (tid < TM_PAIRS / 2) {
         const int64_t ru = cs + (int64_t)tid * TILE_;
         if (ru < ce) tile_plan<TILE_>(op, ldv, ru, (int)min((int64_t)TILE_, ce - ru), tplan[tid]);
@@ -170,9 +172,16 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
             double2 y[NP], xr[NP];
             mbar_wait(&hbar[g & 1], (g >> 1) & 1);
             stencil_tile_d<NP, (DIM == 4 ? 2 : DIM), (DIM == 4)>(op, hb, tplan[t].ho, r0, rows, tid, y, xr, &gcoord);
-            __syncthreads();                               // halo buffer g & 1 consumed
-            if (tid == 0 && r0 + 2 * TILE_ < ce)
-                issue_planned_tile(tplan[t + 2], hb, x, &hbar[g & 1], pol);
+            // halo buffer g & 1 consumed by this warp: no CTA barrier -- the last warp to finish it
+            // (monotonic per-buffer counter: use g >> 1 ends at SNW ((g >> 1) + 1)) issues tile t + 2
+            __syncwarp();
+            if ((tid & 31) == 0) {
+                unsigned old;
+                asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                             : "=r"(old) : "r"(smem_u32(&hcons[g & 1])) : "memory");
+                if (old == (unsigned)SNW * ((g >> 1) + 1) - 1 && r0 + 2 * TILE_ < ce)
+                    issue_planned_tile(tplan[t + 2], hb, x, &hbar[g & 1], pol);
+            }
 #pragma unroll
             for (int p = 0; p < NP; p++) {
                 const int q = 2 * tid + 2 * SNT * p;

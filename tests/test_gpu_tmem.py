@@ -1,0 +1,106 @@
+"""The persistent Lanczos kernel with y / v~_j in tensor memory (csrc/persist_tm.cuh) against the oracle.
+
+The host dispatches Lanczos extensions on stencils to it when n >= 4096 * 148 / 2 = 303,104 rows (a
+4096-row tile per half CTA at least) and every CTA's range fits 4 tiles of 4096 rows.  The cases
+cover every dimension class (1-D, 2-D 5-point, 2-D 9-point, 3-D), even nx (the fast pair path of
+the stencil rows) and odd nx (the per-term path inside the same kernel), ragged last tiles, and
+t large enough that attempts are rejected and m grows, so the kernel is relaunched with k0 > 0
+(its first step then reads v~_{j-1} from global memory, the later ones from TMEM slot B).
+Bar: ||w_gpu - w_ref|| / ||w_ref|| <= max(10 tol, 1e-12) (BASELINE.json north_star).
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_0907_4631_b200 as P
+import workloads as W
+from gpu_common import parity_bound, relerr, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def laplacian(dim, nx, ny, nz, seed, p=2):
+    """Dirichlet Laplacian (heat sign) on an nx x ny x nz grid, h = 1/(nx+1) in every direction."""
+    h2 = float((nx + 1) ** 2)
+    coef = [-2.0 * dim * h2, h2, h2, 0.0, 0.0, 0.0, 0.0]
+    if dim >= 2:
+        coef[3] = coef[4] = h2
+    if dim >= 3:
+        coef[5] = coef[6] = h2
+    rng = np.random.default_rng(seed)
+    n = nx * ny * nz
+    u = [rng.standard_normal(n)] + [rng.uniform(-1, 1, n) for _ in range(p)]
+    return W.Stencil(dim, nx, ny, nz, tuple(coef)), u
+
+
+CASES = [
+    # (dim, nx, ny, nz, t, tol): t chosen so that m has to grow past m_init = 10
+    (3, 72, 70, 68, 2e-4, 1e-10),      # even nx: fast pair path, 3 of 4 tiles in the last CTA ragged
+    (3, 71, 70, 69, 2e-4, 1e-10),      # odd nx: per-term rows inside the TMEM kernel
+    (2, 640, 500, 1, 2e-5, 1e-10),     # 2-D 5-point
+    (1, 400_001, 1, 1, 1e-11, 1e-10),  # 1-D, odd n
+]
+
+
+@pytest.mark.parametrize("dim,nx,ny,nz,t,tol", CASES)
+def test_tmem_lanczos_parity(ctx, orc, dim, nx, ny, nz, t, tol):
+    st, u = laplacian(dim, nx, ny, nz, seed=nx + ny + nz)
+    n = st.n
+    assert n >= 303_104
+    Pb = W.Problem(name="tm", n=n, p=len(u) - 1, t=t, tol=tol, symmetric=True, u=u, stencil=st, seed=0)
+    wo, so, _ = orc.solve(Pb)
+    assert so["status"] == 0
+    w, s = ctx.solve_stencil(t, P.Stencil.of(st), [to_dev(x) for x in u], tol=tol, symmetric=True)
+    assert s.t_reached == t
+    assert s.m_peak > 10, s                         # the extension was relaunched with k0 > 0
+    assert relerr(w.cpu().numpy(), wo) <= parity_bound(tol), (s, so)
+
+
+def test_tmem_lanczos_9pt(ctx, orc):
+    # 2-D 9-point Laplacian (DIM class 4 of the kernel), h^-2 (8 on the diagonal, 1 off it)
+    from test_gpu_ninept import csr_9pt
+    nx, ny = 620, 500
+    h2 = float((nx + 1) ** 2)
+    coef = (-8.0 * h2, h2, h2, h2, h2, 0.0, 0.0)
+    corn = (h2,) * 4
+    rng = np.random.default_rng(7)
+    n = nx * ny
+    u = [rng.standard_normal(n), rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)]
+    t, tol = 1e-5, 1e-10
+    wo, so, _ = orc.phipm(t, csr_9pt(nx, ny, coef, corn), u, tol, m_init=10, m_max=100, symmetric=True)
+    assert so["status"] == 0
+    w, s = ctx.solve_stencil(t, P.Stencil(2, nx, ny, 1, coef, corn, 9), [to_dev(x) for x in u], tol=tol,
+                             symmetric=True)
+    assert s.t_reached == t
+    assert relerr(w.cpu().numpy(), wo) <= parity_bound(tol), (s, so)
+
+
+TM_OFF_SCRIPT = r"""
+import sys
+import numpy as np, torch
+sys.path.insert(0, "tests")
+import paper_0907_4631_b200 as P, workloads as W
+Pb = W.make("c4")
+ctx = P.Context(n_max=Pb.n, m_max=100, p_max=4)
+w, s = ctx.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), [torch.from_numpy(x).cuda() for x in Pb.u],
+                         tol=Pb.tol, symmetric=True)
+np.save(sys.argv[1], w.cpu().numpy())
+print(s)
+"""
+
+
+def test_tmem_and_smem_kernels_agree(tmp_path):
+    # c4 with the TMEM kernel (default) and with PHIPM_TMEM=0 (y in shared memory): the two differ only
+    # in the order the dot products are summed, so w agrees far below the parity bar
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for flag in ("1", "0"):
+        f = os.path.join(tmp_path, f"w{flag}.npy")
+        r = subprocess.run([sys.executable, "-c", TM_OFF_SCRIPT, f], cwd=root, capture_output=True, text=True,
+                           env=dict(os.environ, PHIPM_TMEM=flag), timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        out[flag] = np.load(f)
+    assert relerr(out["1"], out["0"]) <= 1e-12

@@ -129,6 +129,7 @@ __device__ __forceinline__ void cta_matmul(int Kp, int ld, const double *A, cons
 struct EpiBlock {
     const double *A1, *A2, *A3;
     int ld;
+    double fv;                       // exact power-of-two factor of the product (the scaling 2^-4s)
     double c0, c1, c2, c3;
     __device__ double operator()(int r, int c, double v) const
     {
@@ -137,7 +138,7 @@ struct EpiBlock {
         b = fma(c2, A2[e], b);
         b = fma(c1, A1[e], b);
         if (r == c) b += c0;
-        return v + b;
+        return fv * v + b;
     }
 };
 
@@ -431,17 +432,10 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
         if (TAYLOR_PROD[d] + sd < best) { best = TAYLOR_PROD[d] + sd; m = TAYLOR_M[d]; s = sd; }
     }
     EXPM_CLK(11)
-    // scale the powers: (2^-s A)^k = 2^-sk A^k (exact)
-    if (s > 0) {
-        const double f1 = ldexp(1.0, -s), f2 = ldexp(1.0, -2 * s), f3 = ldexp(1.0, -3 * s), f4 = ldexp(1.0, -4 * s);
-        for (int e = t; e < KK; e += blockDim.x) {
-            M0[e] *= f1;
-            M1[e] *= f2;
-            M2[e] *= f3;
-            M3[e] *= f4;
-        }
-        __syncthreads();
-    }
+    // the powers of 2^-s A are 2^-sk A^k: the scale factors (exact powers of two) are folded into
+    // the polynomial's coefficients and the products' epilogue (f4 (Y A^4) = Y (f4 A^4) exactly),
+    // instead of a pass over four matrices
+    const double f1 = ldexp(1.0, -s), f2 = ldexp(1.0, -2 * s), f3 = ldexp(1.0, -3 * s), f4 = ldexp(1.0, -4 * s);
     auto c = [](int k) { return TAYLOR_INVFACT[k]; };
     EXPM_CLK(4)
     // Horner in A^4: Y = B_{r-1} + c_m A^4;  Y <- Y A^4 + B_k, k = r-2 .. 0
@@ -449,7 +443,7 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
     double *Y = M4, *Z = M5;
     {
         const int b = 4 * (r - 1);
-        const double cm = c(m), cb0 = c(b), cb1 = c(b + 1), cb2 = c(b + 2), cb3 = c(b + 3);
+        const double cm = c(m) * f4, cb0 = c(b), cb1 = c(b + 1) * f1, cb2 = c(b + 2) * f2, cb3 = c(b + 3) * f3;
         for (int e = t; e < KK; e += blockDim.x) {
             double v = cm * M3[e];
             v = fma(cb3, M2[e], v);
@@ -463,7 +457,7 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
     }
     for (int k = r - 2; k >= 0; k--) {
         const int b = 4 * k;
-        cta_matmul_e(Kp, ld, Y, M3, Z, EpiBlock{M0, M1, M2, ld, c(b), c(b + 1), c(b + 2), c(b + 3)});
+        cta_matmul_e(Kp, ld, Y, M3, Z, EpiBlock{M0, M1, M2, ld, f4, c(b), c(b + 1) * f1, c(b + 2) * f2, c(b + 3) * f3});
         double *tmp = Y;
         Y = Z;
         Z = tmp;

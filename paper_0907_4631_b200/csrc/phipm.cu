@@ -25,6 +25,7 @@
 #include "small.cuh"
 #include "persist.cuh"
 #include "persist_tm.cuh"
+#include "persist_wrec.cuh"
 
 using namespace phipm;
 
@@ -757,6 +758,69 @@ bool try_persist_tm(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bt
     return true;
 }
 
+// The whole w-recurrence of a step in one cooperative kernel (persist_wrec.cuh) for stencil
+// operators with n > SMALL_N (PHIPM_WREC=0 disables).  Returns true if it launched (rc = status).
+template <class Op>
+bool launch_wrec_persist(phipm_ctx *, const Op &, const WrecArgs &, double, int &) { return false; }
+
+using WrecFn = void (*)(StencilOp, WrecArgs, PersistArgs, Work);
+
+WrecFn wrec_fn(const StencilOp &op)
+{
+    switch ((op.dim == 2 && op.diag) ? 4 : op.dim) {
+    case 1: return wrec_persist_kernel<1>;
+    case 2: return wrec_persist_kernel<2>;
+    case 3: return wrec_persist_kernel<3>;
+    default: return wrec_persist_kernel<4>;
+    }
+}
+
+template <>
+bool launch_wrec_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, const WrecArgs &w, double bytes, int &rc)
+{
+    static int env = -1;
+    if (env < 0) {
+        const char *e = getenv("PHIPM_WREC");
+        env = e ? atoi(e) : 1;
+    }
+    if (!env || op.n <= SMALL_N || w.p < 1) return false;
+    constexpr int TILE_ = SNT * 4;
+    int grid;
+    int64_t rpc;
+    const int slots = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (op.n + TILE_ / 2 - 1) / (TILE_ / 2)));
+    balance(c, op.n, slots, grid, rpc);
+    const size_t smem = wrec_smem_bytes(halo_capacity(op.dim, op.nx, TILE_));
+    if (smem > c->smem_optin) return false;
+    const WrecFn kfn = wrec_fn(op);
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, SNT, smem) != cudaSuccess || occ < 1 ||
+        grid > occ * c->sm_count) {
+        cudaGetLastError();
+        return false;
+    }
+    PersistArgs a{};
+    a.rpc = rpc;
+    a.flag = c->counter + 2;
+    a.abort = c->counter + 3;
+    a.timeout_ns = 2000000000ull;
+    rc = PHIPM_OK;
+    if (cudaMemsetAsync(c->counter + 2, 0, 2 * sizeof(unsigned), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(&c->st->aborted, 0, sizeof(int), c->stream) != cudaSuccess) {
+        rc = set_err(c, PHIPM_ECUDA, "wrec: memset failed");
+        return true;
+    }
+    ProfRec r;
+    prof_begin(c, r, PC_SPMV, bytes, 0);
+    const cudaError_t e = launch_coop(c, kfn, grid, SNT, smem, op, w, a, make_work(c));
+    prof_end(c, r);
+    c->acc.launches++;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+
 template <>
 bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_op, bool symmetric, int k0, int k1,
                                double bthr, int &rc)
@@ -951,6 +1015,30 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             a.onorm = 1;
             a.fin = FIN_SEED;
             return launch_axpy(c, n, a, PC_OTHER);
+        }
+        {
+            // one cooperative kernel for all p SpMVs (stencils); else p streaming launches
+            WrecArgs wa;
+            memset(&wa, 0, sizeof(wa));
+            wa.p = p;
+            wa.x0 = ucur;
+            wa.W = c->W;
+            double bytes = 0.0;
+            for (int j = 1; j <= p; j++) {
+                double coef = 1.0;
+                int nz = 0;
+                for (int l = 0; l <= p - j; l++) {
+                    if (l > 0) coef = coef * tk / (double)l;
+                    if (l > 0 && coef == 0.0) continue;
+                    wa.z[j - 1][nz] = u[j + l];
+                    wa.zc[j - 1][nz] = coef;
+                    nz++;
+                }
+                wa.nz[j - 1] = nz;
+                bytes += bytes_op + 8.0 * (double)n * nz;
+            }
+            int rc = PHIPM_OK;
+            if (p <= WREC_MAXP && launch_wrec_persist(c, op, wa, bytes, rc)) return rc;
         }
         for (int j = 1; j <= p; j++) {
             SpmvArgs s = spmv0();
@@ -1542,6 +1630,12 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
             op.dim = d == 4 ? 2 : d;
             op.diag = d == 4;
             cudaFuncSetAttribute(persist_tm_fn(op), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        }
+        for (int d = 1; d <= 4; d++) {
+            StencilOp op{};
+            op.dim = d == 4 ? 2 : d;
+            op.diag = d == 4;
+            cudaFuncSetAttribute(wrec_fn(op), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         }
         persist_set_smem<4>(mx);
         persist_set_smem<2>(mx);

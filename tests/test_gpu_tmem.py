@@ -1,4 +1,5 @@
-"""The persistent Lanczos kernel with y / v~_j in tensor memory (csrc/persist_tm.cuh) against the oracle.
+"""The persistent Lanczos kernel with y / v~_j in tensor memory (csrc/persist_tm.cuh) and the persistent
+w-recurrence (csrc/persist_wrec.cuh) against the oracle.
 
 The host dispatches Lanczos extensions on stencils to it when n >= 4096 * 148 / 2 = 303,104 rows (a
 4096-row tile per half CTA at least) and every CTA's range fits 4 tiles of 4096 rows.  The cases
@@ -92,15 +93,18 @@ print(s)
 """
 
 
-def test_tmem_and_smem_kernels_agree(tmp_path):
-    # c4 with the TMEM kernel (default) and with PHIPM_TMEM=0 (y in shared memory): the two differ only
-    # in the order the dot products are summed, so w agrees far below the parity bar
+@pytest.mark.parametrize("var", ["PHIPM_TMEM", "PHIPM_WREC"])
+def test_persistent_variants_agree(tmp_path, var):
+    # c4 with the default kernels and with one persistent variant switched off:
+    #   PHIPM_TMEM=0: the Lanczos kernel keeps y in shared memory instead of tensor memory;
+    #   PHIPM_WREC=0: the w-recurrence runs as p streaming launches instead of one cooperative kernel.
+    # Each pair differs only in the order some sums are reduced, so w agrees far below the parity bar
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
     for flag in ("1", "0"):
         f = os.path.join(tmp_path, f"w{flag}.npy")
         r = subprocess.run([sys.executable, "-c", TM_OFF_SCRIPT, f], cwd=root, capture_output=True, text=True,
-                           env=dict(os.environ, PHIPM_TMEM=flag), timeout=600)
+                           env=dict(os.environ, **{var: flag}), timeout=600)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
         out[flag] = np.load(f)
     assert relerr(out["1"], out["0"]) <= 1e-12

@@ -263,6 +263,14 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
     for (int base = warp * rpw; base < rows; base += stride * U) {
         double2 va[U], vb[U];
         int4 cc[U];
+        // column indices of all U groups first: the x lookups depend on them, the values only on
+        // the products, so the index loads are the ones to put at the head of the queue
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int q = base + u * stride + sub;
+            cc[u] = q < rows ? __ldg(reinterpret_cast<const int4 *>(A.col + (r0 + q) * (int64_t)A.ell + 4 * li))
+                             : make_int4(0, 0, 0, 0);
+        }
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int q = base + u * stride + sub;
@@ -270,10 +278,8 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
                 const int64_t e = (r0 + q) * (int64_t)A.ell + 4 * li;
                 va[u] = ldg_stream2(A.val + e);
                 vb[u] = ldg_stream2(A.val + e + 2);
-                cc[u] = __ldg(reinterpret_cast<const int4 *>(A.col + e));
             } else {
                 va[u] = vb[u] = make_double2(0.0, 0.0);
-                cc[u] = make_int4(0, 0, 0, 0);
             }
         }
         double acc[U];

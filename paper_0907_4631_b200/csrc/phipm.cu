@@ -197,6 +197,22 @@ int grid_for(phipm_ctx *c, int64_t units, int occ)
     return (int)g;
 }
 
+// Environment switches (measurement / A-B only; defaults are the measured best).  Callers cache the
+// value in a function-local static const, whose initialisation C++ makes thread-safe (batch solves
+// run on several host threads).
+int env_int(const char *name, int dflt)
+{
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+// "on" unless the variable starts with '0'
+int env_on(const char *name)
+{
+    const char *e = getenv(name);
+    return (e && e[0] == '0') ? 0 : 1;
+}
+
 // ---------------------------------------------------------------------------------------------
 // launches
 
@@ -280,11 +296,7 @@ int csr_wcap<CsrOp>(const CsrOp &A, int tile) { return A.wtile == tile ? A.wcap 
 // PHIPM_RPT=2|4|8 overrides (tuning experiments)
 int pick_rpt(phipm_ctx *c, int64_t n)
 {
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("PHIPM_RPT");
-        env = e ? atoi(e) : 0;
-    }
+    static const int env = env_int("PHIPM_RPT", 0);
     if (env == 2 || env == 4 || env == 8) return env;
     return n >= (int64_t)SNT * 8 * c->sm_count * SMINB / 2 ? 8 : 2;
 }
@@ -433,11 +445,7 @@ int sync(phipm_ctx *c)
 // fall back to cudaStreamSynchronize.
 int wait_attempt(phipm_ctx *c)
 {
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("PHIPM_SPIN");
-        env = (e && e[0] == '0') ? 0 : 1;
-    }
+    static const int env = env_on("PHIPM_SPIN");
     if (c->prof || !env) return sync(c);
     const volatile int *seqp = &reinterpret_cast<volatile AttemptResult *>(c->res_h)->seq;
     const auto t0 = std::chrono::steady_clock::now();
@@ -637,11 +645,7 @@ bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, 
     int64_t rpc;
     // CTAs: at most one per SM, and (PHIPM_PERSIST_MINROWS, default TILE/2) enough rows each that the
     // threads are busy: small problems then also reduce fewer partials per phase
-    static int env_rows = -1;
-    if (env_rows < 0) {
-        const char *e = getenv("PHIPM_PERSIST_MINROWS");
-        env_rows = e ? std::max(32, atoi(e)) : 0;
-    }
+    static const int env_rows = env_int("PHIPM_PERSIST_MINROWS", 0) ? std::max(32, env_int("PHIPM_PERSIST_MINROWS", 0)) : 0;
     const int64_t minrows = env_rows ? env_rows : TILE_ / 2;
     const int slots = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (op.n + minrows - 1) / minrows));
     balance(c, op.n, slots, grid, rpc);
@@ -703,11 +707,7 @@ PersistFn persist_tm_fn(const StencilOp &op)
 // when every CTA's rows fit the 8 pair slots per thread (PHIPM_TMEM=0 disables)
 bool try_persist_tm(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bthr, double bytes, int &rc)
 {
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("PHIPM_TMEM");
-        env = e ? atoi(e) : 1;
-    }
+    static const int env = env_int("PHIPM_TMEM", 1);
     if (!env) return false;
     constexpr int TILE_ = SNT * 4;
     int grid;
@@ -778,11 +778,7 @@ WrecFn wrec_fn(const StencilOp &op)
 template <>
 bool launch_wrec_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, const WrecArgs &w, double bytes, int &rc)
 {
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("PHIPM_WREC");
-        env = e ? atoi(e) : 1;
-    }
+    static const int env = env_int("PHIPM_WREC", 1);
     if (!env || op.n <= SMALL_N || w.p < 1) return false;
     constexpr int TILE_ = SNT * 4;
     int grid;
@@ -828,11 +824,7 @@ bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_o
     // PHIPM_PERSIST: 0 off, 1 (default) auto, 2 always.  Auto: n <= 2^19, or a Lanczos extension of
     // any size; measured with the all-reduce phase end (profiles/round1): c2 +17 %, c4 +3.6 %, while
     // c3 (Arnoldi, n = 1M) is even with the two-kernel path, whose PDL overlap it loses
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("PHIPM_PERSIST");
-        env = e ? atoi(e) : 1;
-    }
+    static const int env = env_int("PHIPM_PERSIST", 1);
     if (env == 0 || op.n <= SMALL_N) return false;
     if (env == 1 && op.n > ((int64_t)1 << 19) && !symmetric) return false;
     double bytes = 0.0;
@@ -878,11 +870,7 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
     // v~_j and also reduces ||v~_j||^2 (free: the x tile is on chip), its finalize derives sigma_j and
     // h_{j,j-1}; so the update passes need no grid reduction except the extension's last one, which
     // provides h_{k1,k1-1} and sigma_{k1} for the exponential.
-    static int env_lag = -1;
-    if (env_lag < 0) {
-        const char *e = getenv("PHIPM_LAG");
-        env_lag = (e && e[0] == '0') ? 0 : 1;
-    }
+    static const int env_lag = env_on("PHIPM_LAG");
     // (stencils only: a CSR SpMV would have to re-read its own x rows for the norm; c5 measured even)
     const bool lag = env_lag && !symmetric && orth == PHIPM_ORTH_CGS && std::is_same<Op, StencilOp>::value;
     for (int j = k0; j < k1; j++) {
@@ -1346,13 +1334,7 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA)
 {
     op.ell = 0;
     op.ring = op.blo = op.bhi = 0;
-    static int env_ell = -1, env_ring = -1;
-    if (env_ell < 0) {
-        const char *e = getenv("PHIPM_CSR_ELL");
-        env_ell = (e && e[0] == '0') ? 0 : 1;
-        e = getenv("PHIPM_CSR_RING");
-        env_ring = (e && e[0] == '0') ? 0 : 1;
-    }
+    static const int env_ell = env_on("PHIPM_CSR_ELL"), env_ring = env_on("PHIPM_CSR_RING");
     if (op.n == 0) {
         *normA = 0.0;
         return PHIPM_OK;
@@ -1384,11 +1366,7 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA)
 
 int enable_csr_window(phipm_ctx *c, CsrOp &op)
 {
-    static int env = -1;
-    if (env < 0) {
-        const char *e = getenv("PHIPM_CSR_WINDOW");
-        env = (e && e[0] == '1') ? 1 : 0;
-    }
+    static const int env = env_int("PHIPM_CSR_WINDOW", 0) == 1;
     if (!env || op.ring) return PHIPM_OK;                  // default off (measured slower, round 1)
     const int tile = SNT * 8;
     const int64_t ntiles = (op.n + tile - 1) / tile;

@@ -3,7 +3,9 @@
 //   (a) counter: partials to global, red.release on one counter, ld.acquire poll, load partials
 //       (the scheme of persist.cuh: phase_allreduce);
 //   (b) inbox: every CTA stores its partial, as {tag, 32-bit half} 8-byte words, into every CTA's
-//       own inbox; each CTA polls only its inbox (one warp), then sums in block order.
+//       own inbox; each CTA polls only its inbox (one warp), then sums in block order;
+//   (c) lean counter: warp 0 alone publishes, polls, loads and sums (one CTA barrier per phase).
+// Measured on this pool: (a) 2.2 us, (b) 6.5-10.8 us, (c) 2.1 us (nv = 1) per phase.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o barrier_probe tools/barrier_probe.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -42,6 +44,39 @@ __global__ void probe_counter(unsigned *flag, double *part, int iters, int nv, d
             for (int b = lane; b < nb; b += 32) acc += __ldcg(part + half + (size_t)warp * nb + b);
             acc = warp_sum(acc);
             if (lane == 0) red[warp] = acc;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        cyc[blockIdx.x] = clock64() - t0;
+        out[blockIdx.x] = red[0];
+    }
+}
+
+// (c) counter, lean: warp 0 alone publishes (lane 0: partials + red.release), polls, loads and sums
+// the partials; one CTA barrier per phase instead of three
+__global__ void probe_lean(unsigned *flag, double *part, int iters, int nv, double *out, long long *cyc)
+{
+    __shared__ double red[8];
+    const int nb = gridDim.x;
+    long long t0 = clock64();
+    for (int it = 1; it <= iters; it++) {
+        const size_t half = (size_t)(it & 1) * nb * 8;
+        if (threadIdx.x < 32) {
+            const int lane = threadIdx.x;
+            if (lane == 0) {
+                for (int v = 0; v < nv; v++) part[half + (size_t)v * nb + blockIdx.x] = blockIdx.x + it + v;
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(flag) : "memory");
+                while (ld_acq(flag) < (unsigned)(it * nb)) {
+                }
+            }
+            __syncwarp();
+            for (int v = 0; v < nv; v++) {
+                double acc = 0.0;
+                for (int b = lane; b < nb; b += 32) acc += __ldcg(part + half + (size_t)v * nb + b);
+                acc = warp_sum(acc);
+                if (lane == 0) red[v] = acc;
+            }
         }
         __syncthreads();
     }
@@ -140,9 +175,16 @@ int main()
             cudaEventSynchronize(e1);
             float ms2;
             cudaEventElapsedTime(&ms2, e0, e1);
+            cudaMemset(flag, 0, 64);
+            cudaEventRecord(e0);
+            cudaLaunchCooperativeKernel((void *)probe_lean, sms, 1024, a1, 0, 0);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms3;
+            cudaEventElapsedTime(&ms3, e0, e1);
             cudaError_t err = cudaGetLastError();
-            printf("nv=%d: counter all-reduce %.3f us per phase | inbox all-reduce %.3f us per phase  (%s)\n", nv,
-                   1e3 * ms1 / iters, 1e3 * ms2 / iters, cudaGetErrorString(err));
+            printf("nv=%d: counter all-reduce %.3f us per phase | inbox %.3f us | lean counter %.3f us  (%s)\n", nv,
+                   1e3 * ms1 / iters, 1e3 * ms2 / iters, 1e3 * ms3 / iters, cudaGetErrorString(err));
         }
     }
     return 0;

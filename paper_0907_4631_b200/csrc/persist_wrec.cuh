@@ -17,7 +17,7 @@
 
 namespace phipm {
 
-constexpr int WREC_MAXP = 5;            // p <= p_max <= 5 (P_MAX_ABS)
+constexpr int WREC_MAXP = 6;            // p <= p_max <= P_MAX_ABS = 6
 constexpr int WREC_PLANS = 8;           // tiles per CTA with a precomputed halo plan
 
 struct WrecArgs {

@@ -108,3 +108,29 @@ def test_persistent_variants_agree(tmp_path, var):
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
         out[flag] = np.load(f)
     assert relerr(out["1"], out["0"]) <= 1e-12
+
+
+@pytest.mark.parametrize("p", [0, 1, 2, 3, 4, 5, 6])
+def test_wrec_persistent_all_p_multistep(orc, p):
+    # 2-D Laplacian 181^2 (n > 8192: the cooperative w-recurrence), t = 5e-4: two steps, so every u-term of
+    # Eq. (wrecurrence) has a nonzero t_k^l / l! on the second.  Eq. (step) sums terms of size
+    # ||tau A||^j ||u|| that cancel to O(||u||), so the accuracy any implementation reaches degrades with p
+    # (the oracle vs the exact DST solution: 1e-14 at p = 0, 6e-12 at p = 3, 4e-8 at p = 6): up to p = 4
+    # the GPU meets the BASELINE bar against the oracle; for p = 5, 6 both are held to the exact solution,
+    # the GPU within 10x the oracle's own error
+    import torch
+    import exact as X
+    st, u = laplacian(2, 181, 181, 1, seed=900 + p, p=p)
+    Pb = W.Problem(name="wr", n=st.n, p=p, t=5e-4, tol=1e-9, symmetric=True, u=u, stencil=st, seed=0)
+    wo, so, _ = orc.solve(Pb)
+    assert so["status"] == 0
+    ctx6 = P.Context(n_max=st.n, m_max=100, p_max=6)
+    w, s = ctx6.solve_stencil(Pb.t, P.Stencil.of(st), [to_dev(x) for x in u], tol=Pb.tol, symmetric=True)
+    assert s.t_reached == Pb.t and s.nsteps > 1, s
+    wg = w.cpu().numpy()
+    if p <= 4:
+        assert relerr(wg, wo) <= parity_bound(Pb.tol), (s, so)
+    else:
+        ref = X.dst_solution(st, u, Pb.t)
+        assert relerr(wg, ref) <= 10 * max(relerr(wo, ref), parity_bound(Pb.tol)), (s, so)
+    torch.cuda.synchronize()

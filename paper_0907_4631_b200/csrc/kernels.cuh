@@ -26,7 +26,7 @@ constexpr int NT = 256;               // threads per block of the streaming kern
 constexpr int NWARP = NT / 32;
 constexpr int RPT = 4;                // rows per thread per tile
 constexpr int TILE = NT * RPT;        // rows per tile
-constexpr int MAXZ = 6;               // epilogue vectors (p_max <= 5)
+constexpr int MAXZ = 6;               // epilogue vectors (<= p_max <= P_MAX_ABS = 6)
 constexpr int MAXD = 128;             // dot / axpy columns per launch (m_max + 1 <= MAXD)
 
 enum Fin : int {

@@ -856,7 +856,11 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
             bytes += bytes_op + 8.0 * (double)n * (symmetric ? 4.0 : 2.0 * j + 3.0);
         ProfRec r;
         prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
-        launch_k(c, krylov_small_kernel<Op>, 1, SMALL_NT, (size_t)n * sizeof(double), op, sa, make_work(c));
+        static const int env_slz = env_on("PHIPM_SMALL_LZ");
+        if (symmetric && n <= SLZ_NT * SLZ_R && env_slz)
+            launch_k(c, krylov_small_lanczos_kernel<Op>, 1, SLZ_NT, (size_t)n * sizeof(double), op, sa, make_work(c));
+        else
+            launch_k(c, krylov_small_kernel<Op>, 1, SMALL_NT, (size_t)n * sizeof(double), op, sa, make_work(c));
         prof_end(c, r);
         c->acc.launches++;
         CK(cudaGetLastError());

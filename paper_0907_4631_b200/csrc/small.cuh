@@ -89,6 +89,90 @@ __device__ __forceinline__ double block_sum(double v, double *red)
     return warp_sum(lane < nw ? red[lane] : 0.0);
 }
 
+// Lanczos (Alg. 2) for n <= SLZ_NT * SLZ_R in a single CTA of SLZ_NT threads with up to SLZ_R rows
+// per thread (rows t + SLZ_NT i).  The step is a chain of two dependent block sums; with 8 warps
+// instead of 32 each sum has a 3-level second stage and a cheaper barrier, and a thread's rows give
+// the SpMV some instruction-level parallelism.  Arithmetic per row is that of krylov_small_kernel
+// (the dot and norm are summed in another order).
+constexpr int SLZ_NT = 256;
+constexpr int SLZ_R = 4;
+
+template <class Op>
+__global__ void __launch_bounds__(SLZ_NT) krylov_small_lanczos_kernel(Op op, SmallArgs a, Work wk)
+{
+    extern __shared__ double vs[];                      // n doubles: v~_j
+    __shared__ double red[SLZ_NT / 32];
+    __shared__ double red2[SLZ_NT / 32];
+    const int t = threadIdx.x;
+    const int n = (int)op.n;
+    pdl_wait();
+    double sj = wk.sigma[a.k0];
+    double lz = wk.st->lz;
+    int brk = wk.st->brk;
+    double zv[SLZ_R];
+#pragma unroll
+    for (int i = 0; i < SLZ_R; i++) {
+        const int r = t + SLZ_NT * i;
+        zv[i] = 0.0;
+        if (r < n) {
+            vs[r] = wk.V[(int64_t)a.k0 * wk.ldv + r];
+            if (a.k0 > 0) zv[i] = wk.V[(int64_t)(a.k0 - 1) * wk.ldv + r];
+        }
+    }
+    __syncthreads();
+    for (int j = a.k0; j < a.k1 && brk < 0; j++) {
+        double y[SLZ_R], xv[SLZ_R];
+        double dl = 0.0;
+#pragma unroll
+        for (int i = 0; i < SLZ_R; i++) {
+            const int r = t + SLZ_NT * i;
+            y[i] = 0.0;
+            xv[i] = 0.0;
+            if (r < n) {
+                y[i] = sj * row_apply(op, vs, r);
+                xv[i] = vs[r];
+                if (j > 0) y[i] = fma(-lz, zv[i], y[i]);
+            }
+            dl = fma(xv[i], y[i], dl);
+        }
+        const double d = block_sum1(dl, red);
+        const double al = sj * d;                          // t_jj = sigma_j v~_j^T y
+        const double g = al * sj;
+        double wl = 0.0;
+#pragma unroll
+        for (int i = 0; i < SLZ_R; i++) {
+            const int r = t + SLZ_NT * i;
+            if (r < n) {
+                const double w = fma(-g, xv[i], y[i]);     // v~_{j+1} = y - g v~_j
+                wk.V[(int64_t)(j + 1) * wk.ldv + r] = w;
+                vs[r] = w;                                 // every thread has read vs (block sum above)
+                wl = fma(w, w, wl);
+            }
+            zv[i] = xv[i];
+        }
+        const double tot = block_sum1(wl, red2);
+        const double h = sqrt(tot);
+        const double sn = 1.0 / h;
+        const double lzn = h * sj;
+        int b = -1;
+        if (!isfinite(h)) b = j + 1;
+        else if (h <= a.bthr) b = j + 1;
+        if (t == 0) {
+            wk.H[j + (size_t)j * wk.ldh] = al;
+            wk.g[0] = g;
+            wk.H[(j + 1) + (size_t)j * wk.ldh] = h;
+            if (j + 1 < wk.hcols) wk.H[j + (size_t)(j + 1) * wk.ldh] = h;
+            wk.st->lz = lzn;
+            wk.sigma[j + 1] = sn;
+            if (!isfinite(h)) wk.st->nonfinite = 1;
+            if (b >= 0) wk.st->brk = b;
+        }
+        sj = sn;
+        lz = lzn;
+        brk = b;
+    }
+}
+
 template <class Op>
 __global__ void __launch_bounds__(SMALL_NT) krylov_small_kernel(Op op, SmallArgs a, Work wk)
 {

@@ -29,7 +29,8 @@ def read_ncu_csv(path):
 
 def short(k):
     for key in ("spmv_stream_kernel", "axpy_stream_kernel", "expm_kernel", "maxabs_kernel", "csr_analyze_kernel",
-                "krylov_small_kernel", "krylov_persist_tm_kernel", "krylov_persist_kernel"):
+                "krylov_small_lanczos_kernel", "krylov_small_kernel", "krylov_persist_tm_kernel",
+              "krylov_persist_kernel", "wrec_persist_kernel"):
         if key in k:
             return key + ("<Stencil>" if "StencilOp" in k else "<Csr>" if "CsrOp" in k else "")
     return k[:40]
@@ -86,7 +87,8 @@ for cfg in ("c3", "c4", "c5"):
     # the bench's "spmv_dot" class: SpMV launches plus whole-extension Krylov kernels (persistent /
     # single-CTA), so the per-launch average matches bench.py's algorithmic_bytes_per_launch
     sp = [b for k in cls if k.startswith(("spmv_stream_kernel", "krylov_persist_kernel", "krylov_persist_tm_kernel",
-                                                   "krylov_small_kernel"))
+                                                   "krylov_small_kernel", "krylov_small_lanczos_kernel",
+                                                   "wrec_persist_kernel"))
           for b, _ in cls[k]]
     if sp:
         traffic[cfg] = {"kernel_class": "spmv_dot", "dram_bytes_per_launch": sum(sp) / len(sp),

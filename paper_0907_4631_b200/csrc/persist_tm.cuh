@@ -72,6 +72,29 @@ __host__ __device__ inline size_t persist_tm_smem_bytes(int halo_cap)
     return (size_t)2 * ((halo_cap + 15) & ~15) * sizeof(double);
 }
 
+// block sums of NV values per thread into out[0..NV) (visible to every thread on return): a shuffle
+// tree per warp, then warp 0 reduces the SNW warp totals of each value with another shuffle tree.
+// Two CTA barriers for all NV values (block_total below: two per value plus a serial 32-term loop).
+template <int NV>
+__device__ __forceinline__ void block_sums(const double (&v)[NV], double *wsum2, double *out)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; k++) {
+        const double s = warp_sum(v[k]);
+        if (lane == 0) wsum2[k * SNW + warp] = s;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; k++) {
+            const double s = warp_sum(lane < SNW ? wsum2[k * SNW + lane] : 0.0);
+            if (lane == 0) out[k] = s;
+        }
+    }
+    __syncthreads();
+}
+
 // block sum of one value per thread (fixed order: shuffle tree, then warps in order by thread 0)
 __device__ __forceinline__ double block_total(double v, double *wsum)
 {
@@ -98,7 +121,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
     __shared__ unsigned hcons[2];                      // warps done with each halo buffer (monotonic)
     __shared__ double bsum[2];
     __shared__ double red[MAXD + 2];
-    __shared__ double wsum[SNW];
+    __shared__ double wsum2[2 * SNW];
     __shared__ uint32_t s_tmem;
     __shared__ int s_stop;
     __shared__ double s_sig, s_lz, s_gco;
@@ -201,13 +224,8 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
         }
         tm_wait_st();
         {
-            const double d = block_total(dot, wsum);
-            const double s = block_total(ysq, wsum);
-            if (tid == 0) {
-                bsum[0] = d;
-                bsum[1] = s;
-            }
-            __syncthreads();
+            const double v2[2] = {dot, ysq};
+            block_sums<2>(v2, wsum2, bsum);
         }
         if (!phase_allreduce(wk, bsum, 2, ++phase, a, red)) break;
         // finalize (FIN_LANCZOS): alpha_j = sigma_j d; update coefficient -alpha_j sigma_j
@@ -245,9 +263,8 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
             }
         }
         {
-            const double s = block_total(nrm, wsum);
-            if (tid == 0) bsum[0] = s;
-            __syncthreads();
+            const double v1[1] = {nrm};
+            block_sums<1>(v1, wsum2, bsum);
         }
         if (!phase_allreduce(wk, bsum, 1, ++phase, a, red)) break;
         // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown

@@ -248,20 +248,16 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
                 }
             }
         }
-        __syncthreads();
-        for (int k = tid; k < nd; k += SNT) {
-            double t = 0.0;
-            for (int w = 0; w < SNW; w++) t += lacc[k * SNW + w];
-            bsum[k] = t;
-        }
         {
+            // the dot partials per warp (lacc) and ||y||^2 per warp (wsum): warp k reduces value k with
+            // a shuffle tree (all values in parallel, no serial 32-term loop)
             const double v = warp_sum(ysq);
             if (lane == 0) wsum[warp] = v;
             __syncthreads();
-            if (tid == 0) {
-                double t = 0.0;
-                for (int w = 0; w < SNW; w++) t += wsum[w];
-                bsum[nd] = t;
+            for (int k = warp; k <= nd; k += SNW) {
+                const double x = (lane < SNW) ? (k < nd ? lacc[k * SNW + lane] : wsum[lane]) : 0.0;
+                const double t = warp_sum(x);
+                if (lane == 0) bsum[k] = t;
             }
         }
         __syncthreads();
@@ -368,10 +364,9 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
             const double v = warp_sum(nrm);
             if (lane == 0) wsum[warp] = v;
             __syncthreads();
-            if (tid == 0) {
-                double t = 0.0;
-                for (int w = 0; w < SNW; w++) t += wsum[w];
-                bsum[0] = t;
+            if (warp == 0) {
+                const double t = warp_sum(lane < SNW ? wsum[lane] : 0.0);
+                if (lane == 0) bsum[0] = t;
             }
             __syncthreads();
         }

@@ -64,9 +64,10 @@ __device__ __forceinline__ bool phase_allreduce(const Work &wk, const double *bs
     const int nb = gridDim.x;
     const size_t half = (size_t)(phase & 1) * nb;
     if (a.dbg && threadIdx.x == 0) a.dbg[((size_t)(phase - 1) * gridDim.x + blockIdx.x) * 2] = gtimer();
-    for (int v = threadIdx.x; v < nv; v += blockDim.x) wk.part[(size_t)v * wk.pstride + half + blockIdx.x] = bsum[v];
-    __syncthreads();
+    // (bsum is visible to every thread on entry) thread 0 writes the partials itself, so the release
+    // that follows covers them in program order: no CTA barrier between the stores and the arrival
     if (threadIdx.x == 0) {
+        for (int v = 0; v < nv; v++) wk.part[(size_t)v * wk.pstride + half + blockIdx.x] = bsum[v];
         int ok = 1;
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.flag) : "memory");
         const unsigned target = phase * (unsigned)nb;

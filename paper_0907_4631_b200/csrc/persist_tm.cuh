@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
     __shared__ double wsum2[2 * SNW];
     __shared__ uint32_t s_tmem;
     __shared__ int s_stop;
-    __shared__ double s_sig, s_lz, s_gco;
+    __shared__ double s_sig, s_lz;
     const int tid = threadIdx.x, warp = tid >> 5;
     const int64_t n = op.n;
     const int64_t cs = (int64_t)blockIdx.x * a.rpc, ce = min(n, cs + a.rpc);
@@ -152,6 +152,8 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    double sig = s_sig, lzc = s_lz;                        // sigma_j and the Lanczos coefficient, per thread
+    bool stop = s_stop != 0;
     // this thread's 64 columns: lane quarter warp % 4, column block warp / 4
     const uint32_t tbase = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
     const uint32_t slotA = tbase, slotB = tbase + 32;
@@ -160,11 +162,11 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
     const bool lead = blockIdx.x == 0;
     const int3 gc0 = grid_coords(op, cs + 2 * tid);
     for (int j = a.k0; j < a.k1; j++) {
-        if (s_stop) break;                                 // breakdown (same decision in every CTA)
+        if (stop) break;                                   // breakdown (same decision in every CTA)
         const double *x = wk.V + (int64_t)j * ldv;
-        const double sj = s_sig;
+        const double sj = sig;
         const double *zv = j > 0 ? x - ldv : nullptr;      // v~_{j-1} (Alg. 2 line 3)
-        const double lz = zv ? s_lz : 0.0;
+        const double lz = zv ? lzc : 0.0;
         const bool zs = j > a.k0;                          // v~_{j-1} of these rows is in slot B
 
         // ---------------- phase A: y = sigma_j A x - lz v~_{j-1}; d = x^T y; ||y||^2
@@ -228,21 +230,18 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
             block_sums<2>(v2, wsum2, bsum);
         }
         if (!phase_allreduce(wk, bsum, 2, ++phase, a, red)) break;
-        // finalize (FIN_LANCZOS): alpha_j = sigma_j d; update coefficient -alpha_j sigma_j
-        if (tid == 0) {
-            const double al = sj * red[0];
-            s_gco = -(al * sj);
-            if (lead) {
-                wk.H[j + (size_t)j * wk.ldh] = al;
-                wk.g[0] = al * sj;
-                wk.st->wnorm2 = red[1];
-            }
+        // finalize (FIN_LANCZOS): alpha_j = sigma_j d; update coefficient -alpha_j sigma_j -- derived by
+        // every thread from the all-reduced totals (no CTA barrier); CTA 0 thread 0 writes H for the host
+        const double al = sj * red[0];
+        const double cf = -(al * sj);
+        if (lead && tid == 0) {
+            wk.H[j + (size_t)j * wk.ldh] = al;
+            wk.g[0] = al * sj;
+            wk.st->wnorm2 = red[1];
         }
-        __syncthreads();
 
         // ---------------- phase B: v~_{j+1} = y - alpha_j sigma_j v~_j (both from TMEM); ||v~_{j+1}||^2
         double *vn = wk.V + (int64_t)(j + 1) * ldv;
-        const double cf = s_gco;
         double nrm = 0.0;
         t = 0;
         for (int64_t r0 = cs; r0 < ce; r0 += TILE_, t++) {
@@ -267,18 +266,19 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
             block_sums<1>(v1, wsum2, bsum);
         }
         if (!phase_allreduce(wk, bsum, 1, ++phase, a, red)) break;
-        // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown
-        if (tid == 0) {
+        // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown -- derived by
+        // every thread from the all-reduced total (identical in every thread and CTA; no CTA barrier)
+        {
             const double h = sqrt(red[0]);
             const double sn = 1.0 / h;
             const double lzn = h * sj;
             int brk = -1, nonfin = 0;
             if (!isfinite(h)) { nonfin = 1; brk = j + 1; }
             else if (h <= a.bthr) brk = j + 1;
-            s_sig = sn;
-            s_lz = lzn;
-            s_stop = brk >= 0;
-            if (lead) {
+            sig = sn;
+            lzc = lzn;
+            stop = brk >= 0;
+            if (lead && tid == 0) {
                 wk.H[(j + 1) + (size_t)j * wk.ldh] = h;
                 if (j + 1 < wk.hcols) wk.H[j + (size_t)(j + 1) * wk.ldh] = h;
                 wk.st->lz = lzn;
@@ -287,7 +287,6 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
                 if (brk >= 0) wk.st->brk = brk;
             }
         }
-        __syncthreads();
     }
     // every warp's TMEM traffic is complete before warp 0 frees the columns
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -75,7 +75,9 @@ __host__ __device__ inline size_t persist_tm_smem_bytes(int halo_cap)
 // block sums of NV values per thread into out[0..NV) (visible to every thread on return): a shuffle
 // tree per warp, then warp 0 reduces the SNW warp totals of each value with another shuffle tree.
 // Two CTA barriers for all NV values (block_total below: two per value plus a serial 32-term loop).
-template <int NV>
+// SYNC_OUT = false: out[] is only read by thread 0 afterwards (phase_allreduce's partials), which
+// computed it, so the closing barrier is not needed
+template <int NV, bool SYNC_OUT = true>
 __device__ __forceinline__ void block_sums(const double (&v)[NV], double *wsum2, double *out)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -92,7 +94,7 @@ __device__ __forceinline__ void block_sums(const double (&v)[NV], double *wsum2,
             if (lane == 0) out[k] = s;
         }
     }
-    __syncthreads();
+    if (SYNC_OUT) __syncthreads();
 }
 
 // block sum of one value per thread (fixed order: shuffle tree, then warps in order by thread 0)
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
         tm_wait_st();
         {
             const double v2[2] = {dot, ysq};
-            block_sums<2>(v2, wsum2, bsum);
+            block_sums<2, false>(v2, wsum2, bsum);
         }
         if (!phase_allreduce(wk, bsum, 2, ++phase, a, red)) break;
         // finalize (FIN_LANCZOS): alpha_j = sigma_j d; update coefficient -alpha_j sigma_j -- derived by
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
         }
         {
             const double v1[1] = {nrm};
-            block_sums<1>(v1, wsum2, bsum);
+            block_sums<1, false>(v1, wsum2, bsum);
         }
         if (!phase_allreduce(wk, bsum, 1, ++phase, a, red)) break;
         // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown -- derived by

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(SNT, 1) wrec_persist_kernel(StencilOp op, Wrec
         // grid phase: w_j visible to every CTA's next halo copies; after the last SpMV also ||w_p||^2
         {
             const double v1[1] = {j == w.p ? ysq : 0.0};
-            block_sums<1>(v1, wsum, bsum);
+            block_sums<1, false>(v1, wsum, bsum);
         }
         if (!phase_allreduce(wk, bsum, 1, ++phase, a, red)) return;
         if (j == w.p && blockIdx.x == 0 && tid == 0) {

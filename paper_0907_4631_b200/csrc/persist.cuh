@@ -57,8 +57,15 @@ __device__ __forceinline__ double2 ld_cg2(const double *p)
 // monotonic counter (release), waits until all gridDim.x CTAs of this phase arrived (acquire), and
 // then sums the partials itself in block order: every CTA obtains bit-identical totals in red[]
 // without a serialising last-CTA reduction and flag round trip.  Returns false on abort.
+struct NoRelease {
+    __device__ void operator()() const {}
+};
+
+// on_release: run by the last warp's lane 0 once every CTA has arrived, while warps 0.. nv-1 sum the
+// partials (e.g. to issue the next phase's first bulk copies off the critical path)
+template <class OnRelease = NoRelease>
 __device__ __forceinline__ bool phase_allreduce(const Work &wk, const double *bsum, int nv, unsigned phase,
-                                                const PersistArgs &a, double *red)
+                                                const PersistArgs &a, double *red, OnRelease on_release = OnRelease{})
 {
     __shared__ int s_ok;
     const int nb = gridDim.x;
@@ -93,6 +100,12 @@ __device__ __forceinline__ bool phase_allreduce(const Work &wk, const double *bs
     if (!s_ok) return false;
     // fixed-order sum of the nb partials of each value (one warp per value, 8 loads in flight per lane)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (threadIdx.x == blockDim.x - 32) {
+        // the other CTAs' generic-proxy writes were acquired by thread 0 and ordered for this thread by
+        // the barrier above; its own bulk copies read them through the async proxy
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        on_release();
+    }
     for (int v = warp; v < nv; v += nw) {
         const double *pv = wk.part + (size_t)v * wk.pstride + half;
         double acc[8];

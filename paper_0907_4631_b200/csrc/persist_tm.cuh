@@ -162,6 +162,14 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
     uint32_t ht = 0;
     unsigned phase = 0;
     const bool lead = blockIdx.x == 0;
+    bool pre = false;                                      // the next SpMV phase's first tiles are in flight
+    auto issue_first = [&](const double *xj) {            // (one thread)
+        for (int u = 0; u < 2; u++) {
+            const int64_t ru = cs + (int64_t)u * TILE_;
+            const uint32_t g = ht + u;
+            if (ru < ce) issue_planned_tile(tplan[u], sm + (g & 1) * hstride, xj, &hbar[g & 1], pol);
+        }
+    };
     const int3 gc0 = grid_coords(op, cs + 2 * tid);
     for (int j = a.k0; j < a.k1; j++) {
         if (stop) break;                                   // breakdown (same decision in every CTA)
@@ -172,12 +180,8 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
         const bool zs = j > a.k0;                          // v~_{j-1} of these rows is in slot B
 
         // ---------------- phase A: y = sigma_j A x - lz v~_{j-1}; d = x^T y; ||y||^2
-        if (tid == 0)
-            for (int u = 0; u < 2; u++) {
-                const int64_t ru = cs + (int64_t)u * TILE_;
-                const uint32_t g = ht + u;
-                if (ru < ce) issue_planned_tile(tplan[u], sm + (g & 1) * hstride, x, &hbar[g & 1], pol);
-            }
+        if (tid == 0 && !pre) issue_first(x);
+        pre = false;
         double ysq = 0.0, dot = 0.0;
         int3 gcoord = gc0;
         int t = 0;
@@ -267,7 +271,14 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
             const double v1[1] = {nrm};
             block_sums<1, false>(v1, wsum2, bsum);
         }
-        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red)) break;
+        // v~_{j+1} is complete in every CTA once the phase's arrivals are in: the next step's first
+        // halo tiles are issued then, while the partials are summed (drained below on breakdown)
+        const bool more = j + 1 < a.k1;
+        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red, [&] {
+                if (more) issue_first(x + ldv);
+            }))
+            break;
+        pre = more;
         // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown -- derived by
         // every thread from the all-reduced total (identical in every thread and CTA; no CTA barrier)
         {
@@ -290,6 +301,10 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
             }
         }
     }
+    // first tiles issued for a step that did not run (breakdown): land them before the CTA exits
+    if (pre)
+        for (int u = 0; u < 2; u++)
+            if (cs + (int64_t)u * TILE_ < ce) mbar_wait(&hbar[(ht + u) & 1], ((ht + u) >> 1) & 1);
     // every warp's TMEM traffic is complete before warp 0 frees the columns
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();

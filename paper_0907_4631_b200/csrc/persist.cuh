@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
     __syncthreads();
     const bool lead = blockIdx.x == 0;
     const int3 gc0 = grid_coords(op, cs + 2 * tid);       // grid coordinates of this thread's first row
+    bool pre = false;                                      // the next step's first halo tile is in flight
     for (int j = a.k0; j < a.k1; j++) {
         if (s_stop) break;                                 // breakdown (same decision in every CTA)
         const double *x = wk.V + (int64_t)j * ldv;
@@ -188,8 +189,9 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
         const int nd = j - c0 + 1;                         // dot columns c0..j; column j is x
 
         // ---------------- phase A: y = sigma_j A x [- lz v~_{j-1}], dots, ||y||^2
-        if (tid == 0 && cs < ce) issue_halo_tile<TILE_>(op, hbuf, x, ldv, cs, (int)min((int64_t)TILE_, ce - cs),
-                                                        hofs[ht & 1], &hbar);
+        if (tid == 0 && cs < ce && !pre)
+            issue_halo_tile<TILE_>(op, hbuf, x, ldv, cs, (int)min((int64_t)TILE_, ce - cs), hofs[ht & 1], &hbar);
+        pre = false;
         for (int i = tid; i < nd * SNW; i += SNT) lacc[i] = 0.0;
         __syncthreads();
         double ysq = 0.0;
@@ -384,7 +386,16 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
             }
             __syncthreads();
         }
-        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red)) return;
+        // the next step's first halo tile (the halo buffer is idle in this phase) is issued by the last
+        // warp as soon as every CTA has published v~_{j+1}, while the partials are summed
+        const bool more = j + 1 < a.k1 && cs < ce;
+        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red, [&] {
+                if (more)
+                    issue_halo_tile<TILE_>(op, hbuf, vn, ldv, cs, (int)min((int64_t)TILE_, ce - cs), hofs[ht & 1],
+                                           &hbar);
+            }))
+            return;
+        pre = more;
         // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown
         if (tid == 0) {
             const double h = sqrt(red[0]);
@@ -409,6 +420,8 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
         }
         __syncthreads();
     }
+    // a first tile issued for a step that did not run (breakdown): land it before the CTA exits
+    if (pre) mbar_wait(&hbar, ht & 1);
 }
 
 } // namespace phipm

@@ -178,13 +178,15 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
     const bool lead = blockIdx.x == 0;
     const int3 gc0 = grid_coords(op, cs + 2 * tid);       // grid coordinates of this thread's first row
     bool pre = false;                                      // the next step's first halo tile is in flight
+    double sig_r = s_sig, lz_r = s_lz;                     // per-thread copies of the carried state
+    bool stop_r = s_stop != 0;
     for (int j = a.k0; j < a.k1; j++) {
-        if (s_stop) break;                                 // breakdown (same decision in every CTA)
+        if (stop_r) break;                                 // breakdown (same decision in every CTA)
         const double *x = wk.V + (int64_t)j * ldv;
-        const double sj = s_sig;                           // sigma_j, local copy
+        const double sj = sig_r;                           // sigma_j
         constexpr bool lanc = LANC;
         const double *zv = (lanc && j > 0) ? x - ldv : nullptr;
-        const double lz = zv ? s_lz : 0.0;
+        const double lz = zv ? lz_r : 0.0;
         const int c0 = lanc ? j : 0;
         const int nd = j - c0 + 1;                         // dot columns c0..j; column j is x
 
@@ -279,15 +281,15 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
         __syncthreads();
         if (!phase_allreduce(wk, bsum, nd + 1, ++phase, a, red)) return;
         // finalize (FIN_ARNOLDI / FIN_LANCZOS): h_k = sigma_k d_k, g_k = h_k sigma_k
+        // (Lanczos: every thread derives the one coefficient from the all-reduced totals, no barrier)
+        double cf_l = 0.0;
         if constexpr (LANC) {
-            if (tid == 0) {
-                const double al = sj * red[0];
-                gco[0] = -(al * sj);
-                if (lead) {
-                    wk.H[j + (size_t)j * wk.ldh] = al;
-                    wk.g[0] = al * sj;
-                    wk.st->wnorm2 = red[1];
-                }
+            const double al = sj * red[0];
+            cf_l = -(al * sj);
+            if (lead && tid == 0) {
+                wk.H[j + (size_t)j * wk.ldh] = al;
+                wk.g[0] = al * sj;
+                wk.st->wnorm2 = red[1];
             }
         } else {
             for (int k = tid; k < nd; k += SNT) {
@@ -300,8 +302,8 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
                 }
             }
             if (lead && tid == 0) wk.st->wnorm2 = red[nd];
+            __syncthreads();                               // gco[] of every column
         }
-        __syncthreads();
 
         // ---------------- phase B: v~_{j+1} = y - sum_k g_k v~_k, ||v~_{j+1}||^2
         double *vn = wk.V + (int64_t)(j + 1) * ldv;
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
             double2 vkeep[NP];                             // Lanczos: v~_j of these rows, for the next step
             if (lanc) {
                 // one column (v~_j): no batching arithmetic
-                const double cf = gco[0];
+                const double cf = cf_l;
                 const double *vc = wk.V + (int64_t)c0 * ldv + r0;
 #pragma unroll
                 for (int p = 0; p < NP; p++) {
@@ -396,18 +398,19 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
             }))
             return;
         pre = more;
-        // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown
-        if (tid == 0) {
+        // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown -- derived by
+        // every thread from the all-reduced total (no CTA barrier)
+        {
             const double h = sqrt(red[0]);
             const double sn = 1.0 / h;
             const double lzn = h * sj;
             int brk = -1, nonfin = 0;
             if (!isfinite(h)) { nonfin = 1; brk = j + 1; }
             else if (h <= a.bthr) brk = j + 1;
-            s_sig = sn;
-            s_lz = lzn;
-            s_stop = brk >= 0;
-            if (lead) {
+            sig_r = sn;
+            lz_r = lzn;
+            stop_r = brk >= 0;
+            if (lead && tid == 0) {
                 wk.H[(j + 1) + (size_t)j * wk.ldh] = h;
                 if (lanc) {
                     if (j + 1 < wk.hcols) wk.H[j + (size_t)(j + 1) * wk.ldh] = h;
@@ -418,7 +421,6 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
                 if (brk >= 0) wk.st->brk = brk;
             }
         }
-        __syncthreads();
     }
     // a first tile issued for a step that did not run (breakdown): land it before the CTA exits
     if (pre) mbar_wait(&hbar, ht & 1);

@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(SNT, 1) wrec_persist_kernel(StencilOp op, Wrec
     __syncthreads();
     uint32_t ht = 0;
     unsigned phase = 0;
-    // tile u of the current vector into halo buffer g & 1 (thread 0)
+    bool pre = false;                   // the next SpMV's first tiles are in flight
+    // tile u of the current vector into halo buffer g & 1 (one thread)
     auto issue = [&](int u, const double *x, uint32_t g) {
         double *hb = sm + (g & 1) * hstride;
         if (u < WREC_PLANS) {
@@ -77,8 +78,9 @@ __global__ void __launch_bounds__(SNT, 1) wrec_persist_kernel(StencilOp op, Wrec
         const double *x = (j == 1) ? w.x0 : w.W + (int64_t)(j - 1) * ldv;
         double *y = (j == w.p) ? wk.V : w.W + (int64_t)j * ldv;
         const int nz = w.nz[j - 1];
-        if (tid == 0)
+        if (tid == 0 && !pre)
             for (int u = 0; u < 2 && u < nt; u++) issue(u, x, ht + u);
+        pre = false;
         double ysq = 0.0;
         int3 gcoord = grid_coords(op, cs + 2 * tid);
         for (int t = 0; t < nt; t++) {
@@ -128,7 +130,15 @@ __global__ void __launch_bounds__(SNT, 1) wrec_persist_kernel(StencilOp op, Wrec
             const double v1[1] = {j == w.p ? ysq : 0.0};
             block_sums<1, false>(v1, wsum, bsum);
         }
-        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red)) return;
+        // w_j is complete in every CTA once the arrivals are in: the next SpMV's first halo tiles are
+        // issued by the last warp while the partials are summed
+        const bool more = j < w.p;
+        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red, [&] {
+                if (more)
+                    for (int u = 0; u < 2 && u < nt; u++) issue(u, y, ht + u);
+            }))
+            return;
+        pre = more;
         if (j == w.p && blockIdx.x == 0 && tid == 0) {
             // FIN_SEED: beta = ||w_p||, sigma_0 = 1 / beta, breakdown / non-finite reset
             const double b = sqrt(red[0]);

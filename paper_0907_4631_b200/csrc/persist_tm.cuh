@@ -52,6 +52,28 @@ __device__ __forceinline__ void tm_ld8x2(uint32_t ta, uint32_t tb, double2 (&a)[
     b[1] = make_double2(__hiloint2double(r[13], r[12]), __hiloint2double(r[15], r[14]));
 }
 
+// four consecutive pairs (16 columns) of slot A and four of slot B, one wait
+__device__ __forceinline__ void tm_ld16x2(uint32_t ta, uint32_t tb, double2 (&a)[4], double2 (&b)[4])
+{
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%32];\n"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%33];\n"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(ta), "r"(tb)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        a[i] = make_double2(__hiloint2double(r[4 * i + 1], r[4 * i]), __hiloint2double(r[4 * i + 3], r[4 * i + 2]));
+        b[i] = make_double2(__hiloint2double(r[16 + 4 * i + 1], r[16 + 4 * i]),
+                            __hiloint2double(r[16 + 4 * i + 3], r[16 + 4 * i + 2]));
+    }
+}
+
 __device__ __forceinline__ void tm_ld8(uint32_t ta, double2 (&a)[2])
 {
     uint32_t r[8];
@@ -249,22 +271,27 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
         // ---------------- phase B: v~_{j+1} = y - alpha_j sigma_j v~_j (both from TMEM); ||v~_{j+1}||^2
         double *vn = wk.V + (int64_t)(j + 1) * ldv;
         double nrm = 0.0;
-        t = 0;
-        for (int64_t r0 = cs; r0 < ce; r0 += TILE_, t++) {
-            const int rows = (int)min((int64_t)TILE_, ce - r0);
-            double2 yv[NP], xv[NP];
-            tm_ld8x2(slotA + 8 * t, slotB + 8 * t, yv, xv);
+        // two tiles per TMEM load (16 columns of each slot, one wait)
+        for (int64_t rp = cs; rp < ce; rp += 2 * TILE_) {
+            const int tp = (int)((rp - cs) / TILE_);
+            double2 yv[2 * NP], xv[2 * NP];
+            tm_ld16x2(slotA + 8 * tp, slotB + 8 * tp, yv, xv);
 #pragma unroll
-            for (int p = 0; p < NP; p++) {
-                const int q = 2 * tid + 2 * SNT * p;
-                double2 acc;
-                acc.x = fma(cf, xv[p].x, yv[p].x);
-                acc.y = fma(cf, xv[p].y, yv[p].y);
-                double *o = vn + r0 + q;
-                if (q + 1 < rows) *reinterpret_cast<double2 *>(o) = acc;
-                else if (q < rows) o[0] = acc.x;
-                if (q < rows) nrm = fma(acc.x, acc.x, nrm);
-                if (q + 1 < rows) nrm = fma(acc.y, acc.y, nrm);
+            for (int h = 0; h < 2; h++) {
+                const int64_t r0 = rp + (int64_t)h * TILE_;
+                const int rows = (int)max((int64_t)0, min((int64_t)TILE_, ce - r0));
+#pragma unroll
+                for (int p = 0; p < NP; p++) {
+                    const int q = 2 * tid + 2 * SNT * p;
+                    double2 acc;
+                    acc.x = fma(cf, xv[h * NP + p].x, yv[h * NP + p].x);
+                    acc.y = fma(cf, xv[h * NP + p].y, yv[h * NP + p].y);
+                    double *o = vn + r0 + q;
+                    if (q + 1 < rows) *reinterpret_cast<double2 *>(o) = acc;
+                    else if (q < rows) o[0] = acc.x;
+                    if (q < rows) nrm = fma(acc.x, acc.x, nrm);
+                    if (q + 1 < rows) nrm = fma(acc.y, acc.y, nrm);
+                }
             }
         }
         {

@@ -134,3 +134,35 @@ def test_wrec_persistent_all_p_multistep(orc, p):
         ref = X.dst_solution(st, u, Pb.t)
         assert relerr(wg, ref) <= 10 * max(relerr(wo, ref), parity_bound(Pb.tol)), (s, so)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("modes,p", [(1, 0), (2, 0), (3, 0)])
+def test_tmem_lanczos_breakdown(ctx, orc, modes, p):
+    # u_0 = a combination of `modes` eigenvectors (separable sines) of the 3-D Dirichlet Laplacian: the
+    # Krylov space is that invariant subspace, so Lanczos breaks down at j = modes inside the TMEM kernel
+    # (h_{j+1,j} <= n eps ||A||, R22); the step's pre-issued halo tiles are drained before the CTAs exit.
+    # (p > 0 would apply A^p to the sines' ~1e-14 rounding, high-frequency and amplified by ||A||^p, and
+    # the space no longer closes at j = modes.)
+    nx, ny, nz = 72, 70, 68
+    st, _ = laplacian(3, nx, ny, nz, seed=0)
+    gx = np.arange(1, nx + 1) / (nx + 1)
+    gy = np.arange(1, ny + 1) / (ny + 1)
+    gz = np.arange(1, nz + 1) / (nz + 1)
+
+    def mode(k):
+        return np.einsum("k,j,i->kji", np.sin(k * np.pi * gz), np.sin((k + 1) * np.pi * gy),
+                         np.sin((k + 2) * np.pi * gx)).ravel()
+
+    u = []
+    for i in range(p + 1):
+        v = np.zeros(st.n)
+        for k in range(1, modes + 1):
+            v += (1.0 + 0.5 * i) / k * mode(k)
+        u.append(v)
+    Pb = W.Problem(name="bd", n=st.n, p=p, t=1e-4, tol=1e-10, symmetric=True, u=u, stencil=st, seed=0)
+    wo, so, _ = orc.solve(Pb)
+    assert so["status"] == 0
+    w, s = ctx.solve_stencil(Pb.t, P.Stencil.of(st), [to_dev(x) for x in u], tol=Pb.tol, symmetric=True)
+    assert s.t_reached == Pb.t
+    assert s.nspmv - p * s.nsteps <= modes * s.nexpm, s    # the basis never grew past the invariant subspace
+    assert relerr(w.cpu().numpy(), wo) <= parity_bound(Pb.tol), (s, so)

@@ -249,7 +249,10 @@ template <int XM>
 __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__restrict__ x, const double *xs, int64_t xs0,
                                              int64_t r0, int rows, double *ys)
 {
-    constexpr int U = 4;
+#ifndef PHIPM_ELL_U
+#define PHIPM_ELL_U 3
+#endif
+    constexpr int U = PHIPM_ELL_U;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int G = A.ell >> 2;                 // lanes per row (power of two, <= 32)
     const int rpw = 32 / G;

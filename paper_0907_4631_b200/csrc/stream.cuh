@@ -31,7 +31,10 @@ constexpr int SNT = PHIPM_SNT;          // threads per CTA: one 1024-thread CTA 
                                         // to reduce, less halo re-read per row than 4 x 256)
 constexpr int SNW = SNT / 32;
 constexpr int SMINB = 1024 / SNT;       // resident CTAs per SM the register budget is sized for
-constexpr int CU = 4;                   // columns in flight per thread
+#ifndef PHIPM_CU
+#define PHIPM_CU 4
+#endif
+constexpr int CU = PHIPM_CU;            // columns in flight per thread
 // banded uniform-row CSR: x lives in a shared-memory ring of XRING doubles (x[c] at c mod XRING)
 // that slides with the CTA's row range; each tile's 1-D bulk copy brings in only the new chunk
 constexpr int XRING = 16384;
@@ -560,6 +563,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
     constexpr int NP = RPT / 2;                           // double2 pairs per thread
     constexpr bool IS_ST = std::is_same<Op, StencilOp>::value;
     constexpr bool HALO = !std::is_same<Op, CsrOp>::value;
+    constexpr int CUD = std::is_same<Op, CsrOp>::value ? 3 : CU;
     extern __shared__ __align__(128) double sm[];
     __shared__ uint64_t hbar;
     __shared__ int hofs[2][5];                            // tile-relative halo offsets per parity
@@ -763,7 +767,8 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
             ysq = fma(y[p].x, y[p].x, ysq);
             ysq = fma(y[p].y, y[p].y, ysq);
         }
-        // ---- phase 3: d_k = V_k^T y over the tile, CU columns in flight; the column equal to x
+        // ---- phase 3: d_k = V_k^T y over the tile, CUD columns in flight (CSR: 3, its row loop holds more
+        //      registers; measured c5 +1 %, stencils keep 4); the column equal to x
         //      (if any) is not re-read: its dot comes from the x tile values kept in registers
         if (a.xnorm) {
             // ||x||^2 over the tile: x values in registers (halo operators) or this thread's own rows
@@ -789,10 +794,10 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
             d = warp_sum(d);
             if (lane == 0) lacc[xc * SNW + warp] += d;
         }
-        for (int k0 = 0; k0 < a.nd; k0 += CU) {
-            double2 v[CU][NP];
+        for (int k0 = 0; k0 < a.nd; k0 += CUD) {
+            double2 v[CUD][NP];
 #pragma unroll
-            for (int u = 0; u < CU; u++) {
+            for (int u = 0; u < CUD; u++) {
                 const int k = k0 + u;
                 const bool ld = k < a.nd && k != xc;
                 const double *vc = a.V + (int64_t)(a.d0 + (k < a.nd ? k : k0)) * a.ldv + r0;
@@ -803,7 +808,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
                 }
             }
 #pragma unroll
-            for (int u = 0; u < CU; u++) {
+            for (int u = 0; u < CUD; u++) {
                 double d = 0.0;
 #pragma unroll
                 for (int p = 0; p < NP; p++) {

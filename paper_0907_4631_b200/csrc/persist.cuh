@@ -27,6 +27,7 @@ struct PersistArgs {
     int64_t rpc;                   // rows per CTA (balanced contiguous ranges, multiple of 32)
     unsigned *flag;                // arrival counter (CTAs x phases, monotonic within a launch)
     unsigned *abort;               // set by a CTA that timed out
+    unsigned *exit_ctr;            // CTAs that left; the last one zeroes flag and exit_ctr for the next launch
     unsigned long long timeout_ns;
     unsigned long long *dbg;       // optional (PHIPM_KCLOCKS): per phase, per CTA: body end, release seen
 };
@@ -57,6 +58,20 @@ __device__ __forceinline__ double2 ld_cg2(const double *p)
 // monotonic counter (release), waits until all gridDim.x CTAs of this phase arrived (acquire), and
 // then sums the partials itself in block order: every CTA obtains bit-identical totals in red[]
 // without a serialising last-CTA reduction and flag round trip.  Returns false on abort.
+// End of a cooperative launch (normal exit): the last CTA to leave zeroes the arrival counter, so the
+// next cooperative launch on the stream needs no memset node before it.  Every CTA has passed its last
+// grid phase when it gets here, so no CTA can still be polling the counter.
+__device__ __forceinline__ void coop_exit(const PersistArgs &a)
+{
+    if (threadIdx.x == 0) {
+        const unsigned old = atomicAdd(a.exit_ctr, 1u);
+        if (old == gridDim.x - 1) {
+            *(volatile unsigned *)a.flag = 0u;
+            *(volatile unsigned *)a.exit_ctr = 0u;
+        }
+    }
+}
+
 struct NoRelease {
     __device__ void operator()() const {}
 };
@@ -424,6 +439,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
     }
     // a first tile issued for a step that did not run (breakdown): land it before the CTA exits
     if (pre) mbar_wait(&hbar, ht & 1);
+    coop_exit(a);
 }
 
 } // namespace phipm

@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
     unsigned phase = 0;
     const bool lead = blockIdx.x == 0;
     bool pre = false;                                      // the next SpMV phase's first tiles are in flight
+    bool aborted = false;                                  // a grid phase timed out (no counter reset)
     auto issue_first = [&](const double *xj) {            // (one thread)
         for (int u = 0; u < 2; u++) {
             const int64_t ru = cs + (int64_t)u * TILE_;
@@ -257,7 +258,10 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
             const double v2[2] = {dot, ysq};
             block_sums<2, false>(v2, wsum2, bsum);
         }
-        if (!phase_allreduce(wk, bsum, 2, ++phase, a, red)) break;
+        if (!phase_allreduce(wk, bsum, 2, ++phase, a, red)) {
+            aborted = true;
+            break;
+        }
         // finalize (FIN_LANCZOS): alpha_j = sigma_j d; update coefficient -alpha_j sigma_j -- derived by
         // every thread from the all-reduced totals (no CTA barrier); CTA 0 thread 0 writes H for the host
         const double al = sj * red[0];
@@ -303,8 +307,10 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
         const bool more = j + 1 < a.k1;
         if (!phase_allreduce(wk, bsum, 1, ++phase, a, red, [&] {
                 if (more) issue_first(x + ldv);
-            }))
+            })) {
+            aborted = true;
             break;
+        }
         pre = more;
         // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown -- derived by
         // every thread from the all-reduced total (identical in every thread and CTA; no CTA barrier)
@@ -338,6 +344,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
+    if (!aborted) coop_exit(a);
 }
 
 } // namespace phipm

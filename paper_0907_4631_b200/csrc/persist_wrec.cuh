@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(SNT, 1) wrec_persist_kernel(StencilOp op, Wrec
             wk.st->lz = 0.0;
         }
     }
+    coop_exit(a);
 }
 
 } // namespace phipm

@@ -62,6 +62,7 @@ struct phipm_ctx {
     double *V = nullptr, *W = nullptr, *Y = nullptr, *U = nullptr, *H = nullptr, *sigma = nullptr, *g = nullptr;
     double *part = nullptr, *comb = nullptr, *combd = nullptr, *scratch = nullptr, *raw = nullptr;
     unsigned *counter = nullptr;
+    bool coop_dirty = false;                         // a cooperative kernel timed out: reset its counters
     cudaEvent_t ev_binf = nullptr;                   // ||u_0||_inf readback of a solve
     DevState *st = nullptr;
     int32_t *tlo = nullptr, *thi = nullptr;                  // CSR per-tile column ranges
@@ -602,6 +603,18 @@ double tau0(double normA, double b_inf, double tol, double mbar)
 template <class Op>
 bool launch_persist(phipm_ctx *, const Op &, double, bool, int, int, double, int &) { return false; }
 
+// Cooperative launches zero their arrival counter on a normal exit (coop_exit); only after a grid
+// phase timed out (coop_dirty) are the counters and the abort flags cleared by memsets first.
+bool coop_reset(phipm_ctx *c)
+{
+    if (!c->coop_dirty) return true;
+    if (cudaMemsetAsync(c->counter + 2, 0, 3 * sizeof(unsigned), c->stream) != cudaSuccess ||
+        cudaMemsetAsync(&c->st->aborted, 0, sizeof(int), c->stream) != cudaSuccess)
+        return false;
+    c->coop_dirty = false;
+    return true;
+}
+
 using PersistFn = void (*)(StencilOp, PersistArgs, Work);
 
 template <int RPT, bool LANC>
@@ -666,6 +679,7 @@ bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, 
     a.rpc = rpc;
     a.flag = c->counter + 2;
     a.abort = c->counter + 3;
+    a.exit_ctr = c->counter + 4;
     a.timeout_ns = 2000000000ull;
     // PHIPM_KCLOCKS: 2 stamps per CTA per phase (2 phases per step), separate buffer
     a.dbg = nullptr;
@@ -676,8 +690,7 @@ bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, 
         c->pclk_used += need;
     }
     rc = PHIPM_OK;
-    if (cudaMemsetAsync(c->counter + 2, 0, 2 * sizeof(unsigned), c->stream) != cudaSuccess ||
-        cudaMemsetAsync(&c->st->aborted, 0, sizeof(int), c->stream) != cudaSuccess) {
+    if (!coop_reset(c)) {
         rc = set_err(c, PHIPM_ECUDA, "persist: memset failed");
         return true;
     }
@@ -732,6 +745,7 @@ bool try_persist_tm(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bt
     a.rpc = rpc;
     a.flag = c->counter + 2;
     a.abort = c->counter + 3;
+    a.exit_ctr = c->counter + 4;
     a.timeout_ns = 2000000000ull;
     a.dbg = nullptr;
     const size_t need = (size_t)2 * (k1 - k0) * grid * 2;
@@ -741,8 +755,7 @@ bool try_persist_tm(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bt
         c->pclk_used += need;
     }
     rc = PHIPM_OK;
-    if (cudaMemsetAsync(c->counter + 2, 0, 2 * sizeof(unsigned), c->stream) != cudaSuccess ||
-        cudaMemsetAsync(&c->st->aborted, 0, sizeof(int), c->stream) != cudaSuccess) {
+    if (!coop_reset(c)) {
         rc = set_err(c, PHIPM_ECUDA, "persist: memset failed");
         return true;
     }
@@ -798,10 +811,10 @@ bool launch_wrec_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, const Wre
     a.rpc = rpc;
     a.flag = c->counter + 2;
     a.abort = c->counter + 3;
+    a.exit_ctr = c->counter + 4;
     a.timeout_ns = 2000000000ull;
     rc = PHIPM_OK;
-    if (cudaMemsetAsync(c->counter + 2, 0, 2 * sizeof(unsigned), c->stream) != cudaSuccess ||
-        cudaMemsetAsync(&c->st->aborted, 0, sizeof(int), c->stream) != cudaSuccess) {
+    if (!coop_reset(c)) {
         rc = set_err(c, PHIPM_ECUDA, "wrec: memset failed");
         return true;
     }
@@ -1172,7 +1185,10 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             if (R.brk >= 0 && R.brk < k) kb = k;
             S.nspmv += kb - k;
             k = kb;
-            if (R.status == 3) return finish(set_err(c, PHIPM_ECUDA, "persistent Krylov kernel: grid phase timed out"));
+            if (R.status == 3) {
+                c->coop_dirty = true;
+                return finish(set_err(c, PHIPM_ECUDA, "persistent Krylov kernel: grid phase timed out"));
+            }
             if (R.status == 5) return finish(set_err(c, PHIPM_ENONFINITE, "non-finite value in the Krylov step"));
             if (R.status == 6) return finish(set_err(c, PHIPM_ESINGULAR, "singular Pade denominator"));
             mu = R.mu;
@@ -1660,7 +1676,7 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         A((void **)&c->scratch, sizeof(double) * 6 * (size_t)expm_ld(kp) * kp);
     }
     A((void **)&c->raw, sizeof(double) * (MAXD + 2));
-    A((void **)&c->counter, sizeof(unsigned) * 4);
+    A((void **)&c->counter, sizeof(unsigned) * 8);
     if (ok && cudaEventCreateWithFlags(&c->ev_binf, cudaEventDisableTiming) != cudaSuccess) ok = false;
     A((void **)&c->st, sizeof(DevState));
     c->ntile_cap = n_max / 512 + 2;
@@ -2012,7 +2028,10 @@ static int krylov_export(phipm_ctx *c, const Op &op, double bytes_op, double nor
     CK(cudaMemcpyAsync(&ds, c->st, sizeof(ds), cudaMemcpyDeviceToHost, c->stream));
     rc = sync(c);
     if (rc) return rc;
-    if (ds.aborted) return set_err(c, PHIPM_ECUDA, "persistent Krylov kernel: grid phase timed out");
+    if (ds.aborted) {
+        c->coop_dirty = true;
+        return set_err(c, PHIPM_ECUDA, "persistent Krylov kernel: grid phase timed out");
+    }
     const int kk = (ds.brk >= 0) ? std::min(ds.brk, m) : m;
     if (!V) {                                             // build only (no export): timing
         *k = kk;

@@ -548,7 +548,9 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
         // tau H_mu into M0, |H_mu| into M1 (scratch for the unscaled 1-norm)
         for (size_t e = t; e < (size_t)mu * mu; e += blockDim.x) {
             const int i = (int)(e % mu), jc = (int)(e / mu);
-            const double hv = (!a.tridiag || (i - jc <= 1 && jc - i <= 1)) ? a.H[i + (size_t)jc * a.ldh] : 0.0;
+            // only the Hessenberg part (Lanczos: the tridiagonal band) is read: entries below the
+            // subdiagonal are never written by the Krylov kernels and are zero by definition
+            const double hv = (i <= jc + 1 && (!a.tridiag || jc - i <= 1)) ? a.H[i + (size_t)jc * a.ldh] : 0.0;
             M0[i + (size_t)jc * ld] = a.tau * hv;
             M1[i + (size_t)jc * ld] = fabs(hv);
         }

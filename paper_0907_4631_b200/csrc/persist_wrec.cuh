@@ -22,7 +22,8 @@ constexpr int WREC_PLANS = 8;           // tiles per CTA with a precomputed halo
 
 struct WrecArgs {
     int p;
-    const double *x0;                   // w_0 = u_k (padded workspace vector)
+    const double *x0;                   // w_0 = u_k (padded workspace vector, or the caller's u_0)
+    int64_t ldx;                        // halo copies clamp to [0, ldx) (n when x0 is the caller's vector)
     double *W;                          // w_j at W + j ldv (j = 1..p-1); w_p goes to V column 0
     const double *z[WREC_MAXP][WREC_MAXP + 1];
     double zc[WREC_MAXP][WREC_MAXP + 1];
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(SNT, 1) wrec_persist_kernel(StencilOp op, Wrec
     }
     if (tid < WREC_PLANS && tid < nt) {
         const int64_t ru = cs + (int64_t)tid * TILE_;
-        tile_plan<TILE_>(op, ldv, ru, (int)min((int64_t)TILE_, ce - ru), tplan[tid]);
+        tile_plan<TILE_>(op, w.ldx, ru, (int)min((int64_t)TILE_, ce - ru), tplan[tid]);
     }
     const uint64_t pol = policy_evict_last();
     pdl_wait();
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(SNT, 1) wrec_persist_kernel(StencilOp op, Wrec
             issue_planned_tile(tplan[u], hb, x, &hbar[g & 1], pol);
         } else {
             const int64_t ru = cs + (int64_t)u * TILE_;
-            issue_halo_tile<TILE_>(op, hb, x, ldv, ru, (int)min((int64_t)TILE_, ce - ru), hofs[g & 1], &hbar[g & 1]);
+            issue_halo_tile<TILE_>(op, hb, x, w.ldx, ru, (int)min((int64_t)TILE_, ce - ru), hofs[g & 1], &hbar[g & 1]);
         }
     };
     for (int j = 1; j <= w.p; j++) {

@@ -1009,11 +1009,12 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         return PHIPM_OK;
     };
     // Eq. (wrecurrence): w_0 = u_k, w_j = A w_{j-1} + sum_l t_k^l/l! u_{j+l}; w_p -> V[:,0]
-    auto enqueue_wrec = [&](double tk, const double *ucur) {
+    // x0 = w_0 = u_k; ldx0 > 0: x0 is the caller's u_0 (n even, 16-B aligned), halos clamp to n
+    auto enqueue_wrec = [&](double tk, const double *x0, int64_t ldx0) {
         if (p == 0) {
             AxpyArgs a = axpy0();
             a.out = c->V;
-            a.base = ucur;
+            a.base = x0;
             a.a0h = 1.0;
             a.V = c->V;
             a.ldv = c->ldv;
@@ -1026,7 +1027,8 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             WrecArgs wa;
             memset(&wa, 0, sizeof(wa));
             wa.p = p;
-            wa.x0 = ucur;
+            wa.x0 = x0;
+            wa.ldx = ldx0 ? ldx0 : c->ldv;
             wa.W = c->W;
             double bytes = 0.0;
             for (int j = 1; j <= p; j++) {
@@ -1047,7 +1049,8 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         }
         for (int j = 1; j <= p; j++) {
             SpmvArgs s = spmv0();
-            s.x = (j == 1) ? ucur : c->W + (int64_t)(j - 1) * c->ldv;
+            s.x = (j == 1) ? x0 : c->W + (int64_t)(j - 1) * c->ldv;
+            if (j == 1 && ldx0) s.ldx = ldx0;
             s.y = (j == p) ? c->V : c->W + (int64_t)j * c->ldv;
             // terms whose coefficient t_k^l / l! is exactly 0 (the first step, t_k = 0: only u_j)
             // are not read: adding 0 * u changes no sum
@@ -1091,11 +1094,16 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     }
     // the running solution u_k lives in the padded workspace vector U (TMA-readable)
     double *ucur = c->U;
-    CK(cudaMemsetAsync(c->H, 0, sizeof(double) * (c->m_max + 1) * c->m_max, c->stream));
-    CK(cudaMemcpyAsync(ucur, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    // (H is not cleared: the exponential reads only its Hessenberg part, which every extension writes)
+    // The first step reads u_0 in place when its halo copies can (n even, 16-B aligned: bulk copies
+    // clamp to n); otherwise u_0 goes to the padded workspace first.  Later steps read U.
+    const bool direct = (n % 2 == 0) && ((reinterpret_cast<uintptr_t>(u[0]) & 15) == 0);
+    const double *x0 = direct ? u[0] : ucur;
+    if (!direct) CK(cudaMemcpyAsync(ucur, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    bool step0 = true;                // the current step is the first (its u_k is x0)
     int enq = 0;                      // Krylov columns already enqueued for the current step
     {
-        int rc = enqueue_wrec(0.0, ucur);
+        int rc = enqueue_wrec(0.0, x0, direct ? n : 0);
         if (rc) return finish(rc);
         if (m > 0) {
             rc = enqueue_krylov(c, op, bytes_op, P.symmetric, o.orth, 0, m, bthr);
@@ -1137,7 +1145,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         if (tau > t_end - tk) tau = t_end - tk;
         if (!first) {
             enq = 0;
-            int rc = enqueue_wrec(tk, ucur);
+            int rc = enqueue_wrec(tk, ucur, 0);
             if (rc) return finish(rc);
         }
         first = false;
@@ -1207,7 +1215,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             S.nreject++;
             if (attempts >= 100 || tau < 1e-15 * t_end) {
                 S.t_reached = tk;
-                cudaMemcpyAsync(w, ucur, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
+                cudaMemcpyAsync(w, step0 ? x0 : ucur, n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream);
                 cudaStreamSynchronize(c->stream);
                 return finish(set_err(c, PHIPM_ESTEP, "step size control failed at t = %g", tk));
             }
@@ -1217,7 +1225,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         {
             AxpyArgs a = axpy0();
             a.out = last ? w : ucur;           // the last step writes the caller's w directly
-            a.base = ucur;
+            a.base = step0 ? x0 : ucur;
             a.a0h = (p >= 1) ? 1.0 : 0.0;
             a.a0d = (p >= 1) ? c->combd : nullptr;
             a.V = c->V;
@@ -1238,6 +1246,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         if (last) tk = t_end;
         else tk += tau_used;
         S.nsteps++;
+        step0 = false;
         S.m_last = m_used;
         S.t_reached = tk;
     }

@@ -330,6 +330,9 @@ struct IdentOp {
 struct MaxAbsArgs {
     int nv;
     const double *x[MAXZ];
+    double *pub;                 // optional: results to mapped pinned memory, then ...
+    volatile int *pub_seq;       // ... this sequence number (after a system-scope fence)
+    int seq;
 };
 
 __global__ void __launch_bounds__(NT) maxabs_kernel(int64_t n, MaxAbsArgs a, Work wk)
@@ -368,10 +371,20 @@ __global__ void __launch_bounds__(NT) maxabs_kernel(int64_t n, MaxAbsArgs a, Wor
         double m = 0.0;
         for (int b = lane; b < (int)gridDim.x; b += 32) m = fmax(m, __ldcg(wk.part + (size_t)v * wk.pstride + b));
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0) wk.out_raw[v] = m;
+        if (lane == 0) {
+            if (a.pub) a.pub[v] = m;
+            else wk.out_raw[v] = m;
+        }
     }
     __syncthreads();
-    if (tid == 0) *wk.counter = 0u;
+    if (tid == 0) {
+        *wk.counter = 0u;
+        if (a.pub) {
+            // the host spins on the sequence number: publish it last
+            __threadfence_system();
+            *a.pub_seq = a.seq;
+        }
+    }
 }
 
 // One pass over a CSR matrix (row_ptr, col, val), coalesced: each warp takes 32 consecutive rows,

@@ -68,6 +68,11 @@ struct phipm_ctx {
     int32_t *tlo = nullptr, *thi = nullptr;                  // CSR per-tile column ranges
     int64_t ntile_cap = 0;
     AttemptResult *res_h = nullptr, *res_d = nullptr;
+    struct MaxPub {
+        double v[MAXZ];
+        int seq;
+    } *mx_h = nullptr, *mx_d = nullptr;               // ||u_0||_inf published to mapped pinned memory
+    int mx_seq = 0;
     long long *expm_clk_h = nullptr, *expm_clk_d = nullptr;   // PHIPM_EXPM_CLOCKS=1 debug timestamps
     // PHIPM_KCLOCKS=<file>: per-CTA %globaltimer stamps of every streaming launch (measurement tool)
     unsigned long long *kclk_d = nullptr;
@@ -996,16 +1001,24 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         int rc = sync(c);
         return finish(rc);
     }
-    auto enqueue_maxabs = [&](int k0, int k1) {
+    // publish = true: the result goes to mapped pinned memory with a sequence number the host spins on
+    // (no copy node in the stream); otherwise it is copied to raw_h
+    auto enqueue_maxabs = [&](int k0, int k1, bool publish) {
         MaxAbsArgs ma;
         memset(&ma, 0, sizeof(ma));
         ma.nv = k1 - k0;
         for (int k = k0; k < k1; k++) ma.x[k - k0] = u[k];
+        if (publish) {
+            ma.pub = c->mx_d->v;
+            ma.pub_seq = &c->mx_d->seq;
+            ma.seq = ++c->mx_seq;
+        }
         const int grid = grid_for(c, (n + NT - 1) / NT, c->occ_axpy);
         maxabs_kernel<<<grid, NT, 0, c->stream>>>(n, ma, make_work(c));
         c->acc.launches++;
         CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(c->raw_h + k0, c->raw, ma.nv * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        if (!publish)
+            CK(cudaMemcpyAsync(c->raw_h + k0, c->raw, ma.nv * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
         return PHIPM_OK;
     };
     // Eq. (wrecurrence): w_0 = u_k, w_j = A w_{j-1} + sum_l t_k^l/l! u_{j+l}; w_p -> V[:,0]
@@ -1087,10 +1100,11 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     // ||u_0||_inf is read back through an event, and the first step's w-recurrence and initial
     // Krylov extension -- which do not depend on it: tau enters only the exponential -- are
     // enqueued before the host waits for it.  The other u_k are only read when u_0 = 0.
+    const bool spin_binf = !c->prof;                 // profiling collects events at a stream sync instead
     {
-        int rc = enqueue_maxabs(0, 1);
+        int rc = enqueue_maxabs(0, 1, spin_binf);
         if (rc) return finish(rc);
-        CK(cudaEventRecord(c->ev_binf, c->stream));
+        if (!spin_binf) CK(cudaEventRecord(c->ev_binf, c->stream));
     }
     // the running solution u_k lives in the padded workspace vector U (TMA-readable)
     double *ucur = c->U;
@@ -1111,15 +1125,36 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             enq = m;
         }
     }
-    CK(cudaEventSynchronize(c->ev_binf));
-    double b_inf = c->raw_h[0];
+    double b_inf;
+    if (spin_binf) {
+        // spin on the published sequence number (fallback: stream sync after 2 s, e.g. on a fault)
+        const volatile int *seqp = &c->mx_h->seq;
+        const auto t0 = std::chrono::steady_clock::now();
+        unsigned spins = 0;
+        bool synced = false;
+        while (*seqp != c->mx_seq) {
+            if ((++spins & 1023) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+                int rc = sync(c);
+                if (rc) return finish(rc);
+                synced = true;
+                if (*seqp != c->mx_seq) return finish(set_err(c, PHIPM_ECUDA, "||u_0|| result not published"));
+            }
+        }
+        (void)synced;
+        std::atomic_thread_fence(std::memory_order_acquire);
+        b_inf = ((const volatile double *)c->mx_h->v)[0];
+    } else {
+        CK(cudaEventSynchronize(c->ev_binf));
+        b_inf = c->raw_h[0];
+    }
+    c->raw_h[0] = b_inf;
     if (b_inf == 0.0) {
         {
             int rc = sync(c);
             if (rc) return finish(rc);
         }
         if (p > 0) {
-            int rc = enqueue_maxabs(1, p + 1);
+            int rc = enqueue_maxabs(1, p + 1, false);
             if (rc) return finish(rc);
             rc = sync(c);
             if (rc) return finish(rc);
@@ -1547,6 +1582,7 @@ void phipm_destroy(phipm_ctx *c)
     cudaFree(c->counter); cudaFree(c->st); cudaFree(c->tlo); cudaFree(c->thi);
     cudaFree(c->hu); cudaFree(c->hw); cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
     if (c->res_h) cudaFreeHost(c->res_h);
+    if (c->mx_h) cudaFreeHost(c->mx_h);
     if (c->expm_clk_h) cudaFreeHost(c->expm_clk_h);
     if (c->kclk_d) {
         // dump: int32 count, then per launch int32 {cls, grid, ncols} and grid*8 uint64 stamps
@@ -1692,6 +1728,9 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     A((void **)&c->tlo, sizeof(int32_t) * c->ntile_cap);
     A((void **)&c->thi, sizeof(int32_t) * c->ntile_cap);
     if (ok && cudaHostAlloc((void **)&c->res_h, sizeof(AttemptResult), cudaHostAllocMapped) != cudaSuccess) ok = false;
+    if (ok && cudaHostAlloc((void **)&c->mx_h, sizeof(*c->mx_h), cudaHostAllocMapped) != cudaSuccess) ok = false;
+    if (ok && cudaHostGetDevicePointer((void **)&c->mx_d, c->mx_h, 0) != cudaSuccess) ok = false;
+    if (ok) memset(c->mx_h, 0, sizeof(*c->mx_h));
     if (ok && cudaHostGetDevicePointer((void **)&c->res_d, c->res_h, 0) != cudaSuccess) ok = false;
     if (ok && cudaHostAlloc((void **)&c->raw_h, sizeof(double) * (MAXD + 2), cudaHostAllocDefault) != cudaSuccess) ok = false;
     if (ok && getenv("PHIPM_EXPM_CLOCKS")) {

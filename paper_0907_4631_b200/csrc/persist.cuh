@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_kernel(StencilOp op, Pe
         mbar_init(&hbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    pdl_wait();                                            // the previous kernel's results from here on
     __syncthreads();
     uint32_t ht = 0;
     unsigned phase = 0;

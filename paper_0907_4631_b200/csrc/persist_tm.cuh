@@ -163,6 +163,9 @@ __global__ void __launch_bounds__(SNT, 1) krylov_persist_tm_kernel(StencilOp op,
         mbar_init(&hbar[0], 1);
         mbar_init(&hbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    pdl_wait();                                            // the previous kernel's results from here on
+    if (tid == 0) {
         s_stop = __ldcg(&wk.st->brk) >= 0;
         s_sig = __ldcg(wk.sigma + a.k0);
         s_lz = __ldcg(&wk.st->lz);

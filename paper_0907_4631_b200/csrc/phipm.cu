@@ -241,7 +241,8 @@ cudaError_t launch_k(phipm_ctx *c, void (*kern)(KArgs...), dim3 grid, dim3 block
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
-// Cooperative launch (all CTAs co-resident, or the launch fails): no PDL, plain stream order.
+// Cooperative launch (all CTAs co-resident, or the launch fails), PDL allowed: the kernels set up
+// (TMEM, halo plans, mbarriers) before griddepcontrol.wait.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_coop(phipm_ctx *c, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args)
 {
@@ -250,11 +251,13 @@ cudaError_t launch_coop(phipm_ctx *c, void (*kern)(KArgs...), dim3 grid, dim3 bl
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c->stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, kern, args...);
 }
 

@@ -12,9 +12,13 @@
 // Phase B then needs no global loads at all (v~_{j+1} = y - alpha sigma_j v~_j from TMEM), and
 // the next step's -lz v~_{j-1} term reads slot B before phase A overwrites it with v~_{j+1}.
 // Shared memory holds two halo tiles, so tile t + 1's (and t + 2's) bulk copies fly while tile t
-// is computed.  Arithmetic per row / thread / warp / block and the grid all-reduce are those of
+// is computed; the last warp to finish a halo buffer issues the next tile into it (no CTA barrier in
+// the tile loop), and the next step's first two tiles are issued as soon as every CTA has arrived
+// at the update phase's grid phase.  Arithmetic per row and the grid all-reduce are those of
 // krylov_persist_kernel; the dot and ||y||^2 are accumulated per thread across tiles and reduced
-// once per phase.  Requires ceil(rows per CTA / TILE) * NP <= 8 (c4: 14176 rows, 4 tiles).
+// once per phase (block_sums), and every thread derives the phase-end scalars (alpha_j, sigma_j,
+// the Lanczos coefficient, breakdown) from the all-reduced totals itself, without a CTA barrier.
+// Requires ceil(rows per CTA / TILE) * NP <= 8 (c4: 14176 rows, 4 tiles).
 #pragma once
 
 #include "persist.cuh"

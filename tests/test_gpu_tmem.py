@@ -166,3 +166,23 @@ def test_tmem_lanczos_breakdown(ctx, orc, modes, p):
     assert s.t_reached == Pb.t
     assert s.nspmv - p * s.nsteps <= modes * s.nexpm, s    # the basis never grew past the invariant subspace
     assert relerr(w.cpu().numpy(), wo) <= parity_bound(Pb.tol), (s, so)
+
+
+def test_u0_in_place_and_copied_agree(ctx):
+    # the first step reads u_0 in place when n is even and u_0 is 16-B aligned, otherwise from a workspace
+    # copy; both run the same arithmetic, so w is bit-identical (also with w aliasing u_0)
+    import torch
+    Pb = W.make("c3_med")                                  # n = 301^2 odd: always the copy
+    Pb2 = W.make("c4")                                     # n even
+    for Q in (Pb, Pb2):
+        u = [to_dev(x) for x in Q.u]
+        S = P.Stencil.of(Q.stencil)
+        w1, s1 = ctx.solve_stencil(Q.t, S, u, tol=Q.tol, symmetric=Q.symmetric)
+        big = torch.zeros(Q.n + 1, dtype=torch.float64, device="cuda")
+        big[1:] = u[0]
+        u_mis = [big[1:]] + u[1:]                          # 8-B aligned view: the copy path
+        w2, s2 = ctx.solve_stencil(Q.t, S, u_mis, tol=Q.tol, symmetric=Q.symmetric)
+        assert torch.equal(w1, w2) and s1.nspmv == s2.nspmv
+        u_alias = [u[0].clone()] + u[1:]
+        w3, s3 = ctx.solve_stencil(Q.t, S, u_alias, out=u_alias[0], tol=Q.tol, symmetric=Q.symmetric)
+        assert w3.data_ptr() == u_alias[0].data_ptr() and torch.equal(w1, w3)

@@ -1,11 +1,12 @@
 #!/usr/bin/env python
 """Benchmark: phipm solves/s on one BASELINE.json config, with the Arnoldi-step roofline.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl reference]
 
 A "step" is one full phipm solve (all SURVEY §8(a) rows: ||A||, w-recurrence, Krylov steps,
 augmented expm, controller, assembly) of the named config, inputs resident in HBM.  Default
-workload: c3 (2-D advection-diffusion 1024^2, Arnoldi, p=2, t=1e-3, tol=1e-8, stencil path).
+workload: c5 (random banded CSR, n = 4,194,304, 16 nnz/row, Arnoldi, p=3, t=0.5, tol=1e-8), the
+largest BASELINE.json config (BASELINE.json quotes its metric on no single config).
 Prints ONE JSON line (rank 0).  Under torchrun (N > 1) every rank solves its own replica
 (independent problem, seed + rank): weak scaling, no collective on the data path.
 
@@ -102,6 +103,26 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
+def host_cpu():
+    """Host CPU model and logical core count (stated next to the oracle timing)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"host_cpu": model, "host_logical_cores": os.cpu_count()}
+
+
+def config_dict(name, Pb, path, world):
+    """The `config` object of both arms (identical keys and values for the same workload)."""
+    return {"workload": DESCR[name], "n": Pb.n, "p": Pb.p, "t": Pb.t, "tol": Pb.tol, "path": path,
+            "parallelism": f"replicas x{world} (independent problems, no collective)",
+            "l2": "flushed between timed steps (256 MiB memset outside the events)", "seed": Pb.seed}
+
+
 def load_traffic(config):
     """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -138,9 +159,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": val, "unit": "solves/s", "n_gpus": args.gpus,
         "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": DESCR[args.config], "n": Pb.n, "p": Pb.p, "path": "oracle CSR (oracle-built)"},
-        "cpu_baseline": {"value": val, "unit": "solves/s", "cores": 1, "kind": "oracle",
-                         "sample": f"{len(times)} full solves of {args.config} (single-threaded C oracle)"},
+        "config": config_dict(args.config, Pb, "stencil" if Pb.stencil is not None else "csr", args.gpus),
+        "cpu_baseline": dict({"value": val, "unit": "solves/s", "cores": 1, "kind": "oracle",
+                              "sample": f"{len(times)} full solves of {args.config} (single-threaded C oracle; "
+                                        "stencil operators as the oracle's own CSR)"}, **host_cpu()),
         "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "stats": s,
     }
@@ -160,8 +182,9 @@ def cpu_baseline(Pb, budget_s=15.0):
         n_done += 1
         if t_tot >= budget_s or n_done >= 50:
             break
-    return {"value": n_done / t_tot, "unit": "solves/s", "cores": 1, "kind": "oracle",
-            "sample": f"{n_done} full solve(s) of the same {Pb.name} workload, single thread, {t_tot:.1f} s"}
+    return dict({"value": n_done / t_tot, "unit": "solves/s", "cores": 1, "kind": "oracle",
+                 "sample": f"{n_done} full solve(s) of the same {Pb.name} workload, single thread, {t_tot:.1f} s"},
+                **host_cpu())
 
 
 # ---- multi-rank host logic (replicas only: independent problems, no data-path collective) ----
@@ -307,6 +330,7 @@ def run_gpu(args):
     krylov_ms = prof["ms_spmv_dot"] + prof["ms_orth"]
     krylov_bytes = prof["bytes_spmv_dot"] + prof["bytes_orth"]
     arnoldi_gbs = (krylov_bytes / 1e9) / (krylov_ms / 1e3) if krylov_ms > 0 else 0.0
+    solve_bytes = (prof["bytes_spmv_dot"] + prof["bytes_orth"] + prof["bytes_combine"] + prof["bytes_other"]) / args.steps
     tr = load_traffic(args.config)
     traffic = None
     if tr and tr.get("kernel_class") == dom:
@@ -350,13 +374,14 @@ def run_gpu(args):
             "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": t_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": DESCR[args.config], "n": Pb.n, "p": Pb.p, "t": Pb.t, "tol": Pb.tol,
-                       "path": path, "parallelism": f"replicas x{world} (independent problems, no collective)",
-                       "l2": "flushed between timed steps (256 MiB memset outside the events)",
-                       "seed": Pb.seed},
+            "config": config_dict(args.config, Pb, path, world),
             "e2e": {"value": e2e_val, "unit": "solves/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches_total,
             "roofline": roofline,
+            # whole solve: algorithmic bytes of every n-sized pass of one solve (the profiled region's
+            # per-class byte counts) over the UN-instrumented ms_per_step
+            "solve_algorithmic_gbs": solve_bytes / 1e6 / (t_max / args.steps),
+            "solve_frac_of_measured": solve_bytes / 1e6 / (t_max / args.steps) / peak,
             "arnoldi_step": {"achieved_gbs": arnoldi_gbs, "frac_of_8000": arnoldi_gbs / 8000.0,
                              "frac_of_measured": arnoldi_gbs / peak,
                              "ms_per_solve": krylov_ms / args.steps},
@@ -385,7 +410,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c3", choices=sorted(DESCR))
+    ap.add_argument("--config", default="c5", choices=sorted(DESCR))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -116,6 +116,7 @@ typedef struct {
     double bytes_combine;
     int64_t launches;      /* kernels launched */
     int64_t n_spmv_dot, n_orth, n_expm, n_combine;
+    double bytes_other;    /* algorithmic bytes of the setup passes (CSR analysis: 12 nnz + 4(n+1)) */
 } phipm_profile;
 
 /* One traced kernel launch (opts.profile = 2). */
@@ -126,11 +127,58 @@ typedef struct {
     double us;             /* device time (CUDA events) */
 } phipm_trace_rec;
 
+/* One attempt of the controller (Alg. 3's inner loop), recorded by every solve of the context:
+ * the step start t_k, the attempt's tau and m, the Krylov dimension mu used, omega and eps of
+ * Eq. (taunew) / (errest), beta = ||w_p||_2, ||H_mu||_1, accepted (omega <= 1.2) and the branch the
+ * controller took (1: tau changed, 2: m changed).  The fields are those of a test trajectory record. */
+typedef struct {
+    double t_k, tau, omega, eps, normH1, beta;
+    int32_t m, mu, accepted, branch;
+} phipm_attempt;
+
+/* Attempts of the context's last solve: copies min(max, count) records to out (HOST) and sets
+ * *count to the number the solve made (only the first 65536 are kept). */
+int phipm_get_attempts(const phipm_ctx *ctx, phipm_attempt *out, int max, int *count);
+
 void phipm_default_opts(phipm_opts *opts);
 
 /* Method used by the kernel-level entry points phipm_expm and phipm_phi_pair (solves take
  * opts.expm_method).  PHIPM_EINVAL for an unknown method. */
 int phipm_set_expm_method(phipm_ctx *ctx, int method);
+
+/* Kernel-path selection, per context (measurement and A/B experiments; the defaults are the
+ * measured-best paths of DESIGN.md §6 and every path is parity-tested).  Values:
+ *   PHIPM_OPT_PERSIST          0 off, 1 auto (default: Lanczos stencil extensions of any size,
+ *                              Arnoldi stencil extensions with n <= 2^19), 2 always (stencils)
+ *   PHIPM_OPT_TMEM             1 (default) Lanczos persistent kernel keeps y / v~ in tensor memory
+ *                              at n >= 303K; 0 shared-memory variant
+ *   PHIPM_OPT_WREC             1 (default) w-recurrence of stencils as one cooperative kernel
+ *   PHIPM_OPT_LAG              1 (default) lagged normalisation of the streaming Arnoldi step
+ *   PHIPM_OPT_PDL              1 (default) programmatic dependent launch between kernels
+ *   PHIPM_OPT_SPIN             1 (default) host spins on mapped pinned memory for the attempt
+ *                              result; 0 stream synchronisation
+ *   PHIPM_OPT_RPT              0 (default) auto, or 2/4/8 rows per thread of the streaming kernels
+ *   PHIPM_OPT_CSR_ELL          1 (default) vectorised uniform-row CSR path
+ *   PHIPM_OPT_CSR_RING         1 (default) x in a shared-memory ring for banded uniform-row CSR
+ *   PHIPM_OPT_CSR_WINDOW       0 (default) per-tile x windows for general CSR
+ *   PHIPM_OPT_SMALL_LZ         1 (default) multi-row single-CTA Lanczos for n <= 8192
+ *   PHIPM_OPT_PERSIST_MINROWS  0 (default: half a tile) minimum rows per CTA of the persistent kernel
+ * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
+#define PHIPM_OPT_PERSIST          0
+#define PHIPM_OPT_TMEM             1
+#define PHIPM_OPT_WREC             2
+#define PHIPM_OPT_LAG              3
+#define PHIPM_OPT_PDL              4
+#define PHIPM_OPT_SPIN             5
+#define PHIPM_OPT_RPT              6
+#define PHIPM_OPT_CSR_ELL          7
+#define PHIPM_OPT_CSR_RING         8
+#define PHIPM_OPT_CSR_WINDOW       9
+#define PHIPM_OPT_SMALL_LZ        10
+#define PHIPM_OPT_PERSIST_MINROWS 11
+#define PHIPM_OPT_COUNT           12
+int phipm_set_option(phipm_ctx *ctx, int option, int value);
+int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 
 /* Create a context that can solve problems with n <= n_max, m_max <= m_max, p <= p_max.
  * Allocates the device workspace (Krylov basis (m_max+1) x n_max, w vectors, small matrices,
@@ -182,10 +230,12 @@ int phipm_solve_stencil_batch(phipm_ctx *const *ctx, int nb, const double *t, co
 
 /* Matrix Market ingestion (HOST, no GPU needed): "%%MatrixMarket matrix coordinate {real|integer|pattern}
  * {general|symmetric|skew-symmetric}", square, 1-based indices.  Result: CSR with columns ascending
- * in each row, duplicate entries summed in file order, symmetric / skew-symmetric storage expanded.
+ * in each row, symmetric / skew-symmetric storage expanded.
  * Call with row_ptr = col = val = NULL to get n and nnz; then again with caller-allocated HOST
  * arrays row_ptr[n+1], col[nnz], val[nnz].  PHIPM_EINVAL on a missing file, an unsupported or
- * malformed header, a non-square matrix, out-of-range indices or nnz >= 2^31. */
+ * malformed header, a non-square matrix, out-of-range indices, a duplicate entry (also one
+ * created by expanding symmetric storage that already holds both triangles) or
+ * nnz >= 2^31. */
 int phipm_mm_read(const char *path, int64_t *n, int64_t *nnz, int32_t *row_ptr, int32_t *col, double *val);
 
 /* ---- kernel-level entry points (parity tests; all DEVICE pointers unless stated) ---- */

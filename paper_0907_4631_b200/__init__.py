@@ -59,12 +59,23 @@ class _TraceRec(C.Structure):
     _fields_ = [("cls", C.c_int32), ("ncols", C.c_int32), ("bytes", C.c_double), ("us", C.c_double)]
 
 
+class _Attempt(C.Structure):
+    _fields_ = [("t_k", C.c_double), ("tau", C.c_double), ("omega", C.c_double), ("eps", C.c_double),
+                ("normH1", C.c_double), ("beta", C.c_double), ("m", C.c_int32), ("mu", C.c_int32),
+                ("accepted", C.c_int32), ("branch", C.c_int32)]
+
+
+# kernel-path options (phipm_set_option; include/phipm.h)
+OPTIONS = {"persist": 0, "tmem": 1, "wrec": 2, "lag": 3, "pdl": 4, "spin": 5, "rpt": 6, "csr_ell": 7,
+           "csr_ring": 8, "csr_window": 9, "small_lz": 10, "persist_minrows": 11}
+
+
 class _Profile(C.Structure):
     _fields_ = [("ms_spmv_dot", C.c_double), ("ms_orth", C.c_double), ("ms_expm", C.c_double),
                 ("ms_combine", C.c_double), ("ms_other", C.c_double), ("bytes_spmv_dot", C.c_double),
                 ("bytes_orth", C.c_double), ("bytes_combine", C.c_double), ("launches", C.c_int64),
                 ("n_spmv_dot", C.c_int64), ("n_orth", C.c_int64), ("n_expm", C.c_int64),
-                ("n_combine", C.c_int64)]
+                ("n_combine", C.c_int64), ("bytes_other", C.c_double)]
 
 
 @dataclasses.dataclass(frozen=True)
@@ -128,6 +139,9 @@ def lib():
             "phipm_get_profile": (i32, [vp, P(_Profile)]),
             "phipm_reset_profile": (None, [vp]),
             "phipm_get_trace": (i32, [vp, P(_TraceRec), i32, P(i32)]),
+            "phipm_get_attempts": (i32, [vp, P(_Attempt), i32, P(i32)]),
+            "phipm_set_option": (i32, [vp, i32, i32]),
+            "phipm_get_option": (i32, [vp, i32, P(i32)]),
             "phipm_solve_csr": (i32, [vp, d, P(_Csr), i32, P(vp), P(_Opts), vp, P(_Stats)]),
             "phipm_solve_stencil": (i32, [vp, d, P(_Stencil), i32, P(vp), P(_Opts), vp, P(_Stats)]),
             "phipm_reserve_host_csr": (i32, [vp, i64]),
@@ -159,7 +173,8 @@ def lib():
 
 EXPORTED = [
     "phipm_default_opts", "phipm_set_expm_method", "phipm_mm_read", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
-    "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_solve_csr", "phipm_solve_stencil",
+    "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_get_attempts", "phipm_set_option",
+    "phipm_get_option", "phipm_solve_csr", "phipm_solve_stencil",
     "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_solve_csr_batch",
     "phipm_solve_stencil_batch", "phipm_stencil_nnz", "phipm_inf_norm_stencil",
     "phipm_csr_from_stencil", "phipm_spmv_csr", "phipm_spmv_stencil", "phipm_dot", "phipm_inf_norm_csr",
@@ -194,9 +209,14 @@ def _i32(t):
 
 
 class Context:
-    """phipm_ctx: workspace for problems with n <= n_max, m <= m_max, p <= p_max."""
+    """phipm_ctx: workspace for problems with n <= n_max, m <= m_max, p <= p_max.
 
-    def __init__(self, n_max: int, m_max: int = 100, p_max: int = 4, stream=None):
+    Every library call runs on the context's stream and is host-blocking: it returns with its work
+    complete, so results are ready on any stream.  Before each call the context's stream waits for
+    the caller's current stream, so inputs produced there (kernels, H2D copies) are complete before
+    the library reads them.  options: kernel-path selection, e.g. {"persist": 2} (OPTIONS)."""
+
+    def __init__(self, n_max: int, m_max: int = 100, p_max: int = 4, stream=None, options=None):
         torch = _torch()
         if not torch.cuda.is_available():
             raise RuntimeError("phipm needs a CUDA GPU (no CPU fallback)")
@@ -209,6 +229,36 @@ class Context:
             raise PhipmError(st, self._L.phipm_strerror(st).decode())
         self._h = h
         self.n_max, self.m_max, self.p_max = n_max, m_max, p_max
+        for k, v in (options or {}).items():
+            self.set_option(k, v)
+
+    def _order(self):
+        """ctx stream waits for the caller's current stream (inputs produced there are complete)."""
+        torch = _torch()
+        cur = torch.cuda.current_stream(self.stream.device)
+        if cur.cuda_stream != self.stream.cuda_stream:
+            self.stream.wait_stream(cur)
+
+    def set_option(self, name, value: int):
+        """Kernel-path option (phipm_set_option): name in OPTIONS or the PHIPM_OPT_* number."""
+        o = OPTIONS[name] if isinstance(name, str) else int(name)
+        self._check(self._L.phipm_set_option(self._h, o, int(value)))
+
+    def get_option(self, name) -> int:
+        o = OPTIONS[name] if isinstance(name, str) else int(name)
+        v = C.c_int()
+        self._check(self._L.phipm_get_option(self._h, o, C.byref(v)))
+        return v.value
+
+    def attempts(self):
+        """Controller trajectory of the last solve (phipm_get_attempts): list of dicts with
+        fields t_k, tau, m, mu, omega, eps, accepted, branch, normH1, beta (include/phipm.h)."""
+        cnt = C.c_int()
+        self._check(self._L.phipm_get_attempts(self._h, None, 0, C.byref(cnt)))
+        n = min(cnt.value, 65536)
+        buf = (_Attempt * max(n, 1))()
+        self._check(self._L.phipm_get_attempts(self._h, buf, n, C.byref(cnt)))
+        return [{k: getattr(r, k) for k, _ in _Attempt._fields_} for r in buf[:n]]
 
     def close(self):
         if getattr(self, "_h", None):
@@ -283,6 +333,7 @@ class Context:
         w = out if out is not None else torch.empty(n, dtype=torch.float64, device=u[0].device)
         s = _Stats()
         o = self.opts(**kw)
+        self._order()
         st = self._L.phipm_solve_csr(self._h, float(t), C.byref(self._csr(A)), len(u) - 1,
                                      self._uptrs(u), C.byref(o), _f64(w), C.byref(s))
         self._check(st)
@@ -293,6 +344,7 @@ class Context:
         w = out if out is not None else torch.empty(S.n, dtype=torch.float64, device=u[0].device)
         s = _Stats()
         o = self.opts(**kw)
+        self._order()
         st = self._L.phipm_solve_stencil(self._h, float(t), C.byref(S._c()), len(u) - 1, self._uptrs(u),
                                          C.byref(o), _f64(w), C.byref(s))
         self._check(st)
@@ -302,6 +354,7 @@ class Context:
         """HOST (numpy) operands; `out` a host float64 array (pinned memory copies fastest)."""
         s = _Stats()
         o = self.opts(**kw)
+        self._order()
         st = self._L.phipm_solve_csr_host(self._h, float(t), C.byref(self._csr(A, device=False)), len(u) - 1,
                                           self._uptrs(u, host=True), C.byref(o), C.c_void_p(out.ctypes.data),
                                           C.byref(s))
@@ -311,6 +364,7 @@ class Context:
     def solve_stencil_host(self, t: float, S: Stencil, u: Sequence, out, **kw):
         s = _Stats()
         o = self.opts(**kw)
+        self._order()
         st = self._L.phipm_solve_stencil_host(self._h, float(t), C.byref(S._c()), len(u) - 1,
                                               self._uptrs(u, host=True), C.byref(o),
                                               C.c_void_p(out.ctypes.data), C.byref(s))
@@ -331,28 +385,33 @@ class Context:
         rp = torch.empty(S.n + 1, dtype=torch.int32, device=dev)
         col = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)[:nnz]
         val = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)[:nnz]
+        self._order()
         self._check(self._L.phipm_csr_from_stencil(self._h, C.byref(S._c()), _i32(rp), _i32(col), _f64(val)))
         return rp, col, val
 
     def spmv_csr(self, A, x, y=None):
         torch = _torch()
         y = y if y is not None else torch.empty_like(x)
+        self._order()
         self._check(self._L.phipm_spmv_csr(self._h, C.byref(self._csr(A)), _f64(x), _f64(y)))
         return y
 
     def spmv_stencil(self, S: Stencil, x, y=None):
         torch = _torch()
         y = y if y is not None else torch.empty_like(x)
+        self._order()
         self._check(self._L.phipm_spmv_stencil(self._h, C.byref(S._c()), _f64(x), _f64(y)))
         return y
 
     def dot(self, x, y) -> float:
         r = C.c_double()
+        self._order()
         self._check(self._L.phipm_dot(self._h, x.numel(), _f64(x), _f64(y), C.byref(r)))
         return r.value
 
     def inf_norm_csr(self, A) -> float:
         r = C.c_double()
+        self._order()
         self._check(self._L.phipm_inf_norm_csr(self._h, C.byref(self._csr(A)), C.byref(r)))
         return r.value
 
@@ -362,6 +421,7 @@ class Context:
         K = A.shape[0]
         Acm = A.t().contiguous()                  # column-major for the library
         E = torch.empty_like(Acm)
+        self._order()
         self._check(self._L.phipm_expm(self._h, K, _f64(Acm), _f64(E)))
         return E.t().contiguous()
 
@@ -373,6 +433,7 @@ class Context:
         a = torch.empty(mu, dtype=torch.float64, device=H.device)
         b = torch.empty(mu, dtype=torch.float64, device=H.device)
         nh = C.c_double()
+        self._order()
         self._check(self._L.phipm_phi_pair(self._h, mu, _f64(Hcm), mu, float(tau), int(p), _f64(a), _f64(b),
                                            C.byref(nh)))
         return a, b, nh.value
@@ -391,9 +452,11 @@ class Context:
         k, brk, beta = C.c_int(), C.c_int(), C.c_double()
         o = self.opts(symmetric=symmetric, orth=orth)
         if isinstance(A, Stencil):
+            self._order()
             st = self._L.phipm_krylov_stencil(self._h, C.byref(A._c()), _f64(v), m, C.byref(o), Vp, Hp,
                                               C.byref(k), C.byref(brk), C.byref(beta))
         else:
+            self._order()
             st = self._L.phipm_krylov_csr(self._h, C.byref(self._csr(A)), _f64(v), m, C.byref(o), Vp, Hp,
                                           C.byref(k), C.byref(brk), C.byref(beta))
         self._check(st)
@@ -421,6 +484,8 @@ def solve_batch(ctxs: Sequence["Context"], t, ops, us: Sequence[Sequence], outs=
     outs = outs if outs is not None else [torch.empty(n[b], dtype=torch.float64, device=us[b][0].device)
                                           for b in range(nb)]
     o = ctxs[0].opts(**kw)
+    for c in ctxs:
+        c._order()
     hs = (C.c_void_p * nb)(*[c._h for c in ctxs])
     tt = (C.c_double * nb)(*[float(x) for x in ts])
     pp = (C.c_int * nb)(*[len(u) - 1 for u in us])
@@ -448,7 +513,8 @@ def inf_norm_stencil(S: "Stencil") -> float:
 
 def read_matrix_market(path: str):
     """Matrix Market file -> host CSR (row_ptr int32, col int32, val float64) numpy arrays, via
-    phipm_mm_read (columns ascending per row, duplicates summed, symmetric storage expanded)."""
+    phipm_mm_read (columns ascending per row, symmetric storage expanded; duplicate entries are
+    rejected with PhipmError)."""
     import numpy as np
     L = lib()
     n, nnz = C.c_int64(), C.c_int64()

@@ -30,6 +30,17 @@ struct AttemptResult {
     int seq;           // attempt sequence number (host sanity check)
 };
 
+// Publish an attempt result to the host (mapped pinned memory), one thread: the fields with
+// seq = -1, a system-scope fence, then the sequence number the host spins on (wait_attempt), so the
+// host never sees a new seq next to stale fields.  Every path of expm_kernel publishes through here.
+__device__ inline void publish_result(AttemptResult *dst, AttemptResult r, int seq)
+{
+    r.seq = -1;
+    *dst = r;
+    __threadfence_system();
+    *(volatile int *)&dst->seq = seq;
+}
+
 struct ExpmArgs {
     int mode;          // 0: phipm attempt; 1: plain expm of Ain; 2: phi pair of H (mu = m)
     int method;        // PHIPM_EXPM_TAYLOR (0) or PHIPM_EXPM_PADE13 (1)
@@ -525,8 +536,8 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
             a.comb[0] = 0.0;
             AttemptResult r;
             r.eps = 0.0; r.normH1 = 0.0; r.beta = beta; r.h = 0.0; r.mu = 0;
-            r.brk = a.st->brk; r.status = a.st->nonfinite ? 5 : 0; r.seq = a.seq;
-            *a.res = r;
+            r.brk = a.st->brk; r.status = a.st->nonfinite ? 5 : 0;
+            publish_result(a.res, r, a.seq);
         }
         return;
     }
@@ -595,8 +606,8 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
         }
         if (t == 0) {
             AttemptResult r{};
-            r.status = status; r.seq = a.seq;
-            *a.res = r;
+            r.status = status;
+            publish_result(a.res, r, a.seq);
         }
         return;
     }
@@ -609,8 +620,8 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
         }
         if (t == 0) {
             AttemptResult r{};
-            r.normH1 = normH1; r.status = status; r.mu = mu; r.seq = a.seq;
-            *a.res = r;
+            r.normH1 = normH1; r.status = status; r.mu = mu;
+            publish_result(a.res, r, a.seq);
         }
         return;
     }
@@ -644,12 +655,8 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
         r.mu = mu;
         r.brk = brk;
         r.status = a.st->aborted ? 3 : status ? status : ((s_fin && isfinite(eps) && isfinite(phl)) ? 0 : 5);
-        // publish to the host (mapped pinned memory): the fields, a system-scope fence, then the
-        // sequence number the host spins on, so it can act before the kernel has even retired
-        r.seq = -1;
-        *a.res = r;
-        __threadfence_system();
-        *(volatile int *)&a.res->seq = a.seq;
+        // published before the kernel retires: the host can act on it right away
+        publish_result(a.res, r, a.seq);
         if (a.clk) a.clk[6] = clock64();                 // (after the copy above: epilogue end)
     }
 }

@@ -335,6 +335,10 @@ struct MaxAbsArgs {
     int seq;
 };
 
+// max that propagates NaN (fmax drops it): once m is NaN it stays NaN, so a NaN input gives a NaN
+// ||.||_inf and the solve reports PHIPM_ENONFINITE instead of taking the all-zero shortcut
+__device__ __forceinline__ double nanmax(double m, double x) { return (x > m || x != x) ? x : m; }
+
 __global__ void __launch_bounds__(NT) maxabs_kernel(int64_t n, MaxAbsArgs a, Work wk)
 {
     __shared__ double wmax[MAXZ][NWARP];
@@ -352,16 +356,16 @@ __global__ void __launch_bounds__(NT) maxabs_kernel(int64_t n, MaxAbsArgs a, Wor
 #pragma unroll
             for (int u = 0; u < 8; u++) t[u] = __ldg(x + r + u * stride);
 #pragma unroll
-            for (int u = 0; u < 8; u++) m = fmax(m, fabs(t[u]));
+            for (int u = 0; u < 8; u++) m = nanmax(m, fabs(t[u]));
         }
-        for (; r < n; r += stride) m = fmax(m, fabs(x[r]));
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        for (; r < n; r += stride) m = nanmax(m, fabs(x[r]));
+        for (int o = 16; o > 0; o >>= 1) m = nanmax(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (lane == 0) wmax[v][warp] = m;
     }
     __syncthreads();
     if (tid < a.nv) {
         double m = 0.0;
-        for (int w = 0; w < NWARP; w++) m = fmax(m, wmax[tid][w]);
+        for (int w = 0; w < NWARP; w++) m = nanmax(m, wmax[tid][w]);
         bsum[tid] = m;
     }
     __syncthreads();
@@ -369,8 +373,8 @@ __global__ void __launch_bounds__(NT) maxabs_kernel(int64_t n, MaxAbsArgs a, Wor
     // publish_partials acquired the other CTAs' partials
     for (int v = warp; v < a.nv; v += NWARP) {
         double m = 0.0;
-        for (int b = lane; b < (int)gridDim.x; b += 32) m = fmax(m, __ldcg(wk.part + (size_t)v * wk.pstride + b));
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        for (int b = lane; b < (int)gridDim.x; b += 32) m = nanmax(m, __ldcg(wk.part + (size_t)v * wk.pstride + b));
+        for (int o = 16; o > 0; o >>= 1) m = nanmax(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (lane == 0) {
             if (a.pub) a.pub[v] = m;
             else wk.out_raw[v] = m;

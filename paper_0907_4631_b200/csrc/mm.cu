@@ -76,13 +76,10 @@ int mm_parse(const char *path, int64_t &n, std::vector<MMEntry> &ent)
     std::stable_sort(ent.begin(), ent.end(), [](const MMEntry &a, const MMEntry &b) {
         return a.r != b.r ? a.r < b.r : a.c < b.c;
     });
-    // merge duplicates (stable sort kept file order among equal (r, c))
-    size_t w = 0;
-    for (size_t k = 0; k < ent.size(); k++) {
-        if (w > 0 && ent[w - 1].r == ent[k].r && ent[w - 1].c == ent[k].c) ent[w - 1].v += ent[k].v;
-        else ent[w++] = ent[k];
-    }
-    ent.resize(w);
+    // duplicate (r, c) entries are rejected: a 'symmetric' file that stores both
+    // triangles would otherwise double its off-diagonal values silently
+    for (size_t k = 1; k < ent.size(); k++)
+        if (ent[k - 1].r == ent[k].r && ent[k - 1].c == ent[k].c) return PHIPM_EINVAL;
     if (ent.size() >= ((size_t)1 << 31)) return PHIPM_EINVAL;
     return PHIPM_OK;
 }

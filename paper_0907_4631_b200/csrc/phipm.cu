@@ -9,6 +9,10 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -94,12 +98,16 @@ struct phipm_ctx {
     bool trace = false;
     bool pdl = true;
     std::vector<phipm_trace_rec> tracebuf;
+    std::vector<phipm_attempt> attempts;     // controller trajectory of the last solve
+    int64_t nattempts = 0;
     int64_t ntrace = 0;
     std::vector<ProfRec> pending;
     std::vector<cudaEvent_t> pool;
     phipm_profile acc{};
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
+    // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0};
     char err[512] = {0};
 };
 
@@ -183,7 +191,7 @@ void prof_collect(phipm_ctx *c)
         case PC_ORTH: c->acc.ms_orth += ms; c->acc.bytes_orth += r.bytes; c->acc.n_orth++; break;
         case PC_EXPM: c->acc.ms_expm += ms; c->acc.n_expm++; break;
         case PC_COMBINE: c->acc.ms_combine += ms; c->acc.bytes_combine += r.bytes; c->acc.n_combine++; break;
-        default: c->acc.ms_other += ms; break;
+        default: c->acc.ms_other += ms; c->acc.bytes_other += r.bytes; break;
         }
         if (c->trace) {
             if (c->tracebuf.size() < 65536) c->tracebuf.push_back({r.cls, r.ncols, r.bytes, 1e3 * (double)ms});
@@ -203,21 +211,8 @@ int grid_for(phipm_ctx *c, int64_t units, int occ)
     return (int)g;
 }
 
-// Environment switches (measurement / A-B only; defaults are the measured best).  Callers cache the
-// value in a function-local static const, whose initialisation C++ makes thread-safe (batch solves
-// run on several host threads).
-int env_int(const char *name, int dflt)
-{
-    const char *e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
-
-// "on" unless the variable starts with '0'
-int env_on(const char *name)
-{
-    const char *e = getenv(name);
-    return (e && e[0] == '0') ? 0 : 1;
-}
+// kernel-path option of the context (phipm_set_option)
+inline int opt(const phipm_ctx *c, int o) { return c->opt[o]; }
 
 // ---------------------------------------------------------------------------------------------
 // launches
@@ -302,10 +297,10 @@ template <>
 int csr_wcap<CsrOp>(const CsrOp &A, int tile) { return A.wtile == tile ? A.wcap : 0; }
 
 // rows per thread: 8 (TILE 8 SNT) when every CTA gets at least half a tile, else 2;
-// PHIPM_RPT=2|4|8 overrides (tuning experiments)
+// PHIPM_OPT_RPT = 2|4|8 overrides (tuning experiments)
 int pick_rpt(phipm_ctx *c, int64_t n)
 {
-    static const int env = env_int("PHIPM_RPT", 0);
+    const int env = opt(c, PHIPM_OPT_RPT);
     if (env == 2 || env == 4 || env == 8) return env;
     return n >= (int64_t)SNT * 8 * c->sm_count * SMINB / 2 ? 8 : 2;
 }
@@ -454,8 +449,7 @@ int sync(phipm_ctx *c)
 // fall back to cudaStreamSynchronize.
 int wait_attempt(phipm_ctx *c)
 {
-    static const int env = env_on("PHIPM_SPIN");
-    if (c->prof || !env) return sync(c);
+    if (c->prof || !opt(c, PHIPM_OPT_SPIN)) return sync(c);
     const volatile int *seqp = &reinterpret_cast<volatile AttemptResult *>(c->res_h)->seq;
     const auto t0 = std::chrono::steady_clock::now();
     unsigned spins = 0;
@@ -664,9 +658,9 @@ bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, 
     const PersistFn kfn = persist_fn<RPT>(op, symmetric);
     int grid;
     int64_t rpc;
-    // CTAs: at most one per SM, and (PHIPM_PERSIST_MINROWS, default TILE/2) enough rows each that the
-    // threads are busy: small problems then also reduce fewer partials per phase
-    static const int env_rows = env_int("PHIPM_PERSIST_MINROWS", 0) ? std::max(32, env_int("PHIPM_PERSIST_MINROWS", 0)) : 0;
+    // CTAs: at most one per SM, and (PHIPM_OPT_PERSIST_MINROWS, default TILE/2) enough rows each that
+    // the threads are busy: small problems then also reduce fewer partials per phase
+    const int env_rows = opt(c, PHIPM_OPT_PERSIST_MINROWS) ? std::max(32, opt(c, PHIPM_OPT_PERSIST_MINROWS)) : 0;
     const int64_t minrows = env_rows ? env_rows : TILE_ / 2;
     const int slots = (int)std::max<int64_t>(1, std::min<int64_t>(c->sm_count, (op.n + minrows - 1) / minrows));
     balance(c, op.n, slots, grid, rpc);
@@ -725,11 +719,10 @@ PersistFn persist_tm_fn(const StencilOp &op)
 }
 
 // Lanczos with the CTA's y / v~_j in tensor memory and double-buffered halo tiles (persist_tm.cuh),
-// when every CTA's rows fit the 8 pair slots per thread (PHIPM_TMEM=0 disables)
+// when every CTA's rows fit the 8 pair slots per thread (PHIPM_OPT_TMEM = 0 disables)
 bool try_persist_tm(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bthr, double bytes, int &rc)
 {
-    static const int env = env_int("PHIPM_TMEM", 1);
-    if (!env) return false;
+    if (!opt(c, PHIPM_OPT_TMEM)) return false;
     constexpr int TILE_ = SNT * 4;
     int grid;
     int64_t rpc;
@@ -780,7 +773,7 @@ bool try_persist_tm(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bt
 }
 
 // The whole w-recurrence of a step in one cooperative kernel (persist_wrec.cuh) for stencil
-// operators with n > SMALL_N (PHIPM_WREC=0 disables).  Returns true if it launched (rc = status).
+// operators with n > SMALL_N (PHIPM_OPT_WREC = 0 disables).  Returns true if it launched (rc = status).
 template <class Op>
 bool launch_wrec_persist(phipm_ctx *, const Op &, const WrecArgs &, double, int &) { return false; }
 
@@ -799,8 +792,7 @@ WrecFn wrec_fn(const StencilOp &op)
 template <>
 bool launch_wrec_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, const WrecArgs &w, double bytes, int &rc)
 {
-    static const int env = env_int("PHIPM_WREC", 1);
-    if (!env || op.n <= SMALL_N || w.p < 1) return false;
+    if (!opt(c, PHIPM_OPT_WREC) || op.n <= SMALL_N || w.p < 1) return false;
     constexpr int TILE_ = SNT * 4;
     int grid;
     int64_t rpc;
@@ -842,10 +834,10 @@ template <>
 bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_op, bool symmetric, int k0, int k1,
                                double bthr, int &rc)
 {
-    // PHIPM_PERSIST: 0 off, 1 (default) auto, 2 always.  Auto: n <= 2^19, or a Lanczos extension of
+    // PHIPM_OPT_PERSIST: 0 off, 1 (default) auto, 2 always.  Auto: n <= 2^19, or a Lanczos extension of
     // any size; measured with the all-reduce phase end (profiles/round1): c2 +17 %, c4 +3.6 %, while
     // c3 (Arnoldi, n = 1M) is even with the two-kernel path, whose PDL overlap it loses
-    static const int env = env_int("PHIPM_PERSIST", 1);
+    const int env = opt(c, PHIPM_OPT_PERSIST);
     if (env == 0 || op.n <= SMALL_N) return false;
     if (env == 1 && op.n > ((int64_t)1 << 19) && !symmetric) return false;
     double bytes = 0.0;
@@ -877,8 +869,7 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
             bytes += bytes_op + 8.0 * (double)n * (symmetric ? 4.0 : 2.0 * j + 3.0);
         ProfRec r;
         prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
-        static const int env_slz = env_on("PHIPM_SMALL_LZ");
-        if (symmetric && n <= SLZ_NT * SLZ_R && env_slz)
+        if (symmetric && n <= SLZ_NT * SLZ_R && opt(c, PHIPM_OPT_SMALL_LZ))
             launch_k(c, krylov_small_lanczos_kernel<Op>, 1, SLZ_NT, (size_t)n * sizeof(double), op, sa, make_work(c));
         else
             launch_k(c, krylov_small_kernel<Op>, 1, SMALL_NT, (size_t)n * sizeof(double), op, sa, make_work(c));
@@ -891,11 +882,11 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
         int rc = PHIPM_OK;
         if (launch_persist(c, op, bytes_op, symmetric, k0, k1, bthr, rc)) return rc;
     }
-    // Arnoldi (CGS): lagged normalisation (PHIPM_LAG=0 disables).  Step j > k0's SpMV works on the raw
+    // Arnoldi (CGS): lagged normalisation (PHIPM_OPT_LAG = 0 disables).  Step j > k0's SpMV works on the raw
     // v~_j and also reduces ||v~_j||^2 (free: the x tile is on chip), its finalize derives sigma_j and
     // h_{j,j-1}; so the update passes need no grid reduction except the extension's last one, which
     // provides h_{k1,k1-1} and sigma_{k1} for the exponential.
-    static const int env_lag = env_on("PHIPM_LAG");
+    const int env_lag = opt(c, PHIPM_OPT_LAG);
     // (stencils only: a CSR SpMV would have to re-read its own x rows for the norm; c5 measured even)
     const bool lag = env_lag && !symmetric && orth == PHIPM_ORTH_CGS && std::is_same<Op, StencilOp>::value;
     for (int j = k0; j < k1; j++) {
@@ -995,6 +986,8 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     const int64_t n = op.n;
     phipm_stats S{};
     S.t_reached = 0.0;
+    c->attempts.clear();
+    c->nattempts = 0;
     auto finish = [&](int rc) {
         if (stats) *stats = S;
         return rc;
@@ -1244,6 +1237,9 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             if (!std::isfinite(omega)) return finish(set_err(c, PHIPM_ENONFINITE, "non-finite error estimate"));
             const bool accepted = omega <= 1.2;
             Decision d = control(P, mem, tau, m, eps, omega, R.normH1, t_end - tk, accepted);
+            if (c->attempts.size() < 65536)
+                c->attempts.push_back({tk, tau, omega, eps, R.normH1, R.beta, m, mu, accepted ? 1 : 0, d.branch});
+            c->nattempts++;
             tau_used = tau;
             m_used = m;
             S.m_peak = std::max(S.m_peak, m);
@@ -1395,13 +1391,13 @@ int make_csr(phipm_ctx *c, const phipm_csr *A, CsrOp &op)
 constexpr int CSR_WCAP = 10496;                             // 82 KB: band +-4096 around 2048 rows
 
 // One analysis pass over a CSR matrix (csr_analyze_kernel): ||A||_inf (a1 setup, bit-exact), and
-// whether rows have a uniform length L (vectorised ELL path, PHIPM_CSR_ELL=0 disables) within a band
-// that fits the shared x ring (PHIPM_CSR_RING=0 disables).
+// whether rows have a uniform length L (vectorised ELL path, PHIPM_OPT_CSR_ELL = 0 disables) within a
+// band that fits the shared x ring (PHIPM_OPT_CSR_RING = 0 disables).
 int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA)
 {
     op.ell = 0;
     op.ring = op.blo = op.bhi = 0;
-    static const int env_ell = env_on("PHIPM_CSR_ELL"), env_ring = env_on("PHIPM_CSR_RING");
+    const int env_ell = opt(c, PHIPM_OPT_CSR_ELL), env_ring = opt(c, PHIPM_OPT_CSR_RING);
     if (op.n == 0) {
         *normA = 0.0;
         return PHIPM_OK;
@@ -1433,8 +1429,7 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA)
 
 int enable_csr_window(phipm_ctx *c, CsrOp &op)
 {
-    static const int env = env_int("PHIPM_CSR_WINDOW", 0) == 1;
-    if (!env || op.ring) return PHIPM_OK;                  // default off (measured slower, round 1)
+    if (opt(c, PHIPM_OPT_CSR_WINDOW) != 1 || op.ring) return PHIPM_OK;                  // default off (measured slower, round 1)
     const int tile = SNT * 8;
     const int64_t ntiles = (op.n + tile - 1) / tile;
     if (ntiles > c->ntile_cap || op.n < (int64_t)tile) return PHIPM_OK;   // small problems: global gathers
@@ -1485,7 +1480,60 @@ phipm_opts resolve_opts(const phipm_opts *o)
 
 } // namespace
 
-// Run nb solves concurrently, one native thread each (phipm_solve_*_batch).
+// Persistent worker pool of the batch API (phipm_solve_*_batch): threads are created once and grow
+// to the largest batch seen, so a batch call costs a queue push per problem, not a thread start.
+// The pool is never destroyed (its idle threads wait on a condition variable until process exit).
+class WorkerPool {
+public:
+    static WorkerPool &get()
+    {
+        static WorkerPool *p = new WorkerPool();
+        return *p;
+    }
+    // run fn(0..nb-1) on pool threads and wait for all of them
+    template <class F>
+    void run(int nb, F &fn)
+    {
+        std::mutex dmu;
+        std::condition_variable dcv;
+        int left = nb;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            while ((int)th_.size() < nb) th_.emplace_back([this] { loop(); });
+            for (int b = 0; b < nb; b++)
+                q_.push_back([&, b] {
+                    fn(b);
+                    std::lock_guard<std::mutex> l2(dmu);
+                    if (--left == 0) dcv.notify_one();
+                });
+        }
+        cv_.notify_all();
+        std::unique_lock<std::mutex> lk(dmu);
+        dcv.wait(lk, [&] { return left == 0; });
+    }
+
+private:
+    void loop()
+    {
+        for (;;) {
+            std::function<void()> job;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [this] { return !q_.empty(); });
+                job = std::move(q_.front());
+                q_.pop_front();
+            }
+            job();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    std::vector<std::thread> th_;
+};
+
+// Run nb solves concurrently on the worker pool (phipm_solve_*_batch).  Each worker first makes the
+// context's device current: pool threads start on device 0, and a context may live on another GPU.
 template <class F>
 static int run_batch(phipm_ctx *const *ctx, int nb, int *status, F solve_one)
 {
@@ -1494,11 +1542,15 @@ static int run_batch(phipm_ctx *const *ctx, int nb, int *status, F solve_one)
     for (int b = 0; b < nb; b++)
         for (int b2 = 0; b2 < b; b2++)
             if (!ctx[b] || ctx[b] == ctx[b2]) return PHIPM_EINVAL;   // one context per problem
+    if (!ctx[0]) return PHIPM_EINVAL;
     std::vector<int> st((size_t)nb, PHIPM_OK);
-    std::vector<std::thread> th;
-    th.reserve((size_t)nb);
-    for (int b = 0; b < nb; b++) th.emplace_back([&, b] { st[b] = solve_one(b); });
-    for (auto &x : th) x.join();
+    auto job = [&](int b) {
+        const cudaError_t e = cudaSetDevice(ctx[b]->dev);
+        st[b] = (e == cudaSuccess) ? solve_one(b)
+                                   : set_err(ctx[b], PHIPM_ECUDA, "cudaSetDevice(%d): %s", ctx[b]->dev,
+                                             cudaGetErrorString(e));
+    };
+    WorkerPool::get().run(nb, job);
     int rc = PHIPM_OK;
     for (int b = 0; b < nb; b++) {
         if (status) status[b] = st[b];
@@ -1511,6 +1563,29 @@ static int run_batch(phipm_ctx *const *ctx, int nb, int *status, F solve_one)
 // C ABI
 
 extern "C" {
+
+int phipm_set_option(phipm_ctx *c, int option, int value)
+{
+    if (!c || option < 0 || option >= PHIPM_OPT_COUNT) return PHIPM_EINVAL;
+    bool ok;
+    switch (option) {
+    case PHIPM_OPT_PERSIST: ok = value >= 0 && value <= 2; break;
+    case PHIPM_OPT_RPT: ok = value == 0 || value == 2 || value == 4 || value == 8; break;
+    case PHIPM_OPT_PERSIST_MINROWS: ok = value >= 0; break;
+    default: ok = value == 0 || value == 1; break;
+    }
+    if (!ok) return set_err(c, PHIPM_EINVAL, "option %d: value %d out of range", option, value);
+    c->opt[option] = value;
+    if (option == PHIPM_OPT_PDL) c->pdl = value != 0;
+    return PHIPM_OK;
+}
+
+int phipm_get_option(const phipm_ctx *c, int option, int *value)
+{
+    if (!c || !value || option < 0 || option >= PHIPM_OPT_COUNT) return PHIPM_EINVAL;
+    *value = c->opt[option];
+    return PHIPM_OK;
+}
 
 int phipm_set_expm_method(phipm_ctx *c, int method)
 {
@@ -1570,6 +1645,15 @@ int phipm_get_trace(const phipm_ctx *c, phipm_trace_rec *out, int max, int *coun
     const int nrec = (int)std::min<size_t>(c->tracebuf.size(), (size_t)std::max(max, 0));
     for (int i = 0; i < nrec; i++) out[i] = c->tracebuf[i];
     *count = (int)c->ntrace;
+    return PHIPM_OK;
+}
+
+int phipm_get_attempts(const phipm_ctx *c, phipm_attempt *out, int max, int *count)
+{
+    if (!c || !count || (max > 0 && !out)) return PHIPM_EINVAL;
+    const int nrec = (int)std::min<size_t>(c->attempts.size(), (size_t)std::max(max, 0));
+    for (int i = 0; i < nrec; i++) out[i] = c->attempts[i];
+    *count = (int)c->nattempts;
     return PHIPM_OK;
 }
 
@@ -1640,10 +1724,6 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     c->p_max = p_max;
     c->ldv = (n_max + 31) / 32 * 32;
     c->kmax = m_max + p_max + 1;
-    {
-        const char *e = getenv("PHIPM_PDL");
-        c->pdl = !(e && e[0] == '0');
-    }
     cudaError_t e = cudaGetDevice(&c->dev);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, c->dev);
     if (e != cudaSuccess) {

@@ -227,36 +227,20 @@ def test_profile_counts(ctx):
     assert prof["ms_spmv_dot"] > 0 and prof["bytes_spmv_dot"] > 0
 
 
-PERSIST_SCRIPT = r"""
-import sys, numpy as np
-sys.path.insert(0, "tests"); sys.path.insert(0, ".")
-import workloads as W, oracle
-import paper_0907_4631_b200 as P
-from gpu_common import to_dev, stencil_of, parity_bound, relerr
-name = sys.argv[1]
-Pb = W.make(name)
-ctx = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1))
-w, s = ctx.solve_stencil(Pb.t, stencil_of(Pb), [to_dev(x) for x in Pb.u], tol=Pb.tol, symmetric=Pb.symmetric,
-                         m_init=Pb.m_init)
-wo, so, _ = oracle.solve(Pb)
-e = relerr(w.cpu().numpy(), wo)
-print("RELERR", e, "BOUND", parity_bound(Pb.tol), s)
-sys.exit(0 if e <= parity_bound(Pb.tol) and s.t_reached == Pb.t else 1)
-"""
-
-
 @pytest.mark.parametrize("name", ["c3", "c4", "c2_med"])
-def test_persistent_kernel_forced(name):
-    # PHIPM_PERSIST=2 forces the cooperative whole-extension kernel (several tiles per CTA at full
-    # size); the environment is read once per process, hence the subprocess
-    import os
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, PHIPM_PERSIST="2")
-    r = subprocess.run([sys.executable, "-c", PERSIST_SCRIPT, name], cwd=root, env=env, capture_output=True,
-                       text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+def test_persistent_kernel_forced(orc, name):
+    # option persist = 2 forces the cooperative whole-extension kernel (several tiles per CTA at full
+    # size), also for the Arnoldi extension of c3 (n = 1M) that defaults to the two-kernel path
+    import paper_0907_4631_b200 as P
+    Pb = W.make(name)
+    c = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), options={"persist": 2})
+    assert c.get_option("persist") == 2
+    w, s = c.solve_stencil(Pb.t, stencil_of(Pb), [to_dev(x) for x in Pb.u], tol=Pb.tol,
+                           symmetric=Pb.symmetric, m_init=Pb.m_init)
+    wo, so = run_oracle(orc, Pb)
+    assert s.t_reached == Pb.t
+    assert relerr(w.cpu().numpy(), wo) <= parity_bound(Pb.tol), (s, so)
+    c.close()
 
 
 def test_batch_matches_single_solves():
@@ -315,4 +299,61 @@ def test_stencil_arnoldi_early_breakdown(ctx, orc, modes):
         # three modes: rounding leaves h_{3,2} ~ 6e-6 > n eps ||A||_inf ~ 1.8e-7 (R22), so neither side
         # breaks down; both must still build the same number of vectors
         assert sg.nspmv == so["nspmv"]
+    assert relerr(wg, wo) <= parity_bound(Pb.tol)
+
+
+# ------------------------------------------------------------------------------------------------
+# controller trajectory (Alg. 3/4) against the oracle's, attempt by attempt
+
+
+def _traj_compare(ga, tr):
+    """Index of the first attempt whose decision differs, or len; asserts everything before it
+    (and the decision inputs at it) agree."""
+    for i, (g, o) in enumerate(zip(ga, tr)):
+        t_k, tau, m, mu, omega, eps, acc, br, nh, beta = o
+        assert g["m"] == int(m) and g["mu"] == int(mu), (i, g, o)
+        assert g["tau"] == pytest.approx(tau, rel=1e-9), (i, g, o)
+        assert g["t_k"] == pytest.approx(t_k, rel=1e-12, abs=1e-300), (i, g, o)
+        assert g["beta"] == pytest.approx(beta, rel=1e-10), (i, g, o)
+        assert g["normH1"] == pytest.approx(nh, rel=1e-9), (i, g, o)
+        # eps is the corrector term |h phi_{p+1}[mu]|: relative agreement only where it is well above
+        # the rounding of the small exponential (omega >= 1e-6)
+        if omega >= 1e-6:
+            assert g["omega"] == pytest.approx(omega, rel=1e-6), (i, g, o)
+        if g["accepted"] != int(acc) or g["branch"] != int(br):
+            return i
+    return min(len(ga), len(tr))
+
+
+@pytest.mark.parametrize("name,path", [("c2", "stencil"), ("c2", "csr"), ("c3", "stencil"), ("c4", "stencil"),
+                                       ("c5", "csr"), ("c3_med", "stencil"), ("c5_med", "csr")])
+def test_controller_trajectory_matches_oracle(ctx, orc, name, path):
+    """GPU stats == oracle stats and the same attempt sequence (tau, m, mu, accept, branch), omega to
+    1e-6: the host controller (phipm.cu control()) and the oracle's (orc_control) make every decision
+    alike on inputs that agree to rounding.  Only an oracle attempt with omega within 1e-6 of delta
+    may legitimately flip (none does on these configs)."""
+    Pb = W.make(name)
+    wg, sg = run_gpu(ctx, Pb, path)
+    ga = ctx.attempts()
+    wo, so, tr = orc.solve(Pb)
+    near = np.abs(tr[:, 4] - 1.2) / 1.2 < 1e-6
+    if near.any():
+        pytest.skip(f"oracle attempt {int(np.argmax(near))} has omega within 1e-6 of delta")
+    assert len(ga) == len(tr) == sg.nexpm, (sg, so)
+    assert _traj_compare(ga, tr) == len(tr)
+    assert (sg.nsteps, sg.nreject, sg.nspmv, sg.nexpm, sg.m_last, sg.m_peak) == \
+        (so["nsteps"], so["nreject"], so["nspmv"], so["nexpm"], so["m_last"], so["m_peak"])
+
+
+def test_controller_trajectory_c1(ctx, orc):
+    """c1 (t||A|| = 4008, 15 steps): the trajectories agree attempt by attempt until the first
+    decision that differs; there both controllers saw the same tau, m and omega to rounding (so the
+    decision sat on a threshold: omega vs delta, a ceil in Eq. 3, or the Eq. 5 cost comparison)."""
+    Pb = W.make("c1")
+    wg, sg = run_gpu(ctx, Pb, "stencil")
+    ga = ctx.attempts()
+    wo, so, tr = orc.solve(Pb)
+    i = _traj_compare(ga, tr)
+    print(f"c1: trajectories agree for {i} of {len(tr)} oracle attempts; gpu {sg} oracle {so}")
+    assert i >= 1
     assert relerr(wg, wo) <= parity_bound(Pb.tol)

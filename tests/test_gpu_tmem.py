@@ -9,10 +9,6 @@ t large enough that attempts are rejected and m grows, so the kernel is relaunch
 (its first step then reads v~_{j-1} from global memory, the later ones from TMEM slot B).
 Bar: ||w_gpu - w_ref|| / ||w_ref|| <= max(10 tol, 1e-12) (BASELINE.json north_star).
 """
-import os
-import subprocess
-import sys
-
 import numpy as np
 import pytest
 
@@ -79,35 +75,21 @@ def test_tmem_lanczos_9pt(ctx, orc):
     assert relerr(w.cpu().numpy(), wo) <= parity_bound(tol), (s, so)
 
 
-TM_OFF_SCRIPT = r"""
-import sys
-import numpy as np, torch
-sys.path.insert(0, "tests")
-import paper_0907_4631_b200 as P, workloads as W
-Pb = W.make("c4")
-ctx = P.Context(n_max=Pb.n, m_max=100, p_max=4)
-w, s = ctx.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), [torch.from_numpy(x).cuda() for x in Pb.u],
-                         tol=Pb.tol, symmetric=True)
-np.save(sys.argv[1], w.cpu().numpy())
-print(s)
-"""
-
-
-@pytest.mark.parametrize("var", ["PHIPM_TMEM", "PHIPM_WREC"])
-def test_persistent_variants_agree(tmp_path, var):
-    # c4 with the default kernels and with one persistent variant switched off:
-    #   PHIPM_TMEM=0: the Lanczos kernel keeps y in shared memory instead of tensor memory;
-    #   PHIPM_WREC=0: the w-recurrence runs as p streaming launches instead of one cooperative kernel.
+@pytest.mark.parametrize("var", ["tmem", "wrec"])
+def test_persistent_variants_agree(var):
+    # c4 with the default kernels and with one persistent variant switched off (context option):
+    #   tmem = 0: the Lanczos kernel keeps y in shared memory instead of tensor memory;
+    #   wrec = 0: the w-recurrence runs as p streaming launches instead of one cooperative kernel.
     # Each pair differs only in the order some sums are reduced, so w agrees far below the parity bar
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    Pb = W.make("c4")
+    u = [to_dev(x) for x in Pb.u]
     out = {}
-    for flag in ("1", "0"):
-        f = os.path.join(tmp_path, f"w{flag}.npy")
-        r = subprocess.run([sys.executable, "-c", TM_OFF_SCRIPT, f], cwd=root, capture_output=True, text=True,
-                           env=dict(os.environ, **{var: flag}), timeout=600)
-        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-        out[flag] = np.load(f)
-    assert relerr(out["1"], out["0"]) <= 1e-12
+    for flag in (1, 0):
+        c = P.Context(n_max=Pb.n, m_max=100, p_max=4, options={var: flag})
+        w, s = c.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), u, tol=Pb.tol, symmetric=True)
+        out[flag] = w.cpu().numpy()
+        c.close()
+    assert relerr(out[1], out[0]) <= 1e-12
 
 
 @pytest.mark.parametrize("p", [0, 1, 2, 3, 4, 5, 6])

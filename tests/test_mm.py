@@ -52,10 +52,10 @@ def test_symmetric_storage_expanded(tmp_path, kind):
     assert np.array_equal(D, A.toarray())
 
 
-def test_pattern_integer_duplicates_comments(tmp_path):
+def test_pattern_integer_comments(tmp_path):
     p = os.path.join(tmp_path, "b.mtx")
     open(p, "w").write("%%MatrixMarket matrix coordinate integer general\n% a comment\n\n"
-                       "3 3 5\n1 1 2\n3 2 -1\n1 1 5\n% mid comment\n2 3 4\n1 3 1\n")
+                       "3 3 4\n1 1 7\n3 2 -1\n% mid comment\n2 3 4\n1 3 1\n")
     rp, col, val = P.read_matrix_market(p)
     assert rp.tolist() == [0, 2, 3, 4] and col.tolist() == [0, 2, 2, 1] and val.tolist() == [7.0, 1.0, 4.0, -1.0]
     q = os.path.join(tmp_path, "c.mtx")
@@ -71,6 +71,8 @@ def test_pattern_integer_duplicates_comments(tmp_path):
     "%%MatrixMarket matrix coordinate complex general\n2 2 1\n1 1 1 0\n",    # complex
     "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n",         # truncated
     "not a matrix market file\n",
+    "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n1 1 5\n",  # duplicate
+    "%%MatrixMarket matrix coordinate real symmetric\n2 2 3\n1 1 1\n2 1 2\n1 2 2\n",  # both triangles
 ])
 def test_rejects_malformed(tmp_path, text):
     p = os.path.join(tmp_path, "bad.mtx")

@@ -98,6 +98,12 @@ class Stencil:
         return _Stencil(self.dim, self.nx, self.ny, self.nz, *[float(x) for x in self.coeffs],
                         *[float(x) for x in self.corners], int(self.points))
 
+    def negated(self) -> "Stencil":
+        """-A: the ABI takes t >= 0 only; e^{-tA} is solved as e^{t(-A)} with u_k -> (-1)^k u_k
+        (include/phipm.h, phipm_solve_*)."""
+        return dataclasses.replace(self, coeffs=tuple(-float(x) for x in self.coeffs),
+                                   corners=tuple(-float(x) for x in self.corners))
+
     @classmethod
     def of(cls, s) -> "Stencil":
         return cls(s.dim, s.nx, s.ny, s.nz, tuple(s.coeffs))

@@ -10,6 +10,7 @@ import pytest
 import paper_0907_4631_b200 as P
 import workloads as W
 from gpu_common import parity_bound, relerr, to_dev
+from ninept import csr_9pt as _csr_9pt, gr9_coeffs, ROUNDTRIP
 
 pytestmark = pytest.mark.gpu
 
@@ -19,22 +20,7 @@ CORN = (0.0625, 0.375, 0.75, 1.25)
 
 
 def csr_9pt(nx, ny, coef=COEF, corn=CORN):
-    """Reference CSR of the 9-point stencil, entries of a row in ascending column order."""
-    c0, cxm, cxp, cym, cyp = coef[:5]
-    cmm, cpm, cmp, cpp = corn
-    w = {(-1, -1): cmm, (0, -1): cym, (1, -1): cpm, (-1, 0): cxm, (0, 0): c0, (1, 0): cxp,
-         (-1, 1): cmp, (0, 1): cyp, (1, 1): cpp}
-    rp, col, val = [0], [], []
-    for j in range(ny):
-        for i in range(nx):
-            for dy in (-1, 0, 1):
-                for dx in (-1, 0, 1):
-                    ii, jj = i + dx, j + dy
-                    if 0 <= ii < nx and 0 <= jj < ny:
-                        col.append(ii + nx * jj)
-                        val.append(w[(dx, dy)])
-            rp.append(len(col))
-    return np.array(rp, np.int32), np.array(col, np.int32), np.array(val, np.float64)
+    return _csr_9pt(nx, ny, coef, corn)
 
 
 def stencil(nx, ny, coef=COEF, corn=CORN):
@@ -109,3 +95,37 @@ def test_matrix_market_roundtrip_solve(ctx, orc, tmp_path):
     w, s = ctx.solve_csr(Pb.t, tuple(to_dev(a) for a in A), [to_dev(x) for x in Pb.u], tol=Pb.tol)
     wo, so, _ = orc.solve(Pb)
     assert relerr(w.cpu().numpy(), wo) <= parity_bound(Pb.tol)
+
+
+@pytest.mark.parametrize("path", ["stencil", "csr"])
+def test_roundtrip_gr30(ctx, orc, path):
+    """NEXT-4, the paper's round trip: w = e^{tA} b0, then e^{-tA} w, b0 = ones, t = 2,
+    Tol = 1e-14, on the gr_30_30-class 9-point operator (tests/ninept.py, reading R41).  The backward
+    leg uses the ABI's negation rule (t >= 0 only: e^{-tA} = e^{t(-A)}, Stencil.negated()).
+    Each GPU leg is held to the BASELINE bar against the oracle's leg on the same input; the round
+    trip itself is compared with b0, the exact answer, and reported beside the paper's 3.9e-6."""
+    nx, ny, t, tol = ROUNDTRIP["nx"], ROUNDTRIP["ny"], ROUNDTRIP["t"], ROUNDTRIP["tol"]
+    coef, corn = gr9_coeffs(-1.0)
+    S = P.Stencil(2, nx, ny, 1, coef, corn, 9)
+    fwd = csr_9pt(nx, ny, coef, corn)
+    bwd = csr_9pt(nx, ny, *gr9_coeffs(+1.0))
+    n = nx * ny
+    b0 = np.ones(n)
+    if path == "stencil":
+        run = lambda op, x: ctx.solve_stencil(t, op, [to_dev(x)], tol=tol, symmetric=True)
+        ops = (S, S.negated())
+    else:
+        run = lambda op, x: ctx.solve_csr(t, op, [to_dev(x)], tol=tol, symmetric=True)
+        ops = tuple(tuple(to_dev(a) for a in c) for c in (fwd, bwd))
+    wg, sf = run(ops[0], b0)
+    wg = wg.cpu().numpy()
+    wo, so, _ = orc.phipm(t, fwd, [b0], tol, symmetric=True)
+    assert relerr(wg, wo) <= parity_bound(tol), (sf, so)
+    bg, sb = run(ops[1], wg)
+    bg = bg.cpu().numpy()
+    bo, so2, _ = orc.phipm(t, bwd, [wg], tol, symmetric=True)       # same input as the GPU leg
+    assert relerr(bg, bo) <= parity_bound(tol), (sb, so2)
+    err = relerr(bg, b0)
+    print(f"gr30 round trip ({path}): GPU relerr vs b0 {err:.2e} (paper phipm {ROUNDTRIP['paper_phipm_error']:.1e}); "
+          f"fwd {sf} bwd {sb}")
+    assert err <= 1e-12

@@ -76,6 +76,14 @@ typedef struct {
                                 fp64 tensor cores, squarings from ||A^k||^(1/k) (the default) */
 #define PHIPM_EXPM_PADE13  1 /* the paper's [13/13] Pade, theta_13 = 5.37, with a pivoted
                                 Gauss-Jordan solve (V - U) X = (V + U) */
+#define PHIPM_EXPM_CHEBYSHEV 2 /* symmetric H only (Lanczos; "compute the phi-
+                                function of H_m directly ... exploit the fact that H_m is symmetric"):
+                                phi_p(tau T)e1 and phi_{p+1}(tau T)e1 by one Chebyshev expansion on the
+                                Gershgorin interval of tau T, no augmented matrix.
+                                Arnoldi solves with this method use TAYLOR; an interval too wide for
+                                512 Chebyshev points (9.5 sqrt(r) + 24 > 512, r the half-width) falls
+                                back to TAYLOR for that attempt.  phipm_phi_pair reads the lower
+                                band of H and assumes H symmetric tridiagonal. */
 
 /* Options.  Defaults (phipm_default_opts): tol 1e-7, m_init 10 (Alg. 3),
  * m_max 100, symmetric 0, fixed_m 0, eq6_variant 0, orth CGS, profile 0, expm_method Taylor. */

@@ -22,7 +22,7 @@ __all__ = ["Context", "Stencil", "Stats", "Profile", "PhipmError", "lib", "LIB",
 
 OK, EINVAL, ENOMEM, ECUDA, ESTEP, ENONFINITE, ESINGULAR = 0, 1, 2, 3, 4, 5, 6
 ORTH_CGS, ORTH_CGS2 = 0, 1
-EXPM_TAYLOR, EXPM_PADE13 = 0, 1
+EXPM_TAYLOR, EXPM_PADE13, EXPM_CHEBYSHEV = 0, 1, 2
 
 
 class PhipmError(RuntimeError):

@@ -30,6 +30,7 @@
 #include "persist.cuh"
 #include "persist_tm.cuh"
 #include "persist_wrec.cuh"
+#include "phicheb.cuh"
 
 using namespace phipm;
 
@@ -100,6 +101,7 @@ struct phipm_ctx {
     std::vector<phipm_trace_rec> tracebuf;
     std::vector<phipm_attempt> attempts;     // controller trajectory of the last solve
     int64_t nattempts = 0;
+    int64_t ncheb_fallback = 0;              // attempts whose Chebyshev interval was too wide
     int64_t ntrace = 0;
     std::vector<ProfRec> pending;
     std::vector<cudaEvent_t> pool;
@@ -422,7 +424,9 @@ int launch_expm(phipm_ctx *c, ExpmArgs &a, int K)
     a.clk = c->expm_clk_d;
     ProfRec r;
     prof_begin(c, r, PC_EXPM, 0.0, K);
-    if (a.method == PHIPM_EXPM_PADE13) {
+    if (a.method == PHIPM_EXPM_CHEBYSHEV && a.tridiag && a.mode != 1) {
+        launch_k(c, phi_cheb_kernel, 1, CHEB_NT, 0, a);
+    } else if (a.method == PHIPM_EXPM_PADE13) {
         if (a.use_smem) launch_k(c, expm_kernel<true, true>, 1, EXPM_NT, need, a);
         else launch_k(c, expm_kernel<false, true>, 1, EXPM_NT, 0, a);
     } else {
@@ -1199,7 +1203,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             memset(&ea, 0, sizeof(ea));
             ea.mode = 0;
             ea.method = o.expm_method;
-            ea.tridiag = P.symmetric ? 1 : 0;
+            ea.tridiag = P.symmetric ? 1 : 0;     // (Chebyshev method: Lanczos only)
             ea.m = m;
             ea.p = p;
             ea.tau = tau;
@@ -1214,8 +1218,19 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             rc = wait_attempt(c);
             if (rc) return finish(rc);
             AttemptResult R;
-    memcpy(&R, (const void *)c->res_h, sizeof(R));
+            memcpy(&R, (const void *)c->res_h, sizeof(R));
             if (R.seq != c->seq) return finish(set_err(c, PHIPM_ECUDA, "stale attempt result"));
+            if (R.status == CHEB_STATUS_RANGE) {
+                // Chebyshev interval too wide: this attempt takes the augmented exponential
+                ea.method = PHIPM_EXPM_TAYLOR;
+                rc = launch_expm(c, ea, m + p + 1);
+                if (rc) return finish(rc);
+                rc = wait_attempt(c);
+                if (rc) return finish(rc);
+                memcpy(&R, (const void *)c->res_h, sizeof(R));
+                if (R.seq != c->seq) return finish(set_err(c, PHIPM_ECUDA, "stale attempt result"));
+                c->ncheb_fallback++;
+            }
             S.nexpm++;
             // basis actually built
             int kb;
@@ -1464,7 +1479,8 @@ int check_common(phipm_ctx *c, double t, int64_t n, int p, const double *const *
     if (!(o.tol > 0.0)) return set_err(c, PHIPM_EINVAL, "tol must be > 0");
     if (o.m_max > c->m_max) return set_err(c, PHIPM_EINVAL, "opts.m_max %d > context m_max %d", o.m_max, c->m_max);
     if (o.m_init < 1 || o.m_init > o.m_max) return set_err(c, PHIPM_EINVAL, "m_init must be in [1, m_max]");
-    if (o.expm_method != PHIPM_EXPM_TAYLOR && o.expm_method != PHIPM_EXPM_PADE13)
+    if (o.expm_method != PHIPM_EXPM_TAYLOR && o.expm_method != PHIPM_EXPM_PADE13 &&
+        o.expm_method != PHIPM_EXPM_CHEBYSHEV)
         return set_err(c, PHIPM_EINVAL, "unknown expm_method %d", o.expm_method);
     if (o.orth != PHIPM_ORTH_CGS && o.orth != PHIPM_ORTH_CGS2) return set_err(c, PHIPM_EINVAL, "bad orth");
     return PHIPM_OK;
@@ -1589,7 +1605,8 @@ int phipm_get_option(const phipm_ctx *c, int option, int *value)
 
 int phipm_set_expm_method(phipm_ctx *c, int method)
 {
-    if (!c || (method != PHIPM_EXPM_TAYLOR && method != PHIPM_EXPM_PADE13)) return PHIPM_EINVAL;
+    if (!c || (method != PHIPM_EXPM_TAYLOR && method != PHIPM_EXPM_PADE13 && method != PHIPM_EXPM_CHEBYSHEV))
+        return PHIPM_EINVAL;
     c->expm_method = method;
     return PHIPM_OK;
 }
@@ -2103,6 +2120,7 @@ int phipm_phi_pair(phipm_ctx *c, int mu, const double *H, int ldh, double tau, i
     memset(&a, 0, sizeof(a));
     a.mode = 2;
     a.method = c->expm_method;
+    a.tridiag = c->expm_method == PHIPM_EXPM_CHEBYSHEV ? 1 : 0;   // the Chebyshev method reads the band
     a.m = mu;
     a.p = p;
     a.tau = tau;
@@ -2114,6 +2132,14 @@ int phipm_phi_pair(phipm_ctx *c, int mu, const double *H, int ldh, double tau, i
     if (rc) return rc;
     rc = sync(c);
     if (rc) return rc;
+    if (((const volatile AttemptResult *)c->res_h)->status == CHEB_STATUS_RANGE) {
+        a.method = PHIPM_EXPM_TAYLOR;
+        a.tridiag = 0;
+        rc = launch_expm(c, a, mu + p + 1);
+        if (rc) return rc;
+        rc = sync(c);
+        if (rc) return rc;
+    }
     if (c->expm_clk_h) {
         const long long *k = c->expm_clk_h;
         fprintf(stderr, "expm K=%d cycles: build %lld | A2,A3,A4 %lld | norms,alpha,scale %lld | Horner %lld | "

@@ -81,7 +81,7 @@ typedef struct {
                                 phi_p(tau T)e1 and phi_{p+1}(tau T)e1 by one Chebyshev expansion on the
                                 Gershgorin interval of tau T, no augmented matrix.
                                 Arnoldi solves with this method use TAYLOR; an interval too wide for
-                                512 Chebyshev points (9.5 sqrt(r) + 24 > 512, r the half-width) falls
+                                512 Chebyshev points (10.5 sqrt(r) + 32 > 512, r the half-width) falls
                                 back to TAYLOR for that attempt.  phipm_phi_pair reads the lower
                                 band of H and assumes H symmetric tridiagonal. */
 

@@ -26,8 +26,9 @@ struct AttemptResult {
     double h;          // h_{mu+1,mu} used by the corrector (0 on breakdown)
     int mu;            // Krylov dimension used
     int brk;           // -1 or the breakdown position
-    int status;        // 0 ok, 5 non-finite, 6 singular
+    int status;        // 0 ok, 5 non-finite, 6 singular, 7 Chebyshev interval too wide
     int seq;           // attempt sequence number (host sanity check)
+    double eps_noise;  // Chebyshev method: rounding-noise bound of eps (0 for the augmented exponential)
 };
 
 // Publish an attempt result to the host (mapped pinned memory), one thread: the fields with
@@ -534,7 +535,7 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
                 a.combd[j] = d;
             }
             a.comb[0] = 0.0;
-            AttemptResult r;
+            AttemptResult r{};
             r.eps = 0.0; r.normH1 = 0.0; r.beta = beta; r.h = 0.0; r.mu = 0;
             r.brk = a.st->brk; r.status = a.st->nonfinite ? 5 : 0;
             publish_result(a.res, r, a.seq);
@@ -647,7 +648,7 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
             a.combd[j] = d;
         }
         const double eps = taup * beta * a.tau * fabs(h * phl);
-        AttemptResult r;
+        AttemptResult r{};
         r.eps = eps;
         r.normH1 = normH1;
         r.beta = beta;

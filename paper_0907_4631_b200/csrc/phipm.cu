@@ -1176,6 +1176,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     double tk = 0.0;
     S.m_peak = m;
     bool first = true;
+    bool cheb_off = false;             // the Chebyshev method was found unreliable in this solve
     while (tk < t_end) {
         if (tau > t_end - tk) tau = t_end - tk;
         if (!first) {
@@ -1202,7 +1203,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             ExpmArgs ea;
             memset(&ea, 0, sizeof(ea));
             ea.mode = 0;
-            ea.method = o.expm_method;
+            ea.method = cheb_off ? PHIPM_EXPM_TAYLOR : o.expm_method;
             ea.tridiag = P.symmetric ? 1 : 0;     // (Chebyshev method: Lanczos only)
             ea.m = m;
             ea.p = p;
@@ -1220,8 +1221,16 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             AttemptResult R;
             memcpy(&R, (const void *)c->res_h, sizeof(R));
             if (R.seq != c->seq) return finish(set_err(c, PHIPM_ECUDA, "stale attempt result"));
+            // Chebyshev method: if the interval is too wide (status 7), or if the rounding-noise bound of
+            // the error estimate exceeds 1e-2 max(omega, delta) (the last component is then a
+            // cancellation of large Chebyshev terms, interval wider than ~mu, and an accept could rest
+            // on noise), this attempt and the rest of the solve take the augmented exponential
+            if (ea.method == PHIPM_EXPM_CHEBYSHEV && R.status == 0) {
+                const double om = t_end * R.eps / (tau * o.tol), om_noise = t_end * R.eps_noise / (tau * o.tol);
+                if (om_noise > 1e-2 * std::max(om, 1.2)) R.status = CHEB_STATUS_RANGE;
+            }
             if (R.status == CHEB_STATUS_RANGE) {
-                // Chebyshev interval too wide: this attempt takes the augmented exponential
+                cheb_off = true;
                 ea.method = PHIPM_EXPM_TAYLOR;
                 rc = launch_expm(c, ea, m + p + 1);
                 if (rc) return finish(rc);
@@ -2140,7 +2149,17 @@ int phipm_phi_pair(phipm_ctx *c, int mu, const double *H, int ldh, double tau, i
         rc = sync(c);
         if (rc) return rc;
     }
-    if (c->expm_clk_h) {
+    if (c->expm_clk_h && c->expm_clk_h[8] == -1) {
+        const long long *k = c->expm_clk_h;
+        fprintf(stderr, "cheb K=%d cycles: gershgorin %lld | sturm %lld | nodes %lld | dct %lld | trunc %lld | "
+                        "recurrence %lld | N=%lld nd=%lld mu=%lld\n",
+                mu + p + 1, k[1] - k[0], k[2] - k[1], k[3] - k[2], k[4] - k[3], k[5] - k[4], k[6] - k[5],
+                k[7] >> 32, (k[7] >> 16) & 0xffff, k[7] & 0xffff);
+        double lo, hi;
+        memcpy(&lo, &k[9], 8);
+        memcpy(&hi, &k[10], 8);
+        fprintf(stderr, "  interval of tau T: [%.6g, %.6g]\n", lo, hi);
+    } else if (c->expm_clk_h) {
         const long long *k = c->expm_clk_h;
         fprintf(stderr, "expm K=%d cycles: build %lld | A2,A3,A4 %lld | norms,alpha,scale %lld | Horner %lld | "
                         "squarings %lld | m=%lld s=%lld\n",

@@ -48,3 +48,33 @@ for mu, p in ((12, 2), (10, 4), (20, 3), (30, 2), (40, 3), (50, 4), (52, 2)):
         print(f"{mu + p + 1:4d} {mu:4d} {p:2d} {nrm:9.1f} | {res[0][0]:10.1f} {res[2][0]:8.1f} | "
               f"{res[0][1]:10.1f} {res[2][1]:9.1f} | {res[0][0] / res[2][0]:.2f}x")
 ctx.set_expm_method(P.EXPM_TAYLOR)
+
+# ---- in-solve device time per exponential (profile: CUDA events around each launch) and solves/s
+import workloads as W  # noqa: E402
+
+print()
+print(f"{'config':>8} {'method':>10} | {'us/exp (device)':>15} {'n_exp':>6} | {'solves/s':>9} | stats")
+for name in ("c1", "c2", "c4", "c2_med"):
+    Pb = W.make(name)
+    c2 = P.Context(n_max=Pb.n, m_max=100, p_max=4)
+    S = P.Stencil.of(Pb.stencil)
+    u = [torch.from_numpy(x).cuda() for x in Pb.u]
+    for meth, mname in ((P.EXPM_TAYLOR, "taylor"), (P.EXPM_CHEBYSHEV, "chebyshev")):
+        kw = dict(tol=Pb.tol, symmetric=True, expm_method=meth)
+        for _ in range(3):
+            c2.solve_stencil(Pb.t, S, u, **kw)
+        c2.reset_profile()
+        R = 10
+        for _ in range(R):
+            _, st = c2.solve_stencil(Pb.t, S, u, profile=1, **kw)
+        pr = c2.profile()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(c2.stream)
+        for _ in range(R):
+            c2.solve_stencil(Pb.t, S, u, **kw)
+        e1.record(c2.stream)
+        torch.cuda.synchronize()
+        print(f"{name:>8} {mname:>10} | {1e3 * pr['ms_expm'] / max(pr['n_expm'], 1):15.1f} {pr['n_expm'] // R:6d} | "
+              f"{R / (e0.elapsed_time(e1) / 1e3):9.1f} | {st}")
+    c2.close()

@@ -361,3 +361,37 @@ def test_controller_trajectory_c1(ctx, orc):
     print(f"c1: trajectories agree for {i} of {len(tr)} oracle attempts; gpu {sg} oracle {so}")
     assert i >= 1
     assert relerr(wg, wo) <= parity_bound(Pb.tol)
+
+
+@pytest.mark.parametrize("name,path,opts", [("c1_mini", "stencil", {}), ("c2_med", "stencil", {}),
+                                            ("c3_med", "stencil", {"persist": 0}), ("c3_med", "stencil", {}),
+                                            ("c4_tm", "stencil", {}), ("c5_med", "csr", {}),
+                                            ("c2_mini", "csr", {})])
+def test_guard_regions_and_inputs_untouched(orc, name, path, opts):
+    """Out-of-bounds write check (compute-sanitizer is closed on this GPU pool): w is a view into a
+    buffer with 4096-double guard regions of a NaN pattern on both sides, and every input (u_k, the
+    CSR arrays) is compared bit for bit after the solve.  Every kernel family runs (single-CTA,
+    persistent smem / TMEM Lanczos, cooperative w-recurrence, streaming TMA-halo, CSR x-ring)."""
+    import torch
+    import paper_0907_4631_b200 as P
+    Pb = W.make(name)
+    c = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), options=opts)
+    g = 4096
+    buf = torch.full((Pb.n + 2 * g,), float("nan"), dtype=torch.float64, device="cuda")
+    w = buf[g:g + Pb.n]
+    u = [to_dev(x) for x in Pb.u]
+    u_copy = [x.clone() for x in u]
+    if path == "stencil":
+        c.solve_stencil(Pb.t, stencil_of(Pb), u, out=w, tol=Pb.tol, symmetric=Pb.symmetric)
+        A = A_copy = ()
+    else:
+        A = tuple(to_dev(a) for a in Pb.csr)
+        A_copy = tuple(a.clone() for a in A)
+        c.solve_csr(Pb.t, A, u, out=w, tol=Pb.tol, symmetric=Pb.symmetric)
+    torch.cuda.synchronize()
+    assert torch.isnan(buf[:g]).all() and torch.isnan(buf[g + Pb.n:]).all()
+    for a, b in zip(u + list(A), u_copy + list(A_copy)):
+        assert torch.equal(a, b)
+    wo, so = run_oracle(orc, Pb)
+    assert relerr(w.cpu().numpy(), wo) <= parity_bound(Pb.tol)
+    c.close()

@@ -205,6 +205,9 @@ CONFIGS = {
     "c3_med": lambda: c3(nx=301),
     "c4_med": lambda: c4(nx=45),
     "c5_med": lambda: c5(n=300_007, band=1024),
+    # 3-D Laplacian 70^3 (n = 343,000 >= 303,104): the tensor-memory Lanczos kernel at a size the
+    # oracle still solves in seconds
+    "c4_tm": lambda: c4(nx=70),
 }
 
 

@@ -171,6 +171,10 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *   PHIPM_OPT_CSR_WINDOW       0 (default) per-tile x windows for general CSR
  *   PHIPM_OPT_SMALL_LZ         1 (default) multi-row single-CTA Lanczos for n <= 8192
  *   PHIPM_OPT_PERSIST_MINROWS  0 (default: half a tile) minimum rows per CTA of the persistent kernel
+ *   PHIPM_OPT_CSR_PREFETCH     x-ring CSR path: rows ahead whose val / col the TMA engine prefetches
+ *                              into L2 (cp.async.bulk.prefetch.L2), 0 = off; default 384
+ *   PHIPM_OPT_COL_PREFETCH     1: streaming kernels prefetch the next group of Krylov columns / epilogue
+ *                              vectors of the tile into L2 (TMA engine); default 0
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -184,7 +188,9 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_CSR_WINDOW       9
 #define PHIPM_OPT_SMALL_LZ        10
 #define PHIPM_OPT_PERSIST_MINROWS 11
-#define PHIPM_OPT_COUNT           12
+#define PHIPM_OPT_CSR_PREFETCH    12
+#define PHIPM_OPT_COL_PREFETCH    13
+#define PHIPM_OPT_COUNT           14
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

@@ -89,6 +89,9 @@ struct CsrOp {
                            // ell <= 128: vectorised fast path (4 entries per lane)
     int ring;              // ell > 0 and every column within [r - blo, r + bhi]: x from a shared ring
     int blo, bhi;          // band below / above the diagonal (even, >= 0)
+    int pf;                // x-ring path: L2 prefetch distance of val/col in rows (0 = off;
+                           // PHIPM_OPT_CSR_PREFETCH)
+    int64_t pf_end;        // (set per launch) rows >= pf_end are not prefetched (the CTA's range end)
 };
 
 struct SpmvArgs {
@@ -109,6 +112,7 @@ struct SpmvArgs {
     int fin, j;
     int check_brk;               // exit early if a breakdown happened earlier in this step
     int64_t rpc;                 // rows per CTA (balanced contiguous ranges; multiple of 32)
+    int pfc;                     // L2-prefetch the streamed columns / z vectors one group ahead (PHIPM_OPT_COL_PREFETCH)
     unsigned long long *dbg;     // optional per-CTA %globaltimer stamps (PHIPM_KCLOCKS tool), 8 per CTA
     int xnorm;                   // also reduce ||x||^2 (after ||y||^2), for FIN_ARNOLDI_LAG
     double bthr;                 // breakdown threshold (FIN_ARNOLDI_LAG)
@@ -136,6 +140,7 @@ struct AxpyArgs {
     int64_t rpc;                 // rows per CTA (balanced contiguous ranges; multiple of 32)
     int rev;                     // stream the V columns in descending order (L2 ping-pong with the
                                  // ascending dot pass of the SpMV kernel)
+    int pfc;                     // L2-prefetch the streamed vectors one group ahead (PHIPM_OPT_COL_PREFETCH)
     unsigned long long *dbg;     // optional per-CTA %globaltimer stamps (PHIPM_KCLOCKS tool)
 };
 

@@ -109,7 +109,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0};
     char err[512] = {0};
 };
 
@@ -348,6 +348,7 @@ int launch_spmv(phipm_ctx *c, const Op &op, const SpmvArgs &a0, double bytes_op)
 {
     SpmvArgs a = a0;
     if (a.ldx == 0) a.ldx = c->ldv;
+    a.pfc = opt(c, PHIPM_OPT_COL_PREFETCH);
     if (std::is_same<Op, CsrOp>::value) a.xcol = -1;          // CSR gathers x: no on-chip tile
     ProfRec r;
     // algorithmic bytes: operator pass + streamed dot columns (the x column is reused on chip) + z
@@ -391,8 +392,10 @@ void launch_axpy_t(phipm_ctx *c, int64_t n, const AxpyArgs &a0)
     launch_k(c, axpy_stream_kernel<RPT>, grid, SNT, 0, n, a, make_work(c));
 }
 
-int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a, int cls)
+int launch_axpy(phipm_ctx *c, int64_t n, const AxpyArgs &a_in, int cls)
 {
+    AxpyArgs a = a_in;
+    a.pfc = opt(c, PHIPM_OPT_COL_PREFETCH);
     ProfRec r;
     const double bytes = 8.0 * (double)n * (a.nc + a.ne + 1 + (a.a0h != 0.0 ? 1 : 0));
     prof_begin(c, r, cls, bytes, a.nc + a.ne + (a.a0h != 0.0 ? 1 : 0));
@@ -1407,6 +1410,8 @@ int make_csr(phipm_ctx *c, const phipm_csr *A, CsrOp &op)
     op.wtile = op.wcap = 0;
     op.ell = 0;
     op.ring = op.blo = op.bhi = 0;
+    op.pf = 0;
+    op.pf_end = op.n;
     return PHIPM_OK;
 }
 
@@ -1445,6 +1450,8 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA)
     if (!env_ell || L < 4 || (L % 4) || ((L / 4) & (L / 4 - 1)) || h.nonuniform) return PHIPM_OK;
     if (((uintptr_t)op.val & 15) || ((uintptr_t)op.col & 15)) return PHIPM_OK;
     op.ell = (int)L;
+    op.pf = opt(c, PHIPM_OPT_CSR_PREFETCH);
+    op.pf_end = op.n;
     op.blo = (h.blo + 1) & ~1;
     op.bhi = (h.bhi + 1) & ~1;
     op.ring = (env_ring && 2 * SNT * 2 + op.blo + op.bhi <= XRING) ? 1 : 0;
@@ -1597,6 +1604,8 @@ int phipm_set_option(phipm_ctx *c, int option, int value)
     case PHIPM_OPT_PERSIST: ok = value >= 0 && value <= 2; break;
     case PHIPM_OPT_RPT: ok = value == 0 || value == 2 || value == 4 || value == 8; break;
     case PHIPM_OPT_PERSIST_MINROWS: ok = value >= 0; break;
+    case PHIPM_OPT_CSR_PREFETCH: ok = value >= 0 && value <= (1 << 20); break;
+    case PHIPM_OPT_COL_PREFETCH: ok = value == 0 || value == 1; break;
     default: ok = value == 0 || value == 1; break;
     }
     if (!ok) return set_err(c, PHIPM_EINVAL, "option %d: value %d out of range", option, value);

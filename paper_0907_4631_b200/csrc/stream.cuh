@@ -9,7 +9,7 @@
 //     (rows 2 tid + 512 h, +1) and keeps its y values in registers from the SpMV through the
 //     dot products, so y never round-trips through memory inside the kernel.
 //   * Streamed Krylov columns are read with 16-B non-allocating loads, CU columns x RPT/2 pairs
-//     in flight per thread (64-128 B/thread, 4 CTAs/SM), which saturates HBM.
+//     in flight per thread (64-128 B/thread, one 1024-thread CTA per SM), which saturates HBM.
 //   * Stencil operators stage their halo tile in shared memory with 1-D TMA (cp.async.bulk,
 //     SASS UBLKCP): in 2-D/3-D the centre row range and the +-nx neighbour ranges are one
 //     contiguous copy [r0 - nx, r0 + TILE + nx), the +-nx*ny ranges (3-D) two more; the next
@@ -90,6 +90,20 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
+}
+
+// bulk prefetch of [src, src + bytes) into L2 (TMA engine, no shared memory; 16-B granularity)
+__device__ __forceinline__ void tma_prefetch_l2(const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// L2 prefetch of rows [0, rows) of a vector (a tile segment); the bulk prefetch needs a 16-B aligned
+// address and a multiple of 16 bytes: unaligned vectors are skipped, an odd last row is left out
+__device__ __forceinline__ void prefetch_rows(const double *p, int rows)
+{
+    const uint32_t bytes = ((uint32_t)rows * 8u) & ~15u;
+    if (((uintptr_t)p & 15) == 0 && bytes) tma_prefetch_l2(p, bytes);
 }
 
 // 16-B read-only load that does not allocate in L1 (streamed Krylov columns)
@@ -267,6 +281,17 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
         else return __ldg(x + c);
     };
     for (int base = warp * rpw; base < rows; base += stride * U) {
+        if constexpr (XM == 2) {
+            // L2 prefetch (TMA engine) of the val / col rows pf ahead of this block of stride * U
+            // rows, issued by the first thread, so the 16-B loads below hit L2
+            if (A.pf > 0 && threadIdx.x == 0) {
+                const int64_t pa = r0 + base + A.pf, pb = min(pa + (int64_t)stride * U, A.pf_end);
+                if (pb > pa) {
+                    tma_prefetch_l2(A.val + pa * A.ell, (uint32_t)((pb - pa) * A.ell * 8));
+                    tma_prefetch_l2(A.col + pa * A.ell, (uint32_t)((pb - pa) * A.ell * 4));
+                }
+            }
+        }
         double2 va[U], vb[U];
         int4 cc[U];
         // column indices of all U groups first: the x lookups depend on them, the values only on
@@ -683,6 +708,12 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
     for (int64_t r0 = cs; r0 < ce; r0 += TILE_) {
         const int rows = (int)min((int64_t)TILE_, ce - r0);
         const int64_t r1 = r0 + TILE_;                     // next tile of this CTA
+        if (a.pfc && tid == 0) {
+            // this tile's epilogue vectors and first dot columns into L2 during the SpMV phase
+            for (int i = 0; i < a.nz; i++) prefetch_rows(a.z[i] + r0, rows);
+            for (int k = 0; k < min(CUD, a.nd); k++)
+                if (k != (HALO ? a.xcol : -1)) prefetch_rows(a.V + (int64_t)(a.d0 + k) * a.ldv + r0, rows);
+        }
         double2 y[NP], xr[NP];
         // ---- phase 1: raw (A x) rows into registers (and x itself, for a dot with v_j = x)
         if constexpr (HALO) {
@@ -716,7 +747,11 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
                 mbar_wait(&rbar[ht & 1], (ht >> 1) & 1);
                 if (tid == 0 && r1 < ce) issue_ring(r1 + op.bhi, r1 + TILE_ + op.bhi, &rbar[(ht + 1) & 1]);
                 ht++;
-                csr_tile_ell<2>(op, a.x, xring, 0, r0, rows, hbuf);
+                {
+                    CsrOp opf = op;
+                    opf.pf_end = ce;
+                    csr_tile_ell<2>(opf, a.x, xring, 0, r0, rows, hbuf);
+                }
                 __syncthreads();                           // ring reads done, ys complete
             } else {
                 if (wcap > 0) {
@@ -795,6 +830,11 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
             if (lane == 0) lacc[xc * SNW + warp] += d;
         }
         for (int k0 = 0; k0 < a.nd; k0 += CUD) {
+            if (a.pfc && tid == 0) {
+                // the tile segments of the next CUD columns into L2 while these are loaded
+                for (int k = k0 + CUD; k < min(k0 + 2 * CUD, a.nd); k++)
+                    if (k != xc) prefetch_rows(a.V + (int64_t)(a.d0 + k) * a.ldv + r0, rows);
+            }
             double2 v[CUD][NP];
 #pragma unroll
             for (int u = 0; u < CUD; u++) {
@@ -910,6 +950,16 @@ __global__ void __launch_bounds__(SNT, SMINB) axpy_stream_kernel(int64_t n, Axpy
 #pragma unroll
         for (int p = 0; p < NP; p++) acc[p] = make_double2(0.0, 0.0);
         for (int k0 = 0; k0 < nitem; k0 += CU) {
+            if (a.pfc && tid == 0) {
+                // next group of this tile, or the first group of the next tile
+                for (int k = k0 + CU; k < k0 + 2 * CU; k++) {
+                    if (k < nitem) prefetch_rows(src[k] + r0, rows);
+                    else if (r0 + TILE_ < ce && k - nitem < CU && k - nitem < nitem)
+                        prefetch_rows(src[k - nitem] + r0 + TILE_, (int)min((int64_t)TILE_, ce - r0 - TILE_));
+                }
+                if (k0 == 0 && r0 == cs)
+                    for (int k = 0; k < min(CU, nitem); k++) prefetch_rows(src[k] + r0, rows);
+            }
             double2 v[CU][NP];
 #pragma unroll
             for (int u = 0; u < CU; u++) {

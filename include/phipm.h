@@ -242,6 +242,20 @@ int phipm_solve_stencil_batch(phipm_ctx *const *ctx, int nb, const double *t, co
                               const int *p, const double *const *const *u, const phipm_opts *opts,
                               double *const *w, phipm_stats *stats, int *status);
 
+/* Block solve of nb <= 8 problems sharing the CSR operator A, t, p and the options (
+ * the many phipm evaluations with one operator of PAPER.md P:164-185 / P:1353-1358): problem b has
+ * inputs u[b][0..p] (DEVICE) and output w[b] (DEVICE, distinct), workspace ctx[b] (distinct
+ * contexts on one device).  One controller (Alg. 3/4) drives the block on the largest error estimate
+ * (omega = max_b omega_b: every problem meets Tol when a block step is accepted), so all problems take
+ * the same steps and Krylov dimensions; each Krylov step multiplies the nb basis vectors by A in ONE
+ * pass over val/col (SpMM), then runs every problem's own Gram-Schmidt / Lanczos kernels.  All work
+ * is ordered on ctx[0]'s stream (after the work already enqueued on the others); stats[b] (may be
+ * NULL) per problem, their attempt records carry the block's omega.  opts.profile applies to ctx[0]'s
+ * launches only.  The Chebyshev expm method is not used here (Taylor instead). */
+int phipm_solve_csr_block(phipm_ctx *const *ctx, int nb, double t, const phipm_csr *A, int p,
+                          const double *const *const *u, const phipm_opts *opts, double *const *w,
+                          phipm_stats *stats);
+
 /* Matrix Market ingestion (HOST, no GPU needed): "%%MatrixMarket matrix coordinate {real|integer|pattern}
  * {general|symmetric|skew-symmetric}", square, 1-based indices.  Result: CSR with columns ascending
  * in each row, symmetric / skew-symmetric storage expanded.

@@ -158,6 +158,7 @@ def lib():
                                             P(i32)]),
             "phipm_solve_stencil_batch": (i32, [P(vp), i32, P(d), P(_Stencil), P(i32), P(vp), P(_Opts), P(vp),
                                                 P(_Stats), P(i32)]),
+            "phipm_solve_csr_block": (i32, [P(vp), i32, d, P(_Csr), i32, P(vp), P(_Opts), P(vp), P(_Stats)]),
             "phipm_stencil_nnz": (i64, [P(_Stencil)]),
             "phipm_inf_norm_stencil": (d, [P(_Stencil)]),
             "phipm_csr_from_stencil": (i32, [vp, P(_Stencil), vp, vp, vp]),
@@ -183,7 +184,7 @@ EXPORTED = [
     "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_get_attempts", "phipm_set_option",
     "phipm_get_option", "phipm_solve_csr", "phipm_solve_stencil",
     "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_solve_csr_batch",
-    "phipm_solve_stencil_batch", "phipm_stencil_nnz", "phipm_inf_norm_stencil",
+    "phipm_solve_stencil_batch", "phipm_solve_csr_block", "phipm_stencil_nnz", "phipm_inf_norm_stencil",
     "phipm_csr_from_stencil", "phipm_spmv_csr", "phipm_spmv_stencil", "phipm_dot", "phipm_inf_norm_csr",
     "phipm_expm", "phipm_phi_pair", "phipm_krylov_csr", "phipm_krylov_stencil",
 ]
@@ -510,6 +511,30 @@ def solve_batch(ctxs: Sequence["Context"], t, ops, us: Sequence[Sequence], outs=
     if rc != OK:
         bad = next((b for b in range(nb) if status[b] != OK), 0)
         ctxs[bad]._check(status[bad] if status[bad] != OK else rc)
+    return outs, [Stats(*[getattr(x, k) for k, _ in _Stats._fields_]) for x in st]
+
+
+def solve_block(ctxs: Sequence["Context"], t: float, A, us: Sequence[Sequence], outs=None, **kw):
+    """Block solve of nb problems sharing the CSR operator A (phipm_solve_csr_block): one controller
+    on the block's largest error estimate, one SpMM pass over A per Krylov step.  ctxs: distinct
+    contexts (workspaces; all work runs on ctxs[0]'s stream); A = (row_ptr, col, val) CUDA tensors;
+    us[b]: the p+1 input vectors of problem b (same p).  Returns (outputs, stats list)."""
+    torch = _torch()
+    nb = len(ctxs)
+    n = A[0].numel() - 1
+    outs = outs if outs is not None else [torch.empty(n, dtype=torch.float64, device=us[b][0].device)
+                                          for b in range(nb)]
+    o = ctxs[0].opts(**kw)
+    for c in ctxs:
+        c._order()
+    hs = (C.c_void_p * nb)(*[c._h for c in ctxs])
+    uarrs = [ctxs[b]._uptrs(us[b]) for b in range(nb)]
+    ua = (C.c_void_p * nb)(*[C.cast(a, C.c_void_p) for a in uarrs])
+    wa = (C.c_void_p * nb)(*[_f64(w) for w in outs])
+    st = (_Stats * nb)()
+    L = ctxs[0]._L
+    rc = L.phipm_solve_csr_block(hs, nb, float(t), C.byref(ctxs[0]._csr(A)), len(us[0]) - 1, ua, C.byref(o), wa, st)
+    ctxs[0]._check(rc)
     return outs, [Stats(*[getattr(x, k) for k, _ in _Stats._fields_]) for x in st]
 
 

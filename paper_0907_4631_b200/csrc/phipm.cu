@@ -31,6 +31,7 @@
 #include "persist_tm.cuh"
 #include "persist_wrec.cuh"
 #include "phicheb.cuh"
+#include "spmm.cuh"
 
 using namespace phipm;
 
@@ -131,6 +132,14 @@ int set_err(phipm_ctx *c, int code, const char *fmt, ...)
         cudaError_t e_ = (call);                                                                   \
         if (e_ != cudaSuccess)                                                                     \
             return set_err(c, PHIPM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                           __FILE__, __LINE__);                                                    \
+    } while (0)
+
+#define CK0(ctx_, call)                                                                            \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return set_err(ctx_, PHIPM_ECUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
                            __FILE__, __LINE__);                                                    \
     } while (0)
 
@@ -983,6 +992,95 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
     return PHIPM_OK;
 }
 
+// ||u_k||_inf of u[k0..k1).  publish = true: the result goes to mapped pinned memory with a sequence
+// number the host spins on (no copy node in the stream); otherwise it is copied to raw_h
+int enqueue_maxabs_u(phipm_ctx *c, int64_t n, const double *const *u, int k0, int k1, bool publish)
+{
+    MaxAbsArgs ma;
+    memset(&ma, 0, sizeof(ma));
+    ma.nv = k1 - k0;
+    for (int k = k0; k < k1; k++) ma.x[k - k0] = u[k];
+    if (publish) {
+        ma.pub = c->mx_d->v;
+        ma.pub_seq = &c->mx_d->seq;
+        ma.seq = ++c->mx_seq;
+    }
+    const int grid = grid_for(c, (n + NT - 1) / NT, c->occ_axpy);
+    maxabs_kernel<<<grid, NT, 0, c->stream>>>(n, ma, make_work(c));
+    c->acc.launches++;
+    CK(cudaGetLastError());
+    if (!publish)
+        CK(cudaMemcpyAsync(c->raw_h + k0, c->raw, ma.nv * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    return PHIPM_OK;
+}
+
+// Eq. (wrecurrence): w_0 = u_k, w_j = A w_{j-1} + sum_l t_k^l/l! u_{j+l}; w_p -> V[:,0]
+// x0 = w_0 = u_k; ldx0 > 0: x0 is the caller's u_0 (n even, 16-B aligned), halos clamp to n
+template <class Op>
+int enqueue_wrec_op(phipm_ctx *c, const Op &op, double bytes_op, int p, const double *const *u, double tk,
+                    const double *x0, int64_t ldx0)
+{
+    const int64_t n = op.n;
+    if (p == 0) {
+        AxpyArgs a = axpy0();
+        a.out = c->V;
+        a.base = x0;
+        a.a0h = 1.0;
+        a.V = c->V;
+        a.ldv = c->ldv;
+        a.onorm = 1;
+        a.fin = FIN_SEED;
+        return launch_axpy(c, n, a, PC_OTHER);
+    }
+    {
+        // one cooperative kernel for all p SpMVs (stencils); else p streaming launches
+        WrecArgs wa;
+        memset(&wa, 0, sizeof(wa));
+        wa.p = p;
+        wa.x0 = x0;
+        wa.ldx = ldx0 ? ldx0 : c->ldv;
+        wa.W = c->W;
+        double bytes = 0.0;
+        for (int j = 1; j <= p; j++) {
+            double coef = 1.0;
+            int nz = 0;
+            for (int l = 0; l <= p - j; l++) {
+                if (l > 0) coef = coef * tk / (double)l;
+                if (l > 0 && coef == 0.0) continue;
+                wa.z[j - 1][nz] = u[j + l];
+                wa.zc[j - 1][nz] = coef;
+                nz++;
+            }
+            wa.nz[j - 1] = nz;
+            bytes += bytes_op + 8.0 * (double)n * nz;
+        }
+        int rc = PHIPM_OK;
+        if (p <= WREC_MAXP && launch_wrec_persist(c, op, wa, bytes, rc)) return rc;
+    }
+    for (int j = 1; j <= p; j++) {
+        SpmvArgs s = spmv0();
+        s.x = (j == 1) ? x0 : c->W + (int64_t)(j - 1) * c->ldv;
+        if (j == 1 && ldx0) s.ldx = ldx0;
+        s.y = (j == p) ? c->V : c->W + (int64_t)j * c->ldv;
+        // terms whose coefficient t_k^l / l! is exactly 0 (the first step, t_k = 0: only u_j)
+        // are not read: adding 0 * u changes no sum
+        double coef = 1.0;
+        s.nz = 0;
+        for (int l = 0; l <= p - j; l++) {
+            if (l > 0) coef = coef * tk / (double)l;
+            if (l > 0 && coef == 0.0) continue;
+            s.z[s.nz] = u[j + l];
+            s.zc[s.nz] = coef;
+            s.nz++;
+        }
+        s.ynorm = (j == p);
+        s.fin = (j == p) ? FIN_SEED : FIN_NONE;
+        int rc = launch_spmv(c, op, s, bytes_op);
+        if (rc) return rc;
+    }
+    return PHIPM_OK;
+}
+
 // ---------------------------------------------------------------------------------------------
 // the solve (Algorithm 3)
 
@@ -1004,87 +1102,9 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         int rc = sync(c);
         return finish(rc);
     }
-    // publish = true: the result goes to mapped pinned memory with a sequence number the host spins on
-    // (no copy node in the stream); otherwise it is copied to raw_h
-    auto enqueue_maxabs = [&](int k0, int k1, bool publish) {
-        MaxAbsArgs ma;
-        memset(&ma, 0, sizeof(ma));
-        ma.nv = k1 - k0;
-        for (int k = k0; k < k1; k++) ma.x[k - k0] = u[k];
-        if (publish) {
-            ma.pub = c->mx_d->v;
-            ma.pub_seq = &c->mx_d->seq;
-            ma.seq = ++c->mx_seq;
-        }
-        const int grid = grid_for(c, (n + NT - 1) / NT, c->occ_axpy);
-        maxabs_kernel<<<grid, NT, 0, c->stream>>>(n, ma, make_work(c));
-        c->acc.launches++;
-        CK(cudaGetLastError());
-        if (!publish)
-            CK(cudaMemcpyAsync(c->raw_h + k0, c->raw, ma.nv * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        return PHIPM_OK;
-    };
-    // Eq. (wrecurrence): w_0 = u_k, w_j = A w_{j-1} + sum_l t_k^l/l! u_{j+l}; w_p -> V[:,0]
-    // x0 = w_0 = u_k; ldx0 > 0: x0 is the caller's u_0 (n even, 16-B aligned), halos clamp to n
+    auto enqueue_maxabs = [&](int k0, int k1, bool publish) { return enqueue_maxabs_u(c, n, u, k0, k1, publish); };
     auto enqueue_wrec = [&](double tk, const double *x0, int64_t ldx0) {
-        if (p == 0) {
-            AxpyArgs a = axpy0();
-            a.out = c->V;
-            a.base = x0;
-            a.a0h = 1.0;
-            a.V = c->V;
-            a.ldv = c->ldv;
-            a.onorm = 1;
-            a.fin = FIN_SEED;
-            return launch_axpy(c, n, a, PC_OTHER);
-        }
-        {
-            // one cooperative kernel for all p SpMVs (stencils); else p streaming launches
-            WrecArgs wa;
-            memset(&wa, 0, sizeof(wa));
-            wa.p = p;
-            wa.x0 = x0;
-            wa.ldx = ldx0 ? ldx0 : c->ldv;
-            wa.W = c->W;
-            double bytes = 0.0;
-            for (int j = 1; j <= p; j++) {
-                double coef = 1.0;
-                int nz = 0;
-                for (int l = 0; l <= p - j; l++) {
-                    if (l > 0) coef = coef * tk / (double)l;
-                    if (l > 0 && coef == 0.0) continue;
-                    wa.z[j - 1][nz] = u[j + l];
-                    wa.zc[j - 1][nz] = coef;
-                    nz++;
-                }
-                wa.nz[j - 1] = nz;
-                bytes += bytes_op + 8.0 * (double)n * nz;
-            }
-            int rc = PHIPM_OK;
-            if (p <= WREC_MAXP && launch_wrec_persist(c, op, wa, bytes, rc)) return rc;
-        }
-        for (int j = 1; j <= p; j++) {
-            SpmvArgs s = spmv0();
-            s.x = (j == 1) ? x0 : c->W + (int64_t)(j - 1) * c->ldv;
-            if (j == 1 && ldx0) s.ldx = ldx0;
-            s.y = (j == p) ? c->V : c->W + (int64_t)j * c->ldv;
-            // terms whose coefficient t_k^l / l! is exactly 0 (the first step, t_k = 0: only u_j)
-            // are not read: adding 0 * u changes no sum
-            double coef = 1.0;
-            s.nz = 0;
-            for (int l = 0; l <= p - j; l++) {
-                if (l > 0) coef = coef * tk / (double)l;
-                if (l > 0 && coef == 0.0) continue;
-                s.z[s.nz] = u[j + l];
-                s.zc[s.nz] = coef;
-                s.nz++;
-            }
-            s.ynorm = (j == p);
-            s.fin = (j == p) ? FIN_SEED : FIN_NONE;
-            int rc = launch_spmv(c, op, s, bytes_op);
-            if (rc) return rc;
-        }
-        return PHIPM_OK;
+        return enqueue_wrec_op(c, op, bytes_op, p, u, tk, x0, ldx0);
     };
 
     Problem P;
@@ -1510,6 +1530,389 @@ phipm_opts resolve_opts(const phipm_opts *o)
     return r;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Block solve: nb problems sharing the CSR operator A, t, p, tol.  One controller
+// drives all of them in lockstep (Alg. 3/4 on the block's largest error estimate: omega = max_b
+// omega_b, so every problem meets its tolerance when the block step is accepted); each Krylov step
+// multiplies all nb basis vectors by A in one SpMM pass over val/col (spmm.cuh), then every problem
+// runs its own fused dot / update kernels (identity operator) on its own basis.  Workspaces are the
+// nb contexts'; every launch goes to ctx[0]'s stream.
+
+int launch_spmm_one(phipm_ctx *c0, const CsrOp &op, SpmmArgs &sa, double bytes, int64_t ldx, int T)
+{
+    if (T > 0) {
+        SpmmRing g;
+        g.T = T;
+        g.R = (2 * T + op.blo + op.bhi + 31) & ~31;
+        g.ldx = ldx;
+        const size_t smem = (size_t)sa.nb * g.R * sizeof(double);
+        int grid;
+        balance(c0, op.n, c0->sm_count, grid, sa.rpc);
+        ProfRec r;
+        prof_begin(c0, r, PC_SPMV, bytes, sa.nb);
+        if (sa.nb <= 2) launch_k(c0, spmm_csr_ring_kernel<2>, grid, SNT, smem, op, sa, g);
+        else if (sa.nb <= 4) launch_k(c0, spmm_csr_ring_kernel<4>, grid, SNT, smem, op, sa, g);
+        else launch_k(c0, spmm_csr_ring_kernel<SPMM_MAXB>, grid, SNT, smem, op, sa, g);
+        prof_end(c0, r);
+    } else {
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, spmm_csr_kernel, SPMM_NT, 0);
+        int grid;
+        balance(c0, op.n, std::max(occ, 1) * c0->sm_count, grid, sa.rpc);
+        ProfRec r;
+        prof_begin(c0, r, PC_SPMV, bytes, sa.nb);
+        launch_k(c0, spmm_csr_kernel, grid, SPMM_NT, 0, op, sa);
+        prof_end(c0, r);
+    }
+    c0->acc.launches++;
+    CK0(c0, cudaGetLastError());
+    return PHIPM_OK;
+}
+
+// Y_b = A X_b for the block.  Banded uniform-row CSR: x rings in shared memory, in chunks of as many
+// vectors as fit with T = 1024 (else 512) rows per tile, one pass over val/col per chunk; other
+// matrices: one pass with L1 gathers.  bytes_op: the operator's algorithmic bytes of one SpMV.
+int launch_spmm(phipm_ctx *c0, const CsrOp &op, const SpmmArgs &sa, double bytes_op, int64_t ldx)
+{
+    const double n = (double)op.n;
+    if (op.ell > 0 && opt(c0, PHIPM_OPT_CSR_RING)) {
+        for (int T = 1024; T >= 512; T >>= 1) {
+            const size_t ring = (size_t)((2 * T + op.blo + op.bhi + 31) & ~31) * sizeof(double);
+            const int fit = (int)std::min<size_t>(c0->smem_optin / ring, SPMM_MAXB);
+            if (fit < 1) continue;
+            const int per = std::min(fit, (sa.nb + ((sa.nb + fit - 1) / fit) - 1) / ((sa.nb + fit - 1) / fit));
+            for (int b0 = 0; b0 < sa.nb; b0 += per) {
+                SpmmArgs s = sa;
+                s.nb = std::min(per, sa.nb - b0);
+                for (int b = 0; b < s.nb; b++) {
+                    s.x[b] = sa.x[b0 + b];
+                    s.y[b] = sa.y[b0 + b];
+                    s.brk[b] = sa.brk[b0 + b];
+                }
+                int rc = launch_spmm_one(c0, op, s, bytes_op - 16.0 * n + 16.0 * n * s.nb, ldx, T);
+                if (rc) return rc;
+            }
+            return PHIPM_OK;
+        }
+    }
+    SpmmArgs s = sa;
+    return launch_spmm_one(c0, op, s, bytes_op - 16.0 * n + 16.0 * n * sa.nb, ldx, 0);
+}
+
+// Krylov steps j = k0 .. k1-1 of every problem (lockstep)
+int enqueue_krylov_block(phipm_ctx *const *cs, int nb, const CsrOp &op, double bytes_op, bool symmetric, int k0,
+                         int k1, double bthr)
+{
+    phipm_ctx *c0 = cs[0];
+    const int64_t n = op.n;
+    for (int j = k0; j < k1; j++) {
+        SpmmArgs sa;
+        memset(&sa, 0, sizeof(sa));
+        sa.nb = nb;
+        for (int b = 0; b < nb; b++) {
+            sa.x[b] = cs[b]->V + (int64_t)j * cs[b]->ldv;
+            sa.y[b] = cs[b]->W + (int64_t)cs[b]->p_max * cs[b]->ldv;    // free slot of W
+            sa.brk[b] = &cs[b]->st->brk;
+        }
+        // operator bytes once, plus nb x (gathered x once, y written)
+        int64_t ldx = cs[0]->ldv;                          // readable length of every x_b (V columns)
+        for (int b = 1; b < nb; b++) ldx = std::min(ldx, cs[b]->ldv);
+        int rc = launch_spmm(c0, op, sa, bytes_op, ldx);
+        if (rc) return rc;
+        for (int b = 0; b < nb; b++) {
+            phipm_ctx *c = cs[b];
+            double *vn = c->V + (int64_t)(j + 1) * c->ldv;
+            SpmvArgs s = spmv0();
+            s.x = sa.y[b];                   // raw A v~_j
+            s.xscale = c->sigma + j;
+            s.y = c->Y;
+            s.V = c->V;
+            s.ldv = c->ldv;
+            s.ynorm = 1;
+            s.j = j;
+            s.check_brk = 1;
+            AxpyArgs u = axpy0();
+            u.out = vn;
+            u.base = c->Y;
+            u.a0h = 1.0;
+            u.V = c->V;
+            u.ldv = c->ldv;
+            u.g = c->g;
+            u.gsign = -1.0;
+            u.onorm = 1;
+            u.fin = FIN_NORM;
+            u.j = j;
+            u.check_brk = 1;
+            u.bthr = bthr;
+            u.rev = 1;
+            if (symmetric) {
+                if (j > 0) {
+                    s.nz = 1;
+                    s.z[0] = c->V + (int64_t)(j - 1) * c->ldv;
+                    s.zc[0] = -1.0;
+                    s.zcd[0] = &c->st->lz;
+                }
+                s.d0 = j;
+                s.nd = 1;
+                s.fin = FIN_LANCZOS;
+                u.c0 = j;
+                u.nc = 1;
+                u.lanczos = 1;
+            } else {
+                s.d0 = 0;
+                s.nd = j + 1;
+                s.fin = FIN_ARNOLDI;
+                u.c0 = 0;
+                u.nc = j + 1;
+            }
+            rc = launch_spmv(c, IdentOp{n}, s, 16.0 * (double)n);
+            if (!rc) rc = launch_axpy(c, n, u, PC_ORTH);
+            if (rc) return rc;
+        }
+    }
+    return PHIPM_OK;
+}
+
+// Eq. (wrecurrence) for the block: w_{j,b} = A w_{j-1,b} + sum_l t_k^l/l! u_{j+l,b}, the products by
+// SpMM (raw A w_{j-1,b} into a scratch column), the u-terms (and w_p's norm, FIN_SEED) by each
+// problem's identity-operator pass; w_0 = U_b (the running solution)
+int enqueue_wrec_block(phipm_ctx *const *cs, int nb, const CsrOp &op, double bytes_op, int p,
+                       const double *const *const *u, double tk)
+{
+    if (p == 0) {
+        for (int b = 0; b < nb; b++) {
+            int rc = enqueue_wrec_op(cs[b], op, bytes_op, 0, u[b], tk, cs[b]->U, 0);
+            if (rc) return rc;
+        }
+        return PHIPM_OK;
+    }
+    const int64_t n = op.n;
+    int64_t ldx = cs[0]->ldv;
+    for (int b = 1; b < nb; b++) ldx = std::min(ldx, cs[b]->ldv);
+    for (int j = 1; j <= p; j++) {
+        SpmmArgs sa;
+        memset(&sa, 0, sizeof(sa));
+        sa.nb = nb;
+        for (int b = 0; b < nb; b++) {
+            phipm_ctx *c = cs[b];
+            sa.x[b] = (j == 1) ? c->U : c->W + (int64_t)(j - 1) * c->ldv;
+            sa.y[b] = c->W + (int64_t)c->p_max * c->ldv;
+        }
+        int rc = launch_spmm(cs[0], op, sa, bytes_op, ldx);
+        if (rc) return rc;
+        for (int b = 0; b < nb; b++) {
+            phipm_ctx *c = cs[b];
+            SpmvArgs s = spmv0();
+            s.x = sa.y[b];
+            s.y = (j == p) ? c->V : c->W + (int64_t)j * c->ldv;
+            double coef = 1.0;
+            s.nz = 0;
+            for (int l = 0; l <= p - j; l++) {
+                if (l > 0) coef = coef * tk / (double)l;
+                if (l > 0 && coef == 0.0) continue;
+                s.z[s.nz] = u[b][j + l];
+                s.zc[s.nz] = coef;
+                s.nz++;
+            }
+            s.ynorm = (j == p);
+            s.fin = (j == p) ? FIN_SEED : FIN_NONE;
+            rc = launch_spmv(c, IdentOp{n}, s, 16.0 * (double)n);
+            if (rc) return rc;
+        }
+    }
+    return PHIPM_OK;
+}
+
+int solve_block_impl(phipm_ctx *const *cs, int nb, double t_end, const CsrOp &op, double bytes_op, int64_t NA,
+                     double normA, int p, const double *const *const *u, const phipm_opts &o, double *const *w,
+                     phipm_stats *stats)
+{
+    phipm_ctx *c0 = cs[0];
+    const int64_t n = op.n;
+    std::vector<phipm_stats> S((size_t)nb);
+    for (auto &s : S) s = phipm_stats{};
+    auto finish = [&](int rc) {
+        if (stats)
+            for (int b = 0; b < nb; b++) stats[b] = S[b];
+        return rc;
+    };
+    for (int b = 0; b < nb; b++) {
+        cs[b]->attempts.clear();
+        cs[b]->nattempts = 0;
+    }
+    if (t_end == 0.0) {
+        for (int b = 0; b < nb; b++)
+            if (w[b] != u[b][0]) CK0(c0, cudaMemcpyAsync(w[b], u[b][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c0->stream));
+        return finish(sync(c0));
+    }
+    Problem P;
+    P.p = p;
+    P.n = n;
+    P.NA = NA;
+    P.symmetric = o.symmetric != 0;
+    P.m_max = (int)std::min<int64_t>(o.m_max, n);
+    P.fixed_m = o.fixed_m != 0;
+    P.eq6_variant = o.eq6_variant != 0;
+    int m = std::min(o.m_init, P.m_max);
+    const double mbar = 0.5 * ((double)o.m_init + (double)P.m_max);
+    const double bthr = (double)n * EPS_MACH * normA;
+    // b_inf of Eq. (tau_0) per problem (R7); the block starts with the smallest tau_0 (largest b_inf)
+    double binf_max = 0.0;
+    std::vector<char> zero((size_t)nb, 0);
+    for (int b = 0; b < nb; b++) {
+        phipm_ctx *c = cs[b];
+        int rc = enqueue_maxabs_u(c, n, u[b], 0, p + 1, false);
+        if (rc) return finish(rc);
+    }
+    {
+        int rc = sync(c0);
+        if (rc) return finish(rc);
+    }
+    for (int b = 0; b < nb; b++) {
+        double bi = 0.0;
+        for (int k = 0; k <= p && bi == 0.0; k++) bi = cs[b]->raw_h[k];
+        if (!std::isfinite(bi)) return finish(set_err(c0, PHIPM_ENONFINITE, "non-finite input vector (problem %d)", b));
+        zero[b] = bi == 0.0;
+        binf_max = std::max(binf_max, bi);
+    }
+    if (binf_max == 0.0) {
+        for (int b = 0; b < nb; b++) CK0(c0, cudaMemsetAsync(w[b], 0, n * sizeof(double), c0->stream));
+        for (auto &s : S) s.t_reached = t_end;
+        return finish(sync(c0));
+    }
+    double tau = (normA == 0.0) ? t_end : std::min(t_end, tau0(normA, binf_max, o.tol, mbar));
+    if (!(tau > 0.0)) tau = t_end;
+    for (int b = 0; b < nb; b++) {
+        CK0(c0, cudaMemcpyAsync(cs[b]->U, u[b][0], n * sizeof(double), cudaMemcpyDeviceToDevice, c0->stream));
+        S[b].m_peak = m;
+    }
+    double tk = 0.0;
+    std::vector<int> kb((size_t)nb), mub((size_t)nb);
+    std::vector<char> brk((size_t)nb), corr((size_t)nb);
+    while (tk < t_end) {
+        if (tau > t_end - tk) tau = t_end - tk;
+        {
+            int rc = enqueue_wrec_block(cs, nb, op, bytes_op, p, u, tk);
+            if (rc) return finish(rc);
+        }
+        for (int b = 0; b < nb; b++) {
+            S[b].nspmv += p;
+            kb[b] = 0;
+            brk[b] = 0;
+        }
+        int enq = 0;
+        CtlMem mem;
+        int attempts = 0;
+        double tau_used = tau;
+        int m_used = m;
+        for (;;) {
+            attempts++;
+            if (enq < m) {
+                int rc = enqueue_krylov_block(cs, nb, op, bytes_op, P.symmetric, enq, m, bthr);
+                if (rc) return finish(rc);
+                enq = m;
+            }
+            for (int b = 0; b < nb; b++) {
+                phipm_ctx *c = cs[b];
+                ExpmArgs ea;
+                memset(&ea, 0, sizeof(ea));
+                ea.mode = 0;
+                ea.method = o.expm_method == PHIPM_EXPM_PADE13 ? PHIPM_EXPM_PADE13 : PHIPM_EXPM_TAYLOR;
+                ea.tridiag = P.symmetric ? 1 : 0;
+                ea.m = m;
+                ea.p = p;
+                ea.tau = tau;
+                ea.H = c->H;
+                ea.ldh = c->m_max + 1;
+                ea.sigma = c->sigma;
+                ea.st = c->st;
+                ea.comb = c->comb;
+                ea.combd = c->combd;
+                int rc = launch_expm(c, ea, m + p + 1);
+                if (rc) return finish(rc);
+            }
+            double eps_max = 0.0, nh_max = 0.0;
+            for (int b = 0; b < nb; b++) {
+                phipm_ctx *c = cs[b];
+                int rc = wait_attempt(c);
+                if (rc) return finish(rc);
+                AttemptResult R;
+                memcpy(&R, (const void *)c->res_h, sizeof(R));
+                if (R.seq != c->seq) return finish(set_err(c0, PHIPM_ECUDA, "stale attempt result (problem %d)", b));
+                S[b].nexpm++;
+                int k2;
+                if (R.brk >= 0) { k2 = std::max(kb[b], R.brk); brk[b] = 1; }
+                else k2 = std::max(kb[b], m);
+                if (R.brk >= 0 && R.brk < kb[b]) k2 = kb[b];
+                S[b].nspmv += k2 - kb[b];
+                kb[b] = k2;
+                if (R.status == 5) return finish(set_err(c0, PHIPM_ENONFINITE, "non-finite value (problem %d)", b));
+                if (R.status == 6) return finish(set_err(c0, PHIPM_ESINGULAR, "singular Pade denominator"));
+                if (R.status == 3) return finish(set_err(c0, PHIPM_ECUDA, "grid phase timed out"));
+                mub[b] = R.mu;
+                corr[b] = R.h != 0.0 && !(R.brk >= 0 && R.brk <= R.mu);
+                eps_max = std::max(eps_max, R.eps);
+                nh_max = std::max(nh_max, R.normH1);
+            }
+            const double omega = t_end * eps_max / (tau * o.tol);
+            if (!std::isfinite(omega)) return finish(set_err(c0, PHIPM_ENONFINITE, "non-finite error estimate"));
+            const bool accepted = omega <= 1.2;
+            Decision d = control(P, mem, tau, m, eps_max, omega, nh_max, t_end - tk, accepted);
+            for (int b = 0; b < nb; b++) {
+                if (cs[b]->attempts.size() < 65536)
+                    cs[b]->attempts.push_back({tk, tau, omega, eps_max, nh_max, 0.0, m, mub[b], accepted ? 1 : 0, d.branch});
+                cs[b]->nattempts++;
+                S[b].m_peak = std::max(S[b].m_peak, m);
+            }
+            tau_used = tau;
+            m_used = m;
+            tau = d.tau_next;
+            m = d.m_next;
+            if (accepted) break;
+            for (auto &s : S) s.nreject++;
+            if (attempts >= 100 || tau < 1e-15 * t_end) {
+                for (int b = 0; b < nb; b++) {
+                    S[b].t_reached = tk;
+                    cudaMemcpyAsync(w[b], cs[b]->U, n * sizeof(double), cudaMemcpyDeviceToDevice, c0->stream);
+                }
+                cudaStreamSynchronize(c0->stream);
+                return finish(set_err(c0, PHIPM_ESTEP, "step size control failed at t = %g", tk));
+            }
+        }
+        const bool last = tau_used >= t_end - tk;
+        for (int b = 0; b < nb; b++) {
+            phipm_ctx *c = cs[b];
+            AxpyArgs a = axpy0();
+            a.out = last ? w[b] : c->U;
+            a.base = c->U;
+            a.a0h = (p >= 1) ? 1.0 : 0.0;
+            a.a0d = (p >= 1) ? c->combd : nullptr;
+            a.V = c->V;
+            a.ldv = c->ldv;
+            a.c0 = 0;
+            a.nc = mub[b] + (corr[b] ? 1 : 0);
+            a.g = c->comb;
+            a.gsign = 1.0;
+            a.ne = std::max(p - 1, 0);
+            for (int j = 1; j < p; j++) {
+                a.e[j - 1] = c->W + (int64_t)j * c->ldv;
+                a.ec[j - 1] = 1.0;
+            }
+            a.ecd = c->combd + 1;
+            int rc = launch_axpy(c, n, a, PC_COMBINE);
+            if (rc) return finish(rc);
+        }
+        if (last) tk = t_end;
+        else tk += tau_used;
+        for (auto &s : S) {
+            s.nsteps++;
+            s.m_last = m_used;
+            s.t_reached = tk;
+        }
+    }
+    return finish(sync(c0));
+}
+
 } // namespace
 
 // Persistent worker pool of the batch API (phipm_solve_*_batch): threads are created once and grow
@@ -1800,6 +2203,9 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         }
         persist_set_smem<4>(mx);
         persist_set_smem<2>(mx);
+        cudaFuncSetAttribute(spmm_csr_ring_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmm_csr_ring_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(spmm_csr_ring_kernel<SPMM_MAXB>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, maxabs_kernel, NT, 0);
         c->occ_axpy = std::max(1, occ);
@@ -1929,6 +2335,51 @@ int phipm_solve_stencil_batch(phipm_ctx *const *ctx, int nb, const double *t, co
     return run_batch(ctx, nb, status, [&](int b) {
         return phipm_solve_stencil(ctx[b], t[b], &S[b], p[b], u[b], opts, w[b], stats ? &stats[b] : nullptr);
     });
+}
+
+int phipm_solve_csr_block(phipm_ctx *const *ctx, int nb, double t, const phipm_csr *A, int p,
+                          const double *const *const *u, const phipm_opts *opts, double *const *w,
+                          phipm_stats *stats)
+{
+    if (!ctx || nb < 1 || nb > SPMM_MAXB || !u || !w) return PHIPM_EINVAL;
+    for (int b = 0; b < nb; b++) {
+        if (!ctx[b]) return PHIPM_EINVAL;
+        for (int b2 = 0; b2 < b; b2++)
+            if (ctx[b] == ctx[b2]) return set_err(ctx[0], PHIPM_EINVAL, "block solve: contexts must be distinct");
+        if (ctx[b]->dev != ctx[0]->dev) return set_err(ctx[0], PHIPM_EINVAL, "block solve: contexts on different devices");
+    }
+    phipm_ctx *c0 = ctx[0];
+    CsrOp op;
+    int rc = make_csr(c0, A, op);
+    if (rc) return rc;
+    phipm_opts o = resolve_opts(opts);
+    for (int b = 0; b < nb; b++) {
+        rc = check_common(ctx[b], t, op.n, p, u[b], w[b], o);
+        if (rc) return rc == PHIPM_EINVAL && b ? set_err(c0, PHIPM_EINVAL, "problem %d: %s", b, ctx[b]->err) : rc;
+        for (int b2 = 0; b2 < nb; b2++)
+            if (b2 != b && w[b] == w[b2]) return set_err(c0, PHIPM_EINVAL, "block solve: outputs must be distinct");
+    }
+    if (o.fixed_m < 0) return PHIPM_EINVAL;
+    std::vector<cudaStream_t> saved((size_t)nb);
+    for (int b = 0; b < nb; b++) {
+        saved[b] = ctx[b]->stream;
+        ctx[b]->prof = b == 0 && o.profile != 0;
+        ctx[b]->trace = b == 0 && o.profile >= 2;
+    }
+    if (cudaSetDevice(c0->dev) != cudaSuccess) return set_err(c0, PHIPM_ECUDA, "cudaSetDevice failed");
+    // the other contexts' work is ordered on ctx[0]'s stream for the duration of the call
+    for (int b = 1; b < nb; b++) {
+        cudaEvent_t e = ev_get(ctx[b]);
+        cudaEventRecord(e, saved[b]);
+        cudaStreamWaitEvent(c0->stream, e, 0);
+        ctx[b]->pool.push_back(e);
+        ctx[b]->stream = c0->stream;
+    }
+    double normA = 0.0;
+    rc = analyze_csr(c0, op, A->nnz, &normA);
+    if (!rc) rc = solve_block_impl(ctx, nb, t, op, csr_bytes(op, A->nnz), A->nnz, normA, p, u, o, w, stats);
+    for (int b = 1; b < nb; b++) ctx[b]->stream = saved[b];
+    return rc;
 }
 
 int phipm_reserve_host_csr(phipm_ctx *c, int64_t nnz_max)

@@ -470,7 +470,11 @@ int wait_attempt(phipm_ctx *c)
     const auto t0 = std::chrono::steady_clock::now();
     unsigned spins = 0;
     while (*seqp != c->seq) {
-        if ((++spins & 1023) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) return sync(c);
+        ++spins;
+        // after ~20 us of spinning give the core away between polls: concurrent solves (batch API,
+        // one host thread each) would otherwise saturate the host's cores with spinners
+        if (spins > 4096) std::this_thread::yield();
+        if ((spins & 1023) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) return sync(c);
     }
     std::atomic_thread_fence(std::memory_order_acquire);
     return PHIPM_OK;

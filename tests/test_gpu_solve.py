@@ -306,7 +306,7 @@ def test_stencil_arnoldi_early_breakdown(ctx, orc, modes):
 # controller trajectory (Alg. 3/4) against the oracle's, attempt by attempt
 
 
-def _traj_compare(ga, tr, rtol_h=1e-9):
+def _traj_compare(ga, tr, rtol_h=1e-9, rtol_omega=1e-6):
     """Index of the first attempt whose decision differs, or len; asserts everything before it
     (and the decision inputs at it) agree.  rtol_h: ||H_mu||_1 (it only enters the cost model's
     M(.) through ceil(log2(.)), R20)."""
@@ -320,7 +320,7 @@ def _traj_compare(ga, tr, rtol_h=1e-9):
         # eps is the corrector term |h phi_{p+1}[mu]|: relative agreement only where it is well above
         # the rounding of the small exponential (omega >= 1e-6)
         if omega >= 1e-6:
-            assert g["omega"] == pytest.approx(omega, rel=1e-6), (i, g, o)
+            assert g["omega"] == pytest.approx(omega, rel=rtol_omega), (i, g, o)
         if g["accepted"] != int(acc) or g["branch"] != int(br):
             return i
     return min(len(ga), len(tr))
@@ -350,14 +350,15 @@ def test_controller_trajectory_c1(ctx, orc):
     """c1 (t||A|| = 4008, 15 steps): the trajectories agree attempt by attempt until the first
     decision that differs; there both controllers saw the same tau, m and omega to rounding (so the
     decision sat on a threshold: omega vs delta, a ceil in Eq. 3, or the Eq. 5 cost comparison).
-    ||H_mu||_1 is held to 1e-2 only: at m ~ 40 with t||A|| = 4008 the Lanczos vectors have lost
-    orthogonality (the extreme Ritz values converged), and the later T entries of two
-    implementations differ beyond rounding (measured: 2e-4 relative at attempt 7)."""
+    ||H_mu||_1 and omega are held to 1e-2 only: at m ~ 40 with t||A|| = 4008 the Lanczos vectors have
+    lost orthogonality (the extreme Ritz values converged), and the later T entries of two
+    implementations differ beyond rounding (measured at attempt 7: ||H||_1 2e-4, omega 7e-4
+    relative; both accept)."""
     Pb = W.make("c1")
     wg, sg = run_gpu(ctx, Pb, "stencil")
     ga = ctx.attempts()
     wo, so, tr = orc.solve(Pb)
-    i = _traj_compare(ga, tr, rtol_h=1e-2)
+    i = _traj_compare(ga, tr, rtol_h=1e-2, rtol_omega=1e-2)
     print(f"c1: trajectories agree for {i} of {len(tr)} oracle attempts; gpu {sg} oracle {so}")
     assert i >= 1
     assert relerr(wg, wo) <= parity_bound(Pb.tol)
@@ -385,7 +386,7 @@ def test_guard_regions_and_inputs_untouched(orc, name, path, opts):
         c.solve_stencil(Pb.t, stencil_of(Pb), u, out=w, tol=Pb.tol, symmetric=Pb.symmetric)
         A = A_copy = ()
     else:
-        A = tuple(to_dev(a) for a in Pb.csr)
+        A = tuple(to_dev(a) for a in Pb.csr) if Pb.csr is not None else c.csr_from_stencil(stencil_of(Pb))
         A_copy = tuple(a.clone() for a in A)
         c.solve_csr(Pb.t, A, u, out=w, tol=Pb.tol, symmetric=Pb.symmetric)
     torch.cuda.synchronize()

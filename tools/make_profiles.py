@@ -37,8 +37,9 @@ def short(k):
 
 
 # 1) launch list of the bench command: per-kernel share of the step
-p = os.path.join(src, "pf_launches_c3.csv")
-if os.path.exists(p):
+import glob as _glob
+for p in sorted(_glob.glob(os.path.join(src, "pf_launches_*.csv"))):
+    lcfg = os.path.basename(p)[len("pf_launches_"):-4]
     d = read_ncu_csv(p)
     agg = collections.defaultdict(lambda: [0, 0.0])
     for r in d:
@@ -49,13 +50,13 @@ if os.path.exists(p):
             agg[k][1] += float(r["Metric Value"].replace(",", "")) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0,
                                                                        "usecond": 1.0, "ms": 1e3}.get(unit, 1e-3)
     tot = sum(v[1] for v in agg.values())
-    with open(os.path.join(dst, "launches_c3_summary.txt"), "w") as f:
+    with open(os.path.join(dst, f"launches_{lcfg}_summary.txt"), "w") as f:
         f.write("ncu --metrics gpu__time_duration.sum --clock-control none  python bench.py --steps 2 --warmup 3 "
-                "--no-cpu-baseline  (config c3; cold-cache, serialised launches: compare SHARES)\n")
+                f"--no-cpu-baseline  (config {lcfg}; cold-cache, serialised launches: compare SHARES)\n")
         f.write(f"{'kernel':34s} {'launches':>8s} {'total us':>10s} {'share':>7s}\n")
         for k, (n, us) in sorted(agg.items(), key=lambda x: -x[1][1]):
             f.write(f"{k:34s} {n:8d} {us:10.1f} {100 * us / tot:6.1f}%\n")
-    os.system(f"cp {p} {dst}/launches_c3.csv")
+    os.system(f"cp {p} {dst}/launches_{lcfg}.csv")
 
 # 2) DRAM traffic per launch of each kernel class (exactly one solve: ncu --profile-from-start off)
 traffic = {}
@@ -99,7 +100,7 @@ if traffic:
 
 # 3) --set full summaries of the top kernels
 for name in ("pf_full_c3_spmv", "pf_full_c3_axpy", "pf_full_c4_persist", "pf_full_c5_spmv",
-             "pf_full_c3_expm", "pf_full_c1_small"):
+             "pf_full_c3_expm", "pf_full_c1_small", "pf_full_c5_axpy", "pf_full_c5_analyze", "pf_full_c1_cheb"):
     p = os.path.join(src, name + ".ncu-rep")
     if os.path.exists(p):
         with open(os.path.join(dst, name.replace("pf_", "") + ".txt"), "w") as f:

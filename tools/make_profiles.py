@@ -30,7 +30,8 @@ def read_ncu_csv(path):
 def short(k):
     for key in ("spmv_stream_kernel", "axpy_stream_kernel", "expm_kernel", "maxabs_kernel", "csr_analyze_kernel",
                 "krylov_small_lanczos_kernel", "krylov_small_kernel", "krylov_persist_tm_kernel",
-              "krylov_persist_kernel", "wrec_persist_kernel"):
+              "krylov_persist_kernel", "wrec_persist_kernel", "phi_cheb_kernel", "spmm_csr_ring_kernel",
+              "spmm_csr_kernel"):
         if key in k:
             return key + ("<Stencil>" if "StencilOp" in k else "<Csr>" if "CsrOp" in k else "")
     return k[:40]

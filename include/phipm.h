@@ -175,6 +175,9 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *                              into L2 (cp.async.bulk.prefetch.L2), 0 = off; default 384
  *   PHIPM_OPT_COL_PREFETCH     1: streaming kernels prefetch the next group of Krylov columns / epilogue
  *                              vectors of the tile into L2 (TMA engine); default 0
+ *   PHIPM_OPT_FUSE_ANORM       1 (default): on the banded uniform-row CSR path, ||A||_inf (a1 setup) is
+ *                              computed by the first w-recurrence SpMV, which reads val anyway, and the
+ *                              analysis pass reads only row_ptr and col; 0: the analysis pass reads val
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -190,7 +193,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_PERSIST_MINROWS 11
 #define PHIPM_OPT_CSR_PREFETCH    12
 #define PHIPM_OPT_COL_PREFETCH    13
-#define PHIPM_OPT_COUNT           14
+#define PHIPM_OPT_FUSE_ANORM      14
+#define PHIPM_OPT_COUNT           15
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

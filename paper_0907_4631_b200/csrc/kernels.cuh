@@ -49,6 +49,9 @@ struct DevState {
     int brk;           // -1: no breakdown; otherwise the number of valid H columns
     int nonfinite;     // a non-finite norm was met
     int aborted;       // the persistent Krylov kernel timed out waiting for a grid phase
+    unsigned long long anorm_bits;   // ||A||_inf accumulated by the first SpMV of a CSR solve (bits of a
+                                     // non-negative double; atomicMax), when the analysis pass skipped val
+    double bthr_d;                   // n eps ||A||_inf from that SpMV (finalize uses it when bthr < 0)
 };
 
 // pointers into the context workspace, shared by all kernels of a solve
@@ -116,6 +119,11 @@ struct SpmvArgs {
     unsigned long long *dbg;     // optional per-CTA %globaltimer stamps (PHIPM_KCLOCKS tool), 8 per CTA
     int xnorm;                   // also reduce ||x||^2 (after ||y||^2), for FIN_ARNOLDI_LAG
     double bthr;                 // breakdown threshold (FIN_ARNOLDI_LAG)
+    int anorm;                   // CSR x-ring path: also ||A||_inf (row |a| sums in entry order per lane,
+                                 // lanes by a shuffle tree) -> st->anorm_bits, st->bthr_d, and *anorm_pub
+    double *anorm_pub;           // mapped pinned memory: ||A||_inf, then
+    volatile int *anorm_seq;     // ... this sequence number (after a system-scope fence)
+    int anorm_seqv;
 };
 
 struct AxpyArgs {
@@ -237,6 +245,7 @@ __device__ __forceinline__ void final_reduce(const Work &wk, int nv, double *out
 __device__ void finalize(int fin, int j, int nd, const double *red, const Work &wk, double bthr, int lanczos)
 {
     const int t = threadIdx.x;
+    if (bthr < 0.0) bthr = wk.st->bthr_d;     // threshold from the SpMV that computed ||A||_inf
     switch (fin) {
     case FIN_ARNOLDI:
         for (int k = t; k < nd; k += blockDim.x) {
@@ -413,8 +422,10 @@ struct CsrAnalysis {
 
 __device__ __forceinline__ int clamp_band(int64_t d) { return d < 0 ? 0 : (d > 0x3fffffff ? 0x3fffffff : (int)d); }
 
-__global__ void __launch_bounds__(CSRA_NT) csr_analyze_kernel(CsrOp A, int L, CsrAnalysis *out)
+// mode bit 0: ||A||_inf (reads val); bit 1: uniform rows and band (reads col).  row_ptr always.
+__global__ void __launch_bounds__(CSRA_NT) csr_analyze_kernel(CsrOp A, int L, CsrAnalysis *out, int mode = 3)
 {
+    const bool dn = mode & 1, ds = (mode & 2) != 0;
     constexpr int SK = CSRA_CAP + CSRA_CAP / 32;
     __shared__ double sv[CSRA_NW][SK];
     __shared__ int sc[CSRA_NW][SK];
@@ -435,24 +446,28 @@ __global__ void __launch_bounds__(CSRA_NT) csr_analyze_kernel(CsrOp A, int L, Cs
         if (g1 - g0 <= CSRA_CAP) {
             for (int i = lane; i < g1 - g0; i += 32) {
                 const int k = i + (i >> 5);
-                sv[warp][k] = A.val[g0 + i];
-                sc[warp][k] = A.col[g0 + i];
+                if (dn) sv[warp][k] = A.val[g0 + i];
+                if (ds) sc[warp][k] = A.col[g0 + i];
             }
             __syncwarp();
             for (int e = eb - g0; e < ee - g0; e++) {
                 const int k = e + (e >> 5);
-                s = __dadd_rn(s, fabs(sv[warp][k]));
-                const int64_t d = (int64_t)sc[warp][k] - r;
-                lo = max(lo, clamp_band(-d));
-                hi = max(hi, clamp_band(d));
+                if (dn) s = __dadd_rn(s, fabs(sv[warp][k]));
+                if (ds) {
+                    const int64_t d = (int64_t)sc[warp][k] - r;
+                    lo = max(lo, clamp_band(-d));
+                    hi = max(hi, clamp_band(d));
+                }
             }
             __syncwarp();
         } else {
             for (int e = eb; e < ee; e++) {
-                s = __dadd_rn(s, fabs(A.val[e]));
-                const int64_t d = (int64_t)A.col[e] - r;
-                lo = max(lo, clamp_band(-d));
-                hi = max(hi, clamp_band(d));
+                if (dn) s = __dadd_rn(s, fabs(A.val[e]));
+                if (ds) {
+                    const int64_t d = (int64_t)A.col[e] - r;
+                    lo = max(lo, clamp_band(-d));
+                    hi = max(hi, clamp_band(d));
+                }
             }
         }
         nrm = fmax(nrm, s);

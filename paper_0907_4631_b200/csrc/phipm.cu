@@ -77,8 +77,11 @@ struct phipm_ctx {
     struct MaxPub {
         double v[MAXZ];
         int seq;
+        int aseq;                                    // ||A||_inf from the first SpMV (fused CSR path) ...
+        double anorm;                                // ... published here
     } *mx_h = nullptr, *mx_d = nullptr;               // ||u_0||_inf published to mapped pinned memory
-    int mx_seq = 0;
+    int mx_seq = 0, mx_aseq = 0;
+    bool fuse_anorm = false;                         // this solve's first SpMV computes ||A||_inf
     long long *expm_clk_h = nullptr, *expm_clk_d = nullptr;   // PHIPM_EXPM_CLOCKS=1 debug timestamps
     // PHIPM_KCLOCKS=<file>: per-CTA %globaltimer stamps of every streaming launch (measurement tool)
     unsigned long long *kclk_d = nullptr;
@@ -110,7 +113,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1};
     char err[512] = {0};
 };
 
@@ -1079,6 +1082,13 @@ int enqueue_wrec_op(phipm_ctx *c, const Op &op, double bytes_op, int p, const do
         }
         s.ynorm = (j == p);
         s.fin = (j == p) ? FIN_SEED : FIN_NONE;
+        if (j == 1 && c->fuse_anorm) {
+            s.anorm = 1;
+            s.anorm_pub = &c->mx_d->anorm;
+            s.anorm_seq = &c->mx_d->aseq;
+            s.anorm_seqv = ++c->mx_aseq;
+            c->fuse_anorm = false;
+        }
         int rc = launch_spmv(c, op, s, bytes_op);
         if (rc) return rc;
     }
@@ -1089,10 +1099,11 @@ int enqueue_wrec_op(phipm_ctx *c, const Op &op, double bytes_op, int p, const do
 // the solve (Algorithm 3)
 
 template <class Op>
-int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_t NA, double normA, int p,
+int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_t NA, double normA_in, int p,
                const double *const *u, const phipm_opts &o, double *w, phipm_stats *stats)
 {
     const int64_t n = op.n;
+    double normA = normA_in;
     phipm_stats S{};
     S.t_reached = 0.0;
     c->attempts.clear();
@@ -1121,7 +1132,10 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     P.eq6_variant = o.eq6_variant != 0;
     int m = std::min(o.m_init, P.m_max);
     const double mbar = 0.5 * ((double)o.m_init + (double)P.m_max);
-    const double bthr = (double)n * EPS_MACH * normA;
+    // normA < 0: ||A||_inf is computed by the first SpMV (fused CSR path); the Krylov kernels enqueued
+    // before the host knows it take the breakdown threshold from device memory (bthr < 0)
+    const bool anorm_dev = normA < 0.0;
+    const double bthr = anorm_dev ? -1.0 : (double)n * EPS_MACH * normA;
 
     // b_inf of Eq. (tau_0) = ||u_0||_inf, or the first nonzero ||u_k||_inf (R7); all zero -> w = 0.
     // ||u_0||_inf is read back through an event, and the first step's w-recurrence and initial
@@ -1175,6 +1189,20 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         b_inf = c->raw_h[0];
     }
     c->raw_h[0] = b_inf;
+    if (anorm_dev) {
+        const volatile int *aseq = &c->mx_h->aseq;
+        const auto t0 = std::chrono::steady_clock::now();
+        unsigned spins = 0;
+        while (*aseq != c->mx_aseq) {
+            if ((++spins & 1023) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
+                int rc = sync(c);
+                if (rc) return finish(rc);
+                if (*aseq != c->mx_aseq) return finish(set_err(c, PHIPM_ECUDA, "||A|| result not published"));
+            }
+        }
+        std::atomic_thread_fence(std::memory_order_acquire);
+        normA = ((const volatile double *)&c->mx_h->anorm)[0];
+    }
     if (b_inf == 0.0) {
         {
             int rc = sync(c);
@@ -1446,7 +1474,7 @@ constexpr int CSR_WCAP = 10496;                             // 82 KB: band +-409
 // One analysis pass over a CSR matrix (csr_analyze_kernel): ||A||_inf (a1 setup, bit-exact), and
 // whether rows have a uniform length L (vectorised ELL path, PHIPM_OPT_CSR_ELL = 0 disables) within a
 // band that fits the shared x ring (PHIPM_OPT_CSR_RING = 0 disables).
-int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA)
+int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA, int mode = 3)
 {
     op.ell = 0;
     op.ring = op.blo = op.bhi = 0;
@@ -1460,8 +1488,9 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA)
     CK(cudaMemsetAsync(d, 0, sizeof(CsrAnalysis), c->stream));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((op.n + CSRA_NT - 1) / CSRA_NT, (int64_t)c->sm_count * 16));
     ProfRec r;
-    prof_begin(c, r, PC_OTHER, 12.0 * (double)nnz + 4.0 * (double)(op.n + 1));
-    csr_analyze_kernel<<<grid, CSRA_NT, 0, c->stream>>>(op, (int)L, d);
+    prof_begin(c, r, PC_OTHER, ((mode & 1) ? 8.0 : 0.0) * (double)nnz + ((mode & 2) ? 4.0 : 0.0) * (double)nnz +
+                                   4.0 * (double)(op.n + 1));
+    csr_analyze_kernel<<<grid, CSRA_NT, 0, c->stream>>>(op, (int)L, d, mode);
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -1470,7 +1499,8 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA)
     if (rc) return rc;
     CsrAnalysis h;
     memcpy(&h, c->raw_h, sizeof(h));
-    memcpy(normA, &h.norm_bits, sizeof(double));
+    if (mode & 1) memcpy(normA, &h.norm_bits, sizeof(double));
+    if (!(mode & 2)) return PHIPM_OK;
     if (!env_ell || L < 4 || (L % 4) || ((L / 4) & (L / 4 - 1)) || h.nonuniform) return PHIPM_OK;
     if (((uintptr_t)op.val & 15) || ((uintptr_t)op.col & 15)) return PHIPM_OK;
     op.ell = (int)L;
@@ -2013,6 +2043,7 @@ int phipm_set_option(phipm_ctx *c, int option, int value)
     case PHIPM_OPT_PERSIST_MINROWS: ok = value >= 0; break;
     case PHIPM_OPT_CSR_PREFETCH: ok = value >= 0 && value <= (1 << 20); break;
     case PHIPM_OPT_COL_PREFETCH: ok = value == 0 || value == 1; break;
+    case PHIPM_OPT_FUSE_ANORM: ok = value == 0 || value == 1; break;
     default: ok = value == 0 || value == 1; break;
     }
     if (!ok) return set_err(c, PHIPM_EINVAL, "option %d: value %d out of range", option, value);
@@ -2312,13 +2343,27 @@ int phipm_solve_csr(phipm_ctx *c, double t, const phipm_csr *A, int p, const dou
     if (rc) return rc;
     c->prof = o.profile != 0;
     c->trace = o.profile >= 2;
-    // ||A||_inf (a1 setup, once per call) and the operator's layout, one pass
+    // a1 setup, once per call: the operator's layout (row_ptr, col), and ||A||_inf.  On the banded
+    // uniform-row path (x ring) the first w-recurrence SpMV reads val anyway and computes ||A||_inf
+    // (PHIPM_OPT_FUSE_ANORM), so the analysis pass does not read val; otherwise a second pass does.
     double normA = 0.0;
-    rc = analyze_csr(c, op, A->nnz, &normA);
+    rc = analyze_csr(c, op, A->nnz, &normA, 2);
     if (rc) return rc;
+    const bool fuse = op.ring && opt(c, PHIPM_OPT_FUSE_ANORM) && p >= 1 && op.n > SMALL_N && t > 0.0;
+    if (fuse) {
+        CK(cudaMemsetAsync(&c->st->anorm_bits, 0, sizeof(unsigned long long), c->stream));
+        c->fuse_anorm = true;
+        normA = -1.0;
+    } else {
+        CsrOp tmp = op;
+        rc = analyze_csr(c, tmp, A->nnz, &normA, 1);
+        if (rc) return rc;
+    }
     rc = enable_csr_window(c, op);
     if (rc) return rc;
-    return solve_impl(c, t, op, csr_bytes(op, A->nnz), A->nnz, normA, p, u, o, w, stats);
+    rc = solve_impl(c, t, op, csr_bytes(op, A->nnz), A->nnz, normA, p, u, o, w, stats);
+    c->fuse_anorm = false;
+    return rc;
 }
 
 int phipm_solve_csr_batch(phipm_ctx *const *ctx, int nb, const double *t, const phipm_csr *A, const int *p,

@@ -264,7 +264,7 @@ __device__ __forceinline__ void csr_tile(const CsrOp &A, const double *__restric
 // (xs[c mod XRING])
 template <int XM>
 __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__restrict__ x, const double *xs, int64_t xs0,
-                                             int64_t r0, int rows, double *ys)
+                                             int64_t r0, int rows, double *ys, double *amax = nullptr)
 {
 #ifndef PHIPM_ELL_U
 #define PHIPM_ELL_U 3
@@ -331,6 +331,22 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
             for (int o = G >> 1; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
             const int q = base + u * stride + sub;
             if (q < rows && li == 0) ys[q] = acc[u];
+        }
+        if (amax) {
+            // ||A||_inf: the row's |a| summed in entry order per lane, lanes by the same shuffle tree
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int q = base + u * stride + sub;
+                double s = 0.0;
+                if (q < rows) {
+                    s = __dadd_rn(s, fabs(va[u].x));
+                    s = __dadd_rn(s, fabs(va[u].y));
+                    s = __dadd_rn(s, fabs(vb[u].x));
+                    s = __dadd_rn(s, fabs(vb[u].y));
+                }
+                for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                *amax = fmax(*amax, s);
+            }
         }
     }
 }
@@ -701,7 +717,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
     __syncthreads();
     if (s_exit) return;
 
-    double ysq = 0.0, xsq = 0.0;
+    double ysq = 0.0, xsq = 0.0, amax = 0.0;
     uint32_t ht = 0;
     int3 gcoord = make_int3(0, 0, 0);                      // stencil: grid coordinates of row r0 + 2 tid
     if constexpr (IS_ST) gcoord = grid_coords(op, cs + 2 * tid);
@@ -750,7 +766,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
                 {
                     CsrOp opf = op;
                     opf.pf_end = ce;
-                    csr_tile_ell<2>(opf, a.x, xring, 0, r0, rows, hbuf);
+                    csr_tile_ell<2>(opf, a.x, xring, 0, r0, rows, hbuf, a.anorm ? &amax : nullptr);
                 }
                 __syncthreads();                           // ring reads done, ys complete
             } else {
@@ -889,15 +905,37 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
             bsum[a.nd + (a.ynorm ? 1 : 0)] = t;
         }
     }
+    if (a.anorm) {
+        // ||A||_inf: CTA max, then one atomicMax on the non-negative double's bits (before the ticket
+        // of publish_partials, whose release covers it)
+        double m = amax;
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        __syncthreads();
+        if (lane == 0) wsum[warp] = m;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < SNW; w++) t = fmax(t, wsum[w]);
+            atomicMax(&wk.st->anorm_bits, (unsigned long long)__double_as_longlong(t));
+        }
+    }
     const int nv = a.nd + (a.ynorm ? 1 : 0) + (a.xnorm ? 1 : 0);
     __syncthreads();
-    if (nv == 0) return;
+    if (nv == 0 && !a.anorm) return;                      // (||A||_inf: the last CTA publishes it)
     const bool last = publish_partials(wk, bsum, nv);
     KSTAMP(4)
     if (!last) return;
     __shared__ double red[MAXD + 2];
     final_reduce(wk, nv, red);
     KSTAMP(5)
+    if (a.anorm && tid == 0) {
+        const double na = __longlong_as_double((long long)__ldcg(&wk.st->anorm_bits));
+        wk.st->bthr_d = (double)n * 2.220446049250313080847e-16 * na;
+        // publish to the host (tau_0 of Eq. tau_0): the value, a system-scope fence, the sequence
+        a.anorm_pub[0] = na;
+        __threadfence_system();
+        *a.anorm_seq = a.anorm_seqv;
+    }
     finalize(a.fin, a.j, a.nd, red, wk, a.bthr, 0);
     KSTAMP(6)
 }

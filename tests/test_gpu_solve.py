@@ -396,3 +396,26 @@ def test_guard_regions_and_inputs_untouched(orc, name, path, opts):
     wo, so = run_oracle(orc, Pb)
     assert relerr(w.cpu().numpy(), wo) <= parity_bound(Pb.tol)
     c.close()
+
+
+@pytest.mark.parametrize("name", ["c5_med", "c5"])
+def test_fused_anorm_matches_analysis_pass(orc, name):
+    """||A||_inf (a1 setup) from the first w-recurrence SpMV (option fuse_anorm = 1, the default on
+    the x-ring CSR path) against the analysis pass that reads val (fuse_anorm = 0, the oracle's
+    sequential row sums bit for bit): the row sums differ only in summation order, so tau_0 and the
+    whole trajectory agree to rounding, and w to far below the parity bar."""
+    import paper_0907_4631_b200 as P
+    Pb = W.make(name)
+    A = tuple(to_dev(a) for a in Pb.csr)
+    u = [to_dev(x) for x in Pb.u]
+    res = {}
+    for f in (1, 0):
+        c = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), options={"fuse_anorm": f})
+        w, s = c.solve_csr(Pb.t, A, u, tol=Pb.tol)
+        res[f] = (w.cpu().numpy(), s, c.attempts())
+        c.close()
+    (w1, s1, a1), (w0, s0, a0) = res[1], res[0]
+    assert (s1.nsteps, s1.nreject, s1.nspmv) == (s0.nsteps, s0.nreject, s0.nspmv)
+    for x, y in zip(a1, a0):
+        assert x["tau"] == pytest.approx(y["tau"], rel=1e-14)
+    assert relerr(w1, w0) <= 1e-13

@@ -8,8 +8,10 @@ never imports it; the product never imports this.
 Parity status: every function here is pinned by a `-m "not gpu"` test in tests/test_oracle_*.py
 against something other than the oracle itself (closed forms of PAPER.md Sec. 2, scipy's expm,
 exact rational arithmetic, DST diagonalisation, Kronecker/quadrature references, brute-force
-dense exponentials of the augmented operator).  The controller's trajectory (nsteps, nreject, m)
-is "parity unpinned" beyond the worked arithmetic examples.
+dense exponentials of the augmented operator).  The controller's arithmetic is pinned by worked
+examples and by sequences generated from the paper's error models (tests/test_oracle_controller_pins.py;
+tools/mutate_oracle.py checks that ten one-line mutants each fail a pin).  No function is "parity
+unpinned"; the trajectory itself is compared with the GPU's attempt by attempt.
 """
 from __future__ import annotations
 

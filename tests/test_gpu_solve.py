@@ -306,7 +306,7 @@ def test_stencil_arnoldi_early_breakdown(ctx, orc, modes):
 # controller trajectory (Alg. 3/4) against the oracle's, attempt by attempt
 
 
-def _traj_compare(ga, tr, rtol_h=1e-9, rtol_omega=1e-6, rtol_tau=1e-9):
+def _traj_compare(ga, tr, rtol_h=1e-9, rtol_omega=1e-6, rtol_tau=1e-9, rtol_beta=1e-10):
     """Index of the first attempt whose decision differs, or len; asserts everything before it
     (and the decision inputs at it) agree.  rtol_h: ||H_mu||_1 (it only enters the cost model's
     M(.) through ceil(log2(.)), R20)."""
@@ -315,7 +315,7 @@ def _traj_compare(ga, tr, rtol_h=1e-9, rtol_omega=1e-6, rtol_tau=1e-9):
         assert g["m"] == int(m) and g["mu"] == int(mu), (i, g, o)
         assert g["tau"] == pytest.approx(tau, rel=rtol_tau), (i, g, o)
         assert g["t_k"] == pytest.approx(t_k, rel=max(1e-12, rtol_tau), abs=1e-300), (i, g, o)
-        assert g["beta"] == pytest.approx(beta, rel=1e-10), (i, g, o)
+        assert g["beta"] == pytest.approx(beta, rel=rtol_beta), (i, g, o)
         assert g["normH1"] == pytest.approx(nh, rel=rtol_h), (i, g, o)
         # eps is the corrector term |h phi_{p+1}[mu]|: relative agreement only where it is well above
         # the rounding of the small exponential (omega >= 1e-6)
@@ -353,12 +353,13 @@ def test_controller_trajectory_c1(ctx, orc):
     ||H_mu||_1 and omega are held to 1e-2 only: at m ~ 40 with t||A|| = 4008 the Lanczos vectors have
     lost orthogonality (the extreme Ritz values converged), and the later T entries of two
     implementations differ beyond rounding (measured at attempt 7: ||H||_1 2e-4, omega 7e-4
-    relative; both accept), and tau (Eq. 2 of that omega) inherits the drift (5e-5 at the next step)."""
+    relative; both accept), and tau (Eq. 2 of that omega) inherits the drift (5e-5 at the next step),
+    as does beta = ||w_p|| of the later steps (w_p = A^p u_k amplifies the difference of u_k)."""
     Pb = W.make("c1")
     wg, sg = run_gpu(ctx, Pb, "stencil")
     ga = ctx.attempts()
     wo, so, tr = orc.solve(Pb)
-    i = _traj_compare(ga, tr, rtol_h=1e-2, rtol_omega=1e-2, rtol_tau=1e-2)
+    i = _traj_compare(ga, tr, rtol_h=1e-2, rtol_omega=1e-2, rtol_tau=1e-2, rtol_beta=1e-2)
     print(f"c1: trajectories agree for {i} of {len(tr)} oracle attempts; gpu {sg} oracle {so}")
     assert i >= 1
     assert relerr(wg, wo) <= parity_bound(Pb.tol)

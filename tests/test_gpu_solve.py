@@ -347,21 +347,20 @@ def test_controller_trajectory_matches_oracle(ctx, orc, name, path):
 
 
 def test_controller_trajectory_c1(ctx, orc):
-    """c1 (t||A|| = 4008, 15 steps): the trajectories agree attempt by attempt until the first
-    decision that differs; there both controllers saw the same tau, m and omega to rounding (so the
-    decision sat on a threshold: omega vs delta, a ceil in Eq. 3, or the Eq. 5 cost comparison).
-    ||H_mu||_1 and omega are held to 1e-2 only: at m ~ 40 with t||A|| = 4008 the Lanczos vectors have
-    lost orthogonality (the extreme Ritz values converged), and the later T entries of two
-    implementations differ beyond rounding (measured at attempt 7: ||H||_1 2e-4, omega 7e-4
-    relative; both accept), and tau (Eq. 2 of that omega) inherits the drift (5e-5 at the next step),
-    as does beta = ||w_p|| of the later steps (w_p = A^p u_k amplifies the difference of u_k)."""
+    """c1 (t||A|| = 4008, 14-15 steps): the first step's attempts agree with the oracle's to rounding
+    (tau 1e-9, omega 1e-6, same m / accept / branch).  Later the Lanczos vectors lose orthogonality
+    (m ~ 40 with the extreme Ritz values converged) and the T entries of two implementations drift
+    apart beyond rounding (measured: ||H||_1 2e-4, omega 7e-4 at attempt 7, 1.3e-2 at attempt 9; tau and
+    beta inherit it), so the rest is held to the solution (parity bar) and to the trajectory's size."""
     Pb = W.make("c1")
     wg, sg = run_gpu(ctx, Pb, "stencil")
     ga = ctx.attempts()
     wo, so, tr = orc.solve(Pb)
-    i = _traj_compare(ga, tr, rtol_h=1e-2, rtol_omega=1e-2, rtol_tau=1e-2, rtol_beta=1e-2)
-    print(f"c1: trajectories agree for {i} of {len(tr)} oracle attempts; gpu {sg} oracle {so}")
-    assert i >= 1
+    first = int(np.argmax(tr[:, 6] == 1)) + 1           # attempts of the first step (through its accept)
+    assert _traj_compare(ga[:first], tr[:first]) == first
+    print(f"c1: gpu {sg} oracle {so}")
+    assert abs(sg.nsteps - so["nsteps"]) <= 2
+    assert abs(sg.nspmv - so["nspmv"]) <= 0.1 * so["nspmv"]
     assert relerr(wg, wo) <= parity_bound(Pb.tol)
 
 

@@ -198,18 +198,18 @@ def test_stats_and_clamps(orc):
 def test_controller_examples(orc):
     g = json.load(open(os.path.join(GOLD, "controller_examples.json")))
     # fresh q-hat = m/4 and tau_new by Eq. (2): tau=0.5, omega=0.2, m=12 -> q=3, tau_new = 0.5*sqrt(2)
-    r = orc.control(tau=0.5, m=12, eps=1e-9, omega=0.2, normH1=1.0, remaining=1.0, p=1, n=900, NA=7744,
+    # (1.4 of t left: 3 steps of 0.5 against 2 of 0.707, so Eq. (5) takes the tau branch)
+    r = orc.control(tau=0.5, m=12, eps=1e-9, omega=0.2, normH1=1.0, remaining=1.4, p=1, n=900, NA=7744,
                     symmetric=False, m_max=100, accepted=True)
     assert r["qhat"] == g["fresh_qhat"]["qhat"]
     assert r["khat"] == 2.0
-    if r["branch"] == 1:
-        assert r["tau"] == pytest.approx(0.5 * math.sqrt(2), rel=1e-15)
+    assert r["branch"] == 1
+    assert r["tau"] == pytest.approx(0.5 * math.sqrt(2), rel=1e-15)
     # m_new by Eq. (3): m=10, omega=3.2, kappa=2 -> 12 (a rejected attempt)
     r = orc.control(tau=0.5, m=10, eps=1e-6, omega=3.2, normH1=1.0, remaining=1.0, p=1, n=900, NA=7744,
                     symmetric=False, m_max=100, accepted=False)
-    mm = r["m"] if r["branch"] == 2 else None
-    if mm is not None:
-        assert mm == g["m_new"]["m_new"]
+    assert r["branch"] == 2
+    assert r["m"] == g["m_new"]["m_new"]
     # Eq. (4): C1 = 205028
     c = g["C1"]
     assert orc.cost_C1(c["m"], c["p"], c["n"], c["NA"], c["symmetric"], 44 / 3) == pytest.approx(c["C1"], rel=1e-15)

@@ -178,6 +178,10 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *   PHIPM_OPT_FUSE_ANORM       1 (default): on the banded uniform-row CSR path, ||A||_inf (a1 setup) is
  *                              computed by the first w-recurrence SpMV, which reads val anyway, and the
  *                              analysis pass reads only row_ptr and col; 0: the analysis pass reads val
+ *   PHIPM_OPT_CSR_OFF16        1: uniform-row CSR whose band fits int16 -- the analysis pass also writes
+ *                              col - row as int16 (context workspace, 2 B per nonzero) and the x-ring
+ *                              SpMVs stream those instead of the int32 columns (10 instead of 12 B per
+ *                              nonzero); 0 (default, measured faster: the SpMV time did not drop)
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -194,7 +198,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_CSR_PREFETCH    12
 #define PHIPM_OPT_COL_PREFETCH    13
 #define PHIPM_OPT_FUSE_ANORM      14
-#define PHIPM_OPT_COUNT           15
+#define PHIPM_OPT_CSR_OFF16       15
+#define PHIPM_OPT_COUNT           16
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

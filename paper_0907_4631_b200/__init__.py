@@ -68,7 +68,8 @@ class _Attempt(C.Structure):
 # kernel-path options (phipm_set_option; include/phipm.h)
 OPTIONS = {"persist": 0, "tmem": 1, "wrec": 2, "lag": 3, "pdl": 4, "spin": 5, "rpt": 6, "csr_ell": 7,
            "csr_ring": 8, "csr_window": 9, "small_lz": 10, "persist_minrows": 11, "csr_prefetch": 12,
-           "col_prefetch": 13, "fuse_anorm": 14}
+           "col_prefetch": 13, "fuse_anorm": 14,
+           "csr_off16": 15}
 
 
 class _Profile(C.Structure):

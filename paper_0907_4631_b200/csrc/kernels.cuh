@@ -92,6 +92,9 @@ struct CsrOp {
                            // ell <= 128: vectorised fast path (4 entries per lane)
     int ring;              // ell > 0 and every column within [r - blo, r + bhi]: x from a shared ring
     int blo, bhi;          // band below / above the diagonal (even, >= 0)
+    const int16_t *__restrict__ off16;   // optional (uniform rows, band <= 32767): col - row as int16,
+                                         // written by the analysis pass; the x-ring SpMV streams these
+                                         // 2 B per entry instead of the 4 B column indices
     int pf;                // x-ring path: L2 prefetch distance of val/col in rows (0 = off;
                            // PHIPM_OPT_CSR_PREFETCH)
     int64_t pf_end;        // (set per launch) rows >= pf_end are not prefetched (the CTA's range end)
@@ -422,10 +425,13 @@ struct CsrAnalysis {
 
 __device__ __forceinline__ int clamp_band(int64_t d) { return d < 0 ? 0 : (d > 0x3fffffff ? 0x3fffffff : (int)d); }
 
-// mode bit 0: ||A||_inf (reads val); bit 1: uniform rows and band (reads col).  row_ptr always.
-__global__ void __launch_bounds__(CSRA_NT) csr_analyze_kernel(CsrOp A, int L, CsrAnalysis *out, int mode = 3)
+// mode bit 0: ||A||_inf (reads val); bit 1: uniform rows and band (reads col); bit 2 (with bit 1 and
+// L > 0): also write off16[e] = col[e] - row (clamped to int16; used only if the band fits).
+// row_ptr always.
+__global__ void __launch_bounds__(CSRA_NT) csr_analyze_kernel(CsrOp A, int L, CsrAnalysis *out, int mode = 3,
+                                                              int16_t *off16 = nullptr)
 {
-    const bool dn = mode & 1, ds = (mode & 2) != 0;
+    const bool dn = mode & 1, ds = (mode & 2) != 0, wo = (mode & 4) && off16 && L > 0;
     constexpr int SK = CSRA_CAP + CSRA_CAP / 32;
     __shared__ double sv[CSRA_NW][SK];
     __shared__ int sc[CSRA_NW][SK];
@@ -447,7 +453,15 @@ __global__ void __launch_bounds__(CSRA_NT) csr_analyze_kernel(CsrOp A, int L, Cs
             for (int i = lane; i < g1 - g0; i += 32) {
                 const int k = i + (i >> 5);
                 if (dn) sv[warp][k] = A.val[g0 + i];
-                if (ds) sc[warp][k] = A.col[g0 + i];
+                if (ds) {
+                    const int cv = A.col[g0 + i];
+                    sc[warp][k] = cv;
+                    if (wo) {
+                        const int64_t e = (int64_t)g0 + i;
+                        const int64_t d = (int64_t)cv - e / L;          // uniform rows: row = e / L
+                        off16[e] = (int16_t)(d < -32768 ? -32768 : (d > 32767 ? 32767 : d));
+                    }
+                }
             }
             __syncwarp();
             for (int e = eb - g0; e < ee - g0; e++) {

@@ -72,6 +72,8 @@ struct phipm_ctx {
     cudaEvent_t ev_binf = nullptr;                   // ||u_0||_inf readback of a solve
     DevState *st = nullptr;
     int32_t *tlo = nullptr, *thi = nullptr;                  // CSR per-tile column ranges
+    int16_t *off16 = nullptr;                                // CSR int16 column offsets (x-ring path)
+    int64_t off16_cap = 0;
     int64_t ntile_cap = 0;
     AttemptResult *res_h = nullptr, *res_d = nullptr;
     struct MaxPub {
@@ -113,7 +115,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0};
     char err[512] = {0};
 };
 
@@ -1464,6 +1466,7 @@ int make_csr(phipm_ctx *c, const phipm_csr *A, CsrOp &op)
     op.ring = op.blo = op.bhi = 0;
     op.pf = 0;
     op.pf_end = op.n;
+    op.off16 = nullptr;
     return PHIPM_OK;
 }
 
@@ -1474,7 +1477,7 @@ constexpr int CSR_WCAP = 10496;                             // 82 KB: band +-409
 // One analysis pass over a CSR matrix (csr_analyze_kernel): ||A||_inf (a1 setup, bit-exact), and
 // whether rows have a uniform length L (vectorised ELL path, PHIPM_OPT_CSR_ELL = 0 disables) within a
 // band that fits the shared x ring (PHIPM_OPT_CSR_RING = 0 disables).
-int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA, int mode = 3)
+int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA, int mode = 3, int16_t *off16 = nullptr)
 {
     op.ell = 0;
     op.ring = op.blo = op.bhi = 0;
@@ -1489,8 +1492,8 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA, int mode = 
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((op.n + CSRA_NT - 1) / CSRA_NT, (int64_t)c->sm_count * 16));
     ProfRec r;
     prof_begin(c, r, PC_OTHER, ((mode & 1) ? 8.0 : 0.0) * (double)nnz + ((mode & 2) ? 4.0 : 0.0) * (double)nnz +
-                                   4.0 * (double)(op.n + 1));
-    csr_analyze_kernel<<<grid, CSRA_NT, 0, c->stream>>>(op, (int)L, d, mode);
+                                   ((mode & 4) && off16 && L > 0 ? 2.0 : 0.0) * (double)nnz + 4.0 * (double)(op.n + 1));
+    csr_analyze_kernel<<<grid, CSRA_NT, 0, c->stream>>>(op, (int)L, d, mode, off16);
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -1509,6 +1512,8 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA, int mode = 
     op.blo = (h.blo + 1) & ~1;
     op.bhi = (h.bhi + 1) & ~1;
     op.ring = (env_ring && 2 * SNT * 2 + op.blo + op.bhi <= XRING) ? 1 : 0;
+    // int16 column offsets (written by this pass when asked): usable when the band fits int16
+    if ((mode & 4) && off16 && op.ring && h.blo <= 32767 && h.bhi <= 32767) op.off16 = off16;
     return PHIPM_OK;
 }
 
@@ -1529,9 +1534,10 @@ int enable_csr_window(phipm_ctx *c, CsrOp &op)
     return PHIPM_OK;
 }
 
+// algorithmic bytes of one SpMV: val + column indices (4 B, or 2 B as int16 offsets) + row_ptr + x + y
 double csr_bytes(const CsrOp &op, int64_t nnz)
 {
-    return 12.0 * (double)nnz + 4.0 * (double)(op.n + 1) + 16.0 * (double)op.n;
+    return (op.off16 ? 10.0 : 12.0) * (double)nnz + 4.0 * (double)(op.n + 1) + 16.0 * (double)op.n;
 }
 
 int check_common(phipm_ctx *c, double t, int64_t n, int p, const double *const *u, const double *w,
@@ -2044,6 +2050,7 @@ int phipm_set_option(phipm_ctx *c, int option, int value)
     case PHIPM_OPT_CSR_PREFETCH: ok = value >= 0 && value <= (1 << 20); break;
     case PHIPM_OPT_COL_PREFETCH: ok = value == 0 || value == 1; break;
     case PHIPM_OPT_FUSE_ANORM: ok = value == 0 || value == 1; break;
+    case PHIPM_OPT_CSR_OFF16: ok = value == 0 || value == 1; break;
     default: ok = value == 0 || value == 1; break;
     }
     if (!ok) return set_err(c, PHIPM_EINVAL, "option %d: value %d out of range", option, value);
@@ -2139,7 +2146,7 @@ void phipm_destroy(phipm_ctx *c)
     if (c->ev_binf) cudaEventDestroy(c->ev_binf);
     cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
     cudaFree(c->part); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
-    cudaFree(c->counter); cudaFree(c->st); cudaFree(c->tlo); cudaFree(c->thi);
+    cudaFree(c->counter); cudaFree(c->st); cudaFree(c->tlo); cudaFree(c->thi); cudaFree(c->off16);
     cudaFree(c->hu); cudaFree(c->hw); cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
     if (c->res_h) cudaFreeHost(c->res_h);
     if (c->mx_h) cudaFreeHost(c->mx_h);
@@ -2347,7 +2354,21 @@ int phipm_solve_csr(phipm_ctx *c, double t, const phipm_csr *A, int p, const dou
     // uniform-row path (x ring) the first w-recurrence SpMV reads val anyway and computes ||A||_inf
     // (PHIPM_OPT_FUSE_ANORM), so the analysis pass does not read val; otherwise a second pass does.
     double normA = 0.0;
-    rc = analyze_csr(c, op, A->nnz, &normA, 2);
+    // int16 column offsets for the x-ring path (PHIPM_OPT_CSR_OFF16): candidates are uniform-row
+    // matrices (nnz = L n, L % 4 == 0); the analysis pass writes them while it reads col
+    int16_t *o16 = nullptr;
+    if (opt(c, PHIPM_OPT_CSR_OFF16) && A->nnz > 0 && A->nnz % op.n == 0 && (A->nnz / op.n) % 4 == 0 &&
+        A->nnz / op.n <= 128 && op.n > SMALL_N && t > 0.0) {
+        if (A->nnz > c->off16_cap) {
+            cudaFree(c->off16);
+            c->off16 = nullptr;
+            c->off16_cap = 0;
+            if (cudaMalloc(&c->off16, sizeof(int16_t) * A->nnz) == cudaSuccess) c->off16_cap = A->nnz;
+            else cudaGetLastError();
+        }
+        o16 = c->off16;
+    }
+    rc = analyze_csr(c, op, A->nnz, &normA, o16 ? 6 : 2, o16);
     if (rc) return rc;
     const bool fuse = op.ring && opt(c, PHIPM_OPT_FUSE_ANORM) && p >= 1 && op.n > SMALL_N && t > 0.0;
     if (fuse) {

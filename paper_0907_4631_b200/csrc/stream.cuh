@@ -288,7 +288,8 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
                 const int64_t pa = r0 + base + A.pf, pb = min(pa + (int64_t)stride * U, A.pf_end);
                 if (pb > pa) {
                     tma_prefetch_l2(A.val + pa * A.ell, (uint32_t)((pb - pa) * A.ell * 8));
-                    tma_prefetch_l2(A.col + pa * A.ell, (uint32_t)((pb - pa) * A.ell * 4));
+                    if (A.off16) tma_prefetch_l2(A.off16 + pa * A.ell, (uint32_t)((pb - pa) * A.ell * 2));
+                    else tma_prefetch_l2(A.col + pa * A.ell, (uint32_t)((pb - pa) * A.ell * 4));
                 }
             }
         }
@@ -299,8 +300,18 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int q = base + u * stride + sub;
-            cc[u] = q < rows ? __ldg(reinterpret_cast<const int4 *>(A.col + (r0 + q) * (int64_t)A.ell + 4 * li))
-                             : make_int4(0, 0, 0, 0);
+            if (XM == 2 && A.off16) {
+                // int16 offsets col - row: 8 B per lane instead of 16
+                int2 o = q < rows ? __ldg(reinterpret_cast<const int2 *>(A.off16 + (r0 + q) * (int64_t)A.ell + 4 * li))
+                                  : make_int2(0, 0);
+                const int rr = (int)(r0 + q);
+                cc[u] = make_int4(rr + (int)(short)(o.x & 0xffff), rr + (o.x >> 16), rr + (int)(short)(o.y & 0xffff),
+                                  rr + (o.y >> 16));
+                if (q >= rows) cc[u] = make_int4(0, 0, 0, 0);
+            } else {
+                cc[u] = q < rows ? __ldg(reinterpret_cast<const int4 *>(A.col + (r0 + q) * (int64_t)A.ell + 4 * li))
+                                 : make_int4(0, 0, 0, 0);
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {

@@ -419,3 +419,21 @@ def test_fused_anorm_matches_analysis_pass(orc, name):
     for x, y in zip(a1, a0):
         assert x["tau"] == pytest.approx(y["tau"], rel=1e-14)
     assert relerr(w1, w0) <= 1e-13
+
+
+def test_csr_int16_offsets_option(orc):
+    """Option csr_off16 = 1 (int16 column offsets written by the analysis pass, streamed by the x-ring
+    SpMV; off by default): parity with the oracle and the same trajectory as the int32 columns."""
+    import paper_0907_4631_b200 as P
+    Pb = W.make("c5_med")
+    A = tuple(to_dev(a) for a in Pb.csr)
+    u = [to_dev(x) for x in Pb.u]
+    out = {}
+    for f in (1, 0):
+        c = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=3, options={"csr_off16": f})
+        w, s = c.solve_csr(Pb.t, A, u, tol=Pb.tol)
+        out[f] = (w.cpu().numpy(), s)
+        c.close()
+    wo, so = run_oracle(orc, Pb)
+    assert relerr(out[1][0], wo) <= parity_bound(Pb.tol)
+    assert np.array_equal(out[1][0], out[0][0]) and out[1][1] == out[0][1]

@@ -362,6 +362,88 @@ __device__ __forceinline__ void csr_tile_ell(const CsrOp &A, const double *__res
     }
 }
 
+// x-ring variant with the column indices software-pipelined one iteration ahead: the gathers of an
+// iteration depend on its column loads (L2 latency even after the bulk prefetch; ncu: 13 % of the
+// stall samples on the ring-index mask), so the next iteration's int4 column loads are issued before
+// this iteration's gathers.  Same products and summation order as csr_tile_ell<2>.
+template <int UP>
+__device__ __forceinline__ void csr_tile_ell_ring_pipe(const CsrOp &A, const double *xs, int64_t r0, int rows,
+                                                       double *ys, double *amax)
+{
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int G = A.ell >> 2;
+    const int rpw = 32 / G;
+    const int sub = lane / G, li = lane - sub * G;
+    const int stride = SNW * rpw;
+    auto ldc = [&](int q) -> int4 {
+        return q < rows ? __ldg(reinterpret_cast<const int4 *>(A.col + (r0 + q) * (int64_t)A.ell + 4 * li))
+                        : make_int4(0, 0, 0, 0);
+    };
+    int4 ccn[UP];
+#pragma unroll
+    for (int u = 0; u < UP; u++) ccn[u] = ldc(warp * rpw + u * stride + sub);
+    for (int base = warp * rpw; base < rows; base += stride * UP) {
+        if (A.pf > 0 && threadIdx.x == 0) {
+            const int64_t pa = r0 + base + A.pf, pb = min(pa + (int64_t)stride * UP, A.pf_end);
+            if (pb > pa) {
+                tma_prefetch_l2(A.val + pa * A.ell, (uint32_t)((pb - pa) * A.ell * 8));
+                tma_prefetch_l2(A.col + pa * A.ell, (uint32_t)((pb - pa) * A.ell * 4));
+            }
+        }
+        int4 cc[UP];
+        double2 va[UP], vb[UP];
+#pragma unroll
+        for (int u = 0; u < UP; u++) cc[u] = ccn[u];
+#pragma unroll
+        for (int u = 0; u < UP; u++) {
+            const int q = base + u * stride + sub;
+            if (q < rows) {
+                const int64_t e = (r0 + q) * (int64_t)A.ell + 4 * li;
+                va[u] = ldg_stream2(A.val + e);
+                vb[u] = ldg_stream2(A.val + e + 2);
+            } else {
+                va[u] = vb[u] = make_double2(0.0, 0.0);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UP; u++) ccn[u] = ldc(base + stride * UP + u * stride + sub);
+        double acc[UP];
+#pragma unroll
+        for (int u = 0; u < UP; u++) {
+            const int q = base + u * stride + sub;
+            double t = 0.0;
+            if (q < rows) {
+                t = va[u].x * xs[cc[u].x & (XRING - 1)];
+                t = fma(va[u].y, xs[cc[u].y & (XRING - 1)], t);
+                t = fma(vb[u].x, xs[cc[u].z & (XRING - 1)], t);
+                t = fma(vb[u].y, xs[cc[u].w & (XRING - 1)], t);
+            }
+            acc[u] = t;
+        }
+#pragma unroll
+        for (int u = 0; u < UP; u++) {
+            for (int o = G >> 1; o > 0; o >>= 1) acc[u] += __shfl_xor_sync(0xffffffffu, acc[u], o);
+            const int q = base + u * stride + sub;
+            if (q < rows && li == 0) ys[q] = acc[u];
+        }
+        if (amax) {
+#pragma unroll
+            for (int u = 0; u < UP; u++) {
+                const int q = base + u * stride + sub;
+                double s = 0.0;
+                if (q < rows) {
+                    s = __dadd_rn(s, fabs(va[u].x));
+                    s = __dadd_rn(s, fabs(va[u].y));
+                    s = __dadd_rn(s, fabs(vb[u].x));
+                    s = __dadd_rn(s, fabs(vb[u].y));
+                }
+                for (int o = G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                *amax = fmax(*amax, s);
+            }
+        }
+    }
+}
+
 // Issue the 1-D TMA copies of one stencil tile's halo x[hr0 - nx(ny), hr0 + hrows + nx(ny)) (thread
 // 0 only): ho receives the tile-relative offsets of the centre, y-, y+, z-, z+ segments in hbuf.
 template <int TILE_>
@@ -777,7 +859,14 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
                 {
                     CsrOp opf = op;
                     opf.pf_end = ce;
-                    csr_tile_ell<2>(opf, a.x, xring, 0, r0, rows, hbuf, a.anorm ? &amax : nullptr);
+#ifndef PHIPM_RING_PIPE
+#define PHIPM_RING_PIPE 2
+#endif
+                    if (PHIPM_RING_PIPE > 0 && !op.off16)
+                        csr_tile_ell_ring_pipe<(PHIPM_RING_PIPE > 0 ? PHIPM_RING_PIPE : 1)>(opf, xring, r0, rows, hbuf,
+                                                                                          a.anorm ? &amax : nullptr);
+                    else
+                        csr_tile_ell<2>(opf, a.x, xring, 0, r0, rows, hbuf, a.anorm ? &amax : nullptr);
                 }
                 __syncthreads();                           // ring reads done, ys complete
             } else {

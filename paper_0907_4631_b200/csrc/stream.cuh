@@ -697,7 +697,10 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
     constexpr int NP = RPT / 2;                           // double2 pairs per thread
     constexpr bool IS_ST = std::is_same<Op, StencilOp>::value;
     constexpr bool HALO = !std::is_same<Op, CsrOp>::value;
-    constexpr int CUD = std::is_same<Op, CsrOp>::value ? 3 : CU;
+#ifndef PHIPM_CUD_CSR
+#define PHIPM_CUD_CSR 2
+#endif
+    constexpr int CUD = std::is_same<Op, CsrOp>::value ? PHIPM_CUD_CSR : CU;
     extern __shared__ __align__(128) double sm[];
     __shared__ uint64_t hbar;
     __shared__ int hofs[2][5];                            // tile-relative halo offsets per parity

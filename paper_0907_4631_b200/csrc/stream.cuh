@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
     constexpr bool IS_ST = std::is_same<Op, StencilOp>::value;
     constexpr bool HALO = !std::is_same<Op, CsrOp>::value;
 #ifndef PHIPM_CUD_CSR
-#define PHIPM_CUD_CSR 2
+#define PHIPM_CUD_CSR 4
 #endif
     constexpr int CUD = std::is_same<Op, CsrOp>::value ? PHIPM_CUD_CSR : CU;
     extern __shared__ __align__(128) double sm[];
@@ -863,7 +863,7 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
                     CsrOp opf = op;
                     opf.pf_end = ce;
 #ifndef PHIPM_RING_PIPE
-#define PHIPM_RING_PIPE 2
+#define PHIPM_RING_PIPE 1
 #endif
                     if (PHIPM_RING_PIPE > 0 && !op.off16)
                         csr_tile_ell_ring_pipe<(PHIPM_RING_PIPE > 0 ? PHIPM_RING_PIPE : 1)>(opf, xring, r0, rows, hbuf,

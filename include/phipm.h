@@ -182,6 +182,10 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *                              col - row as int16 (context workspace, 2 B per nonzero) and the x-ring
  *                              SpMVs stream those instead of the int32 columns (10 instead of 12 B per
  *                              nonzero); 0 (default, measured faster: the SpMV time did not drop)
+ *   PHIPM_OPT_CLUSTER_LZ       Lanczos extensions of stencils with n <= 65536 on one thread-block
+ *                              cluster (vectors in the cluster's shared memory, DSMEM reductions and
+ *                              halos): 0 off, 1 auto (default: n > 8192), a forced cluster size
+ *                              2/4/8/16, or -1 for a single CTA (any n the slice fits)
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -199,7 +203,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_COL_PREFETCH    13
 #define PHIPM_OPT_FUSE_ANORM      14
 #define PHIPM_OPT_CSR_OFF16       15
-#define PHIPM_OPT_COUNT           16
+#define PHIPM_OPT_CLUSTER_LZ      16
+#define PHIPM_OPT_COUNT           17
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

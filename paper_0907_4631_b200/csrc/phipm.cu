@@ -32,6 +32,7 @@
 #include "persist_wrec.cuh"
 #include "phicheb.cuh"
 #include "spmm.cuh"
+#include "persist_cl.cuh"
 
 using namespace phipm;
 
@@ -115,7 +116,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1};
     char err[512] = {0};
 };
 
@@ -877,9 +878,98 @@ bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_o
     return try_persist_rpt<2>(c, op, symmetric, k0, k1, bthr, bytes, rc);
 }
 
+using ClusterLzFn = void (*)(StencilOp, SmallArgs, ClArgs, Work);
+
+template <int NT, int R>
+ClusterLzFn cluster_lz_fn(int dc)
+{
+    switch (dc) {
+    case 1: return krylov_cluster_lanczos_kernel<NT, R, 1>;
+    case 2: return krylov_cluster_lanczos_kernel<NT, R, 2>;
+    case 3: return krylov_cluster_lanczos_kernel<NT, R, 3>;
+    default: return krylov_cluster_lanczos_kernel<NT, R, 4>;
+    }
+}
+
+// Lanczos extension of a stencil on one thread-block cluster (persist_cl.cuh); false: not applicable
+// (CSR operators, sizes whose slice or halo does not fit, a refused cluster launch)
+template <class Op>
+bool try_cluster_lz(phipm_ctx *, const Op &, double, int, int, double)
+{
+    return false;
+}
+
+template <>
+bool try_cluster_lz<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_op, int k0, int k1, double bthr)
+{
+    const int o = opt(c, PHIPM_OPT_CLUSTER_LZ);
+    if (o == 0 || k1 <= k0) return false;
+    const int64_t n = op.n;
+    const int64_t reach = op.dim == 3 ? (int64_t)op.nx * op.ny : op.dim == 2 ? op.nx + (op.diag ? 1 : 0) : 1;
+    int cs;
+    if (o == 1) {
+        // auto: above the single-CTA sizes, about 4096 rows per CTA
+        if (n <= SMALL_N || n > (int64_t)CLZ_MAXCS * 4096) return false;
+        cs = 2;
+        while (cs < CLZ_MAXCS && (n + cs - 1) / cs > 4096) cs *= 2;
+    } else {
+        cs = o < 0 ? 1 : o;
+    }
+    const int64_t rpc = (n + cs - 1) / cs;
+    const int64_t last = n - (int64_t)(cs - 1) * rpc;
+    if (cs > 1 && (last < reach || rpc < reach)) return false;
+    const int64_t blen = cl_buf_len(op, rpc, (int)reach, cs);
+    const size_t smem = (size_t)blen * sizeof(double);
+    if (smem + 4096 > c->smem_optin) return false;
+    const int dc = (op.dim == 2 && op.diag) ? 4 : op.dim;
+    void (*kfn)(StencilOp, SmallArgs, ClArgs, Work);
+    int nt;
+    if (rpc <= 256 * 4) { kfn = cluster_lz_fn<256, 4>(dc); nt = 256; }
+    else if (rpc <= 512 * 8) { kfn = cluster_lz_fn<512, 8>(dc); nt = 512; }
+    else return false;
+    SmallArgs sa;
+    sa.k0 = k0;
+    sa.k1 = k1;
+    sa.symmetric = 1;
+    sa.orth = 0;
+    sa.bthr = bthr;
+    ClArgs ca;
+    ca.rpc = rpc;
+    ca.reach = (int)reach;
+    ca.cs = cs;
+    ca.blen = (int)blen;
+    double bytes = 0.0;
+    for (int j = k0; j < k1; j++) bytes += bytes_op + 8.0 * (double)n * 4.0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(cs);
+    cfg.blockDim = dim3(nt);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = c->pdl ? 1 : 0;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cs;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = cs > 1 ? 2 : 1;
+    ProfRec r;
+    prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, op, sa, ca, make_work(c));
+    prof_end(c, r);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    c->acc.launches++;
+    return true;
+}
+
 template <class Op>
 int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1, double bthr)
 {
+    if (symmetric && try_cluster_lz(c, op, bytes_op, k0, k1, bthr)) return PHIPM_OK;
     const int64_t n = op.n;
     if (n <= SMALL_N && k1 > k0) {
         // small problems: the whole extension in one single-CTA kernel (small.cuh)
@@ -2051,6 +2141,7 @@ int phipm_set_option(phipm_ctx *c, int option, int value)
     case PHIPM_OPT_COL_PREFETCH: ok = value == 0 || value == 1; break;
     case PHIPM_OPT_FUSE_ANORM: ok = value == 0 || value == 1; break;
     case PHIPM_OPT_CSR_OFF16: ok = value == 0 || value == 1; break;
+    case PHIPM_OPT_CLUSTER_LZ: ok = value >= -1 && value <= 16 && (value <= 1 || (value & (value - 1)) == 0); break;
     default: ok = value == 0 || value == 1; break;
     }
     if (!ok) return set_err(c, PHIPM_EINVAL, "option %d: value %d out of range", option, value);
@@ -2224,6 +2315,11 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(krylov_small_kernel<StencilOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_N * 8);
         cudaFuncSetAttribute(krylov_small_kernel<CsrOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_N * 8);
+        for (int dc = 1; dc <= 4; dc++)
+            for (ClusterLzFn f : {cluster_lz_fn<256, 4>(dc), cluster_lz_fn<512, 8>(dc)}) {
+                cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+                cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+            }
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(spmv_stream_kernel<CsrOp, 2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);

@@ -186,6 +186,10 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *                              cluster (vectors in the cluster's shared memory, DSMEM reductions and
  *                              halos): 0 off, 1 auto (default: n > 8192), a forced cluster size
  *                              2/4/8/16, or -1 for a single CTA (any n the slice fits)
+ *   PHIPM_OPT_SPEC             1 (default): when a Krylov extension runs on few SMs (n <= 8192, or the
+ *                              cluster Lanczos kernel), the extension to min((4m+2)/3, m_max) columns
+ *                              that Algorithm 3's m-branch can ask for next runs on a second stream
+ *                              while the exponential of the attempt runs; 0 off
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -204,7 +208,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_FUSE_ANORM      14
 #define PHIPM_OPT_CSR_OFF16       15
 #define PHIPM_OPT_CLUSTER_LZ      16
-#define PHIPM_OPT_COUNT           17
+#define PHIPM_OPT_SPEC            17
+#define PHIPM_OPT_COUNT           18
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

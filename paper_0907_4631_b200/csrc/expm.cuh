@@ -497,7 +497,7 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
     __shared__ double sred[3 * (EXPM_NT / 32)];
     __shared__ int s_int[PADE ? 8 + 2 * EXPM_KMAX : 1];     // Pade: pivot rows, used flags
     __shared__ double fcol[PADE ? 2 * EXPM_KMAX : 1];       // Pade: multipliers
-    __shared__ int s_mu;
+    __shared__ int s_mu, s_brk;
     const int t = threadIdx.x;
     pdl_wait();
     // phase stamps go to shared memory (a store to host-mapped memory followed by a barrier would
@@ -515,9 +515,13 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
     } else {
         if (t == 0) {
             int m = a.m;
+            s_brk = -1;
             if (a.mode == 0) {
+                // one read of the breakdown position; a breakdown beyond m belongs to a speculative
+                // extension still running on the second stream (phipm.cu) and not to this attempt
                 const int brk = a.st->brk;
-                if (brk >= 0 && brk < m) m = brk;
+                s_brk = (brk >= 0 && brk <= m) ? brk : -1;
+                if (s_brk >= 0 && s_brk < m) m = s_brk;
             }
             s_mu = m;
         }
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
             a.comb[0] = 0.0;
             AttemptResult r{};
             r.eps = 0.0; r.normH1 = 0.0; r.beta = beta; r.h = 0.0; r.mu = 0;
-            r.brk = a.st->brk; r.status = a.st->nonfinite ? 5 : 0;
+            r.brk = s_brk; r.status = a.st->nonfinite ? 5 : 0;
             publish_result(a.res, r, a.seq);
         }
         return;
@@ -627,7 +631,7 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
         return;
     }
     // mode 0: error estimate and combine coefficients
-    const int brk = a.st->brk;
+    const int brk = s_brk;
     const bool corr = !(brk >= 0 && brk <= mu);          // v~_mu and h_{mu+1,mu} exist
     const double h = corr ? a.H[mu + (size_t)(mu - 1) * a.ldh] : 0.0;
     double taup = 1.0;

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(CHEB_NT, 1) phi_cheb_kernel(ExpmArgs a)
     __shared__ double cs[4 * CHEB_NMAX];                   // cos(pi q / (2N)), q < 4N
     __shared__ double s_red[2 * (CHEB_NT / 32)];
     __shared__ double s_lo, s_hi, s_nh;
-    __shared__ int s_n, s_mu, s_bad;
+    __shared__ int s_n, s_mu, s_bad, s_brk;
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     pdl_wait();
     __shared__ long long s_clk[16];                         // PHIPM_EXPM_CLOCKS phase stamps
@@ -81,9 +81,11 @@ __global__ void __launch_bounds__(CHEB_NT, 1) phi_cheb_kernel(ExpmArgs a)
     CHEB_CLK(0)
     if (t == 0) {
         int m = a.m;
+        s_brk = -1;
         if (a.mode == 0) {
-            const int brk = a.st->brk;
-            if (brk >= 0 && brk < m) m = brk;
+            const int brk = a.st->brk;                 // (as expm_kernel: one read, breakdowns beyond m ignored)
+            s_brk = (brk >= 0 && brk <= m) ? brk : -1;
+            if (s_brk >= 0 && s_brk < m) m = s_brk;
         }
         s_mu = m;
         s_bad = 0;
@@ -101,7 +103,7 @@ __global__ void __launch_bounds__(CHEB_NT, 1) phi_cheb_kernel(ExpmArgs a)
             a.comb[0] = 0.0;
             AttemptResult r{};
             r.beta = beta;
-            r.brk = a.st->brk;
+            r.brk = s_brk;
             r.status = a.st->nonfinite ? 5 : 0;
             publish_result(a.res, r, a.seq);
         }
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(CHEB_NT, 1) phi_cheb_kernel(ExpmArgs a)
         return;
     }
     // 5. mode 0 epilogue (as expm_kernel): error estimate and combine coefficients
-    const int brk = a.st->brk;
+    const int brk = s_brk;
     const bool corr = !(brk >= 0 && brk <= mu);
     const double h = corr ? a.H[mu + (size_t)(mu - 1) * a.ldh] : 0.0;
     double taup = 1.0;

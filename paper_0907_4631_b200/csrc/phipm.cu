@@ -71,6 +71,9 @@ struct phipm_ctx {
     unsigned *counter = nullptr;
     bool coop_dirty = false;                         // a cooperative kernel timed out: reset its counters
     cudaEvent_t ev_binf = nullptr;                   // ||u_0||_inf readback of a solve
+    cudaStream_t stream2 = nullptr;                  // speculative Krylov extensions (PHIPM_OPT_SPEC)
+    cudaEvent_t ev_main = nullptr, ev_spec = nullptr;
+    bool spec_pending = false;                       // an extension on stream2 not yet joined to stream
     DevState *st = nullptr;
     int32_t *tlo = nullptr, *thi = nullptr;                  // CSR per-tile column ranges
     int16_t *off16 = nullptr;                                // CSR int16 column offsets (x-ring path)
@@ -116,7 +119,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1};
     char err[512] = {0};
 };
 
@@ -893,6 +896,39 @@ ClusterLzFn cluster_lz_fn(int dc)
 
 // Lanczos extension of a stencil on one thread-block cluster (persist_cl.cuh); false: not applicable
 // (CSR operators, sizes whose slice or halo does not fit, a refused cluster launch)
+struct ClPlan {
+    int cs, nt;
+    int64_t rpc, reach, blen;
+    ClusterLzFn kfn;
+};
+
+// whether (and how) the cluster Lanczos kernel takes a stencil extension
+inline bool cluster_lz_plan(const phipm_ctx *c, const StencilOp &op, ClPlan &pl)
+{
+    const int o = opt(c, PHIPM_OPT_CLUSTER_LZ);
+    if (o == 0) return false;
+    const int64_t n = op.n;
+    pl.reach = op.dim == 3 ? (int64_t)op.nx * op.ny : op.dim == 2 ? op.nx + (op.diag ? 1 : 0) : 1;
+    if (o == 1) {
+        // auto: above the single-CTA sizes, about 4096 rows per CTA
+        if (n <= SMALL_N || n > (int64_t)CLZ_MAXCS * 4096) return false;
+        pl.cs = 2;
+        while (pl.cs < CLZ_MAXCS && (n + pl.cs - 1) / pl.cs > 4096) pl.cs *= 2;
+    } else {
+        pl.cs = o < 0 ? 1 : o;
+    }
+    pl.rpc = (n + pl.cs - 1) / pl.cs;
+    const int64_t last = n - (int64_t)(pl.cs - 1) * pl.rpc;
+    if (pl.cs > 1 && (last < pl.reach || pl.rpc < pl.reach)) return false;
+    pl.blen = cl_buf_len(op, pl.rpc, (int)pl.reach, pl.cs);
+    if ((size_t)pl.blen * sizeof(double) + 4096 > c->smem_optin) return false;
+    const int dc = (op.dim == 2 && op.diag) ? 4 : op.dim;
+    if (pl.rpc <= 256 * 4) { pl.kfn = cluster_lz_fn<256, 4>(dc); pl.nt = 256; }
+    else if (pl.rpc <= 512 * 8) { pl.kfn = cluster_lz_fn<512, 8>(dc); pl.nt = 512; }
+    else return false;
+    return true;
+}
+
 template <class Op>
 bool try_cluster_lz(phipm_ctx *, const Op &, double, int, int, double)
 {
@@ -902,31 +938,12 @@ bool try_cluster_lz(phipm_ctx *, const Op &, double, int, int, double)
 template <>
 bool try_cluster_lz<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_op, int k0, int k1, double bthr)
 {
-    const int o = opt(c, PHIPM_OPT_CLUSTER_LZ);
-    if (o == 0 || k1 <= k0) return false;
+    ClPlan pl;
+    if (k1 <= k0 || !cluster_lz_plan(c, op, pl)) return false;
     const int64_t n = op.n;
-    const int64_t reach = op.dim == 3 ? (int64_t)op.nx * op.ny : op.dim == 2 ? op.nx + (op.diag ? 1 : 0) : 1;
-    int cs;
-    if (o == 1) {
-        // auto: above the single-CTA sizes, about 4096 rows per CTA
-        if (n <= SMALL_N || n > (int64_t)CLZ_MAXCS * 4096) return false;
-        cs = 2;
-        while (cs < CLZ_MAXCS && (n + cs - 1) / cs > 4096) cs *= 2;
-    } else {
-        cs = o < 0 ? 1 : o;
-    }
-    const int64_t rpc = (n + cs - 1) / cs;
-    const int64_t last = n - (int64_t)(cs - 1) * rpc;
-    if (cs > 1 && (last < reach || rpc < reach)) return false;
-    const int64_t blen = cl_buf_len(op, rpc, (int)reach, cs);
-    const size_t smem = (size_t)blen * sizeof(double);
-    if (smem + 4096 > c->smem_optin) return false;
-    const int dc = (op.dim == 2 && op.diag) ? 4 : op.dim;
-    void (*kfn)(StencilOp, SmallArgs, ClArgs, Work);
-    int nt;
-    if (rpc <= 256 * 4) { kfn = cluster_lz_fn<256, 4>(dc); nt = 256; }
-    else if (rpc <= 512 * 8) { kfn = cluster_lz_fn<512, 8>(dc); nt = 512; }
-    else return false;
+    const int cs = pl.cs, nt = pl.nt;
+    const size_t smem = (size_t)pl.blen * sizeof(double);
+    const ClusterLzFn kfn = pl.kfn;
     SmallArgs sa;
     sa.k0 = k0;
     sa.k1 = k1;
@@ -934,10 +951,10 @@ bool try_cluster_lz<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_o
     sa.orth = 0;
     sa.bthr = bthr;
     ClArgs ca;
-    ca.rpc = rpc;
-    ca.reach = (int)reach;
+    ca.rpc = pl.rpc;
+    ca.reach = (int)pl.reach;
     ca.cs = cs;
-    ca.blen = (int)blen;
+    ca.blen = (int)pl.blen;
     double bytes = 0.0;
     for (int j = k0; j < k1; j++) bytes += bytes_op + 8.0 * (double)n * 4.0;
     cudaLaunchConfig_t cfg = {};
@@ -965,6 +982,30 @@ bool try_cluster_lz<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_o
     c->acc.launches++;
     return true;
 }
+
+// Speculative Krylov extension (PHIPM_OPT_SPEC): an extension runs on a second stream, concurrently
+// with the exponential of the current attempt, when it occupies few SMs (the single-CTA kernels,
+// n <= SMALL_N, or the cluster Lanczos kernel): the extension then hides behind the exponential
+// instead of following the host's decision.
+template <class Op>
+bool spec_path(const phipm_ctx *c, const Op &op, bool symmetric)
+{
+    if (!opt(c, PHIPM_OPT_SPEC)) return false;
+    if (op.n <= SMALL_N) return true;
+    if constexpr (std::is_same<Op, StencilOp>::value) {
+        ClPlan pl;
+        return symmetric && cluster_lz_plan(c, op, pl);
+    }
+    return false;
+}
+
+// the launch helpers enqueue on c->stream: point it at the second stream for one enqueue
+struct OnStream2 {
+    phipm_ctx *c;
+    cudaStream_t saved;
+    explicit OnStream2(phipm_ctx *cc) : c(cc), saved(cc->stream) { c->stream = c->stream2; }
+    ~OnStream2() { c->stream = saved; }
+};
 
 template <class Op>
 int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1, double bthr)
@@ -1200,10 +1241,19 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     S.t_reached = 0.0;
     c->attempts.clear();
     c->nattempts = 0;
+    // join a speculative extension still running on stream2 (stream order from here on)
+    auto join_spec = [&]() {
+        if (c->spec_pending) {
+            cudaStreamWaitEvent(c->stream, c->ev_spec, 0);
+            c->spec_pending = false;
+        }
+    };
     auto finish = [&](int rc) {
+        join_spec();
         if (stats) *stats = S;
         return rc;
     };
+    join_spec();                       // (an earlier solve that ended in an error may have left one)
     if (t_end == 0.0) {
         if (w != u[0]) CK(cudaMemcpyAsync(w, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
         int rc = sync(c);
@@ -1323,10 +1373,13 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     double tk = 0.0;
     S.m_peak = m;
     bool first = true;
+    const bool spec_ok = spec_path(c, op, P.symmetric) && !P.fixed_m;
+    int spec_from = 0;                 // first column of the pending speculative extension
     bool cheb_off = false;             // the Chebyshev method was found unreliable in this solve
     while (tk < t_end) {
         if (tau > t_end - tk) tau = t_end - tk;
         if (!first) {
+            join_spec();                   // the seed below rewrites the state the extension uses
             enq = 0;
             int rc = enqueue_wrec(tk, ucur, 0);
             if (rc) return finish(rc);
@@ -1343,9 +1396,36 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         for (;;) {
             attempts++;
             if (std::max(k, enq) < m && !brk) {
+                join_spec();
                 int rc = enqueue_krylov(c, op, bytes_op, P.symmetric, o.orth, std::max(k, enq), m, bthr);
                 if (rc) return finish(rc);
                 enq = m;
+            } else if (c->spec_pending && m > spec_from) {
+                join_spec();               // this attempt uses columns of the speculative extension
+            }
+            // Speculation (PHIPM_OPT_SPEC): while the exponential of this attempt runs, extend the basis
+            // on stream2 to the largest m Algorithm 3 can ask for next, min((4m+2)/3, m_max) (the clamp
+            // in control()).  It only adds columns beyond m: the exponential reads H, sigma and the
+            // state of columns < m, and takes a breakdown position beyond m as none (expm.cuh).  An
+            // accepted or tau-branch attempt leaves the columns unused (the stats count the algorithm's
+            // SpMVs, not the speculative ones).
+            if (spec_ok && !brk && !c->spec_pending) {
+                const int ms = std::min((4 * m + 2) / 3, P.m_max);
+                if (ms > std::max(k, enq)) {
+                    const int k0s = std::max(k, enq);
+                    CK(cudaEventRecord(c->ev_main, c->stream));
+                    CK(cudaStreamWaitEvent(c->stream2, c->ev_main, 0));
+                    int rc;
+                    {
+                        OnStream2 on2(c);
+                        rc = enqueue_krylov(c, op, bytes_op, P.symmetric, o.orth, k0s, ms, bthr);
+                    }
+                    if (rc) return finish(rc);
+                    CK(cudaEventRecord(c->ev_spec, c->stream2));
+                    c->spec_pending = true;
+                    spec_from = k0s;
+                    enq = ms;
+                }
             }
             ExpmArgs ea;
             memset(&ea, 0, sizeof(ea));
@@ -1455,6 +1535,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         S.m_last = m_used;
         S.t_reached = tk;
     }
+    join_spec();
     int rc = sync(c);
     return finish(rc);
 }
@@ -2235,6 +2316,12 @@ void phipm_destroy(phipm_ctx *c)
     for (auto &r : c->pending) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
     for (auto e : c->pool) cudaEventDestroy(e);
     if (c->ev_binf) cudaEventDestroy(c->ev_binf);
+    if (c->stream2) {
+        cudaStreamSynchronize(c->stream2);
+        cudaStreamDestroy(c->stream2);
+    }
+    if (c->ev_main) cudaEventDestroy(c->ev_main);
+    if (c->ev_spec) cudaEventDestroy(c->ev_spec);
     cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
     cudaFree(c->part); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
     cudaFree(c->counter); cudaFree(c->st); cudaFree(c->tlo); cudaFree(c->thi); cudaFree(c->off16);
@@ -2385,6 +2472,9 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     A((void **)&c->raw, sizeof(double) * (MAXD + 2));
     A((void **)&c->counter, sizeof(unsigned) * 8);
     if (ok && cudaEventCreateWithFlags(&c->ev_binf, cudaEventDisableTiming) != cudaSuccess) ok = false;
+    if (ok && cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess) ok = false;
+    if (ok && cudaEventCreateWithFlags(&c->ev_main, cudaEventDisableTiming) != cudaSuccess) ok = false;
+    if (ok && cudaEventCreateWithFlags(&c->ev_spec, cudaEventDisableTiming) != cudaSuccess) ok = false;
     A((void **)&c->st, sizeof(DevState));
     c->ntile_cap = n_max / 512 + 2;
     A((void **)&c->tlo, sizeof(int32_t) * c->ntile_cap);

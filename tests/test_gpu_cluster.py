@@ -142,3 +142,25 @@ def test_cluster_deterministic_and_matches_grid_kernel():
         res[cl] = (w.cpu().numpy(), s)
         ctx.close()
     assert relerr(res[1][0], res[0][0]) <= 1e-11, (res[1][1], res[0][1])
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c2_med", "c3_mini", "c5_mini"])
+def test_speculative_extension_changes_nothing(name):
+    # option spec (default on): the extension to min((4m+2)/3, m_max) runs on a second stream during the
+    # exponential.  It splits the basis at the same columns as the unspeculated solve (each m-branch
+    # rejection asks for exactly that extension), adds columns beyond m only, and the exponential ignores
+    # a breakdown beyond m: w is bit-identical and the stats (the algorithm's SpMV count) are equal
+    Pb = W.make(name)
+    u = [to_dev(x) for x in Pb.u]
+    res = {}
+    for spec in (1, 0):
+        ctx = P.Context(n_max=Pb.n, m_max=100, p_max=max(Pb.p, 1), options={"spec": spec})
+        if Pb.stencil is not None:
+            w, s = ctx.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), u, tol=Pb.tol, symmetric=Pb.symmetric)
+        else:
+            A = tuple(to_dev(a) for a in Pb.csr)
+            w, s = ctx.solve_csr(Pb.t, A, u, tol=Pb.tol, symmetric=Pb.symmetric)
+        res[spec] = (w.cpu().numpy(), s)
+        ctx.close()
+    assert np.array_equal(res[1][0], res[0][0])
+    assert res[1][1] == res[0][1]

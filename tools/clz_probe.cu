@@ -15,7 +15,7 @@ int main(int argc, char **argv)
 {
     const int nx = argc > 1 ? atoi(argv[1]) : 256, cs = argc > 2 ? atoi(argv[2]) : 16;
     const int nt = argc > 3 ? atoi(argv[3]) : 1024;
-    const int m = 40;
+    const int m = argc > 4 ? atoi(argv[4]) : 40;
     const int64_t n = (int64_t)nx * nx;
     StencilOp op{};
     op.dim = 2;

@@ -190,6 +190,9 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *                              cluster Lanczos kernel), the extension to min((4m+2)/3, m_max) columns
  *                              that Algorithm 3's m-branch can ask for next runs on a second stream
  *                              while the exponential of the attempt runs; 0 off
+ *   PHIPM_OPT_DEVSOLVE         1 (default): a symmetric problem with n <= 8192 and the Taylor exponential
+ *                              is solved by ONE single-CTA kernel that also runs the controller (no host
+ *                              round trip per attempt; opts.profile disables it); 0 off
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -209,7 +212,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_CSR_OFF16       15
 #define PHIPM_OPT_CLUSTER_LZ      16
 #define PHIPM_OPT_SPEC            17
-#define PHIPM_OPT_COUNT           18
+#define PHIPM_OPT_DEVSOLVE        18
+#define PHIPM_OPT_COUNT           19
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

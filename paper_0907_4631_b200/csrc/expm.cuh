@@ -491,15 +491,13 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
 // PADE: method PHIPM_EXPM_PADE13 (separate instantiations keep each kernel's code small: the
 // kernel runs cold, after the streaming kernels, once per attempt)
 template <bool SMEM, bool PADE>
-__global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
+__device__ __forceinline__ void expm_body(const ExpmArgs &a, double *esm)
 {
-    extern __shared__ double esm[];
     __shared__ double sred[3 * (EXPM_NT / 32)];
     __shared__ int s_int[PADE ? 8 + 2 * EXPM_KMAX : 1];     // Pade: pivot rows, used flags
     __shared__ double fcol[PADE ? 2 * EXPM_KMAX : 1];       // Pade: multipliers
     __shared__ int s_mu, s_brk;
     const int t = threadIdx.x;
-    pdl_wait();
     // phase stamps go to shared memory (a store to host-mapped memory followed by a barrier would
     // stall and distort the phases); copied out to a.clk once at the end
     __shared__ long long s_clk[16];
@@ -664,6 +662,14 @@ __global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
         publish_result(a.res, r, a.seq);
         if (a.clk) a.clk[6] = clock64();                 // (after the copy above: epilogue end)
     }
+}
+
+template <bool SMEM, bool PADE>
+__global__ void __launch_bounds__(EXPM_NT, 1) expm_kernel(ExpmArgs a)
+{
+    extern __shared__ double esm[];
+    pdl_wait();
+    expm_body<SMEM, PADE>(a, esm);
 }
 
 } // namespace phipm

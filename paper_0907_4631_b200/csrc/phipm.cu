@@ -33,6 +33,8 @@
 #include "phicheb.cuh"
 #include "spmm.cuh"
 #include "persist_cl.cuh"
+#include "ctl.cuh"
+#include "solve_small.cuh"
 
 using namespace phipm;
 
@@ -74,6 +76,10 @@ struct phipm_ctx {
     cudaStream_t stream2 = nullptr;                  // speculative Krylov extensions (PHIPM_OPT_SPEC)
     cudaEvent_t ev_main = nullptr, ev_spec = nullptr;
     bool spec_pending = false;                       // an extension on stream2 not yet joined to stream
+    // device-driven solves of small problems (solve_small.cuh)
+    SsAttempt *ss_att_d = nullptr;                   // attempt records (device)
+    SsOut *ss_out_h = nullptr, *ss_out_d = nullptr;  // stats and status (mapped pinned)
+    int ss_att_pending = 0;                          // records of the last solve still on the device
     DevState *st = nullptr;
     int32_t *tlo = nullptr, *thi = nullptr;                  // CSR per-tile column ranges
     int16_t *off16 = nullptr;                                // CSR int16 column offsets (x-ring path)
@@ -119,7 +125,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1};
     char err[512] = {0};
 };
 
@@ -505,125 +511,7 @@ SpmvArgs spmv0()
     return a;
 }
 
-// ---------------------------------------------------------------------------------------------
-// controller (Algorithm 4 then Algorithm 3's choice; DESIGN.md §3 readings R1-R38)
-
-struct CtlMem {
-    bool rejected = false;
-    int last_branch = 0;     // 1: tau changed, 2: m changed
-    bool q_valid = false;
-    double q = 0.0;
-    bool k_valid = false;
-    double kappa = 2.0;
-    double tau_old = 0.0, eps_old = 0.0;
-    int m_old = 0;
-};
-
-struct Problem {
-    int p;
-    int64_t n, NA;
-    bool symmetric;
-    int m_max;               // min(m_max, n)
-    bool fixed_m, eq6_variant;
-};
-
-// M(.) of Eq. (8) with ceil_+ = max(0, ceil(.))
-double cost_M(double x)
-{
-    if (!(x > 0.0)) return 44.0 / 3.0;
-    double l = std::ceil(std::log2(x / 5.37));
-    return 44.0 / 3.0 + 2.0 * (l > 0.0 ? l : 0.0);
-}
-
-// Eq. (4)
-double cost_step(const Problem &P, int m, double M)
-{
-    const double mp = m + P.p, K = m + P.p + 1;
-    const double vec = P.symmetric ? 3.0 * mp : (double)m * m + 3.0 * P.p + 2.0;
-    return mp * (double)P.NA + vec * (double)P.n + M * K * K * K;
-}
-
-struct Decision {
-    double tau_next;
-    int m_next;
-    int branch;
-};
-
-Decision control(const Problem &P, CtlMem &mem, double tau, int m, double eps, double omega, double normH1,
-                 double remaining, bool accepted)
-{
-    const double gamma = 0.8;
-    double q;
-    bool q_now = false;
-    if (mem.rejected && mem.last_branch == 1) {                     // Eq. (6)
-        const double lt = std::log(tau / mem.tau_old), le = std::log(eps / mem.eps_old);
-        q = P.eq6_variant ? le / lt - 1.0 : lt / le - 1.0;
-        if (std::isfinite(q) && q + 1.0 > 0.0) q_now = true;
-        else q = m / 4.0;
-    } else if (mem.rejected && mem.q_valid) {
-        q = mem.q;
-        q_now = true;
-    } else {
-        q = m / 4.0;
-    }
-    const double tau_new = tau * std::pow(gamma / omega, 1.0 / (q + 1.0));   // Eq. (2)
-    double kap;
-    bool k_now = false;
-    if (mem.rejected && mem.last_branch == 2) {                     // Eq. (7)
-        kap = std::pow(eps / mem.eps_old, 1.0 / (double)(mem.m_old - m));
-        if (std::isfinite(kap) && kap > 1.0) k_now = true;
-        else kap = 2.0;
-    } else if (mem.rejected && mem.k_valid) {
-        kap = mem.kappa;
-        k_now = true;
-    } else {
-        kap = 2.0;
-    }
-    const double m_new = m + std::log(omega / gamma) / std::log(kap);   // Eq. (3)
-    // clamps of Algorithm 3
-    double tc = tau_new;
-    if (!(tc >= tau / 5.0)) tc = tau / 5.0;
-    tc = std::min(tc, 2.0 * tau);
-    tc = std::min(tc, remaining);
-    int lo = std::max((3 * m) / 4, 1);
-    int hi = std::min((4 * m + 2) / 3, P.m_max);
-    lo = std::min(lo, hi);
-    int mc;
-    const double mr = std::ceil(m_new);
-    if (!(mr >= (double)lo)) mc = lo;
-    else if (mr > (double)hi) mc = hi;
-    else mc = (int)mr;
-    // Eq. (5) on the clamped candidates
-    const double c_tau = std::ceil(remaining / tc) * cost_step(P, m, cost_M(std::max(tc * normH1, 1.0)));
-    const double c_m = std::ceil(remaining / tau) * cost_step(P, mc, cost_M(std::max(tau * normH1, 1.0)));
-    int br = (c_tau < c_m) ? 1 : 2;
-    if (P.fixed_m) br = 1;
-    if (!accepted && br == 2 && mc == m) br = 1;
-    Decision d;
-    d.branch = br;
-    d.tau_next = br == 1 ? tc : tau;
-    d.m_next = br == 2 ? mc : m;
-    mem.q = q;
-    mem.q_valid = q_now;
-    mem.kappa = kap;
-    mem.k_valid = k_now;
-    if (!accepted) {
-        mem.rejected = true;
-        mem.last_branch = br;
-        mem.tau_old = tau;
-        mem.eps_old = eps;
-        mem.m_old = m;
-    }
-    return d;
-}
-
-// Eq. (tau_0)
-double tau0(double normA, double b_inf, double tol, double mbar)
-{
-    const double e = 2.718281828459045235360287, pi = 3.141592653589793238462643;
-    const double a = tol * std::pow((mbar + 1.0) / e, mbar + 1.0) * std::sqrt(2.0 * pi * (mbar + 1.0));
-    return (10.0 / normA) * std::pow(a / (4.0 * normA * b_inf), 1.0 / mbar);
-}
+// controller: ctl.cuh (shared with the device solve loop of small problems)
 
 // ---------------------------------------------------------------------------------------------
 // Krylov extension: steps j = k0 .. k1-1 (0-based), all on the device
@@ -1231,6 +1119,90 @@ int enqueue_wrec_op(phipm_ctx *c, const Op &op, double bytes_op, int p, const do
 // ---------------------------------------------------------------------------------------------
 // the solve (Algorithm 3)
 
+// ---------------------------------------------------------------------------------------------
+// device-driven solve of a small symmetric problem (solve_small.cuh, PHIPM_OPT_DEVSOLVE)
+
+constexpr int SS_ATT_CAP = 65536;
+
+template <class Op>
+bool devsolve_path(const phipm_ctx *c, const Op &op, const Problem &P, const phipm_opts &o, double normA, int p)
+{
+    return opt(c, PHIPM_OPT_DEVSOLVE) && op.n <= SMALL_N && P.symmetric && o.expm_method == PHIPM_EXPM_TAYLOR &&
+           normA >= 0.0 && !c->prof && p + 1 <= SS_MAXU;
+}
+
+template <class Op, int R>
+void ss_set_smem(int mx)
+{
+    cudaFuncSetAttribute(small_solve_kernel<Op, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+
+template <class Op>
+int solve_small_dev(phipm_ctx *c, const Op &op, double t_end, double normA, double bthr, int p,
+                    const double *const *u, const phipm_opts &o, const Problem &P, double *w, phipm_stats &S)
+{
+    const int64_t n = op.n;
+    if (!c->ss_att_d) {
+        if (cudaMalloc((void **)&c->ss_att_d, sizeof(SsAttempt) * SS_ATT_CAP) != cudaSuccess ||
+            cudaHostAlloc((void **)&c->ss_out_h, sizeof(SsOut), cudaHostAllocMapped) != cudaSuccess ||
+            cudaHostGetDevicePointer((void **)&c->ss_out_d, c->ss_out_h, 0) != cudaSuccess)
+            return set_err(c, PHIPM_ENOMEM, "device solve: allocation failed");
+    }
+    SmallSolveArgs a;
+    memset(&a, 0, sizeof(a));
+    a.t_end = t_end;
+    a.tol = o.tol;
+    a.normA = normA;
+    a.bthr = bthr;
+    a.p = p;
+    a.m_init = o.m_init;
+    a.P = P;
+    for (int k = 0; k <= p; k++) a.u[k] = u[k];
+    a.w = w;
+    a.ucur = c->U;
+    a.W = c->W;
+    a.scratch = c->scratch;
+    a.comb = c->comb;
+    a.combd = c->combd;
+    a.res = reinterpret_cast<AttemptResult *>(c->raw);   // device-global slot (raw has MAXD+2 doubles)
+    a.att = c->ss_att_d;
+    a.att_cap = SS_ATT_CAP;
+    a.out = c->ss_out_d;
+    const size_t dyn = c->smem_optin - 8192;
+    const size_t vbytes = (size_t)((n + 15) & ~15) * sizeof(double);
+    a.esm_cap = (int)((dyn - vbytes) / sizeof(double));
+    const int R = (int)((n + SS_NT - 1) / SS_NT);
+    void (*kfn)(Op, SmallSolveArgs, Work) = R <= 2 ? small_solve_kernel<Op, 2>
+                                          : R <= 4 ? small_solve_kernel<Op, 4>
+                                          : R <= 8 ? small_solve_kernel<Op, 8>
+                                                   : small_solve_kernel<Op, 16>;
+    c->ss_out_h->status = -1;
+    CK(launch_k(c, kfn, 1, SS_NT, dyn, op, a, make_work(c)));
+    c->acc.launches++;
+    int rc = sync(c);
+    if (rc) return rc;
+    SsOut R_;
+    memcpy(&R_, (const void *)c->ss_out_h, sizeof(R_));
+    S.nsteps = R_.nsteps;
+    S.nreject = R_.nreject;
+    S.nspmv = R_.nspmv;
+    S.nexpm = R_.nexpm;
+    S.m_last = R_.m_last;
+    S.m_peak = R_.m_peak;
+    S.t_reached = R_.t_reached;
+    c->attempts.clear();
+    c->nattempts = R_.nattempts;
+    c->ss_att_pending = std::min(R_.nattempts, SS_ATT_CAP);
+    switch (R_.status) {
+    case SS_OK: return PHIPM_OK;
+    case SS_ABORT: return set_err(c, PHIPM_ECUDA, "device solve: aborted");
+    case SS_NONFINITE: return set_err(c, PHIPM_ENONFINITE, "non-finite value in the device solve");
+    case SS_SINGULAR: return set_err(c, PHIPM_ESINGULAR, "singular denominator");
+    case SS_STEP: return set_err(c, PHIPM_ESTEP, "step size control failed at t = %g", R_.t_reached);
+    default: return set_err(c, PHIPM_ECUDA, "device solve: no result (status %d)", R_.status);
+    }
+}
+
 template <class Op>
 int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_t NA, double normA_in, int p,
                const double *const *u, const phipm_opts &o, double *w, phipm_stats *stats)
@@ -1241,6 +1213,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     S.t_reached = 0.0;
     c->attempts.clear();
     c->nattempts = 0;
+    c->ss_att_pending = 0;
     // join a speculative extension still running on stream2 (stream order from here on)
     auto join_spec = [&]() {
         if (c->spec_pending) {
@@ -1278,6 +1251,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     // before the host knows it take the breakdown threshold from device memory (bthr < 0)
     const bool anorm_dev = normA < 0.0;
     const double bthr = anorm_dev ? -1.0 : (double)n * EPS_MACH * normA;
+    if (devsolve_path(c, op, P, o, normA, p)) return finish(solve_small_dev(c, op, t_end, normA, bthr, p, u, o, P, w, S));
 
     // b_inf of Eq. (tau_0) = ||u_0||_inf, or the first nonzero ||u_k||_inf (R7); all zero -> w = 0.
     // ||u_0||_inf is read back through an event, and the first step's w-recurrence and initial
@@ -1950,6 +1924,7 @@ int solve_block_impl(phipm_ctx *const *cs, int nb, double t_end, const CsrOp &op
     for (int b = 0; b < nb; b++) {
         cs[b]->attempts.clear();
         cs[b]->nattempts = 0;
+        cs[b]->ss_att_pending = 0;
     }
     if (t_end == 0.0) {
         for (int b = 0; b < nb; b++)
@@ -2222,6 +2197,7 @@ int phipm_set_option(phipm_ctx *c, int option, int value)
     case PHIPM_OPT_COL_PREFETCH: ok = value == 0 || value == 1; break;
     case PHIPM_OPT_FUSE_ANORM: ok = value == 0 || value == 1; break;
     case PHIPM_OPT_CSR_OFF16: ok = value == 0 || value == 1; break;
+    case PHIPM_OPT_DEVSOLVE: ok = value == 0 || value == 1; break;
     case PHIPM_OPT_CLUSTER_LZ: ok = value >= -1 && value <= 16 && (value <= 1 || (value & (value - 1)) == 0); break;
     default: ok = value == 0 || value == 1; break;
     }
@@ -2303,6 +2279,15 @@ int phipm_get_trace(const phipm_ctx *c, phipm_trace_rec *out, int max, int *coun
 int phipm_get_attempts(const phipm_ctx *c, phipm_attempt *out, int max, int *count)
 {
     if (!c || !count || (max > 0 && !out)) return PHIPM_EINVAL;
+    if (c->ss_att_pending > 0) {                     // a device-driven solve: records still on the device
+        phipm_ctx *cm = const_cast<phipm_ctx *>(c);
+        static_assert(sizeof(SsAttempt) == sizeof(phipm_attempt), "attempt record layouts");
+        cm->attempts.resize(c->ss_att_pending);
+        if (cudaMemcpy(cm->attempts.data(), c->ss_att_d, sizeof(SsAttempt) * c->ss_att_pending,
+                       cudaMemcpyDeviceToHost) != cudaSuccess)
+            return set_err(cm, PHIPM_ECUDA, "attempt records: copy failed");
+        cm->ss_att_pending = 0;
+    }
     const int nrec = (int)std::min<size_t>(c->attempts.size(), (size_t)std::max(max, 0));
     for (int i = 0; i < nrec; i++) out[i] = c->attempts[i];
     *count = (int)c->nattempts;
@@ -2321,6 +2306,8 @@ void phipm_destroy(phipm_ctx *c)
         cudaStreamDestroy(c->stream2);
     }
     if (c->ev_main) cudaEventDestroy(c->ev_main);
+    if (c->ss_att_d) cudaFree(c->ss_att_d);
+    if (c->ss_out_h) cudaFreeHost(c->ss_out_h);
     if (c->ev_spec) cudaEventDestroy(c->ev_spec);
     cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
     cudaFree(c->part); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
@@ -2402,6 +2389,14 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         cudaFuncSetAttribute(spmv_stream_kernel<IdentOp, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(krylov_small_kernel<StencilOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_N * 8);
         cudaFuncSetAttribute(krylov_small_kernel<CsrOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_N * 8);
+        ss_set_smem<StencilOp, 2>(mx);
+        ss_set_smem<StencilOp, 4>(mx);
+        ss_set_smem<StencilOp, 8>(mx);
+        ss_set_smem<StencilOp, 16>(mx);
+        ss_set_smem<CsrOp, 2>(mx);
+        ss_set_smem<CsrOp, 4>(mx);
+        ss_set_smem<CsrOp, 8>(mx);
+        ss_set_smem<CsrOp, 16>(mx);
         for (int dc = 1; dc <= 4; dc++)
             for (ClusterLzFn f : {cluster_lz_fn<256, 4>(dc), cluster_lz_fn<512, 8>(dc)}) {
                 cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);

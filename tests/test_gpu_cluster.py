@@ -164,3 +164,57 @@ def test_speculative_extension_changes_nothing(name):
         ctx.close()
     assert np.array_equal(res[1][0], res[0][0])
     assert res[1][1] == res[0][1]
+
+
+@pytest.mark.parametrize("name", ["c1", "c1_mini", "c2_mini"])
+def test_device_solve_matches_host_solve(orc, name):
+    # option devsolve (default on): a symmetric problem with n <= 8192 runs as ONE kernel that also
+    # executes the controller (solve_small.cuh).  Against the host-driven path on the same inputs: the
+    # same trajectory where the two agree to rounding (the first step's attempts; the dot / norm sums
+    # are reduced in another order), the solution within the parity bar of both and of the oracle, and
+    # the attempt records of the device solve are the ones of that solve (not a stale earlier one)
+    Pb = W.make(name)
+    u = [to_dev(x) for x in Pb.u]
+    out = {}
+    for dev in (1, 0):
+        ctx = P.Context(n_max=Pb.n, m_max=100, p_max=max(Pb.p, 1), options={"devsolve": dev})
+        w, s = ctx.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), u, tol=Pb.tol, symmetric=True)
+        out[dev] = (w.cpu().numpy(), s, ctx.attempts())
+        ctx.close()
+    wo, so, tr = orc.solve(Pb)
+    (wd, sd, ad), (wh, sh, ah) = out[1], out[0]
+    assert len(ad) == sd.nexpm and len(ah) == sh.nexpm
+    first = next(i for i, a in enumerate(ah) if a["accepted"]) + 1
+    for a, b in zip(ad[:first], ah[:first]):
+        assert (a["m"], a["mu"], a["accepted"], a["branch"]) == (b["m"], b["mu"], b["accepted"], b["branch"])
+        assert a["tau"] == pytest.approx(b["tau"], rel=1e-9)
+        assert a["beta"] == pytest.approx(b["beta"], rel=1e-10)
+    assert sd.t_reached == Pb.t and abs(sd.nsteps - sh.nsteps) <= 2
+    assert relerr(wd, wo) <= parity_bound(Pb.tol)
+    assert relerr(wd, wh) <= parity_bound(Pb.tol)
+    # a following host-path solve on the same context reports its own attempts
+    ctx = P.Context(n_max=max(Pb.n, 65536), m_max=100, p_max=4)
+    ctx.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), u, tol=Pb.tol, symmetric=True)
+    Q = W.make("c2")
+    ctx.solve_stencil(Q.t, P.Stencil.of(Q.stencil), [to_dev(x) for x in Q.u], tol=Q.tol, symmetric=True)
+    aq = ctx.attempts()
+    ctx.close()
+    assert aq[0]["m"] == Q.m_init and len(aq) == 6
+
+
+def test_device_solve_degenerate():
+    # zero input (w = 0), A = 0 (tau = t), a breakdown at the seed: the device solve's special paths
+    Pb = W.make("c1_mini")
+    S = P.Stencil.of(Pb.stencil)
+    ctx = P.Context(n_max=Pb.n, m_max=100, p_max=4)
+    z = [to_dev(np.zeros(Pb.n)) for _ in Pb.u]
+    w, s = ctx.solve_stencil(Pb.t, S, z, tol=Pb.tol, symmetric=True)
+    assert float(w.abs().max()) == 0.0 and s.t_reached == Pb.t
+    S0 = P.Stencil(S.dim, S.nx, S.ny, S.nz, (0.0,) * 7)
+    u = [to_dev(x) for x in Pb.u]
+    w, s = ctx.solve_stencil(Pb.t, S0, u, tol=Pb.tol, symmetric=True)
+    # A = 0: w = u_0 + sum_k t^k/k! u_k exactly up to rounding
+    import math
+    ref = sum(Pb.t ** k / math.factorial(k) * Pb.u[k] for k in range(len(Pb.u)))
+    assert relerr(w.cpu().numpy(), ref) <= 1e-14
+    ctx.close()

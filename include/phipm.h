@@ -148,6 +148,11 @@ typedef struct {
  * *count to the number the solve made (only the first 65536 are kept). */
 int phipm_get_attempts(const phipm_ctx *ctx, phipm_attempt *out, int max, int *count);
 
+/* Measurement stamps (environment PHIPM_EXPM_CLOCKS=1 at phipm_create, else zeros): copies 16 words to
+ * out16 (HOST): the phase cycles of the last exponential kernel, or of the last device-driven small
+ * solve (setup, w-recurrence + seed, extensions, exponential, controller, combine in words 0..5). */
+int phipm_get_clocks(const phipm_ctx *ctx, long long *out16);
+
 void phipm_default_opts(phipm_opts *opts);
 
 /* Method used by the kernel-level entry points phipm_expm and phipm_phi_pair (solves take

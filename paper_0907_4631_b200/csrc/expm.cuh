@@ -96,25 +96,30 @@ __device__ __forceinline__ void cta_matmul_e(int Kp, int ld, const double *A, co
         for (int x = 0; x < 2; x++)
 #pragma unroll
             for (int y = 0; y < 2; y++) c[x][y][0] = c[x][y][1] = 0.0;
-        double a0 = A0[0], a1 = A1[0], b0 = B0[0], b1 = B1[0];
-        for (int k = 0; k < Kp; k += 4) {
-            double na0 = 0.0, na1 = 0.0, nb0 = 0.0, nb1 = 0.0;
-            if (k + 4 < Kp) {
-                na0 = A0[(size_t)(k + 4) * ld];
-                na1 = A1[(size_t)(k + 4) * ld];
-                nb0 = B0[k + 4];
-                nb1 = B1[k + 4];
-            }
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(c[0][0][0]), "+d"(c[0][0][1]) : "d"(a0), "d"(b0));
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(c[0][1][0]), "+d"(c[0][1][1]) : "d"(a0), "d"(b1));
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(c[1][0][0]), "+d"(c[1][0][1]) : "d"(a1), "d"(b0));
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(c[1][1][0]), "+d"(c[1][1][1]) : "d"(a1), "d"(b1));
-            a0 = na0; a1 = na1; b0 = nb0; b1 = nb1;
+        // two k-steps per iteration, both fragment sets loaded first (tools/mm_probe.cu: 5-6 % faster
+        // products than one set prefetched one step ahead at Kp = 40, 56, 64)
+#define EXPM_DMMA4(A0_, A1_, B0_, B1_)                                                                             \
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"                   \
+                 : "+d"(c[0][0][0]), "+d"(c[0][0][1]) : "d"(A0_), "d"(B0_));                                      \
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"                   \
+                 : "+d"(c[0][1][0]), "+d"(c[0][1][1]) : "d"(A0_), "d"(B1_));                                      \
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"                   \
+                 : "+d"(c[1][0][0]), "+d"(c[1][0][1]) : "d"(A1_), "d"(B0_));                                      \
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"                   \
+                 : "+d"(c[1][1][0]), "+d"(c[1][1][1]) : "d"(A1_), "d"(B1_));
+        int k = 0;
+        for (; k + 8 <= Kp; k += 8) {
+            const double a0 = A0[(size_t)k * ld], a1 = A1[(size_t)k * ld], b0 = B0[k], b1 = B1[k];
+            const double e0 = A0[(size_t)(k + 4) * ld], e1 = A1[(size_t)(k + 4) * ld], f0 = B0[k + 4],
+                         f1 = B1[k + 4];
+            EXPM_DMMA4(a0, a1, b0, b1)
+            EXPM_DMMA4(e0, e1, f0, f1)
         }
+        if (k < Kp) {                                    // (not reached: Kp is a multiple of 8)
+            const double a0 = A0[(size_t)k * ld], a1 = A1[(size_t)k * ld], b0 = B0[k], b1 = B1[k];
+            EXPM_DMMA4(a0, a1, b0, b1)
+        }
+#undef EXPM_DMMA4
 #pragma unroll
         for (int x = 0; x < 2; x++)
 #pragma unroll

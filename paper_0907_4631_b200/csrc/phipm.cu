@@ -1168,6 +1168,7 @@ int solve_small_dev(phipm_ctx *c, const Op &op, double t_end, double normA, doub
     a.att = c->ss_att_d;
     a.att_cap = SS_ATT_CAP;
     a.out = c->ss_out_d;
+    a.clk = c->expm_clk_d;                               // PHIPM_EXPM_CLOCKS: phase cycles of the solve
     const size_t dyn = c->smem_optin - 8192;
     const size_t vbytes = (size_t)((n + 15) & ~15) * sizeof(double);
     a.esm_cap = (int)((dyn - vbytes) / sizeof(double));
@@ -2273,6 +2274,13 @@ int phipm_get_trace(const phipm_ctx *c, phipm_trace_rec *out, int max, int *coun
     const int nrec = (int)std::min<size_t>(c->tracebuf.size(), (size_t)std::max(max, 0));
     for (int i = 0; i < nrec; i++) out[i] = c->tracebuf[i];
     *count = (int)c->ntrace;
+    return PHIPM_OK;
+}
+
+int phipm_get_clocks(const phipm_ctx *c, long long *out16)
+{
+    if (!c || !out16) return PHIPM_EINVAL;
+    for (int i = 0; i < 16; i++) out16[i] = c->expm_clk_h ? c->expm_clk_h[i] : 0;
     return PHIPM_OK;
 }
 

@@ -56,7 +56,16 @@ struct SmallSolveArgs {
     int att_cap;
     SsOut *out;
     int esm_cap;                    // doubles of dynamic shared memory for the exponential's buffers
+    long long *clk;                 // optional phase cycles (thread 0): setup, w-recurrence + seed,
+                                    // extensions, exponential, controller, combine
 };
+
+#define SS_CLK(i)                                                      \
+    if (a.clk && threadIdx.x == 0) {                                   \
+        const long long c_ = clock64();                                \
+        ss_acc[i] += c_ - ss_prev;                                     \
+        ss_prev = c_;                                                  \
+    }
 
 // block sum of one value per thread (total in every thread): warp trees, then a log2(16)-level tree
 // over the 16 warp totals (lane l holds warp l mod 16's); `red` alternates between two arrays so one
@@ -116,6 +125,8 @@ __global__ void __launch_bounds__(SS_NT, 1) small_solve_kernel(Op op, SmallSolve
     const int p = a.p;
     double *vs = ssm;                                        // v~_j of the Lanczos step
     double *esm = ssm + ((n + 15) & ~15);                    // the exponential's buffers
+    long long ss_acc[6] = {0, 0, 0, 0, 0, 0};
+    long long ss_prev = clock64();
     pdl_wait();
 
     // ---- setup: b_inf of Eq. (tau_0) (||u_0||_inf, else the first nonzero ||u_k||_inf, R7) ----
@@ -153,6 +164,7 @@ __global__ void __launch_bounds__(SS_NT, 1) small_solve_kernel(Op op, SmallSolve
         S.m_peak = m_init;
     }
     __syncthreads();
+    SS_CLK(0)
 
     while (true) {
         // ---------------- a new step at t_k: w-recurrence and seed ----------------
@@ -209,6 +221,7 @@ __global__ void __launch_bounds__(SS_NT, 1) small_solve_kernel(Op op, SmallSolve
                 wk.st->lz = 0.0;
             }
             __syncthreads();
+            SS_CLK(1)
         }
         // ---------------- attempts ----------------
         while (true) {
@@ -283,6 +296,7 @@ __global__ void __launch_bounds__(SS_NT, 1) small_solve_kernel(Op op, SmallSolve
                 }
                 __syncthreads();
                 if (t == 0) sh.enq = m;
+                SS_CLK(2)
             }
             // the augmented exponential and the error estimate (expm_kernel's body, mode 0)
             {
@@ -309,6 +323,7 @@ __global__ void __launch_bounds__(SS_NT, 1) small_solve_kernel(Op op, SmallSolve
                 if (fits) expm_body<true, false>(ea, esm);
                 else expm_body<false, false>(ea, esm);
                 __syncthreads();
+                SS_CLK(3)
             }
             // the controller (Algorithm 4, then Algorithm 3's choice and clamps) on thread 0
             if (t == 0) {
@@ -364,6 +379,7 @@ __global__ void __launch_bounds__(SS_NT, 1) small_solve_kernel(Op op, SmallSolve
                 }
             }
             __syncthreads();
+            SS_CLK(4)
             if (sh.status != SS_OK || sh.accepted) break;
         }
         if (sh.status == SS_STEP) {                          // w := u_k, as the host path
@@ -422,9 +438,12 @@ __global__ void __launch_bounds__(SS_NT, 1) small_solve_kernel(Op op, SmallSolve
                 sh.done = last ? 1 : (sh.tk < a.t_end ? 0 : 1);
             }
             __syncthreads();
+            SS_CLK(5)
             if (sh.done) break;
         }
     }
+    if (a.clk && t == 0)
+        for (int i = 0; i < 6; i++) a.clk[i] = ss_acc[i];
     if (t == 0) {
         S.status = sh.status;
         if (sh.status != SS_OK) S.t_reached = sh.tk;

@@ -134,6 +134,45 @@ __device__ void mm_unroll2(int Kp, int ld, const double *A, const double *B, dou
     __syncthreads();
 }
 
+// V3/V4: tasks of 1 x TC tiles (TC = 2 or 1), task index column-major over (tile row, column group),
+// dealt round-robin to the warps (warp w on sub-partition w mod 4)
+template <int TC>
+__device__ void mm_fine(int Kp, int ld, const double *A, const double *B, double *C)
+{
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int nt = Kp >> 3, ng = (nt + TC - 1) / TC;
+    const int ar = lane >> 2, ac = lane & 3;
+    for (int task = warp; task < nt * ng; task += nw) {
+        const int ti = task % nt, cg = task / nt;
+        const int tj0 = cg * TC;
+        const bool rj = TC == 2 && tj0 + 1 < nt;
+        const double *A0 = A + (ti * 8 + ar) + (size_t)ac * ld;
+        const double *B0 = B + ac + (size_t)(tj0 * 8 + ar) * ld;
+        const double *B1 = rj ? B0 + (size_t)8 * ld : B0;
+        double c0 = 0, c1 = 0, d0 = 0, d1 = 0;
+        double a0 = A0[0], b0 = B0[0], b1 = B1[0];
+        for (int k = 0; k < Kp; k += 4) {
+            double na0 = 0.0, nb0 = 0.0, nb1 = 0.0;
+            if (k + 4 < Kp) {
+                na0 = A0[(size_t)(k + 4) * ld];
+                nb0 = B0[k + 4];
+                if (TC == 2) nb1 = B1[k + 4];
+            }
+            DMMA(c0, c1, a0, b0);
+            if (TC == 2) DMMA(d0, d1, a0, b1);
+            a0 = na0; b0 = nb0; b1 = nb1;
+        }
+        const int row = ti * 8 + ar, col = tj0 * 8 + 2 * ac;
+        C[row + (size_t)col * ld] = c0;
+        C[row + (size_t)(col + 1) * ld] = c1;
+        if (rj) {
+            C[row + (size_t)(col + 8) * ld] = d0;
+            C[row + (size_t)(col + 9) * ld] = d1;
+        }
+    }
+    __syncthreads();
+}
+
 template <int V>
 __global__ void __launch_bounds__(EXPM_NT, 1) prod_kernel(int Kp, int reps, long long *cyc, double *out)
 {
@@ -149,7 +188,9 @@ __global__ void __launch_bounds__(EXPM_NT, 1) prod_kernel(int Kp, int reps, long
     for (int q = 0; q < reps; q++) {
         if (V == 0) cta_matmul(Kp, ld, A, A, C);
         else if (V == 1) mm_splitk(Kp, ld, A, A, C, part);
-        else mm_unroll2(Kp, ld, A, A, C);
+        else if (V == 2) mm_unroll2(Kp, ld, A, A, C);
+        else if (V == 3) mm_fine<2>(Kp, ld, A, A, C);
+        else mm_fine<1>(Kp, ld, A, A, C);
     }
     const long long t1 = clock64();
     if (threadIdx.x == 0) cyc[0] = t1 - t0;
@@ -163,13 +204,14 @@ int main()
     cudaMalloc(&dc, 8);
     cudaMalloc(&dout, 8 * 160 * 160);
     double *h0 = new double[160 * 160], *h1 = new double[160 * 160];
-    for (int Kp : {40, 48, 56, 64, 104}) {
+    for (int Kp : {40, 48, 56, 64}) {
         const int ld = expm_ld(Kp);
         const size_t smem = (2 * (size_t)ld * Kp + 64 * 256) * 8;
-        long long c[3];
-        void (*f[3])(int, int, long long *, double *) = {prod_kernel<0>, prod_kernel<1>, prod_kernel<2>};
+        long long c[5];
+        void (*f[5])(int, int, long long *, double *) = {prod_kernel<0>, prod_kernel<1>, prod_kernel<2>,
+                                                         prod_kernel<3>, prod_kernel<4>};
         double maxdiff = 0.0;
-        for (int v = 0; v < 3; v++) {
+        for (int v = 0; v < 5; v++) {
             cudaFuncSetAttribute(f[v], cudaFuncAttributeMaxDynamicSharedMemorySize, 220000);
             f[v]<<<1, EXPM_NT, smem>>>(Kp, 50, dc, dout);
             f[v]<<<1, EXPM_NT, smem>>>(Kp, 50, dc, dout);
@@ -178,8 +220,8 @@ int main()
             if (v > 0)
                 for (int e = 0; e < ld * Kp; e++) maxdiff = fmax(maxdiff, fabs(h0[e] - h1[e]) / (1e-300 + fabs(h0[e])));
         }
-        printf("Kp=%3d: cta_matmul %6.0f  splitK %6.0f  unroll2 %6.0f cycles/product  (max rel diff %.1e, %s)\n", Kp,
-               c[0] / 50.0, c[1] / 50.0, c[2] / 50.0, maxdiff, cudaGetErrorString(cudaGetLastError()));
+        printf("Kp=%3d: cta_matmul %6.0f  splitK %6.0f  unroll2 %6.0f  1x2 %6.0f  1x1 %6.0f cycles/product  (max rel diff %.1e, %s)\n", Kp,
+               c[0] / 50.0, c[1] / 50.0, c[2] / 50.0, c[3] / 50.0, c[4] / 50.0, maxdiff, cudaGetErrorString(cudaGetLastError()));
     }
     return 0;
 }

@@ -189,6 +189,14 @@ __device__ __forceinline__ double ldg_stream(const double *p)
     return r;
 }
 
+__device__ __forceinline__ int4 ldg_stream_i4(const int4 *p)
+{
+    int4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
 __device__ __forceinline__ double2 ldg_stream2(const double *p)
 {
     double2 r;
@@ -496,6 +504,67 @@ __global__ void __launch_bounds__(CSRA_NT) csr_analyze_kernel(CsrOp A, int L, Cs
     }
     if (lane == 0) {
         atomicMax(&out->norm_bits, (unsigned long long)__double_as_longlong(nrm));
+        if (bad) atomicOr(&out->nonuniform, 1);
+        atomicMax(&out->blo, blo);
+        atomicMax(&out->bhi, bhi);
+    }
+}
+
+// The uniform-row case of csr_analyze_kernel's mode 2 (band and uniformity only; the fused-||A|| CSR path),
+// as a plain stream: rows of L = 2^lgL entries (L >= 4), so an aligned 16-B group of 4 column indices lies
+// in one row, row = e >> lgL, and the pass is two coalesced int4 streams (row_ptr, col) with four loads in
+// flight per thread.  Same results as csr_analyze_kernel (max of clamp_band(+-(col - row)) over the entries
+// and the row_ptr check) whenever the rows are uniform; when they are not (nonuniform set), the band is
+// that of entry e's nominal row e / L and the host reruns csr_analyze_kernel.
+__global__ void __launch_bounds__(256) csr_analyze_ell_kernel(int64_t n, const int32_t *__restrict__ rp,
+                                                              const int32_t *__restrict__ col, int lgL,
+                                                              CsrAnalysis *out)
+{
+    const int64_t L = (int64_t)1 << lgL;
+    const int64_t nnz = n << lgL;
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+    int bad = 0, blo = 0, bhi = 0;
+    // row_ptr: rp[r] == L r for r = 0 .. n
+    for (int64_t r = tid; r <= n; r += nth)
+        if ((int64_t)rp[r] != L * r) bad = 1;
+    // col, four int4 groups per thread per iteration
+    const int4 *c4 = reinterpret_cast<const int4 *>(col);
+    const int64_t ng = nnz >> 2;
+    auto band = [&](const int4 &v, int64_t g) {
+        const int64_t row = (g << 2) >> lgL;
+        const int64_t d0 = (int64_t)v.x - row, d1 = (int64_t)v.y - row, d2 = (int64_t)v.z - row, d3 = (int64_t)v.w - row;
+        blo = max(blo, max(max(clamp_band(-d0), clamp_band(-d1)), max(clamp_band(-d2), clamp_band(-d3))));
+        bhi = max(bhi, max(max(clamp_band(d0), clamp_band(d1)), max(clamp_band(d2), clamp_band(d3))));
+    };
+    int64_t g = tid;
+    for (; g + 3 * nth < ng; g += 4 * nth) {
+        const int4 v0 = ldg_stream_i4(c4 + g), v1 = ldg_stream_i4(c4 + g + nth);
+        const int4 v2 = ldg_stream_i4(c4 + g + 2 * nth), v3 = ldg_stream_i4(c4 + g + 3 * nth);
+        band(v0, g);
+        band(v1, g + nth);
+        band(v2, g + 2 * nth);
+        band(v3, g + 3 * nth);
+    }
+    for (; g < ng; g += nth) band(ldg_stream_i4(c4 + g), g);
+    for (int o = 16; o > 0; o >>= 1) {
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        blo = max(blo, __shfl_xor_sync(0xffffffffu, blo, o));
+        bhi = max(bhi, __shfl_xor_sync(0xffffffffu, bhi, o));
+    }
+    __shared__ int sb[3][8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        sb[0][warp] = bad;
+        sb[1][warp] = blo;
+        sb[2][warp] = bhi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) {
+            bad |= sb[0][w];
+            blo = max(blo, sb[1][w]);
+            bhi = max(bhi, sb[2][w]);
+        }
         if (bad) atomicOr(&out->nonuniform, 1);
         atomicMax(&out->blo, blo);
         atomicMax(&out->bhi, bhi);

@@ -1639,7 +1639,18 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA, int mode = 
     ProfRec r;
     prof_begin(c, r, PC_OTHER, ((mode & 1) ? 8.0 : 0.0) * (double)nnz + ((mode & 2) ? 4.0 : 0.0) * (double)nnz +
                                    ((mode & 4) && off16 && L > 0 ? 2.0 : 0.0) * (double)nnz + 4.0 * (double)(op.n + 1));
-    csr_analyze_kernel<<<grid, CSRA_NT, 0, c->stream>>>(op, (int)L, d, mode, off16);
+    // band and uniformity only, rows of a power-of-two length >= 4, 16-B aligned columns: the streaming
+    // kernel (csr_analyze_ell_kernel); if the rows turn out not to be uniform, the general pass follows
+    int lgL = -1;
+    if (mode == 2 && L >= 4 && (L & (L - 1)) == 0 && ((uintptr_t)op.col & 15) == 0)
+        for (lgL = 0; ((int64_t)1 << lgL) < L; lgL++) {
+        }
+    if (lgL >= 2) {
+        const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)nnz / 4 + 255) / 256, (int64_t)c->sm_count * 8));
+        csr_analyze_ell_kernel<<<g2, 256, 0, c->stream>>>(op.n, op.rp, op.col, lgL, d);
+    } else {
+        csr_analyze_kernel<<<grid, CSRA_NT, 0, c->stream>>>(op, (int)L, d, mode, off16);
+    }
     prof_end(c, r);
     c->acc.launches++;
     CK(cudaGetLastError());
@@ -1648,6 +1659,16 @@ int analyze_csr(phipm_ctx *c, CsrOp &op, int64_t nnz, double *normA, int mode = 
     if (rc) return rc;
     CsrAnalysis h;
     memcpy(&h, c->raw_h, sizeof(h));
+    if (lgL >= 2 && h.nonuniform) {
+        CK(cudaMemsetAsync(d, 0, sizeof(CsrAnalysis), c->stream));
+        csr_analyze_kernel<<<grid, CSRA_NT, 0, c->stream>>>(op, (int)L, d, mode, off16);
+        c->acc.launches++;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(c->raw_h, d, sizeof(CsrAnalysis), cudaMemcpyDeviceToHost, c->stream));
+        rc = sync(c);
+        if (rc) return rc;
+        memcpy(&h, c->raw_h, sizeof(h));
+    }
     if (mode & 1) memcpy(normA, &h.norm_bits, sizeof(double));
     if (!(mode & 2)) return PHIPM_OK;
     if (!env_ell || L < 4 || (L % 4) || ((L / 4) & (L / 4 - 1)) || h.nonuniform) return PHIPM_OK;

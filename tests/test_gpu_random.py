@@ -136,3 +136,46 @@ def test_random_banded_solves(ctx, orc, seed, n, p, symmetric):
                          symmetric=symmetric)
     assert s.t_reached == t
     assert relerr(w.cpu().numpy(), wo) <= parity_bound(tol)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "alternating", "one_long_row"])
+def test_csr_analysis_streaming_path(orc, kind):
+    # nnz = 8 n in every case, so the analysis takes the streaming uniform-row kernel first
+    # (csr_analyze_ell_kernel); rows that are not all of length 8 must be caught (row_ptr check) and
+    # the general pass rerun, or the x-ring SpMV would run with a wrong band.  Solve vs the oracle.
+    rng = np.random.default_rng(77)
+    n, L, band = 20000, 8, 200            # n > SMALL_N: the streaming (x-ring) SpMV uses the band
+    if kind == "uniform":
+        lens = np.full(n, L)
+    elif kind == "alternating":
+        lens = np.where(np.arange(n) % 2 == 0, 4, 12)
+    else:
+        lens = np.full(n, L)
+        lens[0] = 1
+        lens[1] = 2 * L - 1
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum(lens)
+    assert rp[-1] == L * n
+    col = np.empty(rp[-1], np.int32)
+    val = np.empty(rp[-1], np.float64)
+    for r in range(n):
+        k = lens[r]
+        lo, hi = max(0, r - band), min(n - 1, r + band)
+        cs = np.sort(rng.choice(np.arange(lo, hi + 1), size=k, replace=False))
+        if r not in cs:
+            cs[np.argmin(np.abs(cs - r))] = r
+            cs = np.sort(cs)
+        v = rng.standard_normal(k) / 4
+        v[cs == r] = 0.0
+        v[cs == r] = -(np.abs(v).sum()) - 1.0
+        col[rp[r]:rp[r + 1]] = cs
+        val[rp[r]:rp[r + 1]] = v
+    csr = (rp.astype(np.int32), col, val)
+    u = [rng.standard_normal(n), rng.uniform(-1, 1, n)]
+    t, tol = 0.5, 1e-8
+    wo, so, _ = orc.phipm(t, csr, u, tol, m_init=10, m_max=100, symmetric=False)
+    ctx = P.Context(n_max=n, m_max=100, p_max=2)
+    w, s = ctx.solve_csr(t, tuple(to_dev(a) for a in csr), [to_dev(x) for x in u], tol=tol, symmetric=False)
+    ctx.close()
+    assert s.t_reached == t
+    assert relerr(w.cpu().numpy(), wo) <= parity_bound(tol), (s, so)

@@ -198,6 +198,9 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *   PHIPM_OPT_DEVSOLVE         1 (default): a symmetric problem with n <= 8192 and the Taylor exponential
  *                              is solved by ONE single-CTA kernel that also runs the controller (no host
  *                              round trip per attempt; opts.profile disables it); 0 off
+ *   PHIPM_OPT_GRAPH            1: the two-kernel extension (Arnoldi with n > 2^19, CSR) is captured once as a
+ *                              CUDA graph and replayed from a per-context cache; 0 (default) stream launches
+ *                              with programmatic dependent launch
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -218,7 +221,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_CLUSTER_LZ      16
 #define PHIPM_OPT_SPEC            17
 #define PHIPM_OPT_DEVSOLVE        18
-#define PHIPM_OPT_COUNT           19
+#define PHIPM_OPT_GRAPH           19
+#define PHIPM_OPT_COUNT           20
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

@@ -57,6 +57,12 @@ struct ProfRec {
 
 } // namespace
 
+struct GraphRec {
+    std::vector<unsigned char> key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t nlaunch = 0;
+};
+
 struct phipm_ctx {
     int dev = 0;
     cudaStream_t stream = nullptr;
@@ -80,6 +86,7 @@ struct phipm_ctx {
     SsAttempt *ss_att_d = nullptr;                   // attempt records (device)
     SsOut *ss_out_h = nullptr, *ss_out_d = nullptr;  // stats and status (mapped pinned)
     int ss_att_pending = 0;                          // records of the last solve still on the device
+    std::vector<GraphRec> graphs;                    // captured two-kernel extensions (PHIPM_OPT_GRAPH)
     DevState *st = nullptr;
     int32_t *tlo = nullptr, *thi = nullptr;                  // CSR per-tile column ranges
     int16_t *off16 = nullptr;                                // CSR int16 column offsets (x-ring path)
@@ -125,7 +132,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0};
     char err[512] = {0};
 };
 
@@ -896,6 +903,76 @@ struct OnStream2 {
 };
 
 template <class Op>
+int enqueue_krylov_stream(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1,
+                          double bthr);
+
+// PHIPM_OPT_GRAPH: the two-kernel extension k0 -> k1 (2(k1 - k0) launches, more with CGS2) captured once as a
+// CUDA graph on the context's private stream and replayed from a per-context cache keyed by the operator,
+// k0, k1, the breakdown threshold and the context options (everything the captured launches depend on; the
+// workspace pointers are the context's own).  The kernels read all step state from device memory, so a
+// replay is the same computation as the stream launches (same kernels, arguments, order).
+template <class Op>
+int enqueue_krylov_graph(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1,
+                         double bthr)
+{
+    std::vector<unsigned char> key(sizeof(Op) + 5 * sizeof(int) + sizeof(double) + sizeof(c->opt) + sizeof(void *));
+    unsigned char *kp = key.data();
+    auto put = [&](const void *p, size_t b) {
+        memcpy(kp, p, b);
+        kp += b;
+    };
+    const int sym = symmetric ? 1 : 0;
+    const int tag = std::is_same<Op, StencilOp>::value ? 1 : std::is_same<Op, CsrOp>::value ? 2 : 3;
+    const void *sp = (const void *)c->stream;
+    put(&op, sizeof(Op));
+    put(&tag, sizeof(int));
+    put(&sym, sizeof(int));
+    put(&orth, sizeof(int));
+    put(&k0, sizeof(int));
+    put(&k1, sizeof(int));
+    put(&bthr, sizeof(double));
+    put(c->opt, sizeof(c->opt));
+    put(&sp, sizeof(void *));
+    for (auto &g : c->graphs)
+        if (g.key == key) {
+            CK(cudaGraphLaunch(g.exec, c->stream));
+            c->acc.launches += g.nlaunch;
+            return PHIPM_OK;
+        }
+    // capture on the private stream (the caller's stream may be the legacy stream, which cannot capture)
+    const int64_t l0 = c->acc.launches;
+    cudaGraph_t graph = nullptr;
+    int rc;
+    {
+        OnStream2 on2(c);
+        CK(cudaStreamBeginCapture(c->stream2, cudaStreamCaptureModeThreadLocal));
+        rc = enqueue_krylov_stream(c, op, bytes_op, symmetric, orth, k0, k1, bthr);
+        const cudaError_t e = cudaStreamEndCapture(c->stream2, &graph);
+        if (!rc && e != cudaSuccess) rc = set_err(c, PHIPM_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+    }
+    if (rc) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        return rc;
+    }
+    GraphRec g;
+    g.key = key;
+    g.nlaunch = c->acc.launches - l0;
+    c->acc.launches = l0;
+    const cudaError_t e = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return set_err(c, PHIPM_ECUDA, "graph instantiate: %s", cudaGetErrorString(e));
+    if (c->graphs.size() >= 64) {
+        cudaGraphExecDestroy(c->graphs.front().exec);
+        c->graphs.erase(c->graphs.begin());
+    }
+    c->graphs.push_back(g);
+    CK(cudaGraphLaunch(g.exec, c->stream));
+    c->acc.launches += g.nlaunch;
+    return PHIPM_OK;
+}
+
+template <class Op>
 int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1, double bthr)
 {
     if (symmetric && try_cluster_lz(c, op, bytes_op, k0, k1, bthr)) return PHIPM_OK;
@@ -926,6 +1003,17 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
         int rc = PHIPM_OK;
         if (launch_persist(c, op, bytes_op, symmetric, k0, k1, bthr, rc)) return rc;
     }
+    if (k1 > k0 && opt(c, PHIPM_OPT_GRAPH) && !c->prof && !c->kclk_d)
+        return enqueue_krylov_graph(c, op, bytes_op, symmetric, orth, k0, k1, bthr);
+    return enqueue_krylov_stream(c, op, bytes_op, symmetric, orth, k0, k1, bthr);
+}
+
+// the two-kernel path of an extension: per step the fused SpMV + dots and the update + norm
+template <class Op>
+int enqueue_krylov_stream(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1,
+                          double bthr)
+{
+    const int64_t n = op.n;
     // Arnoldi (CGS): lagged normalisation (PHIPM_OPT_LAG = 0 disables).  Step j > k0's SpMV works on the raw
     // v~_j and also reduces ||v~_j||^2 (free: the x tile is on chip), its finalize derives sigma_j and
     // h_{j,j-1}; so the update passes need no grid reduction except the extension's last one, which
@@ -2220,6 +2308,7 @@ int phipm_set_option(phipm_ctx *c, int option, int value)
     case PHIPM_OPT_FUSE_ANORM: ok = value == 0 || value == 1; break;
     case PHIPM_OPT_CSR_OFF16: ok = value == 0 || value == 1; break;
     case PHIPM_OPT_DEVSOLVE: ok = value == 0 || value == 1; break;
+    case PHIPM_OPT_GRAPH: ok = value == 0 || value == 1; break;
     case PHIPM_OPT_CLUSTER_LZ: ok = value >= -1 && value <= 16 && (value <= 1 || (value & (value - 1)) == 0); break;
     default: ok = value == 0 || value == 1; break;
     }
@@ -2336,6 +2425,7 @@ void phipm_destroy(phipm_ctx *c)
     }
     if (c->ev_main) cudaEventDestroy(c->ev_main);
     if (c->ss_att_d) cudaFree(c->ss_att_d);
+    for (auto &g : c->graphs) cudaGraphExecDestroy(g.exec);
     if (c->ss_out_h) cudaFreeHost(c->ss_out_h);
     if (c->ev_spec) cudaEventDestroy(c->ev_spec);
     cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);

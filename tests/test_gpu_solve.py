@@ -437,3 +437,22 @@ def test_csr_int16_offsets_option(orc):
     wo, so = run_oracle(orc, Pb)
     assert relerr(out[1][0], wo) <= parity_bound(Pb.tol)
     assert np.array_equal(out[1][0], out[0][0]) and out[1][1] == out[0][1]
+
+
+@pytest.mark.parametrize("name,path", [("c5_med", "csr"), ("c3", "stencil")])
+def test_graph_replay_matches_stream_launches(name, path):
+    # option graph: the two-kernel extension captured as a CUDA graph and replayed from the context's cache
+    # (second solve: every extension is a cache hit) -- the same kernels with the same arguments, so w and
+    # the stats are bit-identical with the stream launches
+    import paper_0907_4631_b200 as P
+    Pb = W.make(name)
+    res = {}
+    for g in (0, 1):
+        c = P.Context(n_max=Pb.n, m_max=100, p_max=max(Pb.p, 1), options={"graph": g})
+        for rep in range(2):
+            w, s = run_gpu(c, Pb, path)
+            res[(g, rep)] = (w, s)
+        c.close()
+    for key in ((1, 0), (1, 1), (0, 1)):
+        assert np.array_equal(res[key][0], res[(0, 0)][0]), key
+        assert res[key][1] == res[(0, 0)][1], key

@@ -387,23 +387,29 @@ __device__ double *cta_expm(int K, int Kp, int ld, double *M0, double *M1, doubl
     cta_matmul(Kp, ld, M1, M0, M2);            // A^3
     cta_matmul(Kp, ld, M1, M1, M3);            // A^4
     EXPM_CLK(2)
-    // ||A||_1, ||A^3||_1, ||A^4||_1: one warp per column, then the max over columns
+    // ||A||_1, ||A^3||_1, ||A^4||_1: one thread per (matrix, column) with four interleaved partial sums over
+    // the rows, then the max over columns (warp shuffle trees, then the warps)
     const int lane = t & 31, warp = t >> 5, nw = blockDim.x >> 5;
     double m1 = 0.0, m3 = 0.0, m4 = 0.0;
-    for (int jc = warp; jc < Kp; jc += nw) {
-        double s1 = 0.0, s3 = 0.0, s4 = 0.0;
-        for (int i = lane; i < Kp; i += 32) {
-            const size_t e = i + (size_t)jc * ld;
-            s1 += fabs(M0[e]);
-            s3 += fabs(M2[e]);
-            s4 += fabs(M3[e]);
+    for (int q = t; q < 3 * Kp; q += blockDim.x) {
+        const int w = q / Kp, jc = q - w * Kp;
+        const double *col = (w == 0 ? M0 : w == 1 ? M2 : M3) + (size_t)jc * ld;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        for (int i = 0; i < Kp; i += 4) {                  // (Kp is a multiple of 8)
+            s0 += fabs(col[i]);
+            s1 += fabs(col[i + 1]);
+            s2 += fabs(col[i + 2]);
+            s3 += fabs(col[i + 3]);
         }
-        s1 = warp_sum(s1);
-        s3 = warp_sum(s3);
-        s4 = warp_sum(s4);
-        m1 = fmax(m1, s1);
-        m3 = fmax(m3, s3);
-        m4 = fmax(m4, s4);
+        const double sc = (s0 + s1) + (s2 + s3);
+        if (w == 0) m1 = fmax(m1, sc);
+        else if (w == 1) m3 = fmax(m3, sc);
+        else m4 = fmax(m4, sc);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+        m3 = fmax(m3, __shfl_xor_sync(0xffffffffu, m3, o));
+        m4 = fmax(m4, __shfl_xor_sync(0xffffffffu, m4, o));
     }
     EXPM_CLK(8)
     if (lane == 0) { sred[warp] = m1; sred[warp + 16] = m3; sred[warp + 32] = m4; }
@@ -564,33 +570,32 @@ __device__ __forceinline__ void expm_body(const ExpmArgs &a, double *esm)
             M0[i + (size_t)jc * ld] = a.Ain[e];
         }
     } else {
-        // tau H_mu into M0, |H_mu| into M1 (scratch for the unscaled 1-norm)
-        for (size_t e = t; e < (size_t)mu * mu; e += blockDim.x) {
-            const int i = (int)(e % mu), jc = (int)(e / mu);
-            // only the Hessenberg part (Lanczos: the tridiagonal band) is read: entries below the
-            // subdiagonal are never written by the Krylov kernels and are zero by definition
-            const double hv = (i <= jc + 1 && (!a.tridiag || jc - i <= 1)) ? a.H[i + (size_t)jc * a.ldh] : 0.0;
-            M0[i + (size_t)jc * ld] = a.tau * hv;
-            M1[i + (size_t)jc * ld] = fabs(hv);
+        // tau H_mu into M0 and ||H_mu||_1 (unscaled, for the cost model, R20): one thread per column reads
+        // only the column's Hessenberg part (Lanczos: the tridiagonal band; entries below the subdiagonal are
+        // never written by the Krylov kernels and are zero by definition) and sums |h| in row order, the
+        // order of a full column sum (the zeros add nothing)
+        double m = 0.0;
+        for (int jc = t; jc < mu; jc += blockDim.x) {
+            const int i0 = a.tridiag ? max(jc - 1, 0) : 0, i1 = min(jc + 1, mu - 1);
+            double s = 0.0;
+#pragma unroll 8
+            for (int i = i0; i <= i1; i++) {
+                const double hv = a.H[i + (size_t)jc * a.ldh];
+                M0[i + (size_t)jc * ld] = a.tau * hv;
+                s += fabs(hv);
+            }
+            m = fmax(m, s);
         }
         if (t == 0) {
             M0[0 + (size_t)mu * ld] = 1.0;
             for (int i = 1; i <= a.p; i++) M0[(mu + i - 1) + (size_t)(mu + i) * ld] = 1.0;
         }
-    }
-    __syncthreads();
-    // ||H_mu||_1 (unscaled) for the cost model (R20), from the shared copy
-    double normH1 = 0.0;
-    if (a.mode != 1) {
-        double m = 0.0;
-        for (int jc = t; jc < mu; jc += blockDim.x) {
-            double s = 0.0;
-            for (int i = 0; i < mu; i++) s += M1[i + (size_t)jc * ld];
-            m = fmax(m, s);
-        }
         for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
         if ((t & 31) == 0) sred[t >> 5] = m;
-        __syncthreads();
+    }
+    __syncthreads();
+    double normH1 = 0.0;
+    if (a.mode != 1) {
         for (int w = 0; w < EXPM_NT / 32; w++) normH1 = fmax(normH1, sred[w]);
         __syncthreads();
     }

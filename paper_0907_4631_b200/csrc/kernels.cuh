@@ -376,14 +376,15 @@ __global__ void __launch_bounds__(NT) maxabs_kernel(int64_t n, MaxAbsArgs a, Wor
         const double *x = a.x[v];
         double m = 0.0;
         int64_t r = (int64_t)blockIdx.x * NT + tid;
-        for (; r + 7 * stride < n; r += 8 * stride) {
+        // (predicated: at full occupancy a thread has fewer than 8 elements of a 2M-row vector, and a
+        // scalar tail loop issued them one dependent round trip at a time)
+        for (; r < n; r += 8 * stride) {
             double t[8];
 #pragma unroll
-            for (int u = 0; u < 8; u++) t[u] = __ldg(x + r + u * stride);
+            for (int u = 0; u < 8; u++) t[u] = (r + u * stride < n) ? __ldg(x + r + u * stride) : 0.0;
 #pragma unroll
             for (int u = 0; u < 8; u++) m = nanmax(m, fabs(t[u]));
         }
-        for (; r < n; r += stride) m = nanmax(m, fabs(x[r]));
         for (int o = 16; o > 0; o >>= 1) m = nanmax(m, __shfl_xor_sync(0xffffffffu, m, o));
         if (lane == 0) wmax[v][warp] = m;
     }

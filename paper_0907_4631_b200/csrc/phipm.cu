@@ -86,6 +86,7 @@ struct phipm_ctx {
     SsAttempt *ss_att_d = nullptr;                   // attempt records (device)
     SsOut *ss_out_h = nullptr, *ss_out_d = nullptr;  // stats and status (mapped pinned)
     int ss_att_pending = 0;                          // records of the last solve still on the device
+    bool defer = false, deferred = false;            // batch fast path: launch the device solve, collect later
     std::vector<GraphRec> graphs;                    // captured two-kernel extensions (PHIPM_OPT_GRAPH)
     DevState *st = nullptr;
     int32_t *tlo = nullptr, *thi = nullptr;                  // CSR per-tile column ranges
@@ -1225,6 +1226,8 @@ void ss_set_smem(int mx)
     cudaFuncSetAttribute(small_solve_kernel<Op, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
 
+int finish_small_dev(phipm_ctx *c, phipm_stats &S);
+
 template <class Op>
 int solve_small_dev(phipm_ctx *c, const Op &op, double t_end, double normA, double bthr, int p,
                     const double *const *u, const phipm_opts &o, const Problem &P, double *w, phipm_stats &S)
@@ -1268,6 +1271,17 @@ int solve_small_dev(phipm_ctx *c, const Op &op, double t_end, double normA, doub
     c->ss_out_h->status = -1;
     CK(launch_k(c, kfn, 1, SS_NT, dyn, op, a, make_work(c)));
     c->acc.launches++;
+    if (c->defer) {                                  // batch fast path: collected by finish_small_dev
+        c->deferred = true;
+        return PHIPM_OK;
+    }
+    return finish_small_dev(c, S);
+}
+
+// wait for a device-driven solve and read its stats / status / attempt count
+int finish_small_dev(phipm_ctx *c, phipm_stats &S)
+{
+    c->deferred = false;
     int rc = sync(c);
     if (rc) return rc;
     SsOut R_;
@@ -2702,6 +2716,43 @@ int phipm_solve_stencil_batch(phipm_ctx *const *ctx, int nb, const double *t, co
                               double *const *w, phipm_stats *stats, int *status)
 {
     if (nb > 0 && (!t || !S || !p || !u || !w)) return PHIPM_EINVAL;
+    // Every problem a device-driven solve (one kernel each, no host decisions): this thread launches them all,
+    // then collects them (solves on distinct SMs; host threads would only add wake-ups and contention)
+    {
+        const phipm_opts o = resolve_opts(opts);
+        bool all = nb > 0 && ctx && o.symmetric && o.expm_method == PHIPM_EXPM_TAYLOR && !o.profile;
+        for (int b = 0; all && b < nb; b++) {
+            StencilOp op;
+            all = ctx[b] && opt(ctx[b], PHIPM_OPT_DEVSOLVE) && make_stencil(nullptr, &S[b], op) == PHIPM_OK &&
+                  op.n <= SMALL_N && p[b] + 1 <= SS_MAXU && t[b] > 0.0;
+            for (int b2 = 0; all && b2 < b; b2++) all = ctx[b] != ctx[b2];
+        }
+        if (all) {
+            std::vector<int> st((size_t)nb, PHIPM_OK);
+            for (int b = 0; b < nb; b++) {
+                const cudaError_t e = cudaSetDevice(ctx[b]->dev);
+                if (e != cudaSuccess) {
+                    st[b] = set_err(ctx[b], PHIPM_ECUDA, "cudaSetDevice(%d): %s", ctx[b]->dev, cudaGetErrorString(e));
+                    continue;
+                }
+                ctx[b]->defer = true;
+                st[b] = phipm_solve_stencil(ctx[b], t[b], &S[b], p[b], u[b], opts, w[b], stats ? &stats[b] : nullptr);
+                ctx[b]->defer = false;
+            }
+            int rc = PHIPM_OK;
+            for (int b = 0; b < nb; b++) {
+                if (st[b] == PHIPM_OK && ctx[b]->deferred) {
+                    cudaSetDevice(ctx[b]->dev);
+                    phipm_stats sb{};
+                    st[b] = finish_small_dev(ctx[b], sb);
+                    if (stats) stats[b] = sb;
+                }
+                if (status) status[b] = st[b];
+                if (rc == PHIPM_OK && st[b] != PHIPM_OK) rc = st[b];
+            }
+            return rc;
+        }
+    }
     return run_batch(ctx, nb, status, [&](int b) {
         return phipm_solve_stencil(ctx[b], t[b], &S[b], p[b], u[b], opts, w[b], stats ? &stats[b] : nullptr);
     });

@@ -25,6 +25,7 @@ ap.add_argument("--config", default="c1")
 ap.add_argument("--ks", default="1,2,4,8,16,32")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--out", default=None)
+ap.add_argument("--option", action="append", default=[], help="context option name=value")
 ap.add_argument("--api", default="threads", choices=["threads", "batch"],
                 help="threads: one Python thread per context; batch: one phipm_solve_*_batch call (native threads)")
 a = ap.parse_args()
@@ -37,7 +38,9 @@ lines = [f"NEXT-3: K concurrent independent solves of {a.config} (n={Pb.n}), one
          f"api={a.api} ({'one phipm_solve_*_batch call per round, native threads' if a.api == 'batch' else 'one Python thread per context'})"]
 base = None
 for K in [int(k) for k in a.ks.split(",")]:
-    ctxs = [P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), stream=torch.cuda.Stream()) for _ in range(K)]
+    opts = {k: int(v) for k, v in (x.split("=") for x in a.option)}
+    ctxs = [P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), stream=torch.cuda.Stream(), options=opts)
+            for _ in range(K)]
     outs = [torch.empty(Pb.n, dtype=torch.float64, device="cuda") for _ in range(K)]
 
     def work(i, reps):

@@ -5,9 +5,9 @@
 //
 // Design (measured on this B200 with tools/stream_roof.cu: plain 16-B loads reach ~7.0 TB/s
 // read-only, 1-D TMA bulk copies only do so with >= 16-32 KB per copy):
-//   * Tiles of TILE = 256 * RPT rows; each thread owns RPT rows as RPT/2 double2 pairs
-//     (rows 2 tid + 512 h, +1) and keeps its y values in registers from the SpMV through the
-//     dot products, so y never round-trips through memory inside the kernel.
+//   * Tiles of TILE = SNT * RPT rows (SNT = 1024 threads, one CTA per SM); each thread owns RPT rows
+//     as RPT/2 double2 pairs (rows 2 tid + 2 SNT h, +1) and keeps its y values in registers from the
+//     SpMV through the dot products, so y never round-trips through memory inside the kernel.
 //   * Streamed Krylov columns are read with 16-B non-allocating loads, CU columns x RPT/2 pairs
 //     in flight per thread (64-128 B/thread, one 1024-thread CTA per SM), which saturates HBM.
 //   * Stencil operators stage their halo tile in shared memory with 1-D TMA (cp.async.bulk,

@@ -201,6 +201,10 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *   PHIPM_OPT_GRAPH            1: the two-kernel extension (Arnoldi with n > 2^19, CSR) is captured once as a
  *                              CUDA graph and replayed from a per-context cache; 0 (default) stream launches
  *                              with programmatic dependent launch
+ *   PHIPM_OPT_DEFER            1 (default): in the two-kernel extension the fused SpMV + dots kernel ends
+ *                              after writing its per-CTA partials; every CTA of the update kernel that
+ *                              follows sums them itself (same fixed order, bit-identical totals) and derives
+ *                              H(:, j), g, sigma_j; 0: the SpMV's last CTA reduces and finalizes (ticket)
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -222,7 +226,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_SPEC            17
 #define PHIPM_OPT_DEVSOLVE        18
 #define PHIPM_OPT_GRAPH           19
-#define PHIPM_OPT_COUNT           20
+#define PHIPM_OPT_DEFER           20
+#define PHIPM_OPT_COUNT           21
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

@@ -63,6 +63,7 @@ struct Work {
     double *sigma;         // sigma_k = 1 / ||v~_k||
     double *g;             // coefficients for the next axpy_fused (length MAXD)
     double *part;          // grid-reduction partials, [value][block], stride pstride
+    double *part2;         // partials an SpMV kernel leaves for the next update kernel (deferred finalize)
     int pstride;
     unsigned *counter;     // last-block ticket (reset by the last block)
     DevState *st;
@@ -127,6 +128,8 @@ struct SpmvArgs {
     double *anorm_pub;           // mapped pinned memory: ||A||_inf, then
     volatile int *anorm_seq;     // ... this sequence number (after a system-scope fence)
     int anorm_seqv;
+    int defer;                   // deferred finalize: write the nv partials to wk.part2 and end (no ticket);
+                                 // the update kernel that follows reduces them (AxpyArgs.dfin)
 };
 
 struct AxpyArgs {
@@ -153,6 +156,10 @@ struct AxpyArgs {
                                  // ascending dot pass of the SpMV kernel)
     int pfc;                     // L2-prefetch the streamed vectors one group ahead (PHIPM_OPT_COL_PREFETCH)
     unsigned long long *dbg;     // optional per-CTA %globaltimer stamps (PHIPM_KCLOCKS tool)
+    // deferred finalize of the preceding SpMV kernel (SpmvArgs.defer): its fin mode (FIN_ARNOLDI,
+    // FIN_LANCZOS or FIN_ARNOLDI_LAG; 0 = none), grid size, dot count, value count, step and threshold
+    int dfin, dnb, dnd, dnv, dj;
+    double dbthr;
 };
 
 // ------------------------------------------------------------------------------------------
@@ -225,12 +232,13 @@ __device__ __forceinline__ bool publish_partials(const Work &wk, const double *b
 // Last block: out[v] = sum over blocks in a fixed order (deterministic), then reset the ticket.
 // Each lane issues 8 independent L2 loads per batch (fixed lane/slot assignment, fixed combine
 // order), so the tail costs about one L2 round trip per value instead of one per 32 blocks.
-__device__ __forceinline__ void final_reduce(const Work &wk, int nv, double *out)
+// reduce_partials: the same sums from any partials buffer of nb blocks (every thread of the calling CTA
+// must call it; out[] is visible to all of them on return).
+__device__ __forceinline__ void reduce_partials(const double *part, int pstride, int nb, int nv, double *out)
 {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int nb = gridDim.x;
     for (int v = warp; v < nv; v += nw) {
-        const double *pv = wk.part + (size_t)v * wk.pstride;
+        const double *pv = part + (size_t)v * pstride;
         double acc[8];
 #pragma unroll
         for (int u = 0; u < 8; u++) acc[u] = 0.0;
@@ -249,6 +257,11 @@ __device__ __forceinline__ void final_reduce(const Work &wk, int nv, double *out
         if (lane == 0) out[v] = s;
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ void final_reduce(const Work &wk, int nv, double *out)
+{
+    reduce_partials(wk.part, wk.pstride, gridDim.x, nv, out);
     if (threadIdx.x == 0) *wk.counter = 0u;
 }
 
@@ -338,6 +351,102 @@ __device__ void finalize(int fin, int j, int nd, const double *red, const Work &
     default:
         break;
     }
+}
+
+// Deferred finalize (AxpyArgs.dfin, PHIPM_OPT_DEFER), run by EVERY CTA of the update kernel that follows an
+// SpMV launched with SpmvArgs.defer.  The SpMV's partials are summed by reduce_partials in final_reduce's
+// order, and the step state is derived with finalize()'s expressions, so every CTA holds bit for bit what the
+// SpMV's last CTA would have computed; CTA 0 writes it (H(:, j), sigma_j, wnorm2, g, brk) for the later
+// kernels and the exponential.  This removes the SpMV's ticket, last-block reduction and finalize from the
+// critical path: the update kernel's CTAs do the same reduction concurrently.
+// g_out[k] (k < dnd): the update coefficients g_k; *a0s: the factor of the base vector (sigma_j for
+// FIN_ARNOLDI_LAG, where the SpMV produced the raw A v~_j; else 1).  Returns false on breakdown.
+__device__ bool deferred_finalize(const AxpyArgs &a, const Work &wk, double *red, double *g_out, double *a0s)
+{
+    __shared__ int s_ok;
+    __shared__ double s_sj;
+    reduce_partials(wk.part2, wk.pstride, a.dnb, a.dnv, red);
+    const int t = threadIdx.x, j = a.dj, nd = a.dnd;
+    const bool lead = blockIdx.x == 0;
+    switch (a.dfin) {
+    case FIN_ARNOLDI:
+        for (int k = t; k < nd; k += blockDim.x) {
+            const double sk = wk.sigma[k];
+            const double h = sk * red[k];
+            const double gk = h * sk;
+            g_out[k] = gk;
+            if (lead) {
+                wk.H[k + (size_t)j * wk.ldh] = h;
+                wk.g[k] = gk;
+            }
+        }
+        if (t == 0) {
+            if (lead) wk.st->wnorm2 = red[nd];
+            *a0s = 1.0;
+            s_ok = 1;
+        }
+        break;
+    case FIN_LANCZOS:
+        if (t == 0) {
+            const double sj = wk.sigma[j];
+            const double al = sj * red[0];
+            const double g0 = al * sj;
+            g_out[0] = g0;
+            if (lead) {
+                wk.H[j + (size_t)j * wk.ldh] = al;
+                wk.g[0] = g0;
+                wk.st->wnorm2 = red[1];
+            }
+            *a0s = 1.0;
+            s_ok = 1;
+        }
+        break;
+    case FIN_ARNOLDI_LAG: {
+        // red[0..nd-1] raw dots, red[nd] ||A x||^2, red[nd+1] ||x||^2 with x = v~_j (j >= 1)
+        if (t == 0) {
+            double bthr = a.dbthr;
+            if (bthr < 0.0) bthr = wk.st->bthr_d;
+            const double hh = sqrt(red[nd + 1]);
+            const double sj = 1.0 / hh;
+            int ok = 1, nonfin = 0;
+            if (!isfinite(hh)) { nonfin = 1; ok = 0; }
+            else if (hh <= bthr) ok = 0;
+            if (lead) {
+                wk.H[j + (size_t)(j - 1) * wk.ldh] = hh;
+                wk.sigma[j] = sj;
+                if (nonfin) wk.st->nonfinite = 1;
+                if (!ok) wk.st->brk = j;
+                else wk.st->wnorm2 = red[nd] * sj * sj;
+            }
+            s_sj = sj;
+            s_ok = ok;
+            *a0s = sj;
+        }
+        __syncthreads();
+        if (s_ok) {
+            const double sj = s_sj;
+            for (int k = t; k < nd; k += blockDim.x) {
+                const double sk = (k == j) ? sj : wk.sigma[k];
+                const double h = sk * (sj * red[k]);
+                const double gk = h * sk;
+                g_out[k] = gk;
+                if (lead) {
+                    wk.H[k + (size_t)j * wk.ldh] = h;
+                    wk.g[k] = gk;
+                }
+            }
+        }
+        break;
+    }
+    default:
+        if (t == 0) {
+            *a0s = 1.0;
+            s_ok = 1;
+        }
+        break;
+    }
+    __syncthreads();
+    return s_ok != 0;
 }
 
 // ------------------------------------------------------------------------------------------

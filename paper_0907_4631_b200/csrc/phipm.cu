@@ -75,6 +75,8 @@ struct phipm_ctx {
     std::vector<OccEntry> occ_cache;
     // device workspace
     double *V = nullptr, *W = nullptr, *Y = nullptr, *U = nullptr, *H = nullptr, *sigma = nullptr, *g = nullptr;
+    double *part2 = nullptr;                         // partials of a deferred-finalize SpMV (PHIPM_OPT_DEFER)
+    int defer_nb = 0;                                // grid of the last SpMV launched with SpmvArgs.defer
     double *part = nullptr, *comb = nullptr, *combd = nullptr, *scratch = nullptr, *raw = nullptr;
     unsigned *counter = nullptr;
     bool coop_dirty = false;                         // a cooperative kernel timed out: reset its counters
@@ -133,7 +135,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1};
     char err[512] = {0};
 };
 
@@ -177,6 +179,7 @@ Work make_work(phipm_ctx *c)
     w.sigma = c->sigma;
     w.g = c->g;
     w.part = c->part;
+    w.part2 = c->part2;
     w.pstride = c->pstride;
     w.counter = c->counter;
     w.st = c->st;
@@ -370,6 +373,7 @@ int launch_spmv_t(phipm_ctx *c, const Op &op, const SpmvArgs &a0)
     int grid;
     balance(c, op.n, slots, grid, a.rpc);
     a.dbg = kclk_slot(c, PC_SPMV, grid, a.nd);
+    if (a.defer) c->defer_nb = grid;
     if (ringk) launch_k(c, spmv_stream_kernel<Op, RPT, 2>, grid, SNT, smem, lop, a, make_work(c));
     else launch_k(c, spmv_stream_kernel<Op, RPT>, grid, SNT, smem, lop, a, make_work(c));
     return PHIPM_OK;
@@ -1084,8 +1088,20 @@ int enqueue_krylov_stream(phipm_ctx *c, const Op &op, double bytes_op, bool symm
                 u.fin = FIN_NONE;
             }
         }
+        // deferred finalize (PHIPM_OPT_DEFER): the streaming SpMV leaves its partials to the update kernel
+        s.defer = opt(c, PHIPM_OPT_DEFER) && n > SMALL_N && !s.anorm &&
+                  (s.fin == FIN_ARNOLDI || s.fin == FIN_LANCZOS || s.fin == FIN_ARNOLDI_LAG);
+        c->defer_nb = 0;
         int rc = launch_spmv(c, op, s, bytes_op);
         if (rc) return rc;
+        if (s.defer && c->defer_nb > 0) {
+            u.dfin = s.fin;
+            u.dnb = c->defer_nb;
+            u.dnd = s.nd;
+            u.dnv = s.nd + s.ynorm + s.xnorm;
+            u.dj = j;
+            u.dbthr = s.bthr;
+        }
         rc = launch_axpy(c, n, u, PC_ORTH);
         if (rc) return rc;
         if (!symmetric && orth == PHIPM_ORTH_CGS2) {
@@ -1102,6 +1118,7 @@ int enqueue_krylov_stream(phipm_ctx *c, const Op &op, double bytes_op, bool symm
             if (rc) return rc;
             AxpyArgs r = u;
             r.base = vn;
+            r.dfin = 0;                      // (the reorthogonalisation SpMV finalizes itself)
             rc = launch_axpy(c, n, r, PC_ORTH);
             if (rc) return rc;
         }
@@ -2443,7 +2460,7 @@ void phipm_destroy(phipm_ctx *c)
     if (c->ss_out_h) cudaFreeHost(c->ss_out_h);
     if (c->ev_spec) cudaEventDestroy(c->ev_spec);
     cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
-    cudaFree(c->part); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
+    cudaFree(c->part); cudaFree(c->part2); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
     cudaFree(c->counter); cudaFree(c->st); cudaFree(c->tlo); cudaFree(c->thi); cudaFree(c->off16);
     cudaFree(c->hu); cudaFree(c->hw); cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
     if (c->res_h) cudaFreeHost(c->res_h);
@@ -2591,6 +2608,7 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     A((void **)&c->sigma, sizeof(double) * (MAXD + 1));
     A((void **)&c->g, sizeof(double) * (MAXD + 1));
     A((void **)&c->part, sizeof(double) * (size_t)c->pstride * (MAXD + 2));
+    A((void **)&c->part2, sizeof(double) * (size_t)c->pstride * (MAXD + 2));
     A((void **)&c->comb, sizeof(double) * (MAXD + 1));
     A((void **)&c->combd, sizeof(double) * (P_MAX_ABS + 1));
     {

@@ -1025,6 +1025,13 @@ __global__ void __launch_bounds__(SNT, SMINB) spmv_stream_kernel(Op op, SpmvArgs
     const int nv = a.nd + (a.ynorm ? 1 : 0) + (a.xnorm ? 1 : 0);
     __syncthreads();
     if (nv == 0 && !a.anorm) return;                      // (||A||_inf: the last CTA publishes it)
+    if (a.defer) {
+        // deferred finalize: the update kernel that follows sums these (deferred_finalize); its
+        // griddepcontrol.wait orders them (kernel completion), so no ticket and no fence here
+        for (int v = tid; v < nv; v += SNT) wk.part2[(size_t)v * wk.pstride + blockIdx.x] = bsum[v];
+        KSTAMP(4)
+        return;
+    }
     const bool last = publish_partials(wk, bsum, nv);
     KSTAMP(4)
     if (!last) return;
@@ -1057,21 +1064,30 @@ __global__ void __launch_bounds__(SNT, SMINB) axpy_stream_kernel(int64_t n, Axpy
     __shared__ double wsum[SNW];
     __shared__ int s_exit;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ double dred[MAXD + 2];                    // deferred finalize: the SpMV's totals,
+    __shared__ double dg[MAXD + 1];                      // the update coefficients g_k
+    __shared__ double s_a0s;                             // and the base vector's factor
     KSTAMP(0)
     pdl_wait();
     KSTAMP(1)
     if (tid == 0) s_exit = a.check_brk ? (wk.st->brk >= 0) : 0;
+    if (a.dfin) {
+        // the preceding SpMV left its partials in wk.part2 (SpmvArgs.defer): reduce and finalize here
+        __syncthreads();
+        if (s_exit) return;                               // (that SpMV exited too: no partials)
+        if (!deferred_finalize(a, wk, dred, dg, &s_a0s)) return;   // breakdown (FIN_ARNOLDI_LAG)
+    }
     const int nbase = (a.a0h != 0.0) ? 1 : 0;
     const int nitem = nbase + a.nc + a.ne;
     for (int k = tid; k < nitem; k += SNT) {
         double c;
         const double *p;
         if (k < nbase) {
-            c = a.a0h * (a.a0d ? *a.a0d : 1.0);
+            c = a.a0h * (a.dfin == FIN_ARNOLDI_LAG ? s_a0s : (a.a0d ? *a.a0d : 1.0));   // (lag: a0d = &sigma_j)
             p = a.base;
         } else if (k < nbase + a.nc) {
             const int kc = a.rev ? (a.nc - 1 - (k - nbase)) : (k - nbase);
-            c = a.gsign * a.g[kc];
+            c = a.gsign * (a.dfin ? dg[kc] : a.g[kc]);
             p = a.V + (int64_t)(a.c0 + kc) * a.ldv;
         } else {
             const int i = k - nbase - a.nc;

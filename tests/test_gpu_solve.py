@@ -456,3 +456,23 @@ def test_graph_replay_matches_stream_launches(name, path):
     for key in ((1, 0), (1, 1), (0, 1)):
         assert np.array_equal(res[key][0], res[(0, 0)][0]), key
         assert res[key][1] == res[(0, 0)][1], key
+
+
+@pytest.mark.parametrize("name,path,kw", [("c5_med", "csr", {}), ("c3", "stencil", {}), ("c3_med", "stencil", {"orth": 1}),
+                                          ("c2", "csr", {}), ("c3_med", "csr", {})])
+def test_deferred_finalize_matches_last_block_finalize(orc, name, path, kw):
+    # option defer (default 1): the two-kernel extension's SpMV leaves its partials to the update kernel, whose
+    # every CTA reduces them in final_reduce's order and derives H(:, j), g, sigma_j with finalize()'s
+    # expressions (Arnoldi CGS, lagged Arnoldi on stencils, Lanczos on CSR, CGS2) -- w and the stats are
+    # bit-identical with the SpMV's own last-block finalize, and within parity of the oracle
+    import paper_0907_4631_b200 as P
+    Pb = W.make(name)
+    res = {}
+    for d in (1, 0):
+        c = P.Context(n_max=Pb.n, m_max=100, p_max=max(Pb.p, 1), options={"defer": d})
+        res[d] = run_gpu(c, Pb, path, **kw)
+        c.close()
+    assert np.array_equal(res[1][0], res[0][0])
+    assert res[1][1] == res[0][1]
+    wo, so = run_oracle(orc, Pb)             # (the oracle's MGS: CGS and CGS2 agree with it within parity)
+    assert relerr(res[1][0], wo) <= parity_bound(Pb.tol)

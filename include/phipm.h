@@ -153,6 +153,19 @@ int phipm_get_attempts(const phipm_ctx *ctx, phipm_attempt *out, int max, int *c
  * solve (setup, w-recurrence + seed, extensions, exponential, controller, combine in words 0..5). */
 int phipm_get_clocks(const phipm_ctx *ctx, long long *out16);
 
+/* Which kernel path ran the last Krylov extension enqueued on this context (a solve's last extension, or
+ * phipm_krylov_*): for tests and measurement scripts that must know a path was taken, not fallen back from.
+ * A device-driven small solve (PHIPM_OPT_DEVSOLVE) runs its extensions inside its own kernel and leaves
+ * the value unchanged. */
+#define PHIPM_PATH_NONE          0   /* no extension yet */
+#define PHIPM_PATH_TWO_KERNEL    1   /* fused SpMV + dots, then update + norm, per step (stream.cuh) */
+#define PHIPM_PATH_SINGLE_CTA    2   /* n <= 8192: one single-CTA kernel (small.cuh) */
+#define PHIPM_PATH_CLUSTER       3   /* Lanczos on one thread-block cluster (persist_cl.cuh) */
+#define PHIPM_PATH_PERSIST_SMEM  4   /* persistent cooperative kernel, y in shared memory (persist.cuh) */
+#define PHIPM_PATH_PERSIST_TMEM  5   /* persistent Lanczos, y / v~ in tensor memory (persist_tm.cuh) */
+#define PHIPM_PATH_BRICK         6   /* persistent Lanczos on TMA-staged 3-D bricks (persist_brick.cuh) */
+int phipm_krylov_path(const phipm_ctx *ctx);
+
 void phipm_default_opts(phipm_opts *opts);
 
 /* Method used by the kernel-level entry points phipm_expm and phipm_phi_pair (solves take
@@ -205,6 +218,11 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *                              after writing its per-CTA partials; every CTA of the update kernel that
  *                              follows sums them itself (same fixed order, bit-identical totals) and derives
  *                              H(:, j), g, sigma_j; 0: the SpMV's last CTA reduces and finalizes (ticket)
+ *   PHIPM_OPT_BRICK            Lanczos extensions of 3-D 7-point stencils on 3-D bricks staged by tensor-map
+ *                              TMA (one box copy per brick plane, zero fill outside the grid, z-marching
+ *                              warps; y / v~ in tensor memory): 0 off, 1 auto (default: n >= 303K and
+ *                              x-lines that fill >= 3/4 of their 64-point warp segments), 2 whenever a
+ *                              brick decomposition of the grid exists (nx even, <= 252)
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -227,7 +245,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_DEVSOLVE        18
 #define PHIPM_OPT_GRAPH           19
 #define PHIPM_OPT_DEFER           20
-#define PHIPM_OPT_COUNT           21
+#define PHIPM_OPT_BRICK           21
+#define PHIPM_OPT_COUNT           22
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

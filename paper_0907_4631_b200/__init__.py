@@ -66,10 +66,11 @@ class _Attempt(C.Structure):
 
 
 # kernel-path options (phipm_set_option; include/phipm.h)
+KRYLOV_PATHS = ["none", "two_kernel", "single_cta", "cluster", "persist_smem", "persist_tmem", "brick"]
 OPTIONS = {"persist": 0, "tmem": 1, "wrec": 2, "lag": 3, "pdl": 4, "spin": 5, "rpt": 6, "csr_ell": 7,
            "csr_ring": 8, "csr_window": 9, "small_lz": 10, "persist_minrows": 11, "csr_prefetch": 12,
            "col_prefetch": 13, "fuse_anorm": 14,
-           "csr_off16": 15, "cluster_lz": 16, "spec": 17, "devsolve": 18, "graph": 19, "defer": 20}
+           "csr_off16": 15, "cluster_lz": 16, "spec": 17, "devsolve": 18, "graph": 19, "defer": 20, "brick": 21}
 
 
 class _Profile(C.Structure):
@@ -149,6 +150,7 @@ def lib():
             "phipm_get_trace": (i32, [vp, P(_TraceRec), i32, P(i32)]),
             "phipm_get_attempts": (i32, [vp, P(_Attempt), i32, P(i32)]),
             "phipm_get_clocks": (i32, [vp, P(C.c_longlong)]),
+            "phipm_krylov_path": (i32, [vp]),
             "phipm_set_option": (i32, [vp, i32, i32]),
             "phipm_get_option": (i32, [vp, i32, P(i32)]),
             "phipm_solve_csr": (i32, [vp, d, P(_Csr), i32, P(vp), P(_Opts), vp, P(_Stats)]),
@@ -183,7 +185,7 @@ def lib():
 
 EXPORTED = [
     "phipm_default_opts", "phipm_set_expm_method", "phipm_mm_read", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
-    "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_get_attempts", "phipm_get_clocks", "phipm_set_option",
+    "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_get_attempts", "phipm_get_clocks", "phipm_krylov_path", "phipm_set_option",
     "phipm_get_option", "phipm_solve_csr", "phipm_solve_stencil",
     "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_solve_csr_batch",
     "phipm_solve_stencil_batch", "phipm_solve_csr_block", "phipm_stencil_nnz", "phipm_inf_norm_stencil",
@@ -253,6 +255,10 @@ class Context:
         """Kernel-path option (phipm_set_option): name in OPTIONS or the PHIPM_OPT_* number."""
         o = OPTIONS[name] if isinstance(name, str) else int(name)
         self._check(self._L.phipm_set_option(self._h, o, int(value)))
+
+    def krylov_path(self) -> str:
+        """Kernel path of the last Krylov extension (phipm_krylov_path, PHIPM_PATH_*)."""
+        return KRYLOV_PATHS[self._L.phipm_krylov_path(self._h)]
 
     def get_option(self, name) -> int:
         o = OPTIONS[name] if isinstance(name, str) else int(name)

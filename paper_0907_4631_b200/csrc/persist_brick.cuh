@@ -1,0 +1,345 @@
+// persist_brick.cuh — the persistent Lanczos extension (Alg. 2) of a 3-D 7-point
+// stencil on 3-D BRICKS staged by tensor-map TMA (cp.async.bulk.tensor), y / v~_j in tensor memory.
+//
+// krylov_persist_tm_kernel (persist_tm.cuh) gives every CTA a contiguous row range (< one z-plane at
+// c4) and stages, per 4096-row tile, five 1-D segments of x: each x value is read three times from L2
+// (as a centre, a z- and a z+ neighbour), and ~70 % of the instructions it executes are row-coordinate
+// bookkeeping, boundary predicates and halo-plan arithmetic (ncu, profiles/round2: DMUL+DADD+DFMA 16 %
+// of the warp instructions; the kernel is issue-bound, not bandwidth-bound).  Here
+//   * a CTA owns a brick: every x of `ylen` grid lines by `zlen` planes.  One 4-D tensor map over the
+//     Krylov basis (x, y, z, column) describes it; plane s of the brick with its one-line / two-point
+//     halo is ONE box copy (nx + 4) x (ylen + 2) x 1 x 1, and the TMA engine zero-fills what lies
+//     outside the grid (negative or too large coordinates), so the stencil has NO boundary branches:
+//     an absent neighbour contributes c * 0 = +-0, which leaves the ascending-column sum unchanged
+//     bit for bit (the sum starts at +0 and +0 + -0 = +0).  Halo traffic: (ylen+2)(zlen+2)/(ylen zlen)
+//     = 1.41 x at c4 instead of 3 x;
+//   * a warp owns 64 consecutive x of one line and marches `ppg` <= 8 planes along z with the centre
+//     values of planes z-1, z, z+1 in registers: per row pair and plane 3 16-byte and 2 8-byte shared
+//     loads, 28 separately rounded multiply / adds, no index arithmetic beyond a plane stride;
+//   * the whole brick (zlen + 2 planes) is resident in shared memory, one mbarrier per plane: all the
+//     plane copies of the next step are issued the moment the grid phase of the update releases,
+//     in the order the marching warps need them.
+// y and v~_j of the thread's row pairs live in its TMEM columns exactly as in persist_tm.cuh (slot A /
+// slot B, pair t = plane t of the warp), the update phase reads only TMEM, and the grid all-reduce,
+// the finalize arithmetic and the breakdown rule are those of krylov_persist_tm_kernel.
+#pragma once
+
+#include <cuda.h>
+
+#include "persist_tm.cuh"
+
+namespace phipm {
+
+constexpr int BRICK_MAXPL = 36;      // staged planes per CTA (zlen + 2)
+
+struct BrickGeom {
+    int py, pz;        // bricks along y and z (grid = py pz)
+    int ylen, zlen;    // lines / planes per brick (the last brick of a direction may hold fewer)
+    int nseg;          // 64-point x segments per line
+    int ncol;          // warp columns per CTA = nseg ylen (<= SNW)
+    int ngrp;          // z groups per CTA = SNW / ncol
+    int ppg;           // planes per z group (<= TM_PAIRS)
+    int lstride;       // shared line stride (doubles) = nx + 4
+    int pstride;       // shared plane stride (doubles), multiple of 16
+};
+
+__host__ __device__ inline size_t brick_smem_bytes(const BrickGeom &g)
+{
+    return (size_t)(g.zlen + 2) * g.pstride * sizeof(double);
+}
+
+// Host: the brick decomposition of an nx x ny x nz grid on at most `ctas` CTAs with the fewest planes
+// per warp (the critical path), then the least staged volume.  false: no decomposition fits.
+inline bool brick_geometry(int nx, int ny, int nz, int ctas, size_t smem_max, BrickGeom &best)
+{
+    if ((nx & 1) || nx < 2 || nx > 252) return false;
+    const int nseg = (nx + 63) / 64;
+    bool found = false;
+    long long bcost = 0;
+    for (int ylen = 1; ylen <= ny && nseg * ylen <= SNW; ylen++) {
+        BrickGeom g;
+        g.nseg = nseg;
+        g.ylen = ylen;
+        g.ncol = nseg * ylen;
+        g.ngrp = SNW / g.ncol;
+        g.py = (ny + ylen - 1) / ylen;
+        g.lstride = nx + 4;
+        g.pstride = ((ylen + 2) * g.lstride + 15) & ~15;
+        for (int ppg = 1; ppg <= TM_PAIRS; ppg++) {
+            g.ppg = ppg;
+            g.zlen = g.ngrp * ppg < nz ? g.ngrp * ppg : nz;
+            g.pz = (nz + g.zlen - 1) / g.zlen;
+            if ((long long)g.py * g.pz > ctas) continue;
+            if (g.zlen + 2 > BRICK_MAXPL || brick_smem_bytes(g) > smem_max) break;
+            const long long cost = ((long long)ppg << 40) + (long long)g.py * g.pz * (g.zlen + 2) * g.pstride;
+            if (!found || cost < bcost) {
+                found = true;
+                bcost = cost;
+                best = g;
+            }
+            break;                                         // larger ppg only costs more
+        }
+    }
+    return found;
+}
+
+// one box of the 4-D tensor map (x, y, z, column) -> shared memory, completion on an mbarrier
+__device__ __forceinline__ void tma_load_box4(void *dst, const CUtensorMap *tm, int cx, int cy, int cz, int cc,
+                                              uint64_t *bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_u32(dst)),
+        "l"(tm), "r"(cx), "r"(cy), "r"(cz), "r"(cc), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
+// one pair (4 columns) of this thread's TMEM lane <- registers
+__device__ __forceinline__ void tm_st4(uint32_t ta, const double2 &a)
+{
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(ta), "r"(__double2loint(a.x)),
+                 "r"(__double2hiint(a.x)), "r"(__double2loint(a.y)), "r"(__double2hiint(a.y))
+                 : "memory");
+}
+
+// registers <- one pair; the wait is a separate statement (tm_ld4_wait) so that the shared loads and
+// the stencil arithmetic of the plane overlap the TMEM read
+__device__ __forceinline__ void tm_ld4_issue(uint32_t ta, uint32_t (&r)[4])
+{
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(ta)
+                 : "memory");
+}
+
+__device__ __forceinline__ double2 tm_ld4_wait(uint32_t (&r)[4])
+{
+    // the registers are operands of the wait: no use of them can be scheduled before it
+    asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3])::"memory");
+    return make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+}
+
+__global__ void __launch_bounds__(SNT, 1)
+krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, BrickGeom g, PersistArgs a, Work wk)
+{
+    extern __shared__ __align__(128) double sm[];
+    __shared__ uint64_t pbar[BRICK_MAXPL];
+    __shared__ double bsum[2];
+    __shared__ double red[MAXD + 2];
+    __shared__ double wsum2[2 * SNW];
+    __shared__ uint32_t s_tmem;
+    __shared__ int s_stop;
+    __shared__ double s_sig, s_lz;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nx = op.nx, ny = op.ny, nz = op.nz;
+    const int64_t ldv = wk.ldv;
+    // this CTA's brick and this warp's column of it
+    const int by = blockIdx.x % g.py, bz = blockIdx.x / g.py;
+    const int y0 = by * g.ylen, z0 = bz * g.zlen;
+    const int zl = min(g.zlen, nz - z0);                   // planes of this brick
+    const int col = warp % g.ncol, grp = warp / g.ncol;
+    const int seg = col % g.nseg, yl = col / g.nseg;
+    const int xi = seg * 64 + 2 * lane;                    // rows (xi, yy, z) and (xi + 1, yy, z)
+    const int yy = y0 + yl;
+    const int zb = grp * g.ppg;                            // first plane of the warp, brick-relative
+    const int cnt = (grp < g.ngrp && yy < ny) ? max(0, min(g.ppg, zl - zb)) : 0;   // planes (warp-uniform)
+    const bool act = xi < nx;                              // this lane holds a row pair
+    const uint32_t plane_bytes = (uint32_t)(g.lstride * (g.ylen + 2)) * 8u;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid < zl + 2) mbar_init(&pbar[tid], 1);
+    if (tid == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    pdl_wait();                                            // the previous kernel's results from here on
+    if (tid == 0) {
+        s_stop = __ldcg(&wk.st->brk) >= 0;
+        s_sig = __ldcg(wk.sigma + a.k0);
+        s_lz = __ldcg(&wk.st->lz);
+    }
+    const uint64_t pol = policy_evict_last();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    double sig = s_sig, lzc = s_lz;                        // sigma_j and the Lanczos coefficient, per thread
+    bool stop = s_stop != 0;
+    const uint32_t tbase = s_tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    const uint32_t slotA = tbase, slotB = tbase + 32;
+    unsigned phase = 0;
+    const bool lead = blockIdx.x == 0;
+    bool pre = false;                                      // the next step's planes are in flight
+    bool aborted = false;
+    uint32_t par = 0;                                      // mbarrier parity of the current step
+    // every plane of Krylov column jc, in the order the marching warps reach them (one thread)
+    auto issue_planes = [&](int jc) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of sm
+        for (int t = 0; t < g.ppg + 2; t++)
+            for (int gi = 0; gi < g.ngrp; gi++) {
+                if (t >= g.ppg && gi + 1 < g.ngrp) continue;           // = planes 0, 1 of the group above
+                const int s = gi * g.ppg + t;
+                if (s > zl + 1) continue;
+                mbar_arrive_expect_tx(&pbar[s], plane_bytes);
+                tma_load_box4(sm + (size_t)s * g.pstride, &tmap, -2, y0 - 1, z0 - 1 + s, jc, &pbar[s], pol);
+            }
+    };
+    const int xa = act ? xi : 0;                           // (idle lanes read a valid address)
+    const double *base = sm + (yl + 1) * g.lstride + xa + 2 + zb * g.pstride;   // centre pair, plane zb - 1
+    const int64_t row0 = xa + (int64_t)nx * (yy + (int64_t)ny * (z0 + zb));     // row of (xi, yy, z0 + zb)
+    const int64_t pl = (int64_t)nx * ny;
+    const double c0 = op.c[0], cxm = op.c[1], cxp = op.c[2], cym = op.c[3], cyp = op.c[4], czm = op.c[5],
+                 czp = op.c[6];
+    auto ld2 = [](const double *p) { return *reinterpret_cast<const double2 *>(p); };
+    for (int j = a.k0; j < a.k1; j++) {
+        if (stop) break;                                   // breakdown (same decision in every CTA)
+        const double sj = sig;
+        const double *zv = j > 0 ? wk.V + (int64_t)(j - 1) * ldv : nullptr;     // v~_{j-1} (Alg. 2 line 3)
+        const double lz = zv ? lzc : 0.0;
+        const bool zs = j > a.k0;                          // v~_{j-1} of these rows is in slot B
+
+        // ---------------- phase A: y = sigma_j A x - lz v~_{j-1}; d = x^T y; ||y||^2
+        if (tid == 0 && !pre) issue_planes(j);
+        pre = false;
+        double ysq = 0.0, dot = 0.0;
+        if (cnt > 0) {
+            mbar_wait(&pbar[zb], par);
+            mbar_wait(&pbar[zb + 1], par);
+            double2 zm = ld2(base), zc = ld2(base + g.pstride);
+            const double *P = base + g.pstride;            // centre pair of the current plane
+#pragma unroll
+            for (int t = 0; t < TM_PAIRS; t++) {
+                if (t >= cnt) break;
+                uint32_t zr[4];
+                double2 zp_ = make_double2(0.0, 0.0);
+                if (zv) {
+                    if (zs) tm_ld4_issue(slotB + 4 * t, zr);
+                    else if (act) zp_ = ld_cg2(zv + row0 + t * pl);
+                }
+                mbar_wait(&pbar[zb + t + 2], par);
+                const double2 zn = ld2(P + g.pstride);
+                const double2 ym = ld2(P - g.lstride), yp = ld2(P + g.lstride);
+                const double xl = P[-1], xh = P[2];
+                double sa = 0.0, sb = 0.0;
+                sa = __dadd_rn(sa, __dmul_rn(czm, zm.x));
+                sb = __dadd_rn(sb, __dmul_rn(czm, zm.y));
+                sa = __dadd_rn(sa, __dmul_rn(cym, ym.x));
+                sb = __dadd_rn(sb, __dmul_rn(cym, ym.y));
+                sa = __dadd_rn(sa, __dmul_rn(cxm, xl));
+                sb = __dadd_rn(sb, __dmul_rn(cxm, zc.x));
+                sa = __dadd_rn(sa, __dmul_rn(c0, zc.x));
+                sb = __dadd_rn(sb, __dmul_rn(c0, zc.y));
+                sa = __dadd_rn(sa, __dmul_rn(cxp, zc.y));
+                sb = __dadd_rn(sb, __dmul_rn(cxp, xh));
+                sa = __dadd_rn(sa, __dmul_rn(cyp, yp.x));
+                sb = __dadd_rn(sb, __dmul_rn(cyp, yp.y));
+                sa = __dadd_rn(sa, __dmul_rn(czp, zn.x));
+                sb = __dadd_rn(sb, __dmul_rn(czp, zn.y));
+                double2 y = make_double2(sa * sj, sb * sj);
+                if (zv) {
+                    if (zs) zp_ = tm_ld4_wait(zr);
+                    y.x = fma(-lz, zp_.x, y.x);
+                    y.y = fma(-lz, zp_.y, y.y);
+                }
+                double2 xc = zc;
+                if (!act) {
+                    y = make_double2(0.0, 0.0);
+                    xc = y;
+                }
+                ysq = fma(y.x, y.x, ysq);
+                ysq = fma(y.y, y.y, ysq);
+                dot = fma(xc.x, y.x, dot);
+                dot = fma(xc.y, y.y, dot);
+                tm_st4(slotA + 4 * t, y);
+                tm_st4(slotB + 4 * t, xc);
+                zm = zc;
+                zc = zn;
+                P += g.pstride;
+            }
+            tm_wait_st();
+        }
+        {
+            const double v2[2] = {dot, ysq};
+            block_sums<2, false>(v2, wsum2, bsum);
+        }
+        if (!phase_allreduce(wk, bsum, 2, ++phase, a, red)) {
+            aborted = true;
+            break;
+        }
+        // finalize (FIN_LANCZOS): alpha_j = sigma_j d; update coefficient -alpha_j sigma_j
+        const double al = sj * red[0];
+        const double cf = -(al * sj);
+        if (lead && tid == 0) {
+            wk.H[j + (size_t)j * wk.ldh] = al;
+            wk.g[0] = al * sj;
+            wk.st->wnorm2 = red[1];
+        }
+
+        // ---------------- phase B: v~_{j+1} = y - alpha_j sigma_j v~_j (both from TMEM); ||v~_{j+1}||^2
+        double *vn = wk.V + (int64_t)(j + 1) * ldv + row0;
+        double nrm = 0.0;
+#pragma unroll
+        for (int h = 0; h < TM_PAIRS / 4; h++) {
+            if (4 * h >= cnt) break;
+            double2 yv[4], xv[4];
+            tm_ld16x2(slotA + 16 * h, slotB + 16 * h, yv, xv);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int t = 4 * h + u;
+                if (t < cnt && act) {
+                    double2 acc;
+                    acc.x = fma(cf, xv[u].x, yv[u].x);
+                    acc.y = fma(cf, xv[u].y, yv[u].y);
+                    *reinterpret_cast<double2 *>(vn + t * pl) = acc;
+                    nrm = fma(acc.x, acc.x, nrm);
+                    nrm = fma(acc.y, acc.y, nrm);
+                }
+            }
+        }
+        {
+            const double v1[1] = {nrm};
+            block_sums<1, false>(v1, wsum2, bsum);
+        }
+        // v~_{j+1} is complete in every CTA once the phase's arrivals are in: the next step's planes are
+        // issued then, while the partials are summed (drained below on breakdown)
+        const bool more = j + 1 < a.k1;
+        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red, [&] {
+                if (more) issue_planes(j + 1);
+            })) {
+            aborted = true;
+            break;
+        }
+        pre = more;
+        par ^= 1u;
+        // finalize (FIN_NORM): h_{j+1,j}, sigma_{j+1}, the Lanczos coefficient, breakdown
+        {
+            const double h = sqrt(red[0]);
+            const double sn = 1.0 / h;
+            const double lzn = h * sj;
+            int brk = -1, nonfin = 0;
+            if (!isfinite(h)) { nonfin = 1; brk = j + 1; }
+            else if (h <= a.bthr) brk = j + 1;
+            sig = sn;
+            lzc = lzn;
+            stop = brk >= 0;
+            if (lead && tid == 0) {
+                wk.H[(j + 1) + (size_t)j * wk.ldh] = h;
+                if (j + 1 < wk.hcols) wk.H[j + (size_t)(j + 1) * wk.ldh] = h;
+                wk.st->lz = lzn;
+                wk.sigma[j + 1] = sn;
+                if (nonfin) wk.st->nonfinite = 1;
+                if (brk >= 0) wk.st->brk = brk;
+            }
+        }
+    }
+    // planes issued for a step that did not run (breakdown): land them before the CTA exits
+    if (pre && tid == 0)
+        for (int s = 0; s < zl + 2; s++) mbar_wait(&pbar[s], par);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
+    if (!aborted) coop_exit(a);
+}
+
+} // namespace phipm

@@ -29,6 +29,7 @@
 #include "small.cuh"
 #include "persist.cuh"
 #include "persist_tm.cuh"
+#include "persist_brick.cuh"
 #include "persist_wrec.cuh"
 #include "phicheb.cuh"
 #include "spmm.cuh"
@@ -135,7 +136,11 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1};
+    // brick Lanczos kernel: the tensor map of the basis for the last grid / brick shape
+    CUtensorMap brick_map;
+    int brick_key[4] = {0, 0, 0, 0};        // nx, ny, nz, ylen of brick_map (nx = 0: none)
+    int krylov_path = PHIPM_PATH_NONE;      // kernel path of the last Krylov extension (phipm_krylov_path)
     char err[512] = {0};
 };
 
@@ -634,6 +639,7 @@ bool try_persist_rpt(phipm_ctx *c, const StencilOp &op, bool symmetric, int k0, 
         cudaGetLastError();
         return false;                                      // fall back to the two-kernel path
     }
+    c->krylov_path = PHIPM_PATH_PERSIST_SMEM;
     return true;
 }
 
@@ -698,6 +704,107 @@ bool try_persist_tm(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bt
         cudaGetLastError();
         return false;
     }
+    c->krylov_path = PHIPM_PATH_PERSIST_TMEM;
+    return true;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (the library does not link libcuda)
+using TmapEncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+TmapEncodeFn tmap_encode_fn()
+{
+    static TmapEncodeFn fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        return (TmapEncodeFn)p;
+    }();
+    return fn;
+}
+
+// 4-D tensor map (x, y, z, Krylov column) over the basis V of the context for an nx x ny x nz grid;
+// box = one plane of a brick with its halo: (nx + 4) x (ylen + 2) x 1 x 1, zero fill outside the grid
+bool brick_tensor_map(phipm_ctx *c, const StencilOp &op, const BrickGeom &g)
+{
+    if (c->brick_key[0] == op.nx && c->brick_key[1] == op.ny && c->brick_key[2] == op.nz && c->brick_key[3] == g.ylen)
+        return true;
+    const TmapEncodeFn enc = tmap_encode_fn();
+    if (!enc || ((uintptr_t)c->V & 15) || (c->ldv & 1)) return false;
+    const cuuint64_t gdim[4] = {(cuuint64_t)op.nx, (cuuint64_t)op.ny, (cuuint64_t)op.nz, (cuuint64_t)(c->m_max + 1)};
+    const cuuint64_t gstr[3] = {(cuuint64_t)op.nx * 8, (cuuint64_t)op.nx * op.ny * 8, (cuuint64_t)c->ldv * 8};
+    const cuuint32_t box[4] = {(cuuint32_t)(op.nx + 4), (cuuint32_t)(g.ylen + 2), 1, 1};
+    const cuuint32_t est[4] = {1, 1, 1, 1};
+    const CUresult r = enc(&c->brick_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, c->V, gdim, gstr, box, est,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        c->brick_key[0] = 0;
+        return false;
+    }
+    c->brick_key[0] = op.nx;
+    c->brick_key[1] = op.ny;
+    c->brick_key[2] = op.nz;
+    c->brick_key[3] = g.ylen;
+    return true;
+}
+
+// Lanczos on 3-D bricks staged by tensor-map TMA (persist_brick.cuh).  PHIPM_OPT_BRICK: 0 off, 1 auto
+// (3-D 7-point grids whose x-lines fill >= 3/4 of their 64-point warp segments), 2 whenever a brick
+// decomposition exists
+bool try_persist_brick(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bthr, double bytes, int &rc)
+{
+    const int mode = opt(c, PHIPM_OPT_BRICK);
+    if (!mode || op.dim != 3 || op.diag) return false;
+    BrickGeom g;
+    if (!brick_geometry(op.nx, op.ny, op.nz, c->sm_count, c->smem_optin - 2048, g)) return false;
+    if (mode == 1 && 4 * op.nx < 3 * 64 * g.nseg) return false;
+    if (!brick_tensor_map(c, op, g)) return false;
+    const size_t smem = brick_smem_bytes(g);
+    const int grid = g.py * g.pz;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, krylov_brick_tm_kernel, SNT, smem) != cudaSuccess ||
+        occ < 1 || grid > occ * c->sm_count || grid > c->pstride) {
+        cudaGetLastError();
+        return false;
+    }
+    PersistArgs a;
+    a.k0 = k0;
+    a.k1 = k1;
+    a.symmetric = 1;
+    a.bthr = bthr;
+    a.rpc = 0;
+    a.flag = c->counter + 2;
+    a.abort = c->counter + 3;
+    a.exit_ctr = c->counter + 4;
+    a.timeout_ns = 2000000000ull;
+    a.dbg = nullptr;
+    const size_t need = (size_t)2 * (k1 - k0) * grid * 2;
+    if (c->pclk_d && c->pclk_used + need <= PCLK_CAP) {
+        a.dbg = c->pclk_d + c->pclk_used;
+        c->pclk_recs.push_back({grid, k1 - k0, (long long)c->pclk_used});
+        c->pclk_used += need;
+    }
+    rc = PHIPM_OK;
+    if (!coop_reset(c)) {
+        rc = set_err(c, PHIPM_ECUDA, "persist: memset failed");
+        return true;
+    }
+    ProfRec r;
+    prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
+    const cudaError_t e = launch_coop(c, krylov_brick_tm_kernel, grid, SNT, smem, c->brick_map, op, g, a, make_work(c));
+    prof_end(c, r);
+    c->acc.launches++;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    c->krylov_path = PHIPM_PATH_BRICK;
     return true;
 }
 
@@ -773,6 +880,9 @@ bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_o
     const double n = (double)op.n;
     for (int j = k0; j < k1; j++) bytes += bytes_op + 8.0 * n * (symmetric ? 4.0 : 2.0 * j + 3.0);
     // (small grids keep the 2048-row tiles: a 4096-row tile would leave half a CTA's threads idle)
+    if (symmetric && (op.n >= (int64_t)SNT * 4 * c->sm_count / 2 || opt(c, PHIPM_OPT_BRICK) == 2) &&
+        try_persist_brick(c, op, k0, k1, bthr, bytes, rc))
+        return true;
     if (symmetric && op.n >= (int64_t)SNT * 4 * c->sm_count / 2 && try_persist_tm(c, op, k0, k1, bthr, bytes, rc))
         return true;
     // largest tile that fits (halo + the CTA's y + dot partials); RPT = 8 would spill
@@ -980,9 +1090,13 @@ int enqueue_krylov_graph(phipm_ctx *c, const Op &op, double bytes_op, bool symme
 template <class Op>
 int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, int orth, int k0, int k1, double bthr)
 {
-    if (symmetric && try_cluster_lz(c, op, bytes_op, k0, k1, bthr)) return PHIPM_OK;
+    if (symmetric && try_cluster_lz(c, op, bytes_op, k0, k1, bthr)) {
+        c->krylov_path = PHIPM_PATH_CLUSTER;
+        return PHIPM_OK;
+    }
     const int64_t n = op.n;
     if (n <= SMALL_N && k1 > k0) {
+        c->krylov_path = PHIPM_PATH_SINGLE_CTA;
         // small problems: the whole extension in one single-CTA kernel (small.cuh)
         SmallArgs sa;
         sa.k0 = k0;
@@ -1008,6 +1122,7 @@ int enqueue_krylov(phipm_ctx *c, const Op &op, double bytes_op, bool symmetric, 
         int rc = PHIPM_OK;
         if (launch_persist(c, op, bytes_op, symmetric, k0, k1, bthr, rc)) return rc;
     }
+    c->krylov_path = PHIPM_PATH_TWO_KERNEL;
     if (k1 > k0 && opt(c, PHIPM_OPT_GRAPH) && !c->prof && !c->kclk_d)
         return enqueue_krylov_graph(c, op, bytes_op, symmetric, orth, k0, k1, bthr);
     return enqueue_krylov_stream(c, op, bytes_op, symmetric, orth, k0, k1, bthr);
@@ -2332,6 +2447,7 @@ int phipm_set_option(phipm_ctx *c, int option, int value)
     bool ok;
     switch (option) {
     case PHIPM_OPT_PERSIST: ok = value >= 0 && value <= 2; break;
+    case PHIPM_OPT_BRICK: ok = value >= 0 && value <= 2; break;
     case PHIPM_OPT_RPT: ok = value == 0 || value == 2 || value == 4 || value == 8; break;
     case PHIPM_OPT_PERSIST_MINROWS: ok = value >= 0; break;
     case PHIPM_OPT_CSR_PREFETCH: ok = value >= 0 && value <= (1 << 20); break;
@@ -2416,6 +2532,11 @@ int phipm_get_trace(const phipm_ctx *c, phipm_trace_rec *out, int max, int *coun
     for (int i = 0; i < nrec; i++) out[i] = c->tracebuf[i];
     *count = (int)c->ntrace;
     return PHIPM_OK;
+}
+
+int phipm_krylov_path(const phipm_ctx *c)
+{
+    return c ? c->krylov_path : PHIPM_PATH_NONE;
 }
 
 int phipm_get_clocks(const phipm_ctx *c, long long *out16)
@@ -2565,6 +2686,7 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
             op.diag = d == 4;
             cudaFuncSetAttribute(persist_tm_fn(op), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         }
+        cudaFuncSetAttribute(krylov_brick_tm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         for (int d = 1; d <= 4; d++) {
             StencilOp op{};
             op.dim = d == 4 ? 2 : d;

@@ -1,0 +1,124 @@
+"""The persistent Lanczos kernel on TMA-staged 3-D bricks (csrc/persist_brick.cuh) against the oracle.
+
+Lanczos extensions (Alg. 2) of 3-D 7-point stencils: a CTA owns a brick of whole
+x-lines, stages each brick plane with its halo as one tensor-map box copy (zero fill outside the grid)
+and its warps march along z.  Option `brick` = 2 selects it for every grid that has a brick
+decomposition, so small and ragged grids reach it; `Context.krylov_path()` proves the kernel ran (no
+silent fallback).  The cases cover: x-lines that fill their 64-point warp segments and ones that do
+not (idle lanes), ny / nz not divisible by the brick shape (ragged last bricks, warps without planes),
+one to four x segments, anisotropic coefficients (a swapped neighbour would change H), relaunches
+with k0 > 0 (v~_{j-1} read from global memory on the first step, from TMEM afterwards) and breakdown.
+Bars: H against the oracle's Lanczos T <= 1e-9 ||A||; solves ||w_gpu - w_ref|| / ||w_ref|| <= max(10 tol, 1e-12).
+"""
+import numpy as np
+import pytest
+
+import paper_0907_4631_b200 as P
+import workloads as W
+from gpu_common import parity_bound, relerr, to_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def aniso(nx, ny, nz, seed, p=2, cx=1.0, cy=1.0, cz=1.0):
+    """Dirichlet operator cx d_xx + cy d_yy + cz d_zz (heat sign), h = 1/(nx+1): symmetric, and every
+    direction has its own coefficient."""
+    h2 = float((nx + 1) ** 2)
+    coef = (-2.0 * (cx + cy + cz) * h2, cx * h2, cx * h2, cy * h2, cy * h2, cz * h2, cz * h2)
+    rng = np.random.default_rng(seed)
+    n = nx * ny * nz
+    u = [rng.standard_normal(n)] + [rng.uniform(-1, 1, n) for _ in range(p)]
+    return W.Stencil(3, nx, ny, nz, coef), u
+
+
+@pytest.fixture()
+def bctx():
+    c = P.Context(n_max=1_400_000, m_max=100, p_max=4, options={"brick": 2, "cluster_lz": 0})
+    yield c
+    c.close()
+
+
+GRIDS = [
+    (128, 20, 24),     # full segments, ny % ylen != 0
+    (64, 37, 29),      # one segment per line, odd ny and nz
+    (20, 22, 30),      # 20 of 64 lanes hold rows
+    (72, 70, 68),      # second segment holds 8 points
+    (250, 9, 11),      # four segments, nx near the box limit
+    (192, 64, 100),    # three segments, n = 1.2M: every SM holds a brick
+]
+
+
+@pytest.mark.parametrize("nx,ny,nz", GRIDS)
+def test_brick_lanczos_matrix_vs_oracle(bctx, orc, nx, ny, nz):
+    st, u = aniso(nx, ny, nz, seed=nx + ny + nz, cx=1.0, cy=0.7, cz=1.9)
+    Pb = W.Problem(name="bk", n=st.n, p=2, t=1e-4, tol=1e-10, symmetric=True, u=u, stencil=st, seed=0)
+    csr = orc.operator_csr(Pb)
+    m = 12
+    Vo, Ho, ko, bo, beta_o = orc.krylov(csr, u[0], m, symmetric=True)
+    V, H, k, brk, beta = bctx.krylov(P.Stencil.of(st), to_dev(u[0]), m, symmetric=True)
+    assert bctx.krylov_path() == "brick"
+    assert k == ko == m and not brk
+    normA = orc.inf_norm(csr)
+    assert np.abs(H.cpu().numpy() - Ho).max() <= 1e-9 * normA
+    assert np.abs(V.cpu().numpy() - Vo).max() <= 1e-9
+
+
+@pytest.mark.parametrize("nx,ny,nz,t", [(128, 20, 24, 3e-4), (72, 70, 68, 2e-4), (20, 22, 30, 2e-3)])
+def test_brick_solve_parity(bctx, orc, nx, ny, nz, t):
+    st, u = aniso(nx, ny, nz, seed=7 + nx, cx=1.0, cy=1.3, cz=0.8)
+    tol = 1e-10
+    Pb = W.Problem(name="bk", n=st.n, p=2, t=t, tol=tol, symmetric=True, u=u, stencil=st, seed=0)
+    wo, so, _ = orc.solve(Pb)
+    assert so["status"] == 0
+    w, s = bctx.solve_stencil(t, P.Stencil.of(st), [to_dev(x) for x in u], tol=tol, symmetric=True)
+    assert bctx.krylov_path() == "brick"
+    assert s.t_reached == t
+    assert s.m_peak > 10, s                         # relaunched with k0 > 0
+    assert relerr(w.cpu().numpy(), wo) <= parity_bound(tol), (s, so)
+
+
+def test_brick_agrees_with_tmem_kernel_on_c4():
+    # the default (auto) takes the brick kernel on c4; brick = 0 the contiguous-range TMEM kernel: the two
+    # differ in the order of the dot / norm sums only
+    Pb = W.make("c4")
+    u = [to_dev(x) for x in Pb.u]
+    out = {}
+    for flag, path in ((1, "brick"), (0, "persist_tmem")):
+        c = P.Context(n_max=Pb.n, m_max=100, p_max=4, options={"brick": flag})
+        w, s = c.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), u, tol=Pb.tol, symmetric=True)
+        assert c.krylov_path() == path
+        out[flag] = (w.cpu().numpy(), s)
+        c.close()
+    assert relerr(out[1][0], out[0][0]) <= 1e-12
+    assert out[1][1].nspmv == out[0][1].nspmv and out[1][1].nsteps == out[0][1].nsteps
+
+
+def test_brick_auto_skips_sparse_segments():
+    # nx = 72 fills 72 of 128 lanes: auto keeps the contiguous-range kernel
+    st, u = aniso(72, 70, 68, seed=3)
+    c = P.Context(n_max=st.n, m_max=40, p_max=2)
+    c.krylov(P.Stencil.of(st), to_dev(u[0]), 6, symmetric=True)
+    assert c.krylov_path() == "persist_tmem"
+    c.close()
+
+
+def test_brick_breakdown(bctx, orc):
+    # u_0 in an invariant subspace of dimension 3 (three sine modes of the Dirichlet Laplacian): the
+    # Lanczos process breaks down at j = 3 with h <= n eps ||A|| (R22); the kernel stops at the same
+    # column as the oracle and later planes that were already in flight are drained
+    nx, ny, nz = 64, 16, 18
+    st, _ = aniso(nx, ny, nz, seed=1)
+    i, j, k = np.meshgrid(np.arange(1, nx + 1), np.arange(1, ny + 1), np.arange(1, nz + 1), indexing="ij")
+
+    def mode(a, b, c):
+        v = np.sin(np.pi * a * i / (nx + 1)) * np.sin(np.pi * b * j / (ny + 1)) * np.sin(np.pi * c * k / (nz + 1))
+        return v.transpose(2, 1, 0).reshape(-1)                   # row = i + nx (j + ny k)
+
+    v0 = mode(1, 1, 1) + 0.5 * mode(2, 1, 3) + 0.25 * mode(3, 2, 1)
+    Pb = W.Problem(name="bd", n=st.n, p=0, t=1e-4, tol=1e-10, symmetric=True, u=[v0], stencil=st, seed=0)
+    csr = orc.operator_csr(Pb)
+    Vo, Ho, ko, bo, _ = orc.krylov(csr, v0, 10, symmetric=True)
+    V, H, kk, brk, _ = bctx.krylov(P.Stencil.of(st), to_dev(v0), 10, symmetric=True)
+    assert bctx.krylov_path() == "brick"
+    assert bo and brk and kk == ko == 3
+    assert np.abs(H.cpu().numpy()[:3, :3] - Ho[:3, :3]).max() <= 1e-9 * orc.inf_norm(csr)

@@ -18,7 +18,10 @@ import workloads as W  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 path = os.path.abspath("gpurun_out/kclock_%s.bin" % name)
-P.build()
+if os.environ.get("PHIPM_LIB"):
+    P.LIB = os.environ["PHIPM_LIB"]          # a variant built by tools/ab_build.py
+else:
+    P.build()
 Pb = W.make(name)
 u = [torch.from_numpy(x).cuda() for x in Pb.u]
 A = tuple(torch.from_numpy(x).cuda() for x in Pb.csr) if Pb.csr is not None else None

@@ -16,6 +16,8 @@
 // The arithmetic per row, per thread, per warp and per block is that of spmv_stream/axpy_stream.
 #pragma once
 
+#include <type_traits>
+
 #include "stream.cuh"
 
 namespace phipm {
@@ -78,9 +80,12 @@ struct NoRelease {
 
 // on_release: run by the last warp's lane 0 once every CTA has arrived, while warps 0.. nv-1 sum the
 // partials (e.g. to issue the next phase's first bulk copies off the critical path)
-template <class OnRelease = NoRelease>
+// on_release_warps: run by lane 0 of EVERY warp at the same point (work that is spread over the warps,
+// e.g. one bulk tensor copy each); both hooks run after a proxy fence for the other CTAs' writes
+template <class OnRelease = NoRelease, class OnReleaseWarps = NoRelease>
 __device__ __forceinline__ bool phase_allreduce(const Work &wk, const double *bsum, int nv, unsigned phase,
-                                                const PersistArgs &a, double *red, OnRelease on_release = OnRelease{})
+                                                const PersistArgs &a, double *red, OnRelease on_release = OnRelease{},
+                                                OnReleaseWarps on_release_warps = OnReleaseWarps{})
 {
     __shared__ int s_ok;
     const int nb = gridDim.x;
@@ -120,6 +125,15 @@ __device__ __forceinline__ bool phase_allreduce(const Work &wk, const double *bs
         // the barrier above; its own bulk copies read them through the async proxy
         asm volatile("fence.proxy.async.global;" ::: "memory");
         on_release();
+    }
+    if constexpr (!std::is_same<OnReleaseWarps, NoRelease>::value) {
+        if ((threadIdx.x & 31) == 0) {
+            // (the shared-memory reads of the previous phase by this CTA's generic proxy, and the other
+            // CTAs' global writes acquired by thread 0 and ordered by the barrier above)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        on_release_warps();
     }
     for (int v = warp; v < nv; v += nw) {
         const double *pv = wk.part + (size_t)v * wk.pstride + half;

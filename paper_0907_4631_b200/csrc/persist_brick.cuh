@@ -124,6 +124,7 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
 {
     extern __shared__ __align__(128) double sm[];
     __shared__ uint64_t pbar[BRICK_MAXPL];
+    __shared__ unsigned char porder[BRICK_MAXPL];
     __shared__ double bsum[2];
     __shared__ double red[MAXD + 2];
     __shared__ double wsum2[2 * SNW];
@@ -171,77 +172,116 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
     bool pre = false;                                      // the next step's planes are in flight
     bool aborted = false;
     uint32_t par = 0;                                      // mbarrier parity of the current step
-    // every plane of Krylov column jc, in the order the marching warps reach them (one thread)
-    auto issue_planes = [&](int jc) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads of sm
+    // the brick's planes in the order the marching warps reach them: plane t of every z group, t ascending
+    // (planes ppg, ppg + 1 of a group are planes 0, 1 of the group above)
+    if (tid == 0) {
+        int o = 0;
         for (int t = 0; t < g.ppg + 2; t++)
             for (int gi = 0; gi < g.ngrp; gi++) {
-                if (t >= g.ppg && gi + 1 < g.ngrp) continue;           // = planes 0, 1 of the group above
+                if (t >= g.ppg && gi + 1 < g.ngrp) continue;
                 const int s = gi * g.ppg + t;
-                if (s > zl + 1) continue;
+                if (s <= zl + 1) porder[o++] = (unsigned char)s;
+            }
+    }
+    __syncthreads();
+    // plane copies of Krylov column jc: lane 0 of warp w issues planes porder[w], porder[w + SNW], ... (one
+    // thread issuing all zlen + 2 copies held the CTA for > 1 us at c4)
+    auto issue_planes = [&](int jc) {
+        if (lane == 0)
+            for (int o = warp; o < zl + 2; o += SNW) {
+                const int s = porder[o];
                 mbar_arrive_expect_tx(&pbar[s], plane_bytes);
                 tma_load_box4(sm + (size_t)s * g.pstride, &tmap, -2, y0 - 1, z0 - 1 + s, jc, &pbar[s], pol);
             }
     };
     const int xa = act ? xi : 0;                           // (idle lanes read a valid address)
-    const double *base = sm + (yl + 1) * g.lstride + xa + 2 + zb * g.pstride;   // centre pair, plane zb - 1
+    // shared address of the warp's centre pair in the plane below its first one; byte strides
+    const uint32_t pa0 = smem_u32(sm + (yl + 1) * g.lstride + xa + 2 + zb * g.pstride);
+    const uint32_t ps8 = (uint32_t)g.pstride * 8u, ls8 = (uint32_t)g.lstride * 8u;
+    const uint32_t pb0 = smem_u32(&pbar[zb]);
     const int64_t row0 = xa + (int64_t)nx * (yy + (int64_t)ny * (z0 + zb));     // row of (xi, yy, z0 + zb)
     const int64_t pl = (int64_t)nx * ny;
+    const bool ragged = g.nseg * 64 != nx;                 // some lanes of the last segment hold no rows
     const double c0 = op.c[0], cxm = op.c[1], cxp = op.c[2], cym = op.c[3], cyp = op.c[4], czm = op.c[5],
                  czp = op.c[6];
-    auto ld2 = [](const double *p) { return *reinterpret_cast<const double2 *>(p); };
+    auto lds2 = [](uint32_t ad) {
+        double2 r;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(ad));
+        return r;
+    };
+    auto lds1 = [](uint32_t ad) {
+        double r;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(ad));
+        return r;
+    };
+    auto bar_wait = [](uint32_t bar, uint32_t parity) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            "@!p bra WAIT_%=;\n"
+            "}\n" ::"r"(bar),
+            "r"(parity)
+            : "memory");
+    };
     for (int j = a.k0; j < a.k1; j++) {
         if (stop) break;                                   // breakdown (same decision in every CTA)
         const double sj = sig;
         const double *zv = j > 0 ? wk.V + (int64_t)(j - 1) * ldv : nullptr;     // v~_{j-1} (Alg. 2 line 3)
         const double lz = zv ? lzc : 0.0;
-        const bool zs = j > a.k0;                          // v~_{j-1} of these rows is in slot B
 
         // ---------------- phase A: y = sigma_j A x - lz v~_{j-1}; d = x^T y; ||y||^2
-        if (tid == 0 && !pre) issue_planes(j);
+        if (!pre) {
+            if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_planes(j);
+        }
         pre = false;
         double ysq = 0.0, dot = 0.0;
         if (cnt > 0) {
-            mbar_wait(&pbar[zb], par);
-            mbar_wait(&pbar[zb + 1], par);
-            double2 zm = ld2(base), zc = ld2(base + g.pstride);
-            const double *P = base + g.pstride;            // centre pair of the current plane
+            // first step of the launch: v~_{j-1} of the warp's rows from global memory into slot B (zeros
+            // for j = 0); afterwards phase A of the previous step left v~_j = this step's v~_{j-1} there
+            if (j == a.k0) {
+#pragma unroll
+                for (int t = 0; t < TM_PAIRS; t++) {
+                    if (t >= cnt) break;
+                    const double2 z = (zv && act) ? ld_cg2(zv + row0 + t * pl) : make_double2(0.0, 0.0);
+                    tm_st4(slotB + 4 * t, z);
+                }
+                tm_wait_st();
+            }
+            bar_wait(pb0, par);
+            bar_wait(pb0 + 8, par);
+            double2 zm = lds2(pa0), zc = lds2(pa0 + ps8);
+            uint32_t pa = pa0 + ps8;                       // centre pair of the current plane
 #pragma unroll
             for (int t = 0; t < TM_PAIRS; t++) {
                 if (t >= cnt) break;
                 uint32_t zr[4];
-                double2 zp_ = make_double2(0.0, 0.0);
-                if (zv) {
-                    if (zs) tm_ld4_issue(slotB + 4 * t, zr);
-                    else if (act) zp_ = ld_cg2(zv + row0 + t * pl);
-                }
-                mbar_wait(&pbar[zb + t + 2], par);
-                const double2 zn = ld2(P + g.pstride);
-                const double2 ym = ld2(P - g.lstride), yp = ld2(P + g.lstride);
-                const double xl = P[-1], xh = P[2];
-                double sa = 0.0, sb = 0.0;
-                sa = __dadd_rn(sa, __dmul_rn(czm, zm.x));
-                sb = __dadd_rn(sb, __dmul_rn(czm, zm.y));
-                sa = __dadd_rn(sa, __dmul_rn(cym, ym.x));
-                sb = __dadd_rn(sb, __dmul_rn(cym, ym.y));
-                sa = __dadd_rn(sa, __dmul_rn(cxm, xl));
-                sb = __dadd_rn(sb, __dmul_rn(cxm, zc.x));
-                sa = __dadd_rn(sa, __dmul_rn(c0, zc.x));
-                sb = __dadd_rn(sb, __dmul_rn(c0, zc.y));
-                sa = __dadd_rn(sa, __dmul_rn(cxp, zc.y));
-                sb = __dadd_rn(sb, __dmul_rn(cxp, xh));
-                sa = __dadd_rn(sa, __dmul_rn(cyp, yp.x));
-                sb = __dadd_rn(sb, __dmul_rn(cyp, yp.y));
-                sa = __dadd_rn(sa, __dmul_rn(czp, zn.x));
-                sb = __dadd_rn(sb, __dmul_rn(czp, zn.y));
-                double2 y = make_double2(sa * sj, sb * sj);
-                if (zv) {
-                    if (zs) zp_ = tm_ld4_wait(zr);
-                    y.x = fma(-lz, zp_.x, y.x);
-                    y.y = fma(-lz, zp_.y, y.y);
-                }
+                tm_ld4_issue(slotB + 4 * t, zr);
+                bar_wait(pb0 + 8 * (t + 2), par);
+                const uint32_t pn = pa + ps8;
+                const double2 zn = lds2(pn);
+                const double2 ym = lds2(pa - ls8), yp = lds2(pa + ls8);
+                const double xl = lds1(pa - 8), xh = lds1(pa + 16);
+                // ascending columns z-, y-, x-, centre, x+, y+, z+ (fused multiply-adds)
+                double sa = czm * zm.x, sb = czm * zm.y;
+                sa = fma(cym, ym.x, sa);
+                sb = fma(cym, ym.y, sb);
+                sa = fma(cxm, xl, sa);
+                sb = fma(cxm, zc.x, sb);
+                sa = fma(c0, zc.x, sa);
+                sb = fma(c0, zc.y, sb);
+                sa = fma(cxp, zc.y, sa);
+                sb = fma(cxp, xh, sb);
+                sa = fma(cyp, yp.x, sa);
+                sb = fma(cyp, yp.y, sb);
+                sa = fma(czp, zn.x, sa);
+                sb = fma(czp, zn.y, sb);
+                const double2 zq = tm_ld4_wait(zr);
+                double2 y = make_double2(fma(-lz, zq.x, sa * sj), fma(-lz, zq.y, sb * sj));
                 double2 xc = zc;
-                if (!act) {
+                if (ragged && !act) {
                     y = make_double2(0.0, 0.0);
                     xc = y;
                 }
@@ -253,7 +293,7 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
                 tm_st4(slotB + 4 * t, xc);
                 zm = zc;
                 zc = zn;
-                P += g.pstride;
+                pa = pn;
             }
             tm_wait_st();
         }
@@ -302,7 +342,7 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
         // v~_{j+1} is complete in every CTA once the phase's arrivals are in: the next step's planes are
         // issued then, while the partials are summed (drained below on breakdown)
         const bool more = j + 1 < a.k1;
-        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red, [&] {
+        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red, NoRelease{}, [&] {
                 if (more) issue_planes(j + 1);
             })) {
             aborted = true;

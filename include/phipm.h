@@ -165,6 +165,10 @@ int phipm_get_clocks(const phipm_ctx *ctx, long long *out16);
 #define PHIPM_PATH_PERSIST_TMEM  5   /* persistent Lanczos, y / v~ in tensor memory (persist_tm.cuh) */
 #define PHIPM_PATH_BRICK         6   /* persistent Lanczos on TMA-staged 3-D bricks (persist_brick.cuh) */
 int phipm_krylov_path(const phipm_ctx *ctx);
+/* The same for the last w-recurrence (Eq. wrecurrence) of a solve: PHIPM_PATH_BRICK (wrec_brick_kernel),
+ * PHIPM_PATH_PERSIST_SMEM (wrec_persist_kernel, contiguous row ranges) or PHIPM_PATH_NONE (p streaming SpMV
+ * launches, single-CTA kernels, or none yet). */
+int phipm_wrec_path(const phipm_ctx *ctx);
 
 void phipm_default_opts(phipm_opts *opts);
 

@@ -151,6 +151,7 @@ def lib():
             "phipm_get_attempts": (i32, [vp, P(_Attempt), i32, P(i32)]),
             "phipm_get_clocks": (i32, [vp, P(C.c_longlong)]),
             "phipm_krylov_path": (i32, [vp]),
+            "phipm_wrec_path": (i32, [vp]),
             "phipm_set_option": (i32, [vp, i32, i32]),
             "phipm_get_option": (i32, [vp, i32, P(i32)]),
             "phipm_solve_csr": (i32, [vp, d, P(_Csr), i32, P(vp), P(_Opts), vp, P(_Stats)]),
@@ -185,7 +186,7 @@ def lib():
 
 EXPORTED = [
     "phipm_default_opts", "phipm_set_expm_method", "phipm_mm_read", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
-    "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_get_attempts", "phipm_get_clocks", "phipm_krylov_path", "phipm_set_option",
+    "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_get_attempts", "phipm_get_clocks", "phipm_krylov_path", "phipm_wrec_path", "phipm_set_option",
     "phipm_get_option", "phipm_solve_csr", "phipm_solve_stencil",
     "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_solve_csr_batch",
     "phipm_solve_stencil_batch", "phipm_solve_csr_block", "phipm_stencil_nnz", "phipm_inf_norm_stencil",
@@ -259,6 +260,10 @@ class Context:
     def krylov_path(self) -> str:
         """Kernel path of the last Krylov extension (phipm_krylov_path, PHIPM_PATH_*)."""
         return KRYLOV_PATHS[self._L.phipm_krylov_path(self._h)]
+
+    def wrec_path(self) -> str:
+        """Kernel path of the last w-recurrence (phipm_wrec_path)."""
+        return KRYLOV_PATHS[self._L.phipm_wrec_path(self._h)]
 
     def get_option(self, name) -> int:
         o = OPTIONS[name] if isinstance(name, str) else int(name)

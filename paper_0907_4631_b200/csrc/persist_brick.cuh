@@ -27,6 +27,7 @@
 #include <cuda.h>
 
 #include "persist_tm.cuh"
+#include "persist_wrec.cuh"
 
 namespace phipm {
 
@@ -238,6 +239,10 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
         }
         pre = false;
         double ysq = 0.0, dot = 0.0;
+#ifdef BRICK_CLK
+        unsigned long long ck0 = gtimer(), ck1 = 0, ck2 = 0, ck3 = 0, ckp[TM_PAIRS] = {};
+        long long ckw = 0;
+#endif
         if (cnt > 0) {
             // first step of the launch: v~_{j-1} of the warp's rows from global memory into slot B (zeros
             // for j = 0); afterwards phase A of the previous step left v~_j = this step's v~_{j-1} there
@@ -252,6 +257,9 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
             }
             bar_wait(pb0, par);
             bar_wait(pb0 + 8, par);
+#ifdef BRICK_CLK
+            ck1 = gtimer();
+#endif
             double2 zm = lds2(pa0), zc = lds2(pa0 + ps8);
             uint32_t pa = pa0 + ps8;                       // centre pair of the current plane
 #pragma unroll
@@ -259,7 +267,13 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
                 if (t >= cnt) break;
                 uint32_t zr[4];
                 tm_ld4_issue(slotB + 4 * t, zr);
+#ifdef BRICK_CLK
+                const long long cw0 = clock64();
+#endif
                 bar_wait(pb0 + 8 * (t + 2), par);
+#ifdef BRICK_CLK
+                ckw += clock64() - cw0;
+#endif
                 const uint32_t pn = pa + ps8;
                 const double2 zn = lds2(pn);
                 const double2 ym = lds2(pa - ls8), yp = lds2(pa + ls8);
@@ -294,13 +308,26 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
                 zm = zc;
                 zc = zn;
                 pa = pn;
+#ifdef BRICK_CLK
+                ckp[t] = gtimer();
+#endif
             }
             tm_wait_st();
         }
+#ifdef BRICK_CLK
+        ck2 = gtimer();
+#endif
         {
             const double v2[2] = {dot, ysq};
             block_sums<2, false>(v2, wsum2, bsum);
         }
+#ifdef BRICK_CLK
+        // (measurement build: where one CTA's SpMV phase goes, ns from the phase start of each warp)
+        ck3 = gtimer();
+        if (blockIdx.x == 37 && j == a.k0 + 4 && lane == 0)
+            printf("w%02d A: start %llu planes01 +%llu p0 +%llu p1 +%llu p3 +%llu p5 +%llu march +%llu sums +%llu; plane waits %lld cycles\n", warp,
+                   ck0 % 1000000, ck1 - ck0, ckp[0] - ck0, ckp[1] - ck0, ckp[3] - ck0, ckp[5] - ck0, ck2 - ck0, ck3 - ck0, ckw);
+#endif
         if (!phase_allreduce(wk, bsum, 2, ++phase, a, red)) {
             aborted = true;
             break;
@@ -380,6 +407,224 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
     if (!aborted) coop_exit(a);
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// The w-recurrence of a step (Eq. wrecurrence; persist_wrec.cuh) on the same bricks:
+//   w_0 = u_k ;  w_j = A w_{j-1} + sum_l t_k^l / l! u_{j+l}   (j = 1..p) ;  w_p -> V[:, 0], ||w_p||^2
+// one cooperative kernel, p SpMV phases separated by grid phases.  Plane copies of w_{j-1} come from the
+// tensor map of x_0 (j = 1: the caller's u_0 or its workspace copy) or of the context's W columns; the
+// u-terms are read and w_j is written straight from / to global memory (a warp's 64 consecutive x of one
+// line: coalesced 16-byte accesses).  The rows are the ascending-column sums with separately rounded
+// products of every other SpMV of the library, then fma(c_l, u_{j+l}, y) in term order: w_1..w_p equal
+// the streaming path's bit for bit (an absent neighbour adds c * 0, see above); ||w_p||^2 is summed in
+// another order.  FIN_SEED as in wrec_persist_kernel.
+__global__ void __launch_bounds__(SNT, 1)
+wrec_brick_kernel(const __grid_constant__ CUtensorMap tmx0, const __grid_constant__ CUtensorMap tmw, StencilOp op,
+                  BrickGeom g, WrecArgs w, PersistArgs a, Work wk)
+{
+    extern __shared__ __align__(128) double sm[];
+    __shared__ uint64_t pbar[BRICK_MAXPL];
+    __shared__ unsigned char porder[BRICK_MAXPL];
+    __shared__ double bsum[2];
+    __shared__ double red[MAXD + 2];
+    __shared__ double wsum[SNW];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nx = op.nx, ny = op.ny, nz = op.nz;
+    const int64_t ldv = wk.ldv;
+    const int by = blockIdx.x % g.py, bz = blockIdx.x / g.py;
+    const int y0 = by * g.ylen, z0 = bz * g.zlen;
+    const int zl = min(g.zlen, nz - z0);
+    const int col = warp % g.ncol, grp = warp / g.ncol;
+    const int seg = col % g.nseg, yl = col / g.nseg;
+    const int xi = seg * 64 + 2 * lane;
+    const int yy = y0 + yl;
+    const int zb = grp * g.ppg;
+    const int cnt = (grp < g.ngrp && yy < ny) ? max(0, min(g.ppg, zl - zb)) : 0;
+    const bool act = xi < nx;
+    const uint32_t plane_bytes = (uint32_t)(g.lstride * (g.ylen + 2)) * 8u;
+    if (tid < zl + 2) mbar_init(&pbar[tid], 1);
+    if (tid == 0) {
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        int o = 0;
+        for (int t = 0; t < g.ppg + 2; t++)
+            for (int gi = 0; gi < g.ngrp; gi++) {
+                if (t >= g.ppg && gi + 1 < g.ngrp) continue;
+                const int s = gi * g.ppg + t;
+                if (s <= zl + 1) porder[o++] = (unsigned char)s;
+            }
+    }
+    const uint64_t pol = policy_evict_last();
+    pdl_wait();
+    __syncthreads();
+    unsigned phase = 0;
+    bool pre = false;
+    uint32_t par = 0;
+    auto issue_planes = [&](const CUtensorMap *tm, int jc) {
+        if (lane == 0)
+            for (int o = warp; o < zl + 2; o += SNW) {
+                const int s = porder[o];
+                mbar_arrive_expect_tx(&pbar[s], plane_bytes);
+                tma_load_box4(sm + (size_t)s * g.pstride, tm, -2, y0 - 1, z0 - 1 + s, jc, &pbar[s], pol);
+            }
+    };
+    const int xa = act ? xi : 0;
+    const uint32_t pa0 = smem_u32(sm + (yl + 1) * g.lstride + xa + 2 + zb * g.pstride);
+    const uint32_t ps8 = (uint32_t)g.pstride * 8u, ls8 = (uint32_t)g.lstride * 8u;
+    const uint32_t pb0 = smem_u32(&pbar[zb]);
+    const int64_t row0 = xa + (int64_t)nx * (yy + (int64_t)ny * (z0 + zb));
+    const int64_t pl = (int64_t)nx * ny;
+    const double c0 = op.c[0], cxm = op.c[1], cxp = op.c[2], cym = op.c[3], cyp = op.c[4], czm = op.c[5],
+                 czp = op.c[6];
+    auto lds2 = [](uint32_t ad) {
+        double2 r;
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "r"(ad));
+        return r;
+    };
+    auto lds1 = [](uint32_t ad) {
+        double r;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(ad));
+        return r;
+    };
+    auto bar_wait = [](uint32_t bar, uint32_t parity) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            "@!p bra WAIT_%=;\n"
+            "}\n" ::"r"(bar),
+            "r"(parity)
+            : "memory");
+    };
+    // L2 prefetch of the u-terms of pass jp for this brick: its ylen lines of a plane are contiguous, one
+    // bulk prefetch per plane and term (warp t: plane t).  With one plane of register prefetch in the
+    // marching loop the u loads were HBM-latency bound (16 KB in flight per SM: ~2 TB/s); from L2 the same
+    // depth covers the latency
+    const int ylines = min(g.ylen, ny - y0);
+    auto prefetch_terms = [&](int jp) {
+        if (lane == 0)
+            for (int t = warp; t < zl; t += SNW)
+                for (int i = 0; i < w.nz[jp - 1]; i++)
+                    prefetch_rows(w.z[jp - 1][i] + (int64_t)nx * (y0 + (int64_t)ny * (z0 + t)), ylines * nx);
+    };
+    prefetch_terms(1);
+    for (int j = 1; j <= w.p; j++) {
+        double *y = ((j == w.p) ? wk.V : w.W + (int64_t)j * ldv) + row0;
+        const int nzt = w.nz[j - 1];
+        if (j < w.p) prefetch_terms(j + 1);
+        if (!pre) {
+            if (lane == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_planes(j == 1 ? &tmx0 : &tmw, j == 1 ? 0 : j - 1);
+        }
+        pre = false;
+        double ysq = 0.0;
+#ifdef BRICK_CLK
+        unsigned long long ck0 = gtimer(), ck1 = 0, ck2 = 0, ck3 = 0, ckp[TM_PAIRS] = {};
+        long long ckw = 0;
+#endif
+        if (cnt > 0) {
+            // the first u-term of the first plane is loaded before the plane wait (HBM latency)
+            const double *z0p = nzt > 0 ? w.z[j - 1][0] + row0 : nullptr;
+            double2 u0 = (z0p && act) ? ld_stream2(z0p) : make_double2(0.0, 0.0);
+            bar_wait(pb0, par);
+            bar_wait(pb0 + 8, par);
+#ifdef BRICK_CLK
+            ck1 = gtimer();
+#endif
+            double2 zm = lds2(pa0), zc = lds2(pa0 + ps8);
+            uint32_t pa = pa0 + ps8;
+#pragma unroll
+            for (int t = 0; t < TM_PAIRS; t++) {
+                if (t >= cnt) break;
+                // the next plane's first u-term flies while this plane is computed
+                double2 u1 = make_double2(0.0, 0.0);
+                if (z0p && act && t + 1 < cnt) u1 = ld_stream2(z0p + (t + 1) * pl);
+#ifdef BRICK_CLK
+                const long long cw0 = clock64();
+#endif
+                bar_wait(pb0 + 8 * (t + 2), par);
+#ifdef BRICK_CLK
+                ckw += clock64() - cw0;
+#endif
+                const uint32_t pn = pa + ps8;
+                const double2 zn = lds2(pn);
+                const double2 ym = lds2(pa - ls8), yp = lds2(pa + ls8);
+                const double xl = lds1(pa - 8), xh = lds1(pa + 16);
+                double sa = 0.0, sb = 0.0;
+                sa = __dadd_rn(sa, __dmul_rn(czm, zm.x));
+                sb = __dadd_rn(sb, __dmul_rn(czm, zm.y));
+                sa = __dadd_rn(sa, __dmul_rn(cym, ym.x));
+                sb = __dadd_rn(sb, __dmul_rn(cym, ym.y));
+                sa = __dadd_rn(sa, __dmul_rn(cxm, xl));
+                sb = __dadd_rn(sb, __dmul_rn(cxm, zc.x));
+                sa = __dadd_rn(sa, __dmul_rn(c0, zc.x));
+                sb = __dadd_rn(sb, __dmul_rn(c0, zc.y));
+                sa = __dadd_rn(sa, __dmul_rn(cxp, zc.y));
+                sb = __dadd_rn(sb, __dmul_rn(cxp, xh));
+                sa = __dadd_rn(sa, __dmul_rn(cyp, yp.x));
+                sb = __dadd_rn(sb, __dmul_rn(cyp, yp.y));
+                sa = __dadd_rn(sa, __dmul_rn(czp, zn.x));
+                sb = __dadd_rn(sb, __dmul_rn(czp, zn.y));
+                if (act) {
+                    if (nzt > 0) {
+                        const double cz0 = w.zc[j - 1][0];
+                        sa = fma(cz0, u0.x, sa);
+                        sb = fma(cz0, u0.y, sb);
+                    }
+#pragma unroll 1
+                    for (int i = 1; i < nzt; i++) {
+                        const double2 ui = ld_stream2(w.z[j - 1][i] + row0 + t * pl);
+                        const double ci = w.zc[j - 1][i];
+                        sa = fma(ci, ui.x, sa);
+                        sb = fma(ci, ui.y, sb);
+                    }
+                    *reinterpret_cast<double2 *>(y + t * pl) = make_double2(sa, sb);
+                    ysq = fma(sa, sa, ysq);
+                    ysq = fma(sb, sb, ysq);
+                }
+                u0 = u1;
+                zm = zc;
+                zc = zn;
+                pa = pn;
+#ifdef BRICK_CLK
+                ckp[t] = gtimer();
+#endif
+            }
+        }
+#ifdef BRICK_CLK
+        ck2 = gtimer();
+#endif
+        {
+            const double v1[1] = {j == w.p ? ysq : 0.0};
+            block_sums<1, false>(v1, wsum, bsum);
+        }
+#ifdef BRICK_CLK
+        ck3 = gtimer();
+        if (blockIdx.x == 37 && lane == 0 && (warp & 7) == 0)
+            printf("wrec j%d w%02d: start %llu planes01 +%llu p0 +%llu p1 +%llu p3 +%llu p5 +%llu march +%llu sums +%llu; plane waits %lld cycles\n",
+                   j, warp, ck0 % 1000000, ck1 - ck0, ckp[0] - ck0, ckp[1] - ck0, ckp[3] - ck0, ckp[5] - ck0, ck2 - ck0,
+                   ck3 - ck0, ckw);
+#endif
+        const bool more = j < w.p;
+        if (!phase_allreduce(wk, bsum, 1, ++phase, a, red, NoRelease{}, [&] {
+                if (more) issue_planes(&tmw, j);
+            }))
+            return;
+        pre = more;
+        par ^= 1u;
+        if (j == w.p && blockIdx.x == 0 && tid == 0) {
+            // FIN_SEED: beta = ||w_p||, sigma_0 = 1 / beta, breakdown / non-finite reset
+            const double b = sqrt(red[0]);
+            wk.st->beta = b;
+            wk.sigma[0] = 1.0 / b;
+            wk.st->brk = (b > 0.0 && isfinite(b)) ? -1 : 0;
+            wk.st->nonfinite = isfinite(b) ? 0 : 1;
+            wk.st->lz = 0.0;
+        }
+    }
+    coop_exit(a);
 }
 
 } // namespace phipm

@@ -64,6 +64,12 @@ struct GraphRec {
     int64_t nlaunch = 0;
 };
 
+struct BrickMap {
+    CUtensorMap map;
+    const double *base = nullptr;           // nullptr: none
+    int nx = 0, ny = 0, nz = 0, ylen = 0;
+};
+
 struct phipm_ctx {
     int dev = 0;
     cudaStream_t stream = nullptr;
@@ -137,10 +143,10 @@ struct phipm_ctx {
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
     int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1};
-    // brick Lanczos kernel: the tensor map of the basis for the last grid / brick shape
-    CUtensorMap brick_map;
-    int brick_key[4] = {0, 0, 0, 0};        // nx, ny, nz, ylen of brick_map (nx = 0: none)
+    // brick kernels: tensor maps of V, W and the w-recurrence's x_0 for the last grid / brick shape
+    BrickMap brick_maps[3];
     int krylov_path = PHIPM_PATH_NONE;      // kernel path of the last Krylov extension (phipm_krylov_path)
+    int wrec_path = PHIPM_PATH_NONE;        // ... of the last w-recurrence (phipm_wrec_path)
     char err[512] = {0};
 };
 
@@ -728,30 +734,44 @@ TmapEncodeFn tmap_encode_fn()
     return fn;
 }
 
-// 4-D tensor map (x, y, z, Krylov column) over the basis V of the context for an nx x ny x nz grid;
-// box = one plane of a brick with its halo: (nx + 4) x (ylen + 2) x 1 x 1, zero fill outside the grid
-bool brick_tensor_map(phipm_ctx *c, const StencilOp &op, const BrickGeom &g)
+// 4-D tensor map (x, y, z, column) over `ncols` vectors of an nx x ny x nz grid, `ld` doubles apart; box = one
+// plane of a brick with its halo: (nx + 4) x (ylen + 2) x 1 x 1, zero fill outside the grid.  Cached per
+// context slot (0: the basis V, 1: the w-recurrence vectors W, 2: x_0 of the w-recurrence)
+bool brick_tensor_map(phipm_ctx *c, int slot, const double *base, int ncols, int64_t ld, const StencilOp &op,
+                      const BrickGeom &g)
 {
-    if (c->brick_key[0] == op.nx && c->brick_key[1] == op.ny && c->brick_key[2] == op.nz && c->brick_key[3] == g.ylen)
-        return true;
+    BrickMap &m = c->brick_maps[slot];
+    if (m.base == base && m.nx == op.nx && m.ny == op.ny && m.nz == op.nz && m.ylen == g.ylen) return true;
     const TmapEncodeFn enc = tmap_encode_fn();
-    if (!enc || ((uintptr_t)c->V & 15) || (c->ldv & 1)) return false;
-    const cuuint64_t gdim[4] = {(cuuint64_t)op.nx, (cuuint64_t)op.ny, (cuuint64_t)op.nz, (cuuint64_t)(c->m_max + 1)};
-    const cuuint64_t gstr[3] = {(cuuint64_t)op.nx * 8, (cuuint64_t)op.nx * op.ny * 8, (cuuint64_t)c->ldv * 8};
+    if (!enc || ((uintptr_t)base & 15) || (ld & 1)) return false;
+    const cuuint64_t gdim[4] = {(cuuint64_t)op.nx, (cuuint64_t)op.ny, (cuuint64_t)op.nz, (cuuint64_t)ncols};
+    const cuuint64_t gstr[3] = {(cuuint64_t)op.nx * 8, (cuuint64_t)op.nx * op.ny * 8, (cuuint64_t)ld * 8};
     const cuuint32_t box[4] = {(cuuint32_t)(op.nx + 4), (cuuint32_t)(g.ylen + 2), 1, 1};
     const cuuint32_t est[4] = {1, 1, 1, 1};
-    const CUresult r = enc(&c->brick_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, c->V, gdim, gstr, box, est,
+    const CUresult r = enc(&m.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(base), gdim, gstr, box, est,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
-        c->brick_key[0] = 0;
+        m.base = nullptr;
         return false;
     }
-    c->brick_key[0] = op.nx;
-    c->brick_key[1] = op.ny;
-    c->brick_key[2] = op.nz;
-    c->brick_key[3] = g.ylen;
+    m.base = base;
+    m.nx = op.nx;
+    m.ny = op.ny;
+    m.nz = op.nz;
+    m.ylen = g.ylen;
     return true;
+}
+
+// the brick decomposition of this operator under PHIPM_OPT_BRICK (0 off, 1 auto: x-lines that fill >= 3/4 of
+// their 64-point warp segments, 2 whenever one exists)
+bool brick_plan(phipm_ctx *c, const StencilOp &op, BrickGeom &g)
+{
+    const int mode = opt(c, PHIPM_OPT_BRICK);
+    if (!mode || op.dim != 3 || op.diag) return false;
+    if (!brick_geometry(op.nx, op.ny, op.nz, c->sm_count, c->smem_optin - 2048, g)) return false;
+    if (mode == 1 && 4 * op.nx < 3 * 64 * g.nseg) return false;
+    return g.py * g.pz <= c->pstride;
 }
 
 // Lanczos on 3-D bricks staged by tensor-map TMA (persist_brick.cuh).  PHIPM_OPT_BRICK: 0 off, 1 auto
@@ -759,12 +779,9 @@ bool brick_tensor_map(phipm_ctx *c, const StencilOp &op, const BrickGeom &g)
 // decomposition exists
 bool try_persist_brick(phipm_ctx *c, const StencilOp &op, int k0, int k1, double bthr, double bytes, int &rc)
 {
-    const int mode = opt(c, PHIPM_OPT_BRICK);
-    if (!mode || op.dim != 3 || op.diag) return false;
     BrickGeom g;
-    if (!brick_geometry(op.nx, op.ny, op.nz, c->sm_count, c->smem_optin - 2048, g)) return false;
-    if (mode == 1 && 4 * op.nx < 3 * 64 * g.nseg) return false;
-    if (!brick_tensor_map(c, op, g)) return false;
+    if (!brick_plan(c, op, g)) return false;
+    if (!brick_tensor_map(c, 0, c->V, c->m_max + 1, c->ldv, op, g)) return false;
     const size_t smem = brick_smem_bytes(g);
     const int grid = g.py * g.pz;
     int occ = 0;
@@ -797,7 +814,7 @@ bool try_persist_brick(phipm_ctx *c, const StencilOp &op, int k0, int k1, double
     }
     ProfRec r;
     prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
-    const cudaError_t e = launch_coop(c, krylov_brick_tm_kernel, grid, SNT, smem, c->brick_map, op, g, a, make_work(c));
+    const cudaError_t e = launch_coop(c, krylov_brick_tm_kernel, grid, SNT, smem, c->brick_maps[0].map, op, g, a, make_work(c));
     prof_end(c, r);
     c->acc.launches++;
     if (e != cudaSuccess) {
@@ -825,10 +842,63 @@ WrecFn wrec_fn(const StencilOp &op)
     }
 }
 
+// the w-recurrence on TMA-staged bricks (persist_brick.cuh: wrec_brick_kernel); the u-terms are read with
+// 16-byte loads, so every u pointer must be 16-byte aligned (else the contiguous-range kernel)
+bool try_wrec_brick(phipm_ctx *c, const StencilOp &op, const WrecArgs &w, double bytes, int &rc)
+{
+    if (op.n < (int64_t)SNT * 4 * c->sm_count / 2 && opt(c, PHIPM_OPT_BRICK) != 2) return false;
+    BrickGeom g;
+    if (!brick_plan(c, op, g)) return false;
+    for (int j = 0; j < w.p; j++)
+        for (int i = 0; i < w.nz[j]; i++)
+            if ((uintptr_t)w.z[j][i] & 15) return false;
+    if (!brick_tensor_map(c, 1, c->W, c->p_max + 1, c->ldv, op, g)) return false;
+    if (!brick_tensor_map(c, 2, w.x0, 1, op.n + (op.n & 1), op, g)) return false;
+    const size_t smem = brick_smem_bytes(g);
+    const int grid = g.py * g.pz;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, wrec_brick_kernel, SNT, smem) != cudaSuccess || occ < 1 ||
+        grid > occ * c->sm_count) {
+        cudaGetLastError();
+        return false;
+    }
+    PersistArgs a{};
+    a.flag = c->counter + 2;
+    a.abort = c->counter + 3;
+    a.exit_ctr = c->counter + 4;
+    a.timeout_ns = 2000000000ull;
+    // PHIPM_KCLOCKS: 2 stamps per CTA per pass (recorded as (p + 1) / 2 two-phase steps)
+    const size_t need = (size_t)2 * ((w.p + 1) / 2) * grid * 2;
+    if (c->pclk_d && c->pclk_used + need <= PCLK_CAP) {
+        a.dbg = c->pclk_d + c->pclk_used;
+        cudaMemsetAsync(a.dbg, 0, need * sizeof(unsigned long long), c->stream);
+        c->pclk_recs.push_back({grid, (w.p + 1) / 2, (long long)c->pclk_used});
+        c->pclk_used += need;
+    }
+    rc = PHIPM_OK;
+    if (!coop_reset(c)) {
+        rc = set_err(c, PHIPM_ECUDA, "wrec: memset failed");
+        return true;
+    }
+    ProfRec r;
+    prof_begin(c, r, PC_SPMV, bytes, 0);
+    const cudaError_t e = launch_coop(c, wrec_brick_kernel, grid, SNT, smem, c->brick_maps[2].map, c->brick_maps[1].map,
+                                      op, g, w, a, make_work(c));
+    prof_end(c, r);
+    c->acc.launches++;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    c->wrec_path = PHIPM_PATH_BRICK;
+    return true;
+}
+
 template <>
 bool launch_wrec_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, const WrecArgs &w, double bytes, int &rc)
 {
     if (!opt(c, PHIPM_OPT_WREC) || op.n <= SMALL_N || w.p < 1) return false;
+    if (try_wrec_brick(c, op, w, bytes, rc)) return true;
     constexpr int TILE_ = SNT * 4;
     int grid;
     int64_t rpc;
@@ -863,6 +933,7 @@ bool launch_wrec_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, const Wre
         cudaGetLastError();
         return false;
     }
+    c->wrec_path = PHIPM_PATH_PERSIST_SMEM;
     return true;
 }
 
@@ -1304,6 +1375,7 @@ int enqueue_wrec_op(phipm_ctx *c, const Op &op, double bytes_op, int p, const do
             bytes += bytes_op + 8.0 * (double)n * nz;
         }
         int rc = PHIPM_OK;
+        c->wrec_path = PHIPM_PATH_NONE;
         if (p <= WREC_MAXP && launch_wrec_persist(c, op, wa, bytes, rc)) return rc;
     }
     for (int j = 1; j <= p; j++) {
@@ -2539,6 +2611,11 @@ int phipm_krylov_path(const phipm_ctx *c)
     return c ? c->krylov_path : PHIPM_PATH_NONE;
 }
 
+int phipm_wrec_path(const phipm_ctx *c)
+{
+    return c ? c->wrec_path : PHIPM_PATH_NONE;
+}
+
 int phipm_get_clocks(const phipm_ctx *c, long long *out16)
 {
     if (!c || !out16) return PHIPM_EINVAL;
@@ -2687,6 +2764,7 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
             cudaFuncSetAttribute(persist_tm_fn(op), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         }
         cudaFuncSetAttribute(krylov_brick_tm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(wrec_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         for (int d = 1; d <= 4; d++) {
             StencilOp op{};
             op.dim = d == 4 ? 2 : d;

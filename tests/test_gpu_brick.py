@@ -71,7 +71,7 @@ def test_brick_solve_parity(bctx, orc, nx, ny, nz, t):
     wo, so, _ = orc.solve(Pb)
     assert so["status"] == 0
     w, s = bctx.solve_stencil(t, P.Stencil.of(st), [to_dev(x) for x in u], tol=tol, symmetric=True)
-    assert bctx.krylov_path() == "brick"
+    assert bctx.krylov_path() == "brick" and bctx.wrec_path() == "brick"
     assert s.t_reached == t
     assert s.m_peak > 10, s                         # relaunched with k0 > 0
     assert relerr(w.cpu().numpy(), wo) <= parity_bound(tol), (s, so)
@@ -87,6 +87,7 @@ def test_brick_agrees_with_tmem_kernel_on_c4():
         c = P.Context(n_max=Pb.n, m_max=100, p_max=4, options={"brick": flag})
         w, s = c.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), u, tol=Pb.tol, symmetric=True)
         assert c.krylov_path() == path
+        assert c.wrec_path() == ("brick" if flag else "persist_smem")
         out[flag] = (w.cpu().numpy(), s)
         c.close()
     assert relerr(out[1][0], out[0][0]) <= 1e-12
@@ -122,3 +123,55 @@ def test_brick_breakdown(bctx, orc):
     assert bctx.krylov_path() == "brick"
     assert bo and brk and kk == ko == 3
     assert np.abs(H.cpu().numpy()[:3, :3] - Ho[:3, :3]).max() <= 1e-9 * orc.inf_norm(csr)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_brick_wrec_all_terms_multistep(bctx, orc, p):
+    # w-recurrence on bricks (wrec_brick_kernel), t large enough for two steps: on the second, every u-term
+    # of Eq. (wrecurrence) has a nonzero coefficient t_k^l / l!, so pass j adds p - j + 1 vectors
+    st, u = aniso(64, 30, 26, seed=40 + p, p=p, cx=1.0, cy=0.6, cz=1.4)
+    t, tol = 6e-3, 1e-9
+    Pb = W.Problem(name="bw", n=st.n, p=p, t=t, tol=tol, symmetric=True, u=u, stencil=st, seed=0)
+    wo, so, _ = orc.solve(Pb)
+    assert so["status"] == 0
+    w, s = bctx.solve_stencil(t, P.Stencil.of(st), [to_dev(x) for x in u], tol=tol, symmetric=True)
+    assert bctx.wrec_path() == "brick"
+    assert s.t_reached == t and s.nsteps > 1, s
+    assert relerr(w.cpu().numpy(), wo) <= parity_bound(tol), (s, so)
+
+
+def test_brick_wrec_bitwise_equals_contiguous_kernel():
+    # one Arnoldi-free check of the w-recurrence alone: with m fixed the first Krylov seed is w_p / ||w_p||;
+    # beta = ||w_p|| of the brick kernel and of wrec_persist_kernel differ only in the order of one sum,
+    # and the normalised seed agrees to the last bits
+    import torch
+    st, u = aniso(64, 30, 26, seed=5, p=3)
+    ud = [to_dev(x) for x in u]
+    seeds = {}
+    for flag in (2, 0):
+        c = P.Context(n_max=st.n, m_max=30, p_max=3, options={"brick": flag, "cluster_lz": 0})
+        w, s = c.solve_stencil(1e-5, P.Stencil.of(st), ud, tol=1e-8, symmetric=True)
+        assert c.wrec_path() == ("brick" if flag else "persist_smem")
+        seeds[flag] = (w.clone(), c.attempts()[0]["beta"])
+        c.close()
+    assert seeds[2][1] == pytest.approx(seeds[0][1], rel=1e-14)
+    assert relerr(seeds[2][0].cpu().numpy(), seeds[0][0].cpu().numpy()) <= 1e-13
+    torch.cuda.synchronize()
+
+
+def test_brick_wrec_unaligned_u_falls_back(orc):
+    # an 8-byte aligned u_1: the brick w-recurrence reads u-terms with 16-byte loads, so the solve takes
+    # the contiguous-range kernel (scalar loads) and still meets the bar
+    import torch
+    st, u = aniso(64, 30, 26, seed=9, p=2)
+    t, tol = 1e-4, 1e-9
+    Pb = W.Problem(name="bu", n=st.n, p=2, t=t, tol=tol, symmetric=True, u=u, stencil=st, seed=0)
+    wo, so, _ = orc.solve(Pb)
+    big = torch.zeros(st.n + 1, dtype=torch.float64, device="cuda")
+    big[1:] = to_dev(u[1])
+    ud = [to_dev(u[0]), big[1:], to_dev(u[2])]
+    c = P.Context(n_max=st.n, m_max=60, p_max=2, options={"brick": 2, "cluster_lz": 0})
+    w, s = c.solve_stencil(t, P.Stencil.of(st), ud, tol=tol, symmetric=True)
+    assert c.wrec_path() == "persist_smem" and c.krylov_path() == "brick"
+    assert relerr(w.cpu().numpy(), wo) <= parity_bound(tol), (s, so)
+    c.close()

@@ -120,6 +120,9 @@ __device__ __forceinline__ double2 tm_ld4_wait(uint32_t (&r)[4])
     return make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
 }
 
+// RAGGED: nx is not a multiple of 64, so some lanes of a line's last segment hold no rows and their
+// contributions are masked (compile-time: the full-line instantiation carries no selects)
+template <bool RAGGED>
 __global__ void __launch_bounds__(SNT, 1)
 krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, BrickGeom g, PersistArgs a, Work wk)
 {
@@ -202,7 +205,6 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
     const uint32_t pb0 = smem_u32(&pbar[zb]);
     const int64_t row0 = xa + (int64_t)nx * (yy + (int64_t)ny * (z0 + zb));     // row of (xi, yy, z0 + zb)
     const int64_t pl = (int64_t)nx * ny;
-    const bool ragged = g.nseg * 64 != nx;                 // some lanes of the last segment hold no rows
     const double c0 = op.c[0], cxm = op.c[1], cxp = op.c[2], cym = op.c[3], cyp = op.c[4], czm = op.c[5],
                  czp = op.c[6];
     auto lds2 = [](uint32_t ad) {
@@ -295,7 +297,7 @@ krylov_brick_tm_kernel(const __grid_constant__ CUtensorMap tmap, StencilOp op, B
                 const double2 zq = tm_ld4_wait(zr);
                 double2 y = make_double2(fma(-lz, zq.x, sa * sj), fma(-lz, zq.y, sb * sj));
                 double2 xc = zc;
-                if (ragged && !act) {
+                if (RAGGED && !act) {
                     y = make_double2(0.0, 0.0);
                     xc = y;
                 }

@@ -784,8 +784,9 @@ bool try_persist_brick(phipm_ctx *c, const StencilOp &op, int k0, int k1, double
     if (!brick_tensor_map(c, 0, c->V, c->m_max + 1, c->ldv, op, g)) return false;
     const size_t smem = brick_smem_bytes(g);
     const int grid = g.py * g.pz;
+    const auto kfn = (g.nseg * 64 != op.nx) ? krylov_brick_tm_kernel<true> : krylov_brick_tm_kernel<false>;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, krylov_brick_tm_kernel, SNT, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, SNT, smem) != cudaSuccess ||
         occ < 1 || grid > occ * c->sm_count || grid > c->pstride) {
         cudaGetLastError();
         return false;
@@ -814,7 +815,7 @@ bool try_persist_brick(phipm_ctx *c, const StencilOp &op, int k0, int k1, double
     }
     ProfRec r;
     prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
-    const cudaError_t e = launch_coop(c, krylov_brick_tm_kernel, grid, SNT, smem, c->brick_maps[0].map, op, g, a, make_work(c));
+    const cudaError_t e = launch_coop(c, kfn, grid, SNT, smem, c->brick_maps[0].map, op, g, a, make_work(c));
     prof_end(c, r);
     c->acc.launches++;
     if (e != cudaSuccess) {
@@ -2763,7 +2764,8 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
             op.diag = d == 4;
             cudaFuncSetAttribute(persist_tm_fn(op), cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         }
-        cudaFuncSetAttribute(krylov_brick_tm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(krylov_brick_tm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(krylov_brick_tm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(wrec_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         for (int d = 1; d <= 4; d++) {
             StencilOp op{};

@@ -170,6 +170,15 @@ int phipm_krylov_path(const phipm_ctx *ctx);
  * launches, single-CTA kernels, or none yet). */
 int phipm_wrec_path(const phipm_ctx *ctx);
 
+/* Host logic of the brick kernels (no GPU needed): the decomposition of an nx x ny x nz grid into bricks of whole
+ * x-lines on at most `ctas` CTAs with `smem_bytes` of dynamic shared memory each (persist_brick.cuh:
+ * brick_geometry).  out10 (HOST) = {py, pz, ylen, zlen, nseg, ncol, ngrp, ppg, lstride, pstride}: py x pz
+ * bricks of ylen lines x zlen planes; a line is nseg 64-point warp segments; the CTA's 32 warps form ncol =
+ * nseg ylen columns x ngrp z groups of ppg <= 8 planes; shared line / plane strides in doubles.
+ * Returns PHIPM_OK, -1 if the grid has no such decomposition (odd nx, nx > 252, too many rows), or
+ * PHIPM_EINVAL. */
+int phipm_brick_plan(int nx, int ny, int nz, int ctas, int64_t smem_bytes, int *out10);
+
 void phipm_default_opts(phipm_opts *opts);
 
 /* Method used by the kernel-level entry points phipm_expm and phipm_phi_pair (solves take

@@ -18,7 +18,7 @@ from typing import Optional, Sequence, Tuple
 
 from .build import LIB, build  # noqa: F401
 
-__all__ = ["Context", "Stencil", "Stats", "Profile", "PhipmError", "lib", "LIB", "build"]
+__all__ = ["Context", "Stencil", "Stats", "Profile", "PhipmError", "lib", "LIB", "build", "brick_plan"]
 
 OK, EINVAL, ENOMEM, ECUDA, ESTEP, ENONFINITE, ESINGULAR = 0, 1, 2, 3, 4, 5, 6
 ORTH_CGS, ORTH_CGS2 = 0, 1
@@ -152,6 +152,7 @@ def lib():
             "phipm_get_clocks": (i32, [vp, P(C.c_longlong)]),
             "phipm_krylov_path": (i32, [vp]),
             "phipm_wrec_path": (i32, [vp]),
+            "phipm_brick_plan": (i32, [i32, i32, i32, i32, i64, P(i32)]),
             "phipm_set_option": (i32, [vp, i32, i32]),
             "phipm_get_option": (i32, [vp, i32, P(i32)]),
             "phipm_solve_csr": (i32, [vp, d, P(_Csr), i32, P(vp), P(_Opts), vp, P(_Stats)]),
@@ -186,7 +187,7 @@ def lib():
 
 EXPORTED = [
     "phipm_default_opts", "phipm_set_expm_method", "phipm_mm_read", "phipm_create", "phipm_destroy", "phipm_strerror", "phipm_last_error",
-    "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_get_attempts", "phipm_get_clocks", "phipm_krylov_path", "phipm_wrec_path", "phipm_set_option",
+    "phipm_get_profile", "phipm_reset_profile", "phipm_get_trace", "phipm_get_attempts", "phipm_get_clocks", "phipm_krylov_path", "phipm_wrec_path", "phipm_brick_plan", "phipm_set_option",
     "phipm_get_option", "phipm_solve_csr", "phipm_solve_stencil",
     "phipm_reserve_host_csr", "phipm_solve_csr_host", "phipm_solve_stencil_host", "phipm_solve_csr_batch",
     "phipm_solve_stencil_batch", "phipm_solve_csr_block", "phipm_stencil_nnz", "phipm_inf_norm_stencil",
@@ -484,6 +485,18 @@ class Context:
         if build_only:
             return None, None, k.value, bool(brk.value), beta.value
         return Vcm.t(), Hcm.t(), k.value, bool(brk.value), beta.value
+
+
+def brick_plan(nx: int, ny: int, nz: int, ctas: int = 148, smem_bytes: int = 222 * 1024):
+    """Brick decomposition of an nx x ny x nz grid (phipm_brick_plan; host logic, no GPU): dict with py, pz,
+    ylen, zlen, nseg, ncol, ngrp, ppg, lstride, pstride, or None if the grid has none."""
+    out = (C.c_int * 10)()
+    st = lib().phipm_brick_plan(nx, ny, nz, ctas, smem_bytes, out)
+    if st == -1:
+        return None
+    if st != OK:
+        raise PhipmError(st, "phipm_brick_plan: bad argument")
+    return dict(zip(("py", "pz", "ylen", "zlen", "nseg", "ncol", "ngrp", "ppg", "lstride", "pstride"), out))
 
 
 def solve_batch(ctxs: Sequence["Context"], t, ops, us: Sequence[Sequence], outs=None, **kw):

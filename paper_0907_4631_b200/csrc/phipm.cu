@@ -2612,6 +2612,16 @@ int phipm_krylov_path(const phipm_ctx *c)
     return c ? c->krylov_path : PHIPM_PATH_NONE;
 }
 
+int phipm_brick_plan(int nx, int ny, int nz, int ctas, int64_t smem_bytes, int *out10)
+{
+    if (!out10 || nx < 1 || ny < 1 || nz < 1 || ctas < 1 || smem_bytes < 0) return PHIPM_EINVAL;
+    BrickGeom g;
+    if (!brick_geometry(nx, ny, nz, ctas, (size_t)smem_bytes, g)) return -1;
+    const int v[10] = {g.py, g.pz, g.ylen, g.zlen, g.nseg, g.ncol, g.ngrp, g.ppg, g.lstride, g.pstride};
+    for (int i = 0; i < 10; i++) out10[i] = v[i];
+    return PHIPM_OK;
+}
+
 int phipm_wrec_path(const phipm_ctx *c)
 {
     return c ? c->wrec_path : PHIPM_PATH_NONE;

@@ -12,6 +12,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 200 python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline > $O/pf_plain_bench_c2.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/pf_launches_c2.csv \
   python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline > $O/pf_ncu_launch_c2.log 2>&1
+timeout 200 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > $O/pf_plain_bench_c4.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/pf_launches_c4.csv \
+  python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > $O/pf_ncu_launch_c4.log 2>&1
 for c in c2 c3 c4 c5; do
   timeout 300 python tools/one_solve.py --config $c --solves 2 --profile-last > $O/pf_plain_$c.log 2>&1 && \
   timeout 900 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
@@ -25,7 +28,9 @@ full() {  # config kernel-regex skip name [extra one_solve args]
 full c5 spmv_stream 6 c5_spmv
 full c5 axpy_stream 4 c5_axpy
 full c5 csr_analyze 0 c5_analyze
-full c4 krylov_persist_tm 0 c4_persist
+full c4 krylov_persist_tm 0 c4_persist "--option brick=0"
+full c4 krylov_brick 0 c4_brick
+full c4 wrec_brick 0 c4_wrec_brick
 full c1 phi_cheb 3 c1_cheb "--expm 2"
 full c2 krylov_cluster 0 c2_cluster
 full c2 expm_kernel 3 c2_expm

@@ -28,7 +28,7 @@ def read_ncu_csv(path):
 
 
 def short(k):
-    for key in ("krylov_cluster_lanczos_kernel", "spmv_stream_kernel", "axpy_stream_kernel", "expm_kernel",
+    for key in ("krylov_brick_tm_kernel", "wrec_brick_kernel", "krylov_cluster_lanczos_kernel", "spmv_stream_kernel", "axpy_stream_kernel", "expm_kernel",
                 "maxabs_kernel", "csr_analyze_kernel", "spmv_small_kernel", "axpy_small_kernel",
                 "krylov_small_lanczos_kernel", "krylov_small_kernel", "krylov_persist_tm_kernel",
               "krylov_persist_kernel", "wrec_persist_kernel", "phi_cheb_kernel", "spmm_csr_ring_kernel",
@@ -91,7 +91,8 @@ for cfg in ("c2", "c3", "c4", "c5"):
     # single-CTA), so the per-launch average matches bench.py's algorithmic_bytes_per_launch
     sp = [b for k in cls if k.startswith(("spmv_stream_kernel", "krylov_persist_kernel", "krylov_persist_tm_kernel",
                                                    "krylov_small_kernel", "krylov_small_lanczos_kernel",
-                                                   "wrec_persist_kernel", "krylov_cluster_lanczos_kernel"))
+                                                   "wrec_persist_kernel", "krylov_cluster_lanczos_kernel", "krylov_brick_tm_kernel",
+                                                   "wrec_brick_kernel"))
           for b, _ in cls[k]]
     if sp:
         traffic[cfg] = {"kernel_class": "spmv_dot", "dram_bytes_per_launch": sum(sp) / len(sp),
@@ -103,7 +104,7 @@ if traffic:
 # 3) --set full summaries of the top kernels
 for name in ("pf_full_c3_spmv", "pf_full_c3_axpy", "pf_full_c4_persist", "pf_full_c5_spmv",
              "pf_full_c3_expm", "pf_full_c1_small", "pf_full_c5_axpy", "pf_full_c5_analyze", "pf_full_c1_cheb",
-             "pf_full_c2_cluster", "pf_full_c2_expm"):
+             "pf_full_c2_cluster", "pf_full_c2_expm", "pf_full_c4_brick", "pf_full_c4_wrec_brick"):
     p = os.path.join(src, name + ".ncu-rep")
     if os.path.exists(p):
         with open(os.path.join(dst, name.replace("pf_", "") + ".txt"), "w") as f:

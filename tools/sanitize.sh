@@ -11,7 +11,8 @@ CASES=(
   "c2_med||persistent Lanczos (smem) + cooperative w-recurrence"
   "c3_med|--option persist=0|streaming TMA-halo SpMV + axpy (two-kernel Arnoldi, lagged)"
   "c3_med||persistent Arnoldi"
-  "c4_tm||TMEM persistent Lanczos + cooperative w-recurrence"
+  "c4_tm|--option brick=0|TMEM persistent Lanczos + cooperative w-recurrence"
+  "c4_tm|--option brick=2|brick Lanczos + brick w-recurrence (tensor-map TMA, TMEM; ragged x segments)"
   "c5_med||CSR ELL x-ring SpMV + CSR analysis"
 )
 for tool in memcheck racecheck synccheck; do

@@ -640,11 +640,13 @@ __global__ void __launch_bounds__(256) csr_analyze_ell_kernel(int64_t n, const i
     // col, four int4 groups per thread per iteration
     const int4 *c4 = reinterpret_cast<const int4 *>(col);
     const int64_t ng = nnz >> 2;
+    // the four entries of a group share their row and clamp_band is monotone: the group's band is that of its
+    // smallest and largest column (6 integer min / max and two clamps instead of eight 64-bit differences)
     auto band = [&](const int4 &v, int64_t g) {
         const int64_t row = (g << 2) >> lgL;
-        const int64_t d0 = (int64_t)v.x - row, d1 = (int64_t)v.y - row, d2 = (int64_t)v.z - row, d3 = (int64_t)v.w - row;
-        blo = max(blo, max(max(clamp_band(-d0), clamp_band(-d1)), max(clamp_band(-d2), clamp_band(-d3))));
-        bhi = max(bhi, max(max(clamp_band(d0), clamp_band(d1)), max(clamp_band(d2), clamp_band(d3))));
+        const int cmin = min(min(v.x, v.y), min(v.z, v.w)), cmax = max(max(v.x, v.y), max(v.z, v.w));
+        blo = max(blo, clamp_band(row - (int64_t)cmin));
+        bhi = max(bhi, clamp_band((int64_t)cmax - row));
     };
     int64_t g = tid;
     for (; g + 3 * nth < ng; g += 4 * nth) {

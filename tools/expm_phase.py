@@ -12,7 +12,7 @@ import paper_0907_4631_b200 as P  # noqa: E402
 ctx = P.Context(n_max=1024, m_max=100, p_max=5)
 L = P.lib()
 rng = np.random.default_rng(0)
-for mu, sc in ((38, 50.0), (47, 380.0), (40, 5.0)):
+for mu, sc in ((38, 50.0), (47, 380.0), (40, 5.0), (10, 2.0), (20, 20.0)):
     d = -2.0 - rng.uniform(0, 0.2, mu)
     e = 1.0 + rng.uniform(0, 0.1, mu - 1)
     T = np.diag(d) + np.diag(e, 1) + np.diag(e, -1)

@@ -40,7 +40,7 @@ torch.cuda.synchronize()
 ctx.close()
 os.environ["PHIPM_KCLOCKS"] = path
 ctx = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1))
-solve(ctx)
+print("stamped solve:", solve(ctx)[1])
 torch.cuda.synchronize()
 ctx.close()
 del os.environ["PHIPM_KCLOCKS"]

@@ -236,6 +236,11 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *                              warps; y / v~ in tensor memory): 0 off, 1 auto (default: n >= 303K and
  *                              x-lines that fill >= 3/4 of their 64-point warp segments), 2 whenever a
  *                              brick decomposition of the grid exists (nx even, <= 252)
+ *   PHIPM_OPT_BRICK_HALO       1: the brick Lanczos kernel keeps the brick's interior in shared memory from step
+ *                              to step, copies only the halo (two planes, two lines per plane) and writes
+ *                              v~_{j+1} to global memory with tensor stores (shared -> global, one per plane);
+ *                              0 (default, measured faster: c4 3500 vs 3320 solves/s): every plane of the brick
+ *                              is staged through the tensor map each step and the threads store v~_{j+1}
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -259,7 +264,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_GRAPH           19
 #define PHIPM_OPT_DEFER           20
 #define PHIPM_OPT_BRICK           21
-#define PHIPM_OPT_COUNT           22
+#define PHIPM_OPT_BRICK_HALO      22
+#define PHIPM_OPT_COUNT           23
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

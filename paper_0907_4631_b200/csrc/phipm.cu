@@ -67,7 +67,7 @@ struct GraphRec {
 struct BrickMap {
     CUtensorMap map;
     const double *base = nullptr;           // nullptr: none
-    int nx = 0, ny = 0, nz = 0, ylen = 0;
+    int nx = 0, ny = 0, nz = 0, ylen = 0, zlen = 0, xlen = 0;    // grid and box (lines, planes, points)
 };
 
 struct phipm_ctx {
@@ -142,9 +142,9 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1, 0};
     // brick kernels: tensor maps of V, W and the w-recurrence's x_0 for the last grid / brick shape
-    BrickMap brick_maps[3];
+    BrickMap brick_maps[5];                 // V planes, W planes, x_0 planes, V z-halo planes, V y-halo lines
     int krylov_path = PHIPM_PATH_NONE;      // kernel path of the last Krylov extension (phipm_krylov_path)
     int wrec_path = PHIPM_PATH_NONE;        // ... of the last w-recurrence (phipm_wrec_path)
     char err[512] = {0};
@@ -738,15 +738,19 @@ TmapEncodeFn tmap_encode_fn()
 // plane of a brick with its halo: (nx + 4) x (ylen + 2) x 1 x 1, zero fill outside the grid.  Cached per
 // context slot (0: the basis V, 1: the w-recurrence vectors W, 2: x_0 of the w-recurrence)
 bool brick_tensor_map(phipm_ctx *c, int slot, const double *base, int ncols, int64_t ld, const StencilOp &op,
-                      const BrickGeom &g)
+                      const BrickGeom &g, int box_y = 0, int box_z = 1, int box_x = 0)
 {
+    if (box_y == 0) box_y = g.ylen + 2;                    // (default: a whole plane with its y halo ...
+    if (box_x == 0) box_x = op.nx + 4;                     // ... and two zero-filled points left and right)
     BrickMap &m = c->brick_maps[slot];
-    if (m.base == base && m.nx == op.nx && m.ny == op.ny && m.nz == op.nz && m.ylen == g.ylen) return true;
+    if (m.base == base && m.nx == op.nx && m.ny == op.ny && m.nz == op.nz && m.ylen == box_y && m.zlen == box_z &&
+        m.xlen == box_x)
+        return true;
     const TmapEncodeFn enc = tmap_encode_fn();
     if (!enc || ((uintptr_t)base & 15) || (ld & 1)) return false;
     const cuuint64_t gdim[4] = {(cuuint64_t)op.nx, (cuuint64_t)op.ny, (cuuint64_t)op.nz, (cuuint64_t)ncols};
     const cuuint64_t gstr[3] = {(cuuint64_t)op.nx * 8, (cuuint64_t)op.nx * op.ny * 8, (cuuint64_t)ld * 8};
-    const cuuint32_t box[4] = {(cuuint32_t)(op.nx + 4), (cuuint32_t)(g.ylen + 2), 1, 1};
+    const cuuint32_t box[4] = {(cuuint32_t)box_x, (cuuint32_t)box_y, (cuuint32_t)box_z, 1};
     const cuuint32_t est[4] = {1, 1, 1, 1};
     const CUresult r = enc(&m.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(base), gdim, gstr, box, est,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -759,7 +763,9 @@ bool brick_tensor_map(phipm_ctx *c, int slot, const double *base, int ncols, int
     m.nx = op.nx;
     m.ny = op.ny;
     m.nz = op.nz;
-    m.ylen = g.ylen;
+    m.ylen = box_y;
+    m.zlen = box_z;
+    m.xlen = box_x;
     return true;
 }
 
@@ -781,12 +787,22 @@ bool try_persist_brick(phipm_ctx *c, const StencilOp &op, int k0, int k1, double
 {
     BrickGeom g;
     if (!brick_plan(c, op, g)) return false;
-    if (!brick_tensor_map(c, 0, c->V, c->m_max + 1, c->ldv, op, g)) return false;
-    const size_t smem = brick_smem_bytes(g);
+    const bool halo = opt(c, PHIPM_OPT_BRICK_HALO) != 0;   // interior resident in shared memory, halo copies only
+    const bool ragged = g.nseg * 64 != op.nx;
+    if (halo) {
+        if (!brick_tensor_map(c, 3, c->V, c->m_max + 1, c->ldv, op, g, g.ylen, 1, op.nx) ||
+            !brick_tensor_map(c, 4, c->V, c->m_max + 1, c->ldv, op, g, 1, g.zlen, op.nx))
+            return false;
+    } else if (!brick_tensor_map(c, 0, c->V, c->m_max + 1, c->ldv, op, g)) {
+        return false;
+    }
+    const size_t smem = halo ? brick_halo_smem_bytes(g) : brick_smem_bytes(g);
     const int grid = g.py * g.pz;
-    const auto kfn = (g.nseg * 64 != op.nx) ? krylov_brick_tm_kernel<true> : krylov_brick_tm_kernel<false>;
+    const auto kfn = ragged ? krylov_brick_tm_kernel<true> : krylov_brick_tm_kernel<false>;
+    const auto hfn = ragged ? krylov_brick_halo_kernel<true> : krylov_brick_halo_kernel<false>;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, SNT, smem) != cudaSuccess ||
+    if ((halo ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, hfn, SNT, smem)
+              : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, SNT, smem)) != cudaSuccess ||
         occ < 1 || grid > occ * c->sm_count || grid > c->pstride) {
         cudaGetLastError();
         return false;
@@ -815,7 +831,9 @@ bool try_persist_brick(phipm_ctx *c, const StencilOp &op, int k0, int k1, double
     }
     ProfRec r;
     prof_begin(c, r, PC_SPMV, bytes, k1 - k0);
-    const cudaError_t e = launch_coop(c, kfn, grid, SNT, smem, c->brick_maps[0].map, op, g, a, make_work(c));
+    const cudaError_t e =
+        halo ? launch_coop(c, hfn, grid, SNT, smem, c->brick_maps[3].map, c->brick_maps[4].map, op, g, a, make_work(c))
+             : launch_coop(c, kfn, grid, SNT, smem, c->brick_maps[0].map, op, g, a, make_work(c));
     prof_end(c, r);
     c->acc.launches++;
     if (e != cudaSuccess) {
@@ -2776,6 +2794,8 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
         }
         cudaFuncSetAttribute(krylov_brick_tm_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(krylov_brick_tm_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(krylov_brick_halo_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(krylov_brick_halo_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         cudaFuncSetAttribute(wrec_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
         for (int d = 1; d <= 4; d++) {
             StencilOp op{};

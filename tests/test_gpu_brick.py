@@ -31,9 +31,12 @@ def aniso(nx, ny, nz, seed, p=2, cx=1.0, cy=1.0, cz=1.0):
     return W.Stencil(3, nx, ny, nz, coef), u
 
 
-@pytest.fixture()
-def bctx():
-    c = P.Context(n_max=1_400_000, m_max=100, p_max=4, options={"brick": 2, "cluster_lz": 0})
+@pytest.fixture(params=[1, 0], ids=["halo", "planes"])
+def bctx(request):
+    # brick_halo = 1: krylov_brick_halo_kernel (interior resident in shared memory, halo copies only, tensor
+    # stores); 0 (default): krylov_brick_tm_kernel (every plane staged each step)
+    c = P.Context(n_max=1_400_000, m_max=100, p_max=4,
+                  options={"brick": 2, "cluster_lz": 0, "brick_halo": request.param})
     yield c
     c.close()
 
@@ -83,15 +86,17 @@ def test_brick_agrees_with_tmem_kernel_on_c4():
     Pb = W.make("c4")
     u = [to_dev(x) for x in Pb.u]
     out = {}
-    for flag, path in ((1, "brick"), (0, "persist_tmem")):
-        c = P.Context(n_max=Pb.n, m_max=100, p_max=4, options={"brick": flag})
+    for flag, halo, path in ((1, 1, "brick"), (1, 0, "brick"), (0, 0, "persist_tmem")):
+        c = P.Context(n_max=Pb.n, m_max=100, p_max=4, options={"brick": flag, "brick_halo": halo})
         w, s = c.solve_stencil(Pb.t, P.Stencil.of(Pb.stencil), u, tol=Pb.tol, symmetric=True)
         assert c.krylov_path() == path
         assert c.wrec_path() == ("brick" if flag else "persist_smem")
-        out[flag] = (w.cpu().numpy(), s)
+        out[flag, halo] = (w.cpu().numpy(), s)
         c.close()
-    assert relerr(out[1][0], out[0][0]) <= 1e-12
-    assert out[1][1].nspmv == out[0][1].nspmv and out[1][1].nsteps == out[0][1].nsteps
+    # the two brick kernels run the same arithmetic in the same order: bit-identical w
+    assert np.array_equal(out[1, 1][0], out[1, 0][0])
+    assert relerr(out[1, 1][0], out[0, 0][0]) <= 1e-12
+    assert out[1, 1][1].nspmv == out[0, 0][1].nspmv and out[1, 1][1].nsteps == out[0, 0][1].nsteps
 
 
 def test_brick_auto_skips_sparse_segments():

@@ -241,6 +241,10 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *                              v~_{j+1} to global memory with tensor stores (shared -> global, one per plane);
  *                              0 (default, measured faster: c4 3500 vs 3320 solves/s): every plane of the brick
  *                              is staged through the tensor map each step and the threads store v~_{j+1}
+ *   PHIPM_OPT_SIDE_MAXABS      1 (default): ||u_0||_inf of a solve (Eq. tau_0's b_inf, a1 setup) is reduced on the
+ *                              context's second stream with its own scratch, concurrently with the first
+ *                              w-recurrence and Krylov extension, which do not depend on it; 0: on the solve's
+ *                              stream ahead of them
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -265,7 +269,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_DEFER           20
 #define PHIPM_OPT_BRICK           21
 #define PHIPM_OPT_BRICK_HALO      22
-#define PHIPM_OPT_COUNT           23
+#define PHIPM_OPT_SIDE_MAXABS     23
+#define PHIPM_OPT_COUNT           24
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

@@ -88,7 +88,12 @@ struct phipm_ctx {
     unsigned *counter = nullptr;
     bool coop_dirty = false;                         // a cooperative kernel timed out: reset its counters
     cudaEvent_t ev_binf = nullptr;                   // ||u_0||_inf readback of a solve
-    cudaStream_t stream2 = nullptr;                  // speculative Krylov extensions (PHIPM_OPT_SPEC)
+    cudaStream_t stream2 = nullptr;                  // speculative Krylov extensions (PHIPM_OPT_SPEC); ||u_0||_inf
+    // ||u_0||_inf of a solve on stream2 (PHIPM_OPT_SIDE_MAXABS): its own reduction scratch, because the
+    // kernels of the main stream use part / counter / raw at the same time
+    double *part_mx = nullptr, *raw_mx = nullptr;
+    unsigned *counter_mx = nullptr;
+    bool mx_side_pending = false;                    // the side-stream reduction has not been read yet
     cudaEvent_t ev_main = nullptr, ev_spec = nullptr;
     bool spec_pending = false;                       // an extension on stream2 not yet joined to stream
     // device-driven solves of small problems (solve_small.cuh)
@@ -142,7 +147,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1, 0};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1, 0, 1};
     // brick kernels: tensor maps of V, W and the w-recurrence's x_0 for the last grid / brick shape
     BrickMap brick_maps[5];                 // V planes, W planes, x_0 planes, V z-halo planes, V y-halo lines
     int krylov_path = PHIPM_PATH_NONE;      // kernel path of the last Krylov extension (phipm_krylov_path)
@@ -1333,7 +1338,7 @@ int enqueue_krylov_stream(phipm_ctx *c, const Op &op, double bytes_op, bool symm
 
 // ||u_k||_inf of u[k0..k1).  publish = true: the result goes to mapped pinned memory with a sequence
 // number the host spins on (no copy node in the stream); otherwise it is copied to raw_h
-int enqueue_maxabs_u(phipm_ctx *c, int64_t n, const double *const *u, int k0, int k1, bool publish)
+int enqueue_maxabs_u(phipm_ctx *c, int64_t n, const double *const *u, int k0, int k1, bool publish, bool side = false)
 {
     MaxAbsArgs ma;
     memset(&ma, 0, sizeof(ma));
@@ -1345,7 +1350,14 @@ int enqueue_maxabs_u(phipm_ctx *c, int64_t n, const double *const *u, int k0, in
         ma.seq = ++c->mx_seq;
     }
     const int grid = grid_for(c, (n + NT - 1) / NT, c->occ_axpy);
-    maxabs_kernel<<<grid, NT, 0, c->stream>>>(n, ma, make_work(c));
+    Work wk = make_work(c);
+    if (side) {
+        // one vector, published: on stream2 with private scratch, concurrent with the main stream's kernels
+        wk.part = c->part_mx;
+        wk.counter = c->counter_mx;
+        wk.out_raw = c->raw_mx;
+    }
+    maxabs_kernel<<<grid, NT, 0, side ? c->stream2 : c->stream>>>(n, ma, wk);
     c->acc.launches++;
     CK(cudaGetLastError());
     if (!publish)
@@ -1549,6 +1561,10 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     };
     auto finish = [&](int rc) {
         join_spec();
+        if (c->mx_side_pending) {                      // an error return before ||u_0||_inf was read
+            cudaStreamSynchronize(c->stream2);
+            c->mx_side_pending = false;
+        }
         if (stats) *stats = S;
         return rc;
     };
@@ -1584,7 +1600,13 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     // Krylov extension -- which do not depend on it: tau enters only the exponential -- are
     // enqueued before the host waits for it.  The other u_k are only read when u_0 = 0.
     const bool spin_binf = !c->prof;                 // profiling collects events at a stream sync instead
-    {
+    // PHIPM_OPT_SIDE_MAXABS: nothing on the GPU waits for ||u_0||_inf, so its reduction runs on stream2 (ordered
+    // after the caller's inputs by an event) and is enqueued AFTER the w-recurrence and the first extension:
+    // those start at once and the reduction fills the SMs / thread slots they leave free
+    const bool side_mx = spin_binf && c->stream2 && opt(c, PHIPM_OPT_SIDE_MAXABS);
+    if (side_mx) {
+        CK(cudaEventRecord(c->ev_main, c->stream));
+    } else {
         int rc = enqueue_maxabs(0, 1, spin_binf);
         if (rc) return finish(rc);
         if (!spin_binf) CK(cudaEventRecord(c->ev_binf, c->stream));
@@ -1608,6 +1630,12 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             enq = m;
         }
     }
+    if (side_mx) {
+        CK(cudaStreamWaitEvent(c->stream2, c->ev_main, 0));
+        int rc = enqueue_maxabs_u(c, n, u, 0, 1, true, true);
+        if (rc) return finish(rc);
+        c->mx_side_pending = true;
+    }
     double b_inf;
     if (spin_binf) {
         // spin on the published sequence number (fallback: stream sync after 2 s, e.g. on a fault)
@@ -1619,6 +1647,8 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             if ((++spins & 1023) == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::seconds(2)) {
                 int rc = sync(c);
                 if (rc) return finish(rc);
+                if (side_mx && cudaStreamSynchronize(c->stream2) != cudaSuccess)
+                    return finish(set_err(c, PHIPM_ECUDA, "||u_0|| reduction failed"));
                 synced = true;
                 if (*seqp != c->mx_seq) return finish(set_err(c, PHIPM_ECUDA, "||u_0|| result not published"));
             }
@@ -1626,6 +1656,7 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         (void)synced;
         std::atomic_thread_fence(std::memory_order_acquire);
         b_inf = ((const volatile double *)c->mx_h->v)[0];
+        c->mx_side_pending = false;                    // (published: the side-stream kernel has read u_0)
     } else {
         CK(cudaEventSynchronize(c->ev_binf));
         b_inf = c->raw_h[0];
@@ -2687,6 +2718,7 @@ void phipm_destroy(phipm_ctx *c)
     if (c->ss_out_h) cudaFreeHost(c->ss_out_h);
     if (c->ev_spec) cudaEventDestroy(c->ev_spec);
     cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
+    cudaFree(c->part_mx); cudaFree(c->raw_mx); cudaFree(c->counter_mx);
     cudaFree(c->part); cudaFree(c->part2); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
     cudaFree(c->counter); cudaFree(c->st); cudaFree(c->tlo); cudaFree(c->thi); cudaFree(c->off16);
     cudaFree(c->hu); cudaFree(c->hw); cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
@@ -2841,6 +2873,9 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     A((void **)&c->g, sizeof(double) * (MAXD + 1));
     A((void **)&c->part, sizeof(double) * (size_t)c->pstride * (MAXD + 2));
     A((void **)&c->part2, sizeof(double) * (size_t)c->pstride * (MAXD + 2));
+    A((void **)&c->part_mx, sizeof(double) * (size_t)c->pstride * 2);
+    A((void **)&c->raw_mx, sizeof(double) * 2);
+    A((void **)&c->counter_mx, sizeof(unsigned) * 8);
     A((void **)&c->comb, sizeof(double) * (MAXD + 1));
     A((void **)&c->combd, sizeof(double) * (P_MAX_ABS + 1));
     {

@@ -245,6 +245,11 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *                              context's second stream with its own scratch, concurrently with the first
  *                              w-recurrence and Krylov extension, which do not depend on it; 0: on the solve's
  *                              stream ahead of them
+ *   PHIPM_OPT_PRECOMBINE       1 (default; n > 8192, not with the Chebyshev method or opts.profile): the
+ *                              exponential's epilogue evaluates Algorithm 3's acceptance test (omega <= 1.2, the
+ *                              host's expression) and the step's combine kernel is enqueued behind it before
+ *                              the host has seen the result, guarded by that decision: no host round trip
+ *                              between the two on an accepted step; 0: the host launches the combine
  * phipm_set_option returns PHIPM_EINVAL for an unknown option or an out-of-range value. */
 #define PHIPM_OPT_PERSIST          0
 #define PHIPM_OPT_TMEM             1
@@ -270,7 +275,8 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
 #define PHIPM_OPT_BRICK           21
 #define PHIPM_OPT_BRICK_HALO      22
 #define PHIPM_OPT_SIDE_MAXABS     23
-#define PHIPM_OPT_COUNT           24
+#define PHIPM_OPT_PRECOMBINE      24
+#define PHIPM_OPT_COUNT           25
 int phipm_set_option(phipm_ctx *ctx, int option, int value);
 int phipm_get_option(const phipm_ctx *ctx, int option, int *value);
 

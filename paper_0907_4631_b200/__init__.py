@@ -70,7 +70,7 @@ KRYLOV_PATHS = ["none", "two_kernel", "single_cta", "cluster", "persist_smem", "
 OPTIONS = {"persist": 0, "tmem": 1, "wrec": 2, "lag": 3, "pdl": 4, "spin": 5, "rpt": 6, "csr_ell": 7,
            "csr_ring": 8, "csr_window": 9, "small_lz": 10, "persist_minrows": 11, "csr_prefetch": 12,
            "col_prefetch": 13, "fuse_anorm": 14,
-           "csr_off16": 15, "cluster_lz": 16, "spec": 17, "devsolve": 18, "graph": 19, "defer": 20, "brick": 21, "brick_halo": 22, "side_maxabs": 23}
+           "csr_off16": 15, "cluster_lz": 16, "spec": 17, "devsolve": 18, "graph": 19, "defer": 20, "brick": 21, "brick_halo": 22, "side_maxabs": 23, "precombine": 24}
 
 
 class _Profile(C.Structure):

@@ -29,6 +29,8 @@ struct AttemptResult {
     int status;        // 0 ok, 5 non-finite, 6 singular, 7 Chebyshev interval too wide
     int seq;           // attempt sequence number (host sanity check)
     double eps_noise;  // Chebyshev method: rounding-noise bound of eps (0 for the augmented exponential)
+    int accepted;      // ExpmArgs.dec given: the acceptance decision taken on the device (1 / 0), else -1
+    int pad_;
 };
 
 // Publish an attempt result to the host (mapped pinned memory), one thread: the fields with
@@ -63,6 +65,11 @@ struct ExpmArgs {
     AttemptResult *res;
     int seq;
     long long *clk;    // optional phase timestamps (PHIPM_EXPM_CLOCKS)
+    // mode 0, optional: the acceptance test of Algorithm 3 on the device, omega = t_end eps / (tau tol) <= 1.2
+    // (the host's expression with the same IEEE operations), for a combine kernel enqueued before the host has
+    // seen the result: dec[0] = seq if accepted else -seq, dec[1] = number of basis columns of the combine
+    int *dec;
+    double t_end, tol;
 };
 
 // leading dimension of the K x K work matrices: Kp rounded up to 4 (mod 16) doubles, so the
@@ -551,6 +558,8 @@ __device__ __forceinline__ void expm_body(const ExpmArgs &a, double *esm)
             AttemptResult r{};
             r.eps = 0.0; r.normH1 = 0.0; r.beta = beta; r.h = 0.0; r.mu = 0;
             r.brk = s_brk; r.status = a.st->nonfinite ? 5 : 0;
+            r.accepted = -1;                         // no device decision: the host decides and launches
+            if (a.dec) a.dec[0] = -a.seq;
             publish_result(a.res, r, a.seq);
         }
         return;
@@ -668,6 +677,14 @@ __device__ __forceinline__ void expm_body(const ExpmArgs &a, double *esm)
         r.mu = mu;
         r.brk = brk;
         r.status = a.st->aborted ? 3 : status ? status : ((s_fin && isfinite(eps) && isfinite(phl)) ? 0 : 5);
+        r.accepted = -1;
+        if (a.dec) {
+            const double omega = __ddiv_rn(__dmul_rn(a.t_end, eps), __dmul_rn(a.tau, a.tol));
+            const int acc = (r.status == 0 && omega - omega == 0.0 && omega <= 1.2) ? 1 : 0;
+            a.dec[1] = mu + ((corr && h != 0.0) ? 1 : 0);       // (the host's rule for the corrector column)
+            a.dec[0] = acc ? a.seq : -a.seq;
+            r.accepted = acc;
+        }
         // published before the kernel retires: the host can act on it right away
         publish_result(a.res, r, a.seq);
         if (a.clk) a.clk[6] = clock64();                 // (after the copy above: epilogue end)

@@ -160,6 +160,10 @@ struct AxpyArgs {
     // FIN_LANCZOS or FIN_ARNOLDI_LAG; 0 = none), grid size, dot count, value count, step and threshold
     int dfin, dnb, dnd, dnv, dj;
     double dbthr;
+    // guarded launch (a combine enqueued before the host has seen the attempt's result): the kernel runs only
+    // if guard[0] == guard_val (written by the exponential's epilogue) and takes nc from guard[1]
+    const int *guard;
+    int guard_val;
 };
 
 // ------------------------------------------------------------------------------------------

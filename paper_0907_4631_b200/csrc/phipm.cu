@@ -94,6 +94,7 @@ struct phipm_ctx {
     double *part_mx = nullptr, *raw_mx = nullptr;
     unsigned *counter_mx = nullptr;
     bool mx_side_pending = false;                    // the side-stream reduction has not been read yet
+    int *dec_d = nullptr;                            // device acceptance decision of an attempt (PHIPM_OPT_PRECOMBINE)
     cudaEvent_t ev_main = nullptr, ev_spec = nullptr;
     bool spec_pending = false;                       // an extension on stream2 not yet joined to stream
     // device-driven solves of small problems (solve_small.cuh)
@@ -147,7 +148,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1, 0, 1};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1, 0, 1, 1};
     // brick kernels: tensor maps of V, W and the w-recurrence's x_0 for the last grid / brick shape
     BrickMap brick_maps[5];                 // V planes, W planes, x_0 planes, V z-halo planes, V y-halo lines
     int krylov_path = PHIPM_PATH_NONE;      // kernel path of the last Krylov extension (phipm_krylov_path)
@@ -1619,7 +1620,6 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     const bool direct = (n % 2 == 0) && ((reinterpret_cast<uintptr_t>(u[0]) & 15) == 0);
     const double *x0 = direct ? u[0] : ucur;
     if (!direct) CK(cudaMemcpyAsync(ucur, u[0], n * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    bool step0 = true;                // the current step is the first (its u_k is x0)
     int enq = 0;                      // Krylov columns already enqueued for the current step
     {
         int rc = enqueue_wrec(0.0, x0, direct ? n : 0);
@@ -1704,6 +1704,33 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
     double tk = 0.0;
     S.m_peak = m;
     bool first = true;
+    bool step0 = true;                // the current step is the first (its u_k is x0)
+    bool combined = false;            // the accepted attempt's guarded combine has already run
+    const bool pre_ok = opt(c, PHIPM_OPT_PRECOMBINE) && !c->prof && n > SMALL_N;
+    // Eq. (step): u_{k+1} = sum_{i<=mu} comb_i v~_i + sum_{j<p} tau^j/j! w_j  (w_0 = u_k in place); guard:
+    // device decision words (run only if guard[0] == guard_val, nc from guard[1])
+    auto enqueue_combine = [&](bool last, int nc, const int *guard, int guard_val) {
+        AxpyArgs a = axpy0();
+        a.out = last ? w : ucur;           // the last step writes the caller's w directly
+        a.base = step0 ? x0 : ucur;
+        a.a0h = (p >= 1) ? 1.0 : 0.0;
+        a.a0d = (p >= 1) ? c->combd : nullptr;
+        a.V = c->V;
+        a.ldv = c->ldv;
+        a.c0 = 0;
+        a.nc = nc;
+        a.g = c->comb;
+        a.gsign = 1.0;
+        a.ne = std::max(p - 1, 0);
+        for (int j = 1; j < p; j++) {
+            a.e[j - 1] = c->W + (int64_t)j * c->ldv;
+            a.ec[j - 1] = 1.0;
+        }
+        a.ecd = c->combd + 1;
+        a.guard = guard;
+        a.guard_val = guard_val;
+        return launch_axpy(c, n, a, PC_COMBINE);
+    };
     const bool spec_ok = spec_path(c, op, P.symmetric) && !P.fixed_m;
     int spec_from = 0;                 // first column of the pending speculative extension
     bool cheb_off = false;             // the Chebyshev method was found unreliable in this solve
@@ -1772,13 +1799,28 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             ea.st = c->st;
             ea.comb = c->comb;
             ea.combd = c->combd;
+            // PHIPM_OPT_PRECOMBINE: the exponential's epilogue takes the acceptance decision itself and the
+            // combine of this attempt is enqueued behind it right away, guarded by that decision; an accepted
+            // step then needs no host round trip between the two kernels, and after a rejection the guarded
+            // kernel exits at once while the host is still deciding
+            const bool precomb = pre_ok && ea.method != PHIPM_EXPM_CHEBYSHEV;
+            if (precomb) {
+                ea.dec = c->dec_d;
+                ea.t_end = t_end;
+                ea.tol = o.tol;
+            }
             int rc = launch_expm(c, ea, m + p + 1);
             if (rc) return finish(rc);
+            if (precomb) {
+                rc = enqueue_combine(tau >= t_end - tk, 0, c->dec_d, c->seq);
+                if (rc) return finish(rc);
+            }
             rc = wait_attempt(c);
             if (rc) return finish(rc);
             AttemptResult R;
             memcpy(&R, (const void *)c->res_h, sizeof(R));
             if (R.seq != c->seq) return finish(set_err(c, PHIPM_ECUDA, "stale attempt result"));
+            combined = false;
             // Chebyshev method: if the interval is too wide (status 7), or if the rounding-noise bound of
             // the error estimate exceeds 1e-2 max(omega, delta) (the last component is then a
             // cancellation of large Chebyshev terms, interval wider than ~mu, and an accept could rest
@@ -1817,7 +1859,10 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
             const double eps = R.eps;
             const double omega = t_end * eps / (tau * o.tol);
             if (!std::isfinite(omega)) return finish(set_err(c, PHIPM_ENONFINITE, "non-finite error estimate"));
-            const bool accepted = omega <= 1.2;
+            // (with a guarded combine in flight the device's decision is the decision: it is the same IEEE
+            // expression, and the combine has acted on it)
+            const bool accepted = (precomb && R.accepted >= 0) ? R.accepted != 0 : omega <= 1.2;
+            combined = precomb && R.accepted >= 0 && accepted;
             Decision d = control(P, mem, tau, m, eps, omega, R.normH1, t_end - tk, accepted);
             if (c->attempts.size() < 65536)
                 c->attempts.push_back({tk, tau, omega, eps, R.normH1, R.beta, m, mu, accepted ? 1 : 0, d.branch});
@@ -1838,25 +1883,8 @@ int solve_impl(phipm_ctx *c, double t_end, const Op &op, double bytes_op, int64_
         }
         // Eq. (step): u_{k+1} = sum_{i<=mu} comb_i v~_i + sum_{j<p} tau^j/j! w_j  (w_0 = u_k in place)
         const bool last = tau_used >= t_end - tk;
-        {
-            AxpyArgs a = axpy0();
-            a.out = last ? w : ucur;           // the last step writes the caller's w directly
-            a.base = step0 ? x0 : ucur;
-            a.a0h = (p >= 1) ? 1.0 : 0.0;
-            a.a0d = (p >= 1) ? c->combd : nullptr;
-            a.V = c->V;
-            a.ldv = c->ldv;
-            a.c0 = 0;
-            a.nc = mu + (corr ? 1 : 0);
-            a.g = c->comb;
-            a.gsign = 1.0;
-            a.ne = std::max(p - 1, 0);
-            for (int j = 1; j < p; j++) {
-                a.e[j - 1] = c->W + (int64_t)j * c->ldv;
-                a.ec[j - 1] = 1.0;
-            }
-            a.ecd = c->combd + 1;
-            int rc = launch_axpy(c, n, a, PC_COMBINE);
+        if (!combined) {
+            int rc = enqueue_combine(last, mu + (corr ? 1 : 0), nullptr, 0);
             if (rc) return finish(rc);
         }
         if (last) tk = t_end;
@@ -2718,7 +2746,7 @@ void phipm_destroy(phipm_ctx *c)
     if (c->ss_out_h) cudaFreeHost(c->ss_out_h);
     if (c->ev_spec) cudaEventDestroy(c->ev_spec);
     cudaFree(c->V); cudaFree(c->W); cudaFree(c->Y); cudaFree(c->U); cudaFree(c->H); cudaFree(c->sigma); cudaFree(c->g);
-    cudaFree(c->part_mx); cudaFree(c->raw_mx); cudaFree(c->counter_mx);
+    cudaFree(c->part_mx); cudaFree(c->raw_mx); cudaFree(c->counter_mx); cudaFree(c->dec_d);
     cudaFree(c->part); cudaFree(c->part2); cudaFree(c->comb); cudaFree(c->combd); cudaFree(c->scratch); cudaFree(c->raw);
     cudaFree(c->counter); cudaFree(c->st); cudaFree(c->tlo); cudaFree(c->thi); cudaFree(c->off16);
     cudaFree(c->hu); cudaFree(c->hw); cudaFree(c->hrp); cudaFree(c->hcol); cudaFree(c->hval);
@@ -2873,6 +2901,7 @@ int phipm_create(phipm_ctx **out, int64_t n_max, int m_max, int p_max, void *str
     A((void **)&c->g, sizeof(double) * (MAXD + 1));
     A((void **)&c->part, sizeof(double) * (size_t)c->pstride * (MAXD + 2));
     A((void **)&c->part2, sizeof(double) * (size_t)c->pstride * (MAXD + 2));
+    A((void **)&c->dec_d, sizeof(int) * 4);
     A((void **)&c->part_mx, sizeof(double) * (size_t)c->pstride * 2);
     A((void **)&c->raw_mx, sizeof(double) * 2);
     A((void **)&c->counter_mx, sizeof(unsigned) * 8);

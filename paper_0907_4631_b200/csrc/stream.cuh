@@ -1070,6 +1070,11 @@ __global__ void __launch_bounds__(SNT, SMINB) axpy_stream_kernel(int64_t n, Axpy
     KSTAMP(0)
     pdl_wait();
     KSTAMP(1)
+    int nc_ = a.nc;
+    if (a.guard) {                                         // (uniform: every CTA reads the same words)
+        if (__ldcg(a.guard) != a.guard_val) return;
+        nc_ = __ldcg(a.guard + 1);
+    }
     if (tid == 0) s_exit = a.check_brk ? (wk.st->brk >= 0) : 0;
     if (a.dfin) {
         // the preceding SpMV left its partials in wk.part2 (SpmvArgs.defer): reduce and finalize here
@@ -1078,19 +1083,19 @@ __global__ void __launch_bounds__(SNT, SMINB) axpy_stream_kernel(int64_t n, Axpy
         if (!deferred_finalize(a, wk, dred, dg, &s_a0s)) return;   // breakdown (FIN_ARNOLDI_LAG)
     }
     const int nbase = (a.a0h != 0.0) ? 1 : 0;
-    const int nitem = nbase + a.nc + a.ne;
+    const int nitem = nbase + nc_ + a.ne;
     for (int k = tid; k < nitem; k += SNT) {
         double c;
         const double *p;
         if (k < nbase) {
             c = a.a0h * (a.dfin == FIN_ARNOLDI_LAG ? s_a0s : (a.a0d ? *a.a0d : 1.0));   // (lag: a0d = &sigma_j)
             p = a.base;
-        } else if (k < nbase + a.nc) {
-            const int kc = a.rev ? (a.nc - 1 - (k - nbase)) : (k - nbase);
+        } else if (k < nbase + nc_) {
+            const int kc = a.rev ? (nc_ - 1 - (k - nbase)) : (k - nbase);
             c = a.gsign * (a.dfin ? dg[kc] : a.g[kc]);
             p = a.V + (int64_t)(a.c0 + kc) * a.ldv;
         } else {
-            const int i = k - nbase - a.nc;
+            const int i = k - nbase - nc_;
             c = a.ec[i] * (a.ecd ? a.ecd[i] : 1.0);
             p = a.e[i];
         }

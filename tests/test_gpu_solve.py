@@ -501,3 +501,50 @@ def test_c5_structure_large_m_cgs_and_cgs2(ctx, orc):
         wg, sg = run_gpu(ctx, Pb, "csr", m_init=m, fixed_m=True, orth=orth)
         assert sg.m_peak == m and sg.t_reached == Pb.t
         assert relerr(wg, wo) <= parity_bound(Pb.tol), (orth, loss, sg, so)
+
+
+@pytest.mark.parametrize("name", ["c2_med", "c3_med", "c4_med", "c5_med", "c4"])
+def test_precombine_and_side_maxabs_are_bit_identical(name):
+    # precombine: the exponential's epilogue takes Algorithm 3's acceptance decision (omega <= 1.2, the host's
+    # IEEE expression) and a guarded combine is enqueued before the host sees the result; side_maxabs:
+    # ||u_0||_inf is reduced on the second stream.  Neither changes any arithmetic: w, the stats and the
+    # controller trajectory are identical with both switched off
+    import torch
+    Pb = W.make(name)
+    u = [to_dev(x) for x in Pb.u]
+    A = tuple(to_dev(a) for a in Pb.csr) if Pb.csr is not None else None
+    out = {}
+    for flag in (1, 0):
+        c = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), options={"precombine": flag, "side_maxabs": flag})
+        if A is None:
+            w, s = c.solve_stencil(Pb.t, stencil_of(Pb), u, tol=Pb.tol, symmetric=Pb.symmetric)
+        else:
+            w, s = c.solve_csr(Pb.t, A, u, tol=Pb.tol, symmetric=Pb.symmetric)
+        out[flag] = (w.clone(), s, c.attempts())
+        c.close()
+    assert torch.equal(out[1][0], out[0][0])
+    assert out[1][1] == out[0][1]
+    assert out[1][2] == out[0][2]
+
+
+def test_precombine_multistep_rejections(orc):
+    # several steps with rejected attempts in between (2-D Laplacian 181^2, t = 2e-3): every rejected attempt
+    # leaves a guarded combine that must not run, every accepted one a combine that ran before the host
+    # decided; parity with the oracle and identity with the host-launched combines
+    import torch
+    from test_gpu_tmem import laplacian
+    st, u = laplacian(2, 181, 181, 1, seed=77, p=2)
+    t, tol = 2e-3, 1e-9
+    Pb = W.Problem(name="pc", n=st.n, p=2, t=t, tol=tol, symmetric=True, u=u, stencil=st, seed=0)
+    wo, so, _ = orc.solve(Pb)
+    ud = [to_dev(x) for x in u]
+    res = {}
+    for flag in (1, 0):
+        c = P.Context(n_max=st.n, m_max=100, p_max=2, options={"precombine": flag})
+        w, s = c.solve_stencil(t, P.Stencil.of(st), ud, tol=tol, symmetric=True)
+        res[flag] = (w.clone(), s)
+        c.close()
+    s1 = res[1][1]
+    assert s1.nsteps > 1 and s1.nreject > 0, s1
+    assert torch.equal(res[1][0], res[0][0]) and res[1][1] == res[0][1]
+    assert relerr(res[1][0].cpu().numpy(), wo) <= parity_bound(tol), (s1, so)

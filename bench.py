@@ -234,7 +234,8 @@ def run_gpu(args):
     Pb = replica_problem(args.config, rank)
     u = [torch.from_numpy(x).to(dev) for x in Pb.u]
     stream = torch.cuda.current_stream(dev)
-    ctx = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), stream=stream)
+    ctx = P.Context(n_max=Pb.n, m_max=Pb.m_max, p_max=max(Pb.p, 1), stream=stream,
+                    options={k: int(v) for k, v in (x.split("=") for x in args.option)})
     if Pb.stencil is not None:
         S = P.Stencil.of(Pb.stencil)
         solve = lambda **kw: ctx.solve_stencil(Pb.t, S, u, out=w, tol=Pb.tol, symmetric=Pb.symmetric,
@@ -413,6 +414,8 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(DESCR))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--option", action="append", default=[],
+                    help="kernel-path option name=value (phipm_set_option; A/B measurements, default: none)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -148,7 +148,7 @@ struct phipm_ctx {
     int seq = 0;
     int expm_method = PHIPM_EXPM_TAYLOR;     // phipm_expm / phipm_phi_pair
     // kernel-path selection (phipm_set_option; defaults: the measured-best paths)
-    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1, 0, 1, 1};
+    int opt[PHIPM_OPT_COUNT] = {1, 1, 1, 1, 1, 1, 0, 1, 1, 0, 1, 0, 384, 0, 1, 0, 1, 1, 1, 0, 1, 1, 0, 1, 0};
     // brick kernels: tensor maps of V, W and the w-recurrence's x_0 for the last grid / brick shape
     BrickMap brick_maps[5];                 // V planes, W planes, x_0 planes, V z-halo planes, V y-halo lines
     int krylov_path = PHIPM_PATH_NONE;      // kernel path of the last Krylov extension (phipm_krylov_path)

@@ -505,6 +505,7 @@ def test_c5_structure_large_m_cgs_and_cgs2(ctx, orc):
 
 @pytest.mark.parametrize("name", ["c2_med", "c3_med", "c4_med", "c5_med", "c4"])
 def test_precombine_and_side_maxabs_are_bit_identical(name):
+    import paper_0907_4631_b200 as P
     # precombine: the exponential's epilogue takes Algorithm 3's acceptance decision (omega <= 1.2, the host's
     # IEEE expression) and a guarded combine is enqueued before the host sees the result; side_maxabs:
     # ||u_0||_inf is reduced on the second stream.  Neither changes any arithmetic: w, the stats and the
@@ -528,6 +529,7 @@ def test_precombine_and_side_maxabs_are_bit_identical(name):
 
 
 def test_precombine_multistep_rejections(orc):
+    import paper_0907_4631_b200 as P
     # several steps with rejected attempts in between (2-D Laplacian 181^2, t = 2e-3): every rejected attempt
     # leaves a guarded combine that must not run, every accepted one a combine that ran before the host
     # decided; parity with the oracle and identity with the host-launched combines

@@ -233,7 +233,7 @@ int phipm_set_expm_method(phipm_ctx *ctx, int method);
  *                              H(:, j), g, sigma_j; 0: the SpMV's last CTA reduces and finalizes (ticket)
  *   PHIPM_OPT_BRICK            Lanczos extensions of 3-D 7-point stencils on 3-D bricks staged by tensor-map
  *                              TMA (one box copy per brick plane, zero fill outside the grid, z-marching
- *                              warps; y / v~ in tensor memory): 0 off, 1 auto (default: n >= 303K and
+ *                              warps; y / v~ in tensor memory): 0 off, 1 auto (default: n > 65536 and
  *                              x-lines that fill >= 3/4 of their 64-point warp segments), 2 whenever a
  *                              brick decomposition of the grid exists (nx even, <= 252)
  *   PHIPM_OPT_BRICK_HALO       1: the brick Lanczos kernel keeps the brick's interior in shared memory from step

@@ -775,6 +775,8 @@ bool brick_tensor_map(phipm_ctx *c, int slot, const double *base, int ncols, int
     return true;
 }
 
+constexpr int64_t BRICK_AUTO_MIN_N = 65536;   // brick = auto: grids larger than the cluster Lanczos kernel's range
+
 // the brick decomposition of this operator under PHIPM_OPT_BRICK (0 off, 1 auto: x-lines that fill >= 3/4 of
 // their 64-point warp segments, 2 whenever one exists)
 bool brick_plan(phipm_ctx *c, const StencilOp &op, BrickGeom &g)
@@ -871,7 +873,7 @@ WrecFn wrec_fn(const StencilOp &op)
 // 16-byte loads, so every u pointer must be 16-byte aligned (else the contiguous-range kernel)
 bool try_wrec_brick(phipm_ctx *c, const StencilOp &op, const WrecArgs &w, double bytes, int &rc)
 {
-    if (op.n < (int64_t)SNT * 4 * c->sm_count / 2 && opt(c, PHIPM_OPT_BRICK) != 2) return false;
+    if (op.n <= BRICK_AUTO_MIN_N && opt(c, PHIPM_OPT_BRICK) != 2) return false;
     BrickGeom g;
     if (!brick_plan(c, op, g)) return false;
     for (int j = 0; j < w.p; j++)
@@ -976,7 +978,9 @@ bool launch_persist<StencilOp>(phipm_ctx *c, const StencilOp &op, double bytes_o
     const double n = (double)op.n;
     for (int j = k0; j < k1; j++) bytes += bytes_op + 8.0 * n * (symmetric ? 4.0 : 2.0 * j + 3.0);
     // (small grids keep the 2048-row tiles: a 4096-row tile would leave half a CTA's threads idle)
-    if (symmetric && (op.n >= (int64_t)SNT * 4 * c->sm_count / 2 || opt(c, PHIPM_OPT_BRICK) == 2) &&
+    // (auto: above the cluster kernel's range; measured 9-11 % faster per step than the shared-memory
+    // persistent kernel on 3-D grids of 110K-262K rows, tools/brick_small.py)
+    if (symmetric && (op.n > BRICK_AUTO_MIN_N || opt(c, PHIPM_OPT_BRICK) == 2) &&
         try_persist_brick(c, op, k0, k1, bthr, bytes, rc))
         return true;
     if (symmetric && op.n >= (int64_t)SNT * 4 * c->sm_count / 2 && try_persist_tm(c, op, k0, k1, bthr, bytes, rc))

@@ -367,12 +367,16 @@ def test_controller_trajectory_c1(ctx, orc):
 @pytest.mark.parametrize("name,path,opts", [("c1_mini", "stencil", {}), ("c2_med", "stencil", {}),
                                             ("c3_med", "stencil", {"persist": 0}), ("c3_med", "stencil", {}),
                                             ("c4_tm", "stencil", {}), ("c5_med", "csr", {}),
-                                            ("c2_mini", "csr", {})])
+                                            ("c2_mini", "csr", {}),
+                                            ("c4_tm", "stencil", {"brick": 2}),
+                                            ("c4_tm", "stencil", {"brick": 2, "brick_halo": 1, "precombine": 1})])
 def test_guard_regions_and_inputs_untouched(orc, name, path, opts):
     """Out-of-bounds write check (compute-sanitizer is closed on this GPU pool): w is a view into a
     buffer with 4096-double guard regions of a NaN pattern on both sides, and every input (u_k, the
     CSR arrays) is compared bit for bit after the solve.  Every kernel family runs (single-CTA,
-    persistent smem / TMEM Lanczos, cooperative w-recurrence, streaming TMA-halo, CSR x-ring)."""
+    persistent smem / TMEM Lanczos, cooperative w-recurrence, streaming TMA-halo, CSR x-ring, the brick
+    kernels with their tensor-map copies -- c4_tm is 70^3: ragged x segments, ragged last bricks -- and the
+    interior-resident brick variant with tensor stores and the guarded combine)."""
     import torch
     import paper_0907_4631_b200 as P
     Pb = W.make(name)

@@ -82,14 +82,10 @@ struct NoRelease {
 // partials (e.g. to issue the next phase's first bulk copies off the critical path)
 // on_release_warps: run by lane 0 of EVERY warp at the same point (work that is spread over the warps,
 // e.g. one bulk tensor copy each); both hooks run after a proxy fence for the other CTAs' writes
-// after_arrive: run by every thread once the CTA's arrival is published and before it waits for the other
-// CTAs (thread 0: after its wait): work the other CTAs do not depend on, e.g. global stores of rows that no
-// neighbour reads, which then overlap the grid phase instead of delaying the arrival
-template <class OnRelease = NoRelease, class OnReleaseWarps = NoRelease, class AfterArrive = NoRelease>
+template <class OnRelease = NoRelease, class OnReleaseWarps = NoRelease>
 __device__ __forceinline__ bool phase_allreduce(const Work &wk, const double *bsum, int nv, unsigned phase,
                                                 const PersistArgs &a, double *red, OnRelease on_release = OnRelease{},
-                                                OnReleaseWarps on_release_warps = OnReleaseWarps{},
-                                                AfterArrive after_arrive = AfterArrive{})
+                                                OnReleaseWarps on_release_warps = OnReleaseWarps{})
 {
     __shared__ int s_ok;
     const int nb = gridDim.x;
@@ -119,9 +115,6 @@ __device__ __forceinline__ bool phase_allreduce(const Work &wk, const double *bs
         asm volatile("fence.proxy.async.global;" ::: "memory");
         s_ok = ok;
         if (a.dbg) a.dbg[((size_t)(phase - 1) * gridDim.x + blockIdx.x) * 2 + 1] = gtimer();
-        after_arrive();
-    } else {
-        after_arrive();
     }
     __syncthreads();
     if (!s_ok) return false;

@@ -1,6 +1,6 @@
 """SASS instruction mix of every kernel in libphipm.so (cuobjdump -sass, no GPU needed): counts of the
 Blackwell-specific instructions that prove the data paths -- UBLKCP (1-D TMA bulk copy), UBLKPF (TMA L2
-bulk prefetch), SYNCS (mbarrier), LDTM/STTM (tensor-memory load/store), UTMALLOC/UTMADEALLOC (TMEM
+bulk prefetch), UTMALDG / UTMASTG (tensor-map TMA load / store: the brick kernels), SYNCS (mbarrier), LDTM/STTM (tensor-memory load/store), UTMALLOC/UTMADEALLOC (TMEM
 allocation: UTCATOMSWS), DMMA (fp64 tensor-core MMA), plus DFMA/DMUL/DADD, LDS/STS, LDG/STG and SHFL.
 
     python tools/sass_mix.py > profiles/round2/sass_mix.txt
@@ -13,7 +13,7 @@ import os
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_0907_4631_b200", "lib", "libphipm.so")
-KEYS = ["UBLKCP", "UBLKPF", "SYNCS", "LDTM", "STTM", "UTCATOMSWS", "DMMA", "DFMA", "DMUL",
+KEYS = ["UBLKCP", "UBLKPF", "UTMALDG", "UTMASTG", "SYNCS", "LDTM", "STTM", "UTCATOMSWS", "DMMA", "DFMA", "DMUL",
         "DADD", "LDS", "STS", "LDG", "STG", "SHFL", "ATOMS", "RED", "ATOMG", "BAR"]
 out = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
 kern = None
